@@ -1,0 +1,340 @@
+"""bench.py — joined rows scored/sec of the fused query+MLP path (BASELINE.json metric).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c2] [--impl reference]
+
+One step = one flern_run_query over this rank's whole fact shard (scan -> probe -> gather ->
+tcgen05 MLP -> predicate -> group-by: every §8(a) row, one kernel launch) + (N > 1) the NCCL
+reduce of the per-group partials. Inputs are resident in HBM when the timed region starts; the
+fact columns (312 MB/GPU at SF1) exceed the 126 MB L2, so no flush is needed between steps.
+Weak scaling: every rank holds an SF1-sized lineitem shard of an SF=N database (orders table
+and weights replicated). `--impl reference` times the CPU oracle (the reference arm for this
+tier) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import datagen as D  # noqa: E402
+
+WORKLOADS = {
+    "c2": "TPC-H-shaped lineitem⋈orders (SF1 per GPU), 16 features -> MLP 16-256-256-1 (ReLU, sigmoid), "
+          "score>0.5, GROUP BY o_orderpriority COUNT/SUM(l_extendedprice)",
+    "c1": "TPC-H-shaped lineitem⋈orders (SF0.01 per GPU), 8 features -> MLP 8-64-1, score>0.5, GROUP BY "
+          "o_orderpriority COUNT/SUM(l_extendedprice)",
+    "c1x": "C1 query shape at SF10 per GPU (HBM-bound supplementary row), MLP 8-64-1",
+    "c4p": "SF10 per GPU, l_shipdate pre-filter (~2%) before inference, lineitem⋈orders, MLP 16-256-256-1",
+}
+METRIC = "joined rows scored/sec (query+MLP, whole box)"
+
+
+def flops_per_row(dims):
+    return 2 * sum(dims[i] * dims[i + 1] for i in range(len(dims) - 1))
+
+
+def workload_cfg(name, world):
+    if name == "c2":
+        base, sf1 = D.CONFIGS["c2"], 1.0
+    elif name == "c1":
+        base, sf1 = D.CONFIGS["c1"], 0.01
+    elif name == "c1x":
+        base, sf1 = D.CONFIGS["c1"], 10.0
+    elif name == "c4p":
+        base, sf1 = D.CONFIGS["c4p"], 10.0
+    else:
+        raise SystemExit(f"unknown workload {name}")
+    return D.with_sf(base, sf1 * world), sf1
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            j = json.load(f)
+        return float(j.get("bf16_tflops", 1590.0)), float(j.get("hbm_gbs", 6650.0)), "measured"
+    return 1590.0, 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 6:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx.append(float(f[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def cpu_baseline(cfg, db, model, seconds=15.0):
+    """The oracle, as it stands, on the host's cores: a bounded prefix of this workload."""
+    import oracle as O
+    threads = os.cpu_count() or 1
+    probe = min(db.fact_n, 2000 * threads)
+    t0 = time.perf_counter()
+    O.run(cfg, db, model, nthreads=threads, row_lo=0, row_hi=probe)
+    dt = max(1e-3, time.perf_counter() - t0)
+    rows = int(min(db.fact_n, max(probe, probe / dt * seconds)))
+    t0 = time.perf_counter()
+    r = O.run(cfg, db, model, nthreads=threads, row_lo=0, row_hi=rows)
+    dt = time.perf_counter() - t0
+    return {"value": r.rows_joined / dt, "unit": "rows/s", "cores": threads, "kind": "oracle",
+            "sample": f"first {rows} of {db.fact_n} lineitem rows of this rank's shard, full query "
+                      f"(unordered_map join + scalar fp64 MLP + predicate + group-by), {dt:.1f} s"}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def run_reference(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    import oracle as O
+    cfg, sf1 = workload_cfg(args.workload, world)
+    db = D.make_database(cfg, rank=0, world=world)
+    model = D.make_model(cfg, db)
+    threads = os.cpu_count() or 1
+    # bounded sample per step: ~ (budget / (W+K)) seconds of oracle work each
+    probe = min(db.fact_n, 1000 * threads)
+    t0 = time.perf_counter()
+    O.run(cfg, db, model, nthreads=threads, row_lo=0, row_hi=probe)
+    rate = probe / max(1e-3, time.perf_counter() - t0)
+    per_step_s = min(20.0, 150.0 / max(1, args.steps + args.warmup))
+    rows = int(min(db.fact_n, max(1000, rate * per_step_s)))
+    for i in range(args.warmup):
+        O.run(cfg, db, model, nthreads=threads, row_lo=0, row_hi=rows)
+    scored, t_total = 0, 0.0
+    for i in range(args.steps):
+        lo = (i * rows) % max(1, db.fact_n - rows + 1)
+        t0 = time.perf_counter()
+        r = O.run(cfg, db, model, nthreads=threads, row_lo=lo, row_hi=lo + rows)
+        t_total += time.perf_counter() - t0
+        scored += r.rows_joined
+    value = scored / t_total
+    sample = f"{rows} consecutive lineitem rows per step of {db.fact_n} ({args.workload}), {threads} threads"
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "rows/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t_total / max(1, args.steps),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOADS[args.workload], "sf_per_gpu": sf1, "rows_per_gpu": db.fact_n,
+                   "parallelism": f"oracle on rank 0 host cores (N={world})"},
+        "cpu_baseline": {"value": value, "unit": "rows/s", "cores": threads, "kind": "oracle", "sample": sample},
+        "e2e": {"value": value, "unit": "rows/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
+    ap.add_argument("--impl", default="flern", choices=["flern", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+    from paper_2311_02781_b200 import flern as F
+    from paper_2311_02781_b200.session import GpuQuery
+
+    world, rank, local = dist_env()
+    if world != args.gpus:
+        if world == 1 and args.gpus > 1:
+            raise SystemExit("run N>1 under torchrun (python -m torch.distributed.run --nproc-per-node N ...)")
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+
+    cfg, sf1 = workload_cfg(args.workload, world)
+    db = D.make_database(cfg, rank=rank, world=world)
+    model = D.make_model(cfg, db)
+    # fact shard resident in HBM (torch tensors borrowed by the library, no copy)
+    fact_dev = {k: torch.from_numpy(v).to(f"cuda:{local}") for k, v in db.fact.items()}
+    gq = GpuQuery(cfg, db, model, device=local, stream=stream.cuda_stream, load_fact=False)
+    gq.set_fact(F.flern_load_table(gq.ctx, "fact", fact_dev, F.FLERN_BORROW_DEVICE))
+    G = cfg.ngroups
+    out_count = torch.zeros(G, dtype=torch.int64, device=f"cuda:{local}")
+    out_sum = torch.zeros(G, dtype=torch.int64, device=f"cuda:{local}")
+    counters = torch.zeros(4, dtype=torch.int64, device=f"cuda:{local}")
+    partial = torch.zeros(2 * G, dtype=torch.int64, device=f"cuda:{local}")
+    q_async = gq.make_query(gq.fact_id, flags=F.FLERN_Q_RESULT_DEVICE | F.FLERN_Q_ASYNC)
+
+    # rows scored by this rank (deterministic): one synchronous run
+    r0 = gq.run(gq.make_query(gq.fact_id), count=np.zeros(G, np.int64), sum=np.zeros(G, np.int64))
+    rows_scored_rank = int(r0.rows_scored)
+
+    def step(ev_pair=None):
+        if ev_pair:
+            ev_pair[0].record(stream)
+        F.flern_run_query(gq.ctx, q_async, count=out_count, sum=out_sum, counters=counters)
+        if ev_pair:
+            ev_pair[1].record(stream)
+        if world > 1:
+            partial[:G].copy_(out_count)
+            partial[G:].copy_(out_sum)
+            dist.reduce(partial, dst=0)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        t_start.record(stream)
+        for i in range(args.steps):
+            step(evs[i])
+        t_end.record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+    ms_total = t_start.elapsed_time(t_end)
+    kernel_ms = [a.elapsed_time(b) for a, b in evs]
+    t = torch.tensor([ms_total, float(rows_scored_rank)], dtype=torch.float64, device=f"cuda:{local}")
+    if world > 1:
+        tmax = t[:1].clone()
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+        rows_all = t[1:].clone()
+        dist.all_reduce(rows_all, op=dist.ReduceOp.SUM)
+        ms_total, rows_total = float(tmax.item()), float(rows_all.item())
+    else:
+        rows_total = float(rows_scored_rank)
+    ms_per_step = ms_total / args.steps
+    value = rows_total / (ms_per_step / 1e3)
+
+    # ---- end to end through the public API with host buffers (pinned), every step:
+    #      H2D of the fact shard + query + D2H of the result
+    pinned = {k: torch.from_numpy(v).pin_memory() for k, v in db.fact.items()}
+    h2d = sum(v.numel() * 4 for v in pinned.values())
+    host_count, host_sum = np.zeros(G, np.int64), np.zeros(G, np.int64)
+    d2h = 2 * G * 8 + 4 * 8
+
+    def e2e_step():
+        tid = F.flern_load_table(gq.ctx, "fact_e2e", pinned, F.FLERN_COPY_HOST)
+        q = gq.make_query(tid)
+        r = F.flern_run_query(gq.ctx, q, count=host_count, sum=host_sum)
+        F.flern_drop_table(gq.ctx, tid)
+        return r
+
+    for _ in range(2):
+        e2e_step()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(args.e2e_steps):
+        e2e_step()
+    torch.cuda.synchronize()
+    e2e_s = (time.perf_counter() - t0) / args.e2e_steps
+    et = torch.tensor([e2e_s], dtype=torch.float64, device=f"cuda:{local}")
+    if world > 1:
+        dist.all_reduce(et, op=dist.ReduceOp.MAX)
+    e2e_value = rows_total / float(et.item())
+
+    if rank == 0:
+        tf_peak, hbm_peak, peak_src = peaks()
+        fpr = flops_per_row(cfg.dims)
+        avg_kernel_ms = sum(kernel_ms) / len(kernel_ms)
+        achieved = fpr * rows_scored_rank / (avg_kernel_ms / 1e3) / 1e12
+        traffic = None
+        tp = os.path.join(ROOT, "profiles", "traffic.json")
+        if os.path.exists(tp):
+            with open(tp) as f:
+                traffic = json.load(f).get(args.workload)
+        line = {
+            "metric": METRIC, "value": value, "unit": "rows/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": WORKLOADS[args.workload], "sf_per_gpu": sf1, "rows_per_gpu": db.fact_n,
+                       "rows_scored_per_gpu": rows_scored_rank,
+                       "l2": "no flush: inputs larger than L2 (fact columns %.0f MB/GPU > 126 MB)" % (h2d / 1e6),
+                       "parallelism": f"dp{world}: fact sharded by orderkey range, orders + weights replicated, "
+                                      "NCCL reduce of int64 group partials"},
+            "roofline": {"bound": "tensor", "achieved": achieved, "peak": tf_peak, "unit": "TFLOP/s",
+                         "frac": achieved / tf_peak, "traffic": traffic,
+                         "kernel": "flern_query_kernel", "peak_source": f"{peak_src} bf16_tflops (burst)",
+                         "flops_per_row": fpr, "avg_launch_ms": avg_kernel_ms},
+            "e2e": {"value": e2e_value, "unit": "rows/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+            "gpu_launches": args.steps * F.flern_query_launches(),
+            "clocks": clk.summary(),
+        }
+        if not args.no_cpu_baseline and world == 1:
+            line["cpu_baseline"] = cpu_baseline(cfg, db, model)
+        print(json.dumps(line), flush=True)
+    gq.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

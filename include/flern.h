@@ -1,0 +1,181 @@
+/* flern.h — C ABI of the B200-native Flern hot path (arXiv 2311.02781).
+ *
+ * The path (BASELINE.json north_star): scan a columnar fact table ->
+ * probe hash joins on dimension keys -> gather the model's feature columns straight into an
+ * on-chip tile -> dense MLP on tcgen05 tensor cores (bf16 in, fp32 accumulate) -> prediction
+ * predicate -> group-by aggregate. One persistent sm_100a kernel does all of it per query.
+ *
+ * The calls follow the paper's statement of the problem:
+ *   flern_load_table       "struct r_record* data = /" "* load data *" "/" (Fig. fig:classifier_generated,
+ *                          P:750): relational data is loaded once and stays where the model runs.
+ *   flern_load_model       sql.register_udf("classifier", model) / the udfMap.
+ *   flern_build_hashtable  the build side of HashJoinOp, map.update(leftHash(tuple), tuple)
+ *                          over the left child (Fig. code:lb2_join).
+ *   flern_run_query        sql("select ... classifier(xs) ..."): the fused record loop
+ *                          of Fig. fig:classifier_generated with the join probe
+ *                           and GROUP BY COUNT/SUM.
+ *
+ * Conventions
+ *   - Plain C; every call returns a flern_status (0 = ok, < 0 = error). The message of the
+ *     last error is flern_last_error(ctx); messages name the offending table/column/model.
+ *   - Every validation happens before any kernel launch; after an error other than
+ *     FLERN_E_CUDA the context stays usable.
+ *   - One context = one device + one CUDA stream. Not thread-safe; use one context per rank
+ *     (one process per GPU). All device work is ordered on the context's stream.
+ *   - There is no CPU fallback: without an sm_100 device flern_create fails.
+ */
+#ifndef FLERN_H
+#define FLERN_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FLERN_API __attribute__((visibility("default")))
+
+typedef int32_t flern_status;
+enum {
+  FLERN_OK = 0,
+  FLERN_E_INVALID_ARG = -1, /* NULL pointer, bad size, NaN threshold, key == INT32_MIN, ... */
+  FLERN_E_NOT_FOUND = -2,   /* unknown table / column / model / hash table (message names it) */
+  FLERN_E_DUPLICATE = -3,   /* a table or model of that name is already loaded */
+  FLERN_E_TYPE = -4,        /* join keys, group and sum columns must be integer-typed */
+  FLERN_E_ARITY = -5,       /* number of UDF feature arguments != model input width */
+  FLERN_E_SHAPE = -6,       /* layer dims do not chain, or output width != 1 */
+  FLERN_E_DUP_KEY = -7,     /* build-side key not unique (inner PK-FK join, reading Q2) */
+  FLERN_E_CUDA = -8,        /* CUDA runtime error (message has the CUDA error string) */
+  FLERN_E_OOM = -9,         /* device allocation failed */
+  FLERN_E_UNSUPPORTED = -10 /* valid request outside what this build implements (message says why) */
+};
+
+/* Column element types. Every column is 4 bytes per row. */
+typedef enum {
+  FLERN_I32 = 1,    /* int32 */
+  FLERN_F32 = 2,    /* float32 */
+  FLERN_DATE32 = 3, /* int32 days since 1970-01-01 */
+  FLERN_DEC32 = 4,  /* int32 fixed point, value * 10^-scale (e.g. cents); summed exactly as integers */
+  FLERN_DICT32 = 5  /* int32 dictionary code */
+} flern_dtype;
+
+typedef struct flern_ctx flern_ctx;
+
+/* Create a context on `device` (must be compute capability 10.0, sm_100a). `cuda_stream` is a
+ * cudaStream_t (e.g. torch.cuda.current_stream().cuda_stream) the context orders its work on;
+ * NULL = the context creates its own non-blocking stream. */
+FLERN_API flern_status flern_create(int device, void* cuda_stream, flern_ctx** out);
+/* Frees every device buffer the context owns (tables copied in, hash tables, models, scratch). */
+FLERN_API void flern_destroy(flern_ctx* ctx);
+FLERN_API const char* flern_last_error(const flern_ctx* ctx);
+FLERN_API const char* flern_version(void);
+
+/* ------------------------------------------------------------------------------------------ */
+typedef struct {
+  const char* name;  /* column name, unique within the table */
+  flern_dtype dtype;
+  int32_t scale;     /* DEC32 only: decimal scale (informational) */
+  const void* data;  /* nrows elements; host or device pointer per the load flags */
+} flern_column;
+
+enum {
+  FLERN_COPY_HOST = 0x1,     /* data are host pointers (pageable or pinned): copied into context-owned HBM */
+  FLERN_COPY_DEVICE = 0x2,   /* data are device pointers: copied into context-owned HBM */
+  FLERN_BORROW_DEVICE = 0x4  /* data are device pointers owned by the caller (e.g. torch tensors), used
+                                in place; they must stay valid until the table is dropped / ctx destroyed */
+};
+
+/* Load table `name` with `ncols` columns of `nrows` rows (this rank's shard for a sharded fact
+ * table). Exactly one of the flags above. Columns are 4-byte aligned. Writes *table_id.
+ * Errors: FLERN_E_DUPLICATE (name in use), FLERN_E_INVALID_ARG, FLERN_E_OOM, FLERN_E_CUDA. */
+FLERN_API flern_status flern_load_table(flern_ctx* ctx, const char* name, int64_t nrows, int32_t ncols,
+                                        const flern_column* cols, uint32_t flags, int32_t* table_id);
+/* Drop a table (frees copied columns; borrowed ones stay the caller's). Hash tables built on it
+ * stay valid (they hold their own key slots and payload). */
+FLERN_API flern_status flern_drop_table(flern_ctx* ctx, int32_t table_id);
+
+/* ------------------------------------------------------------------------------------------ */
+/* Register an MLP classifier as a UDF (udfMap P:823-824).
+ *   nlayers weight layers, dims[0..nlayers]; dims[nlayers] must be 1 (one score per record).
+ *   W[l]: host fp32 row-major [dims[l+1]][dims[l]] (torch.nn.Linear layout), rounded to bf16
+ *         (round-to-nearest-even) on load; b[l]: host fp32 [dims[l+1]], kept in fp32.
+ *   Hidden activation ReLU, output sigmoid (reading Q5).
+ *   in_shift/in_scale: host fp32 [dims[0]] per-feature normalisation applied in fp32 in the
+ *   gather, x = (v - shift) * scale, before the bf16 rounding (reading Q4).
+ * Everything is copied; the caller may free its arrays on return. Writes *model_id.
+ * Supported shapes (this build): dims[0] <= 48; 1 or 2 hidden layers; hidden width a multiple
+ * of 16 in [16, 256] (equal widths); others -> FLERN_E_UNSUPPORTED. Errors: FLERN_E_SHAPE,
+ * FLERN_E_DUPLICATE, FLERN_E_INVALID_ARG (NULL / non-finite weights). */
+FLERN_API flern_status flern_load_model(flern_ctx* ctx, const char* name, int32_t nlayers, const int32_t* dims,
+                                        const float* const* W, const float* const* b, const float* in_shift,
+                                        const float* in_scale, int32_t* model_id);
+
+/* ------------------------------------------------------------------------------------------ */
+/* Build side of an inner PK-FK equi-join (Fig. code:lb2_join P:323-326): an open-addressing
+ * table (power-of-two capacity >= 2*nrows, linear probing) mapping key_col -> build row, plus a
+ * row-major payload of `payload_cols` (the build columns the query later uses as features,
+ * group key, sum column or the key of a chained probe). key_col must be integer-typed and
+ * != INT32_MIN. Errors: FLERN_E_DUP_KEY (key not unique), FLERN_E_NOT_FOUND, FLERN_E_TYPE.
+ * Synchronous. Writes *ht_id. */
+FLERN_API flern_status flern_build_hashtable(flern_ctx* ctx, int32_t table_id, const char* key_col,
+                                             int32_t npayload, const char* const* payload_cols, int32_t* ht_id);
+
+/* ------------------------------------------------------------------------------------------ */
+typedef struct {
+  int32_t ht_id;       /* hash table to probe */
+  int32_t src;         /* where the probe key comes from: -1 = fact table, p = payload of probe p < this */
+  const char* key_col; /* key column name on src */
+} flern_probe;
+
+typedef struct {
+  int32_t src;     /* -1 = fact table column; p >= 0 = payload column of probe p's build row */
+  const char* col;
+} flern_colref;
+
+typedef struct {
+  int32_t fact_table;
+  const char* prefilter_col;      /* integer fact column; keep rows with pf_lo <= v < pf_hi; NULL = none */
+  int64_t pf_lo, pf_hi;
+  int32_t nprobes;                /* 1 or 2 inner joins, applied in order; a miss drops the row */
+  const flern_probe* probes;
+  int32_t model_id;
+  int32_t nfeat;                  /* UDF arguments; must equal the model's dims[0] (FLERN_E_ARITY) */
+  const flern_colref* feats;
+  float threshold;                /* select rows with score > threshold. <= 0: all; >= 1: none;
+                                     NaN: FLERN_E_INVALID_ARG */
+  flern_colref group_col;         /* integer codes in [0, ngroups) */
+  int32_t ngroups;                /* 1..64 */
+  flern_colref sum_col;           /* integer column, summed exactly in int64 */
+  uint32_t flags;                 /* FLERN_Q_* below */
+} flern_query;
+
+enum {
+  FLERN_Q_RESULT_DEVICE = 0x1, /* every result pointer is a device pointer (else host) */
+  FLERN_Q_ASYNC = 0x2,         /* with RESULT_DEVICE: enqueue only, no host sync; the rows_* counters
+                                  and elapsed_ms are not filled (read `counters` instead) */
+  FLERN_Q_BOTH_CLASSES = 0x4   /* count/sum hold [2][ngroups]: [0] score > t, [1] joined rows with score <= t
+                                  (the CASE WHEN sentiment < 0.5 / >= 0.5 query of P:1346-1354) */
+};
+
+typedef struct {
+  int64_t* count;          /* [ngroups] (x2 with BOTH_CLASSES), written */
+  int64_t* sum;            /* same shape */
+  int64_t* counters;       /* optional [4]: rows_scanned, rows_joined (= scored), rows_selected, bad_group */
+  float* dbg_score;        /* optional [fact rows]: fp32 score of each row that reached the model, NaN otherwise */
+  int32_t* dbg_match;      /* optional [fact rows * nprobes]: build row id of each probe, -1 = miss/not reached */
+  uint32_t* dbg_selected;  /* optional bitmap [ceil(rows/32)]: bit set if selected */
+  int64_t rows_scanned, rows_joined, rows_scored, rows_selected; /* filled unless FLERN_Q_ASYNC */
+  float elapsed_ms;        /* device time of the query kernel (CUDA events), unless FLERN_Q_ASYNC */
+} flern_result;
+
+/* Run the query on the context's stream (synchronous unless FLERN_Q_ASYNC). One kernel launch.
+ * A group code outside [0, ngroups) is a data error: FLERN_E_INVALID_ARG after the run (sync mode)
+ * and counted in counters[3]. */
+FLERN_API flern_status flern_run_query(flern_ctx* ctx, const flern_query* q, flern_result* res);
+
+/* Number of CUDA kernels flern_run_query launches per call (for launch accounting): 1. */
+FLERN_API int32_t flern_query_launches(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FLERN_H */

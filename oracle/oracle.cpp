@@ -77,7 +77,9 @@ double mlp_logit(const or_model& m, const double* x, std::vector<double>& h, std
       for (int32_t k = 0; k < in; ++k) z += (double)m.W[l][(int64_t)j * in + k] * h[k];
       if (l + 1 < m.nlayers) {
         z = z > 0.0 ? z : 0.0;                        // ReLU
-        if (emu) z = (double)or_bf16_rne((float)z);   // diagnostic: GPU stores hidden h as bf16
+        // diagnostic mode only: activations that feed another tensor-core (hidden) layer are
+        // stored as bf16 on the GPU; the last hidden layer feeds the fp32 output dot unrounded
+        if (emu && l + 2 < m.nlayers) z = (double)or_bf16_rne((float)z);
       }
       hn[j] = z;
     }

@@ -51,7 +51,10 @@ typedef struct {
   or_colref group; int32_t ngroups;                   /* dense codes in [0, ngroups) */
   or_colref sum;                                      /* int32 column summed in int64 */
   double band;                                        /* band half-width for parity rule 3 */
-  int32_t emulate_bf16;                               /* diagnostic: round x, h to bf16 like the GPU */
+  int32_t emulate_bf16;                               /* diagnostic: the GPU's documented numeric format
+                                                         (DESIGN.md): x = bf16(fp32 normalise), hidden
+                                                         activations feeding another hidden layer bf16,
+                                                         the output layer an unrounded dot */
   int32_t nthreads;                                   /* 0 = hardware concurrency */
   int64_t row_lo, row_hi;                             /* fact row range; row_hi < 0 = all rows */
 } or_query;

@@ -1,0 +1,50 @@
+// build_kernel.cuh — hash-join build side (Fig. code:lb2_join):
+//   map.update(leftHash(tuple), tuple) over the dimension table, as an open-addressing table
+//   of 8-byte {key, row} slots (power-of-two capacity, linear probing) filled with one 64-bit
+//   atomicCAS per insert, plus a row-major payload of the columns the query later reads.
+#pragma once
+#include "query_kernel.cuh"
+
+namespace flern {
+
+constexpr unsigned long long kEmptySlot = 0xFFFFFFFF80000000ull;  // {key = INT32_MIN, row = -1}
+
+__global__ void fill_slots_kernel(unsigned long long* slots, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    slots[i] = kEmptySlot;
+}
+
+// flags[0]: duplicate key seen, flags[1]: reserved key (INT32_MIN) seen
+__global__ void build_insert_kernel(const int32_t* __restrict__ keys, int64_t nrows,
+                                    unsigned long long* __restrict__ slots, uint32_t mask, uint32_t shift,
+                                    int32_t* __restrict__ flags) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nrows; i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t key = keys[i];
+    if (key == kEmptyKey) { atomicExch(&flags[1], 1); continue; }
+    const unsigned long long item = (unsigned long long)(uint32_t)key | ((unsigned long long)(uint32_t)i << 32);
+    uint32_t h = hash_key(key, shift);
+    while (true) {
+      const unsigned long long prev = atomicCAS(slots + h, kEmptySlot, item);
+      if (prev == kEmptySlot) break;
+      if ((int32_t)(uint32_t)prev == key) { atomicExch(&flags[0], 1); break; }
+      h = (h + 1) & mask;
+    }
+  }
+}
+
+struct PayloadCols {
+  const int32_t* col[kMaxFeat + 4];
+};
+
+// payload[row][w] = col_w[row] (w < npay), zero padding up to pstride
+__global__ void pack_payload_kernel(const __grid_constant__ PayloadCols cols, int32_t npay, int32_t pstride,
+                                    int64_t nrows, int32_t* __restrict__ payload) {
+  const int64_t total = nrows * pstride;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / pstride;
+    const int32_t w = (int32_t)(i - r * pstride);
+    payload[i] = w < npay ? cols.col[w][r] : 0;
+  }
+}
+
+}  // namespace flern

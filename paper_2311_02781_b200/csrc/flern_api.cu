@@ -1,0 +1,643 @@
+// flern_api.cu — the C ABI (include/flern.h): context, tables, models, hash tables, queries.
+// Host-side validation happens before any launch; every device step is one of this library's
+// sm_100a kernels (query_kernel.cuh, build_kernel.cuh). There is no CPU compute path.
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "flern.h"
+#include "build_kernel.cuh"
+#include "query_kernel.cuh"
+
+using namespace flern;
+
+namespace {
+
+struct Column {
+  std::string name;
+  flern_dtype dtype;
+  int32_t scale;
+  void* dptr;
+  bool owned;
+};
+struct Table {
+  std::string name;
+  int64_t nrows = 0;
+  std::vector<Column> cols;
+  bool alive = false;
+  const Column* find(const char* n) const {
+    for (const auto& c : cols)
+      if (c.name == n) return &c;
+    return nullptr;
+  }
+};
+struct Model {
+  std::string name;
+  std::vector<int32_t> dims;
+  int K0 = 0, K0P = 0, H = 0, NL = 0;
+  uint8_t* dbuf = nullptr;   // [wimg | bias | wout | shift | scale]
+  size_t wimg_bytes = 0, off_bias = 0, off_wout = 0, off_shift = 0, off_scale = 0;
+  float bout = 0.f;
+};
+struct HashTable {
+  int32_t table_id = -1;
+  std::string key_col;
+  flern_dtype key_type;
+  int64_t nrows = 0;
+  uint32_t log2cap = 0;
+  unsigned long long* slots = nullptr;
+  int32_t* payload = nullptr;
+  int32_t pstride = 0;
+  std::vector<std::string> pcols;
+  std::vector<flern_dtype> ptypes;
+  int find(const char* n) const {
+    for (size_t i = 0; i < pcols.size(); ++i)
+      if (pcols[i] == n) return (int)i;
+    return -1;
+  }
+};
+
+bool is_int_type(flern_dtype t) { return t == FLERN_I32 || t == FLERN_DATE32 || t == FLERN_DEC32 || t == FLERN_DICT32; }
+bool is_valid_type(int t) { return t >= FLERN_I32 && t <= FLERN_DICT32; }
+
+}  // namespace
+
+struct flern_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  int num_sms = 148;
+  std::string err;
+  std::vector<Table> tables;
+  std::vector<Model> models;
+  std::vector<HashTable> hts;
+  // query scratch
+  int64_t* partials = nullptr;
+  unsigned int* ticket = nullptr;
+  int64_t* dres = nullptr;        // [2*kMaxGroups count | 2*kMaxGroups sum | kCounters]
+  int32_t* dflags = nullptr;      // build flags
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+};
+
+namespace {
+
+flern_status fail(flern_ctx* ctx, flern_status code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  if (ctx) ctx->err = buf;
+  return code;
+}
+
+#define CUDA_TRY(ctx, expr)                                                                          \
+  do {                                                                                               \
+    cudaError_t e_ = (expr);                                                                         \
+    if (e_ != cudaSuccess) {                                                                         \
+      flern_status c_ = (e_ == cudaErrorMemoryAllocation) ? FLERN_E_OOM : FLERN_E_CUDA;              \
+      return fail(ctx, c_, "CUDA error in %s: %s", #expr, cudaGetErrorString(e_));                   \
+    }                                                                                                \
+  } while (0)
+
+uint16_t bf16_rne_bits(float f) {
+  uint32_t u;
+  std::memcpy(&u, &f, 4);
+  if ((u & 0x7F800000u) == 0x7F800000u) return (uint16_t)((u >> 16) | ((u & 0xFFFF) ? 0x40 : 0));
+  u = u + 0x7FFFu + ((u >> 16) & 1u);
+  return (uint16_t)(u >> 16);
+}
+
+int grid_for(int64_t n, int threads = 256) {
+  int64_t g = (n + threads - 1) / threads;
+  if (g < 1) g = 1;
+  if (g > 4096) g = 4096;
+  return (int)g;
+}
+
+// ---------------------------------------------------------------- kernel dispatch table
+using KernelFn = void (*)(const QueryParams);
+struct KernelEntry {
+  int K0P, H, NL;
+  KernelFn fn;
+  uint32_t smem;
+  bool attr_set;
+};
+
+template <int K0P, int H, int NL>
+constexpr bool plan_fits() {
+  constexpr uint32_t WH = (NL >= 2) ? (uint32_t)H * H * 2 : 0;
+  constexpr uint32_t HB = (NL >= 2) ? (uint32_t)kTile * H * 2 : 0;
+  constexpr uint32_t W1 = (uint32_t)H * K0P * 2;
+  constexpr uint32_t XS = (uint32_t)kTile * K0P * 2;
+  constexpr uint32_t META = 16 + 9 * kTile;
+  constexpr uint32_t FIXED = WH + HB + W1 + NL * H * 4 + H * 4 + kMaxGroups * 4 * 8 + 2 * kTile * 4 + kMaxFeat * 8 +
+                             64 * 8 + 128;
+  return FIXED + 3 * (XS + META) <= 232448;
+}
+
+#define FLERN_KERNELS(X) \
+  X(16, 64, 1) X(16, 128, 1) X(16, 256, 1) X(32, 64, 1) X(32, 128, 1) X(32, 256, 1) X(48, 64, 1) X(48, 128, 1) \
+  X(48, 256, 1) X(16, 64, 2) X(16, 128, 2) X(16, 256, 2) X(32, 64, 2) X(32, 128, 2) X(48, 64, 2) X(48, 128, 2)
+
+#define FLERN_ENTRY(a, b, c) {a, b, c, flern_query_kernel<a, b, c>, SmemPlan<a, b, c>::total, false},
+KernelEntry g_kernels[] = {FLERN_KERNELS(FLERN_ENTRY)};
+#define FLERN_FITS(a, b, c) static_assert(plan_fits<a, b, c>(), "plan");
+FLERN_KERNELS(FLERN_FITS)
+
+KernelEntry* find_kernel(int K0P, int H, int NL) {
+  for (auto& e : g_kernels)
+    if (e.K0P == K0P && e.H == H && e.NL == NL) return &e;
+  return nullptr;
+}
+
+}  // namespace
+
+// ================================================================================ context
+extern "C" FLERN_API const char* flern_version(void) { return "flern-b200 0.1 (sm_100a)"; }
+
+extern "C" FLERN_API flern_status flern_create(int device, void* cuda_stream, flern_ctx** out) {
+  if (!out) return FLERN_E_INVALID_ARG;
+  *out = nullptr;
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess || ndev == 0) return FLERN_E_UNSUPPORTED;
+  if (device < 0 || device >= ndev) return FLERN_E_INVALID_ARG;
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, device) != cudaSuccess) return FLERN_E_CUDA;
+  if (prop.major != 10) return FLERN_E_UNSUPPORTED;   // sm_100a only; no fallback
+  std::unique_ptr<flern_ctx> ctx(new flern_ctx());
+  ctx->device = device;
+  ctx->num_sms = prop.multiProcessorCount;
+  if (cudaSetDevice(device) != cudaSuccess) return FLERN_E_CUDA;
+  if (cuda_stream) {
+    ctx->stream = static_cast<cudaStream_t>(cuda_stream);
+  } else {
+    if (cudaStreamCreate(&ctx->stream) != cudaSuccess) return FLERN_E_CUDA;  // blocking w.r.t. legacy stream
+    ctx->own_stream = true;
+  }
+  const size_t W = (size_t)kMaxGroups * 4 + kCounters;
+  if (cudaMalloc(&ctx->partials, (size_t)ctx->num_sms * W * sizeof(int64_t)) != cudaSuccess) return FLERN_E_OOM;
+  if (cudaMalloc(&ctx->ticket, 64) != cudaSuccess) return FLERN_E_OOM;
+  if (cudaMalloc(&ctx->dres, (4 * kMaxGroups + kCounters) * sizeof(int64_t)) != cudaSuccess) return FLERN_E_OOM;
+  if (cudaMalloc(&ctx->dflags, 64) != cudaSuccess) return FLERN_E_OOM;
+  if (cudaMemsetAsync(ctx->ticket, 0, 64, ctx->stream) != cudaSuccess) return FLERN_E_CUDA;
+  if (cudaEventCreate(&ctx->ev0) != cudaSuccess || cudaEventCreate(&ctx->ev1) != cudaSuccess) return FLERN_E_CUDA;
+  if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) return FLERN_E_CUDA;
+  *out = ctx.release();
+  return FLERN_OK;
+}
+
+extern "C" FLERN_API void flern_destroy(flern_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  for (auto& t : ctx->tables)
+    for (auto& c : t.cols)
+      if (c.owned && c.dptr) cudaFree(c.dptr);
+  for (auto& m : ctx->models) cudaFree(m.dbuf);
+  for (auto& h : ctx->hts) { cudaFree(h.slots); cudaFree(h.payload); }
+  cudaFree(ctx->partials);
+  cudaFree(ctx->ticket);
+  cudaFree(ctx->dres);
+  cudaFree(ctx->dflags);
+  if (ctx->ev0) cudaEventDestroy(ctx->ev0);
+  if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+  if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+}
+
+extern "C" FLERN_API const char* flern_last_error(const flern_ctx* ctx) {
+  return ctx ? ctx->err.c_str() : "null context";
+}
+
+extern "C" FLERN_API int32_t flern_query_launches(void) { return 1; }
+
+// ================================================================================ tables
+extern "C" FLERN_API flern_status flern_load_table(flern_ctx* ctx, const char* name, int64_t nrows, int32_t ncols,
+                                                   const flern_column* cols, uint32_t flags, int32_t* table_id) {
+  if (!ctx) return FLERN_E_INVALID_ARG;
+  if (!name || !table_id || nrows < 0 || ncols <= 0 || !cols)
+    return fail(ctx, FLERN_E_INVALID_ARG, "flern_load_table: bad arguments for table '%s'", name ? name : "(null)");
+  if (nrows >= (int64_t)1 << 31) return fail(ctx, FLERN_E_UNSUPPORTED, "table '%s': more than 2^31-1 rows per shard", name);
+  const uint32_t mode = flags & (FLERN_COPY_HOST | FLERN_COPY_DEVICE | FLERN_BORROW_DEVICE);
+  if (mode != FLERN_COPY_HOST && mode != FLERN_COPY_DEVICE && mode != FLERN_BORROW_DEVICE)
+    return fail(ctx, FLERN_E_INVALID_ARG, "table '%s': exactly one of COPY_HOST / COPY_DEVICE / BORROW_DEVICE", name);
+  for (const auto& t : ctx->tables)
+    if (t.alive && t.name == name) return fail(ctx, FLERN_E_DUPLICATE, "table '%s' already loaded", name);
+  for (int32_t i = 0; i < ncols; ++i) {
+    if (!cols[i].name) return fail(ctx, FLERN_E_INVALID_ARG, "table '%s': column %d has no name", name, i);
+    if (!is_valid_type(cols[i].dtype))
+      return fail(ctx, FLERN_E_TYPE, "table '%s': column '%s' has an unknown dtype", name, cols[i].name);
+    if (nrows > 0 && !cols[i].data)
+      return fail(ctx, FLERN_E_INVALID_ARG, "table '%s': column '%s' has no data", name, cols[i].name);
+    if (reinterpret_cast<uintptr_t>(cols[i].data) % 4 != 0)
+      return fail(ctx, FLERN_E_INVALID_ARG, "table '%s': column '%s' is not 4-byte aligned", name, cols[i].name);
+    for (int32_t j = 0; j < i; ++j)
+      if (std::strcmp(cols[i].name, cols[j].name) == 0)
+        return fail(ctx, FLERN_E_DUPLICATE, "table '%s': column '%s' appears twice", name, cols[i].name);
+  }
+  CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+  Table t;
+  t.name = name;
+  t.nrows = nrows;
+  t.alive = true;
+  const size_t bytes = (size_t)nrows * 4;
+  for (int32_t i = 0; i < ncols; ++i) {
+    Column c{cols[i].name, cols[i].dtype, cols[i].scale, nullptr, false};
+    if (mode == FLERN_BORROW_DEVICE) {
+      c.dptr = const_cast<void*>(cols[i].data);
+    } else if (bytes > 0) {
+      cudaError_t e = cudaMalloc(&c.dptr, bytes);
+      if (e != cudaSuccess) {
+        for (auto& cc : t.cols) if (cc.owned) cudaFree(cc.dptr);
+        return fail(ctx, FLERN_E_OOM, "table '%s': cannot allocate %zu bytes for column '%s'", name, bytes, c.name.c_str());
+      }
+      c.owned = true;
+      e = cudaMemcpyAsync(c.dptr, cols[i].data, bytes,
+                          mode == FLERN_COPY_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, ctx->stream);
+      if (e != cudaSuccess) {
+        cudaFree(c.dptr);
+        for (auto& cc : t.cols) if (cc.owned) cudaFree(cc.dptr);
+        return fail(ctx, FLERN_E_CUDA, "table '%s': copy failed: %s", name, cudaGetErrorString(e));
+      }
+    }
+    t.cols.push_back(c);
+  }
+  if (mode == FLERN_COPY_HOST) CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));  // host buffer may be freed
+  // reuse a dead slot
+  for (size_t i = 0; i < ctx->tables.size(); ++i) {
+    if (!ctx->tables[i].alive) {
+      ctx->tables[i] = std::move(t);
+      *table_id = (int32_t)i;
+      return FLERN_OK;
+    }
+  }
+  ctx->tables.push_back(std::move(t));
+  *table_id = (int32_t)ctx->tables.size() - 1;
+  return FLERN_OK;
+}
+
+extern "C" FLERN_API flern_status flern_drop_table(flern_ctx* ctx, int32_t table_id) {
+  if (!ctx) return FLERN_E_INVALID_ARG;
+  if (table_id < 0 || table_id >= (int32_t)ctx->tables.size() || !ctx->tables[table_id].alive)
+    return fail(ctx, FLERN_E_NOT_FOUND, "no table with id %d", table_id);
+  CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+  CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  Table& t = ctx->tables[table_id];
+  for (auto& c : t.cols)
+    if (c.owned && c.dptr) cudaFree(c.dptr);
+  t.cols.clear();
+  t.alive = false;
+  t.name.clear();
+  return FLERN_OK;
+}
+
+// ================================================================================ models
+extern "C" FLERN_API flern_status flern_load_model(flern_ctx* ctx, const char* name, int32_t nlayers,
+                                                   const int32_t* dims, const float* const* W, const float* const* b,
+                                                   const float* in_shift, const float* in_scale, int32_t* model_id) {
+  if (!ctx) return FLERN_E_INVALID_ARG;
+  if (!name || !dims || !W || !b || !in_shift || !in_scale || !model_id || nlayers < 1)
+    return fail(ctx, FLERN_E_INVALID_ARG, "flern_load_model: bad arguments for model '%s'", name ? name : "(null)");
+  for (const auto& m : ctx->models)
+    if (m.name == name) return fail(ctx, FLERN_E_DUPLICATE, "model '%s' already registered", name);
+  for (int32_t l = 0; l <= nlayers; ++l)
+    if (dims[l] <= 0) return fail(ctx, FLERN_E_SHAPE, "model '%s': dims[%d] = %d", name, l, dims[l]);
+  if (dims[nlayers] != 1) return fail(ctx, FLERN_E_SHAPE, "model '%s': output width %d != 1", name, dims[nlayers]);
+  const int NL = nlayers - 1;   // hidden layers
+  const int K0 = dims[0];
+  if (NL < 1 || NL > 2)
+    return fail(ctx, FLERN_E_UNSUPPORTED, "model '%s': %d hidden layers (this build: 1 or 2)", name, NL);
+  const int H = dims[1];
+  for (int l = 1; l <= NL; ++l)
+    if (dims[l] != H) return fail(ctx, FLERN_E_UNSUPPORTED, "model '%s': hidden widths must be equal", name);
+  if (H % 64 != 0 || H > 256)
+    return fail(ctx, FLERN_E_UNSUPPORTED, "model '%s': hidden width %d (this build: 64, 128, 192->no, 256)", name, H);
+  if (K0 > kMaxFeat) return fail(ctx, FLERN_E_UNSUPPORTED, "model '%s': %d inputs > %d", name, K0, kMaxFeat);
+  const int K0P = (K0 + 15) / 16 * 16;
+  if (!find_kernel(K0P, H, NL))
+    return fail(ctx, FLERN_E_UNSUPPORTED, "model '%s': shape %d-%d x%d does not fit the on-chip plan", name, K0, H, NL);
+  for (int l = 0; l < nlayers; ++l) {
+    if (!W[l] || !b[l]) return fail(ctx, FLERN_E_INVALID_ARG, "model '%s': layer %d has no weights", name, l);
+    for (int64_t i = 0; i < (int64_t)dims[l] * dims[l + 1]; ++i)
+      if (!std::isfinite(W[l][i])) return fail(ctx, FLERN_E_INVALID_ARG, "model '%s': non-finite weight in layer %d", name, l);
+    for (int i = 0; i < dims[l + 1]; ++i)
+      if (!std::isfinite(b[l][i])) return fail(ctx, FLERN_E_INVALID_ARG, "model '%s': non-finite bias in layer %d", name, l);
+  }
+  for (int k = 0; k < K0; ++k)
+    if (!std::isfinite(in_shift[k]) || !std::isfinite(in_scale[k]))
+      return fail(ctx, FLERN_E_INVALID_ARG, "model '%s': non-finite normalisation for input %d", name, k);
+
+  Model m;
+  m.name = name;
+  m.dims.assign(dims, dims + nlayers + 1);
+  m.K0 = K0; m.K0P = K0P; m.H = H; m.NL = NL;
+  const size_t WH = NL >= 2 ? (size_t)H * H * 2 : 0;
+  const size_t W1 = (size_t)H * K0P * 2;
+  m.wimg_bytes = WH + W1;
+  m.off_bias = (m.wimg_bytes + 255) / 256 * 256;
+  m.off_wout = m.off_bias + (size_t)NL * H * 4;
+  m.off_shift = m.off_wout + (size_t)H * 4;
+  m.off_scale = m.off_shift + (size_t)K0P * 4;
+  const size_t total = m.off_scale + (size_t)K0P * 4;
+  std::vector<uint8_t> img(total, 0);
+  uint16_t* wh = reinterpret_cast<uint16_t*>(img.data());
+  uint16_t* w1 = reinterpret_cast<uint16_t*>(img.data() + WH);
+  // W1: [H x K0P] interleaved K-major: (k/8)*(H*16) + (n/8)*128 + (n%8)*16 + (k%8)*2 bytes
+  for (int n = 0; n < H; ++n)
+    for (int k = 0; k < K0P; ++k) {
+      const float v = k < K0 ? W[0][(int64_t)n * K0 + k] : 0.f;
+      const size_t off = (size_t)(k / 8) * (H * 16) + (n / 8) * 128 + (n % 8) * 16 + (k % 8) * 2;
+      w1[off / 2] = bf16_rne_bits(v);
+    }
+  // W2: [H x H] 128B-swizzled K-major: (k/64)*(H*128) + (n/8)*1024 + (n%8)*128 + (((k%64)/8) ^ (n%8))*16 + (k%8)*2
+  if (NL >= 2)
+    for (int n = 0; n < H; ++n)
+      for (int k = 0; k < H; ++k) {
+        const size_t off = (size_t)(k / 64) * (H * 128) + (n / 8) * 1024 + (n % 8) * 128 +
+                           (size_t)((((k % 64) / 8) ^ (n % 8)) * 16) + (k % 8) * 2;
+        wh[off / 2] = bf16_rne_bits(W[1][(int64_t)n * H + k]);
+      }
+  float* bias = reinterpret_cast<float*>(img.data() + m.off_bias);
+  for (int l = 0; l < NL; ++l)
+    for (int j = 0; j < H; ++j) bias[l * H + j] = b[l][j];
+  float* wout = reinterpret_cast<float*>(img.data() + m.off_wout);   // output layer stays fp32 (CUDA-core dot)
+  for (int j = 0; j < H; ++j) wout[j] = W[NL][j];
+  m.bout = b[NL][0];
+  float* sh = reinterpret_cast<float*>(img.data() + m.off_shift);
+  float* sc = reinterpret_cast<float*>(img.data() + m.off_scale);
+  for (int k = 0; k < K0; ++k) { sh[k] = in_shift[k]; sc[k] = in_scale[k]; }
+  CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+  CUDA_TRY(ctx, cudaMalloc(&m.dbuf, total));
+  CUDA_TRY(ctx, cudaMemcpyAsync(m.dbuf, img.data(), total, cudaMemcpyHostToDevice, ctx->stream));
+  CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  ctx->models.push_back(std::move(m));
+  *model_id = (int32_t)ctx->models.size() - 1;
+  return FLERN_OK;
+}
+
+// ================================================================================ hash tables
+extern "C" FLERN_API flern_status flern_build_hashtable(flern_ctx* ctx, int32_t table_id, const char* key_col,
+                                                        int32_t npayload, const char* const* payload_cols,
+                                                        int32_t* ht_id) {
+  if (!ctx) return FLERN_E_INVALID_ARG;
+  if (!key_col || !ht_id || npayload < 0 || (npayload > 0 && !payload_cols))
+    return fail(ctx, FLERN_E_INVALID_ARG, "flern_build_hashtable: bad arguments");
+  if (npayload > kMaxFeat + 4) return fail(ctx, FLERN_E_UNSUPPORTED, "at most %d payload columns", kMaxFeat + 4);
+  if (table_id < 0 || table_id >= (int32_t)ctx->tables.size() || !ctx->tables[table_id].alive)
+    return fail(ctx, FLERN_E_NOT_FOUND, "no table with id %d", table_id);
+  const Table& t = ctx->tables[table_id];
+  const Column* kc = t.find(key_col);
+  if (!kc) return fail(ctx, FLERN_E_NOT_FOUND, "table '%s' has no column '%s'", t.name.c_str(), key_col);
+  if (!is_int_type(kc->dtype)) return fail(ctx, FLERN_E_TYPE, "join key '%s' must be integer-typed", key_col);
+  HashTable h;
+  h.table_id = table_id;
+  h.key_col = key_col;
+  h.key_type = kc->dtype;
+  h.nrows = t.nrows;
+  PayloadCols pc{};
+  for (int32_t i = 0; i < npayload; ++i) {
+    const Column* c = payload_cols[i] ? t.find(payload_cols[i]) : nullptr;
+    if (!c) return fail(ctx, FLERN_E_NOT_FOUND, "table '%s' has no column '%s'", t.name.c_str(),
+                        payload_cols[i] ? payload_cols[i] : "(null)");
+    h.pcols.push_back(c->name);
+    h.ptypes.push_back(c->dtype);
+    pc.col[i] = static_cast<const int32_t*>(c->dptr);
+  }
+  h.pstride = npayload <= 0 ? 1 : (npayload + 3) / 4 * 4;   // 16-byte rows
+  uint32_t lg = 6;
+  while (((int64_t)1 << lg) < 2 * t.nrows) ++lg;           // load factor <= 0.5
+  h.log2cap = lg;
+  const int64_t cap = (int64_t)1 << lg;
+  CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+  CUDA_TRY(ctx, cudaMalloc(&h.slots, cap * sizeof(unsigned long long)));
+  CUDA_TRY(ctx, cudaMalloc(&h.payload, std::max<int64_t>(1, t.nrows) * h.pstride * sizeof(int32_t)));
+  CUDA_TRY(ctx, cudaMemsetAsync(ctx->dflags, 0, 64, ctx->stream));
+  fill_slots_kernel<<<grid_for(cap), 256, 0, ctx->stream>>>(h.slots, cap);
+  if (t.nrows > 0) {
+    build_insert_kernel<<<grid_for(t.nrows), 256, 0, ctx->stream>>>(static_cast<const int32_t*>(kc->dptr), t.nrows,
+                                                                    h.slots, (uint32_t)(cap - 1), 32u - lg, ctx->dflags);
+    if (npayload > 0)
+      pack_payload_kernel<<<grid_for(t.nrows * h.pstride), 256, 0, ctx->stream>>>(pc, npayload, h.pstride, t.nrows,
+                                                                                  h.payload);
+  }
+  CUDA_TRY(ctx, cudaGetLastError());
+  int32_t flags[2] = {0, 0};
+  CUDA_TRY(ctx, cudaMemcpyAsync(flags, ctx->dflags, sizeof(flags), cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  if (flags[0] || flags[1]) {
+    cudaFree(h.slots);
+    cudaFree(h.payload);
+    if (flags[1]) return fail(ctx, FLERN_E_INVALID_ARG, "key column '%s' contains the reserved value INT32_MIN", key_col);
+    return fail(ctx, FLERN_E_DUP_KEY, "key column '%s' of table '%s' is not unique", key_col, t.name.c_str());
+  }
+  ctx->hts.push_back(std::move(h));
+  *ht_id = (int32_t)ctx->hts.size() - 1;
+  return FLERN_OK;
+}
+
+// ================================================================================ queries
+extern "C" FLERN_API flern_status flern_run_query(flern_ctx* ctx, const flern_query* q, flern_result* res) {
+  if (!ctx) return FLERN_E_INVALID_ARG;
+  if (!q || !res) return fail(ctx, FLERN_E_INVALID_ARG, "flern_run_query: null query or result");
+  const bool dev_out = (q->flags & FLERN_Q_RESULT_DEVICE) != 0;
+  const bool async = (q->flags & FLERN_Q_ASYNC) != 0;
+  const bool both = (q->flags & FLERN_Q_BOTH_CLASSES) != 0;
+  if (async && !dev_out) return fail(ctx, FLERN_E_INVALID_ARG, "FLERN_Q_ASYNC requires FLERN_Q_RESULT_DEVICE");
+  if (!res->count || !res->sum) return fail(ctx, FLERN_E_INVALID_ARG, "result count/sum pointers are required");
+  if (q->fact_table < 0 || q->fact_table >= (int32_t)ctx->tables.size() || !ctx->tables[q->fact_table].alive)
+    return fail(ctx, FLERN_E_NOT_FOUND, "no fact table with id %d", q->fact_table);
+  const Table& fact = ctx->tables[q->fact_table];
+  if (q->model_id < 0 || q->model_id >= (int32_t)ctx->models.size())
+    return fail(ctx, FLERN_E_NOT_FOUND, "no model with id %d", q->model_id);
+  const Model& m = ctx->models[q->model_id];
+  if (q->nfeat != m.K0)
+    return fail(ctx, FLERN_E_ARITY, "UDF '%s' takes %d arguments, query passes %d", m.name.c_str(), m.K0, q->nfeat);
+  if (q->nfeat > 0 && !q->feats) return fail(ctx, FLERN_E_INVALID_ARG, "null feature list");
+  if (q->nprobes < 1 || q->nprobes > kMaxProbes || !q->probes)
+    return fail(ctx, FLERN_E_UNSUPPORTED, "queries need 1..%d probes (got %d)", kMaxProbes, q->nprobes);
+  if (q->ngroups < 1 || q->ngroups > kMaxGroups)
+    return fail(ctx, FLERN_E_UNSUPPORTED, "ngroups %d outside 1..%d", q->ngroups, kMaxGroups);
+  if (std::isnan(q->threshold)) return fail(ctx, FLERN_E_INVALID_ARG, "threshold is NaN");
+
+  QueryParams p;
+  std::memset(&p, 0, sizeof(p));
+  p.nrows = fact.nrows;
+  p.nprobes = q->nprobes;
+  for (int i = 0; i < q->nprobes; ++i) {
+    const flern_probe& pr = q->probes[i];
+    if (pr.ht_id < 0 || pr.ht_id >= (int32_t)ctx->hts.size())
+      return fail(ctx, FLERN_E_NOT_FOUND, "probe %d: no hash table with id %d", i, pr.ht_id);
+    const HashTable& h = ctx->hts[pr.ht_id];
+    if (!pr.key_col) return fail(ctx, FLERN_E_INVALID_ARG, "probe %d: null key column", i);
+    if (pr.src < -1 || pr.src >= i) return fail(ctx, FLERN_E_INVALID_ARG, "probe %d: source must be -1 or an earlier probe", i);
+    if ((i == 0) != (pr.src == -1))
+      return fail(ctx, FLERN_E_UNSUPPORTED, "probe %d: the first probe is keyed by a fact column, the second by probe 0", i);
+    ProbeDesc& d = p.probe[i];
+    d.slots = reinterpret_cast<const int2*>(h.slots);
+    d.mask = (uint32_t)(((int64_t)1 << h.log2cap) - 1);
+    d.shift = 32u - h.log2cap;
+    d.payload = h.payload;
+    d.pstride = h.pstride;
+    d.src = pr.src;
+    if (pr.src < 0) {
+      const Column* c = fact.find(pr.key_col);
+      if (!c) return fail(ctx, FLERN_E_NOT_FOUND, "fact table '%s' has no column '%s'", fact.name.c_str(), pr.key_col);
+      if (!is_int_type(c->dtype)) return fail(ctx, FLERN_E_TYPE, "probe key '%s' must be integer-typed", pr.key_col);
+      d.fact_key = static_cast<const int32_t*>(c->dptr);
+    } else {
+      const HashTable& hs = ctx->hts[q->probes[pr.src].ht_id];
+      const int w = hs.find(pr.key_col);
+      if (w < 0) return fail(ctx, FLERN_E_NOT_FOUND, "probe %d: '%s' is not a payload column of probe %d", i, pr.key_col, pr.src);
+      if (!is_int_type(hs.ptypes[w])) return fail(ctx, FLERN_E_TYPE, "probe key '%s' must be integer-typed", pr.key_col);
+      d.key_word = w;
+    }
+  }
+  auto resolve = [&](const flern_colref& r, ColDesc* out, bool need_int, const char* what) -> flern_status {
+    if (!r.col) return fail(ctx, FLERN_E_INVALID_ARG, "%s: null column name", what);
+    if (r.src == -1) {
+      const Column* c = fact.find(r.col);
+      if (!c) return fail(ctx, FLERN_E_NOT_FOUND, "%s: fact table '%s' has no column '%s'", what, fact.name.c_str(), r.col);
+      if (need_int && !is_int_type(c->dtype)) return fail(ctx, FLERN_E_TYPE, "%s: column '%s' must be integer-typed", what, r.col);
+      out->base = static_cast<const int32_t*>(c->dptr);
+      out->stride = 1;
+      out->src = 0;
+      out->is_float = c->dtype == FLERN_F32;
+      return FLERN_OK;
+    }
+    if (r.src < 0 || r.src >= q->nprobes) return fail(ctx, FLERN_E_INVALID_ARG, "%s: bad source %d", what, r.src);
+    const HashTable& h = ctx->hts[q->probes[r.src].ht_id];
+    const int w = h.find(r.col);
+    if (w < 0) return fail(ctx, FLERN_E_NOT_FOUND, "%s: '%s' is not a payload column of probe %d", what, r.col, r.src);
+    if (need_int && !is_int_type(h.ptypes[w])) return fail(ctx, FLERN_E_TYPE, "%s: column '%s' must be integer-typed", what, r.col);
+    out->base = h.payload + w;
+    out->stride = h.pstride;
+    out->src = 1 + r.src;
+    out->is_float = h.ptypes[w] == FLERN_F32;
+    return FLERN_OK;
+  };
+  flern_status st;
+  p.nfeat = q->nfeat;
+  for (int k = 0; k < q->nfeat; ++k) {
+    char what[32];
+    snprintf(what, sizeof(what), "feature %d", k);
+    if ((st = resolve(q->feats[k], &p.feat[k], false, what)) != FLERN_OK) return st;
+  }
+  if ((st = resolve(q->group_col, &p.grp, true, "group column")) != FLERN_OK) return st;
+  if ((st = resolve(q->sum_col, &p.sum, true, "sum column")) != FLERN_OK) return st;
+  if (q->prefilter_col) {
+    const Column* c = fact.find(q->prefilter_col);
+    if (!c) return fail(ctx, FLERN_E_NOT_FOUND, "pre-filter: fact table '%s' has no column '%s'", fact.name.c_str(), q->prefilter_col);
+    if (!is_int_type(c->dtype)) return fail(ctx, FLERN_E_TYPE, "pre-filter column '%s' must be integer-typed", q->prefilter_col);
+    p.pf_col = static_cast<const int32_t*>(c->dptr);
+    p.pf_lo = q->pf_lo;
+    p.pf_hi = q->pf_hi;
+  }
+  p.ngroups = q->ngroups;
+  p.both_classes = both ? 1 : 0;
+  const double t = (double)q->threshold;
+  p.thr_logit = t <= 0.0 ? -INFINITY : (t >= 1.0 ? INFINITY : (float)std::log(t / (1.0 - t)));
+  p.wimg = m.dbuf;
+  p.bias = reinterpret_cast<const float*>(m.dbuf + m.off_bias);
+  p.wout = reinterpret_cast<const float*>(m.dbuf + m.off_wout);
+  p.bout = m.bout;
+  p.shift = reinterpret_cast<const float*>(m.dbuf + m.off_shift);
+  p.scale = reinterpret_cast<const float*>(m.dbuf + m.off_scale);
+  KernelEntry* ke = find_kernel(m.K0P, m.H, m.NL);
+  if (!ke) return fail(ctx, FLERN_E_UNSUPPORTED, "no kernel for model '%s'", m.name.c_str());
+
+  CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+  const int G = q->ngroups;
+  const int nout = both ? 2 * G : G;
+  int64_t* d_count = dev_out ? res->count : ctx->dres;
+  int64_t* d_sum = dev_out ? res->sum : ctx->dres + 2 * kMaxGroups;
+  int64_t* d_counters = (dev_out && res->counters) ? res->counters : ctx->dres + 4 * kMaxGroups;
+  p.out_count = d_count;
+  p.out_sum = d_sum;
+  p.out_counters = d_counters;
+  p.partials = ctx->partials;
+  p.ticket = ctx->ticket;
+  // debug exports: device pointers as given, or temporary device buffers copied back
+  const int64_t n = fact.nrows;
+  float* d_score = nullptr;
+  int32_t* d_match = nullptr;
+  uint32_t* d_sel = nullptr;
+  const int64_t nwords = (n + 31) / 32;
+  std::vector<void*> temps;
+  auto temp = [&](size_t bytes, void** out) -> flern_status {
+    cudaError_t e = cudaMalloc(out, std::max<size_t>(bytes, 4));
+    if (e != cudaSuccess) {
+      for (void* v : temps) cudaFree(v);
+      return fail(ctx, FLERN_E_OOM, "cannot allocate %zu bytes of debug output", bytes);
+    }
+    temps.push_back(*out);
+    return FLERN_OK;
+  };
+  if (res->dbg_score) {
+    if (dev_out) d_score = res->dbg_score;
+    else if ((st = temp(n * 4, (void**)&d_score)) != FLERN_OK) return st;
+    CUDA_TRY(ctx, cudaMemsetAsync(d_score, 0xFF, n * 4, ctx->stream));   // NaN = never reached the model
+  }
+  if (res->dbg_match) {
+    if (dev_out) d_match = res->dbg_match;
+    else if ((st = temp(n * q->nprobes * 4, (void**)&d_match)) != FLERN_OK) return st;
+  }
+  if (res->dbg_selected) {
+    if (dev_out) d_sel = res->dbg_selected;
+    else if ((st = temp(nwords * 4, (void**)&d_sel)) != FLERN_OK) return st;
+    CUDA_TRY(ctx, cudaMemsetAsync(d_sel, 0, nwords * 4, ctx->stream));
+  }
+  p.dbg_score = d_score;
+  p.dbg_match = d_match;
+  p.dbg_selected = d_sel;
+
+  const int64_t batch = batch_rows(m.K0P);
+  int grid = (int)std::min<int64_t>(ctx->num_sms, std::max<int64_t>(1, (n + batch - 1) / batch));
+  int64_t per = (n + grid - 1) / grid;
+  per = (per + batch - 1) / batch * batch;
+  if (per < batch) per = batch;
+  p.rows_per_cta = per;
+  if (!ke->attr_set) {
+    CUDA_TRY(ctx, cudaFuncSetAttribute(ke->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ke->smem));
+    ke->attr_set = true;
+  }
+  if (!async) CUDA_TRY(ctx, cudaEventRecord(ctx->ev0, ctx->stream));
+  ke->fn<<<grid, kThreads, ke->smem, ctx->stream>>>(p);
+  CUDA_TRY(ctx, cudaGetLastError());
+  if (async) return FLERN_OK;
+  CUDA_TRY(ctx, cudaEventRecord(ctx->ev1, ctx->stream));
+  int64_t hres[4 * kMaxGroups + kCounters];
+  CUDA_TRY(ctx, cudaMemcpyAsync(hres, ctx->dres, sizeof(hres), cudaMemcpyDeviceToHost, ctx->stream));
+  int64_t hcnt[kCounters];
+  if (dev_out) CUDA_TRY(ctx, cudaMemcpyAsync(hcnt, d_counters, sizeof(hcnt), cudaMemcpyDeviceToHost, ctx->stream));
+  if (!dev_out) {
+    if (res->dbg_score) CUDA_TRY(ctx, cudaMemcpyAsync(res->dbg_score, d_score, n * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    if (res->dbg_match)
+      CUDA_TRY(ctx, cudaMemcpyAsync(res->dbg_match, d_match, n * q->nprobes * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    if (res->dbg_selected)
+      CUDA_TRY(ctx, cudaMemcpyAsync(res->dbg_selected, d_sel, nwords * 4, cudaMemcpyDeviceToHost, ctx->stream));
+  }
+  CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  for (void* v : temps) cudaFree(v);
+  const int64_t* cnt = dev_out ? hcnt : hres + 4 * kMaxGroups;
+  if (!dev_out) {
+    std::memcpy(res->count, hres, nout * sizeof(int64_t));
+    std::memcpy(res->sum, hres + 2 * kMaxGroups, nout * sizeof(int64_t));
+    if (res->counters) std::memcpy(res->counters, cnt, kCounters * sizeof(int64_t));
+  }
+  res->rows_scanned = cnt[0];
+  res->rows_joined = cnt[1];
+  res->rows_scored = cnt[1];
+  res->rows_selected = cnt[2];
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
+  res->elapsed_ms = ms;
+  if (cnt[3] != 0)
+    return fail(ctx, FLERN_E_INVALID_ARG, "%lld joined rows have a group code outside [0, %d)", (long long)cnt[3], G);
+  return FLERN_OK;
+}

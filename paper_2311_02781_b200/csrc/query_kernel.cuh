@@ -1,0 +1,559 @@
+// query_kernel.cuh — the fused persistent sm_100a query kernel:
+//   scan -> (pre-filter) -> hash probe(s) -> gather+normalise -> bf16 tile in SMEM ->
+//   tcgen05 MLP (TMEM accumulators, hidden activations stay in SMEM) -> logit -> predicate ->
+//   per-CTA group-by in SMEM -> per-CTA partials -> last CTA reduces (one launch per query).
+//
+// Paper mapping: the whole kernel is the generated record loop of
+// Fig. fig:classifier_generated with the join of Fig. code:lb2_join
+// fused in (cross-system loop fusion) and batched into 128-row tiles
+// (VectorizedUDF). `float *tensor = data[i]->xs; // conversion` becomes the
+// producer writing the joined row's features straight into the MMA operand tile (no HBM
+// intermediate). GROUP BY COUNT/SUM follows P:1346-1354.
+//
+// Warp roles (512 threads, 1 CTA per SM):
+//   warps 0-3  producers: 128 threads x ROWS rows per batch; scan, filter, probe, compact,
+//              gather+normalise+bf16 into X stage ring (S stages of 128 rows), row metadata
+//   warp  4    TMEM allocator + single-thread tcgen05.mma issuer
+//   warps 5-7  idle
+//   warps 8-15 epilogue: two warpgroups, each owns half of the hidden columns; TMEM -> regs ->
+//              bias+ReLU+bf16 -> SMEM (next layer's A operand) or bias+ReLU+dot(w_out) -> logit;
+//              warpgroup 0 then applies the predicate and aggregates.
+#pragma once
+#include "sm100.cuh"
+
+namespace flern {
+
+constexpr int kMaxFeat = 48;
+constexpr int kMaxGroups = 64;
+constexpr int kMaxProbes = 2;
+constexpr int kTile = 128;
+constexpr int kThreads = 512;
+constexpr int kProducerThreads = 128;
+// rows per producer thread per batch: 2 for narrow inputs (register budget)
+__host__ __device__ constexpr int rows_per_thread(int K0P) { return K0P <= 16 ? 2 : 1; }
+__host__ __device__ constexpr int batch_rows(int K0P) { return kProducerThreads * rows_per_thread(K0P); }
+constexpr int32_t kEmptyKey = (int32_t)0x80000000;         // INT32_MIN marks an empty slot
+constexpr int kCounters = 4;                               // scanned, joined(=scored), selected, bad_group
+
+__host__ __device__ constexpr uint32_t hash_key(int32_t key, uint32_t shift) {
+  return ((uint32_t)key * 0x9E3779B1u) >> shift;  // Fibonacci hashing, top log2(capacity) bits
+}
+
+struct ProbeDesc {
+  const int2* slots;        // {key, build row}, capacity = mask + 1
+  uint32_t mask, shift;     // shift = 32 - log2(capacity)
+  const int32_t* payload;   // row-major [build rows][pstride]
+  int32_t pstride;
+  int32_t src;              // -1: key from fact column `fact_key`; p: payload word `key_word` of probe p
+  const int32_t* fact_key;
+  int32_t key_word;
+};
+
+struct ColDesc {            // a column reference resolved to base pointer + row stride
+  const int32_t* base;      // fact column, or probe payload + word
+  int32_t stride;           // 1 for a fact column, the payload row stride otherwise
+  int32_t src;              // 0 = fact row, 1 + p = build row of probe p
+  int32_t is_float;
+};
+
+struct QueryParams {
+  int64_t nrows;            // fact rows (< 2^31)
+  int64_t rows_per_cta;     // multiple of batch_rows(K0P)
+  int32_t nprobes;
+  ProbeDesc probe[kMaxProbes];
+  const int32_t* pf_col;    // nullptr = no pre-filter
+  int64_t pf_lo, pf_hi;
+  int32_t nfeat;
+  ColDesc feat[kMaxFeat];
+  ColDesc grp, sum;
+  int32_t ngroups;
+  int32_t both_classes;
+  float thr_logit;          // select logit > thr_logit  (score > t  <=>  logit > ln(t/(1-t)))
+  const uint8_t* wimg;      // weight image: [Wh (SW128) | W1 (interleave)] bf16, exact SMEM layout
+  const float* bias;        // [NL][H]
+  const float* wout;        // [H]
+  float bout;
+  const float* shift;       // [K0P]
+  const float* scale;       // [K0P]
+  int64_t* partials;        // [gridDim.x][ngroups*4 + kCounters]
+  unsigned int* ticket;     // zero between launches (the last CTA resets it)
+  int64_t* out_count;       // [ngroups] (x2 both classes)
+  int64_t* out_sum;
+  int64_t* out_counters;    // [kCounters]
+  float* dbg_score;         // optional
+  int32_t* dbg_match;       // optional [nrows * nprobes]
+  uint32_t* dbg_selected;   // optional bitmap
+};
+
+// Shared-memory plan (byte offsets from a 1024-aligned base), identical on host and device.
+template <int K0P, int H, int NL>
+struct SmemPlan {
+  static constexpr uint32_t WH = (NL >= 2) ? (uint32_t)H * H * 2 : 0;         // hidden->hidden W, SW128
+  static constexpr uint32_t HB = (NL >= 2) ? (uint32_t)kTile * H * 2 : 0;     // hidden activation, SW128
+  static constexpr uint32_t W1 = (uint32_t)H * K0P * 2;                       // layer-1 W, interleave
+  static constexpr uint32_t XS = (uint32_t)kTile * K0P * 2;                   // one X stage, interleave
+  static constexpr uint32_t META = 16 + 4 * kTile + 4 * kTile + kTile;        // count, rowid, val, grp
+  static constexpr uint32_t FIXED = WH + HB + W1 + NL * H * 4 + H * 4 + kMaxGroups * 4 * 8 + 2 * kTile * 4 +
+                                    kMaxFeat * 8 + 64 * 8 + 128;
+  static constexpr int S = (FIXED + 4 * (XS + META) <= 232448) ? 4 : 3;
+  static constexpr uint32_t off_wh = 0;                                       // [Wh | W1] = weight image
+  static constexpr uint32_t off_w1 = off_wh + WH;
+  static constexpr uint32_t off_hb = off_w1 + W1;
+  static constexpr uint32_t off_x = off_hb + HB;
+  static constexpr uint32_t off_meta = off_x + S * XS;
+  static constexpr uint32_t off_bias = off_meta + S * META;
+  static constexpr uint32_t off_wout = off_bias + NL * H * 4;
+  static constexpr uint32_t off_acc = off_wout + H * 4;
+  static constexpr uint32_t off_xchg = off_acc + kMaxGroups * 4 * 8;
+  static constexpr uint32_t off_norm = off_xchg + 2 * kTile * 4;               // shift[48], scale[48]
+  static constexpr uint32_t off_bar = off_norm + kMaxFeat * 8;
+  static constexpr uint32_t off_misc = off_bar + 64 * 8;    // tmem base, warp counts, counters
+  static constexpr uint32_t total = off_misc + 128;
+  static constexpr uint32_t wimg_bytes = WH + W1;                              // contiguous [Wh | W1]
+  static_assert(total <= 232448, "shared-memory plan exceeds 227 KB");
+  static_assert(K0P % 16 == 0 && K0P <= kMaxFeat, "K0P");
+  static_assert(H % 64 == 0 && H >= 64 && H <= 256, "hidden width");
+  static_assert(NL == 1 || NL == 2, "hidden layers");
+};
+
+struct Meta {  // view of one stage's metadata block
+  int32_t* count;
+  int32_t* rowid;
+  int32_t* val;
+  uint8_t* grp;
+};
+
+template <int K0P, int H, int NL>
+__device__ __forceinline__ Meta meta_of(uint8_t* base, int s) {
+  using P = SmemPlan<K0P, H, NL>;
+  uint8_t* m = base + P::off_meta + s * P::META;
+  return Meta{reinterpret_cast<int32_t*>(m), reinterpret_cast<int32_t*>(m + 16),
+              reinterpret_cast<int32_t*>(m + 16 + 4 * kTile), m + 16 + 8 * kTile};
+}
+
+template <int K0P, int H, int NL>
+__global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_constant__ QueryParams p) {
+  using P = SmemPlan<K0P, H, NL>;
+  constexpr int S = P::S;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + P::off_bar);
+  uint64_t* full = bars;            // [S]   producers -> MMA/epilogue (128 arrivals)
+  uint64_t* empty = bars + S;       // [S]   epilogue WG0 -> producers (4 arrivals)
+  uint64_t* dfull = bars + 2 * S;   // [2]   MMA commit -> epilogue
+  uint64_t* dempty = bars + 2 * S + 2;  // [2] epilogue (8 warps) -> MMA
+  uint64_t* hfull = bars + 2 * S + 4;   // epilogue (8 warps) -> MMA
+  uint64_t* hempty = bars + 2 * S + 5;  // MMA commit -> epilogue
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + P::off_misc);
+  int32_t* wcnt = reinterpret_cast<int32_t*>(smem + P::off_misc + 16);     // [2][4] warp counts
+  unsigned long long* acc = reinterpret_cast<unsigned long long*>(smem + P::off_acc);
+  float* s_bias = reinterpret_cast<float*>(smem + P::off_bias);
+  float* s_wout = reinterpret_cast<float*>(smem + P::off_wout);
+  float* s_shift = reinterpret_cast<float*>(smem + P::off_norm);
+  float* s_scale = s_shift + kMaxFeat;
+  float* xchg = reinterpret_cast<float*>(smem + P::off_xchg);
+  int64_t* s_cnt = reinterpret_cast<int64_t*>(smem + P::off_misc + 64);   // [kCounters]
+  unsigned int* s_is_last = reinterpret_cast<unsigned int*>(smem + P::off_misc + 96);
+
+  if ((smem_u32(smem) & 1023u) != 0) __trap();  // SW128 operands need a 1024-aligned base
+
+  // ---- one-time setup: weights image -> SMEM, constants, barriers, TMEM ----
+  {
+    const int4* src = reinterpret_cast<const int4*>(p.wimg);
+    int4* dst = reinterpret_cast<int4*>(smem + P::off_wh);   // [Wh | W1] contiguous, same layout
+    for (uint32_t i = tid; i < P::wimg_bytes / 16; i += kThreads) dst[i] = ldg_nc(src + i);
+    for (int i = tid; i < NL * H; i += kThreads) s_bias[i] = p.bias[i];
+    for (int i = tid; i < H; i += kThreads) s_wout[i] = p.wout[i];
+    for (int i = tid; i < kMaxFeat; i += kThreads) {
+      s_shift[i] = i < K0P ? p.shift[i] : 0.f;
+      s_scale[i] = i < K0P ? p.scale[i] : 0.f;
+    }
+    for (int i = tid; i < kMaxGroups * 4; i += kThreads) acc[i] = 0ull;
+    if (tid < kCounters) s_cnt[tid] = 0;
+    fence_proxy_async_smem();   // weights written by st.shared are read by the tensor core
+  }
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) { mbar_init(&full[s], kProducerThreads); mbar_init(&empty[s], 4); }
+    for (int i = 0; i < 2; ++i) { mbar_init(&dfull[i], 1); mbar_init(&dempty[i], 8); }
+    mbar_init(hfull, 8);
+    mbar_init(hempty, 1);
+    fence_mbar_init();
+  }
+  constexpr uint32_t kTmemCols = (NL >= 2) ? (2 * H <= 256 ? 256 : 512) : (H <= 32 ? 32 : (H <= 64 ? 64 : (H <= 128 ? 128 : 256)));
+  if (warp == 4) { tmem_alloc(tmem_slot, kTmemCols); tmem_relinquish(); }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  const int64_t row_begin = (int64_t)blockIdx.x * p.rows_per_cta;
+  const int64_t row_end = min(p.nrows, row_begin + p.rows_per_cta);
+
+  if (warp < 4) {
+    // =============================== PRODUCERS =============================================
+    constexpr int R = rows_per_thread(K0P);
+    constexpr int kBatch = batch_rows(K0P);
+    const int t = tid;                   // 0..127
+    int stage = 0;                       // stage currently being filled (acquired)
+    uint32_t acq = 0;                    // number of stages acquired so far
+    int fill = 0;                        // rows already in `stage`
+    int64_t n_joined = 0;
+    int buf = 0;
+    mbar_wait(&empty[0], ((acq / S) & 1) ^ 1, 1);   // acquire the first stage
+    acq = 1;
+    for (int64_t base = row_begin; base < row_end; base += kBatch) {
+      int64_t row[R];
+      bool valid[R];
+      int32_t brow[R][kMaxProbes];
+      int32_t v[R][K0P];
+      int32_t gv[R], sv[R], key[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        row[r] = base + r * kProducerThreads + t;
+        valid[r] = row[r] < row_end;
+        if (p.pf_col && valid[r]) {   // pre-filter on a fact column (config 4): before anything else
+          const int64_t x = ldg_nc(p.pf_col + row[r]);
+          valid[r] = (p.pf_lo <= x) && (x < p.pf_hi);
+        }
+      }
+      // fact-side loads of surviving rows, all independent: probe key, fact features, group/sum.
+      // Issued before the probe so their latency overlaps the probe's dependent loads.
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        key[r] = valid[r] ? ldg_nc(p.probe[0].fact_key + row[r]) : 0;
+#pragma unroll
+        for (int k = 0; k < K0P; ++k) {
+          v[r][k] = 0;
+          if (k < p.nfeat && p.feat[k].src == 0 && valid[r]) v[r][k] = ldg_nc(p.feat[k].base + row[r]);
+        }
+        gv[r] = (p.grp.src == 0 && valid[r]) ? ldg_nc(p.grp.base + row[r]) : 0;
+        sv[r] = (p.sum.src == 0 && valid[r]) ? ldg_nc(p.sum.base + row[r]) : 0;
+      }
+      // probes: linear probing until the key or an empty slot; a miss drops the row
+#pragma unroll
+      for (int q = 0; q < kMaxProbes; ++q) {
+        if (q >= p.nprobes) break;
+        const ProbeDesc& pd = p.probe[q];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          brow[r][q] = -1;
+          if (!valid[r]) continue;
+          // probe 0 is keyed by a fact column; probe 1 by a payload word of probe 0's build row
+          const int32_t k = q == 0 ? key[r]
+                                   : ldg_nc(p.probe[0].payload + (int64_t)brow[r][0] * p.probe[0].pstride + pd.key_word);
+          uint32_t h = hash_key(k, pd.shift);
+          while (true) {
+            const int2 sl = ldg_nc(pd.slots + h);
+            if (sl.x == k) { brow[r][q] = sl.y; break; }
+            if (sl.x == kEmptyKey) break;
+            h = (h + 1) & pd.mask;
+          }
+          valid[r] = brow[r][q] >= 0;
+        }
+      }
+      if (p.dbg_match) {
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+          if (row[r] < row_end)
+            for (int q = 0; q < p.nprobes; ++q) p.dbg_match[row[r] * p.nprobes + q] = brow[r][q];
+      }
+      // dimension-side loads (payload rows of the matched build rows), all independent
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int32_t b0 = brow[r][0], b1 = p.nprobes > 1 ? brow[r][1] : 0;
+#pragma unroll
+        for (int k = 0; k < K0P; ++k) {
+          const int fs = p.feat[k].src;
+          if (k < p.nfeat && fs > 0 && valid[r])
+            v[r][k] = ldg_nc(p.feat[k].base + (int64_t)(fs == 1 ? b0 : b1) * p.feat[k].stride);
+        }
+        if (p.grp.src > 0 && valid[r]) gv[r] = ldg_nc(p.grp.base + (int64_t)(p.grp.src == 1 ? b0 : b1) * p.grp.stride);
+        if (p.sum.src > 0 && valid[r]) sv[r] = ldg_nc(p.sum.base + (int64_t)(p.sum.src == 1 ? b0 : b1) * p.sum.stride);
+      }
+      // compaction: position of each surviving row in the batch (warp scan + per-warp counts)
+      int my_cnt = 0;
+#pragma unroll
+      for (int r = 0; r < R; ++r) my_cnt += valid[r] ? 1 : 0;
+      int incl = my_cnt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int x = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += x;
+      }
+      if (lane == 31) wcnt[buf * 4 + warp] = incl;
+      named_bar_sync(1, kProducerThreads);
+      int woff = 0, total = 0;
+#pragma unroll
+      for (int w = 0; w < 4; ++w) {
+        const int c = wcnt[buf * 4 + w];
+        woff += (w < warp) ? c : 0;
+        total += c;
+      }
+      buf ^= 1;
+      n_joined += my_cnt;
+      // acquire every further stage this batch spills into
+      const int end = fill + total;
+      const int nspill = (end - 1) / kTile;
+      for (int e = 1; e <= nspill && total > 0; ++e) {
+        mbar_wait(&empty[(stage + e) % S], ((acq / S) & 1) ^ 1, 2);
+        ++acq;
+      }
+      // normalise (fp32, two separately rounded ops: reading Q4) -> bf16 -> X tile + metadata
+      int pos = fill + woff + incl - my_cnt;
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        if (!valid[r]) continue;
+        const int ts = (stage + pos / kTile) % S, tp = pos % kTile;
+        ++pos;
+        uint8_t* xs = smem + P::off_x + ts * P::XS;
+        const Meta m = meta_of<K0P, H, NL>(smem, ts);
+        uint32_t packed[K0P / 2];
+#pragma unroll
+        for (int k = 0; k < K0P; k += 2) {
+          float f[2];
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            const int kk = k + u;
+            const float x = p.feat[kk].is_float ? __int_as_float(v[r][kk]) : (float)v[r][kk];
+            f[u] = kk < p.nfeat ? __fmul_rn(__fsub_rn(x, s_shift[kk]), s_scale[kk]) : 0.f;
+          }
+          packed[k / 2] = bf16x2(f[0], f[1]);
+        }
+        // interleaved K-major layout: (k/8)*2048 + (row/8)*128 + (row%8)*16
+#pragma unroll
+        for (int c8 = 0; c8 < K0P / 8; ++c8)
+          st_shared_v4(smem_u32(xs + c8 * (kTile * 16) + (tp >> 3) * 128 + (tp & 7) * 16), packed[4 * c8],
+                       packed[4 * c8 + 1], packed[4 * c8 + 2], packed[4 * c8 + 3]);
+        m.rowid[tp] = (int32_t)row[r];
+        m.grp[tp] = (gv[r] >= 0 && gv[r] < p.ngroups) ? (uint8_t)gv[r] : (uint8_t)255;
+        m.val[tp] = sv[r];
+      }
+      fence_proxy_async_smem();
+      // publish completed stages
+      const int ncomplete = end / kTile;
+      for (int e = 0; e < ncomplete; ++e) {
+        const int ts = (stage + e) % S;
+        if (t == 0) *meta_of<K0P, H, NL>(smem, ts).count = kTile;
+        mbar_arrive(&full[ts]);
+      }
+      stage = (stage + ncomplete) % S;
+      fill = end % kTile;
+      if (ncomplete > 0 && fill == 0 && nspill < ncomplete) {
+        // the batch ended exactly on a tile boundary: acquire the next stage now
+        mbar_wait(&empty[stage], ((acq / S) & 1) ^ 1, 3);
+        ++acq;
+      }
+    }
+    if (fill > 0) {   // flush the partial tile
+      if (t == 0) *meta_of<K0P, H, NL>(smem, stage).count = fill;
+      mbar_arrive(&full[stage]);
+      stage = (stage + 1) % S;
+      mbar_wait(&empty[stage], ((acq / S) & 1) ^ 1, 4);
+      ++acq;
+    }
+    // end-of-stream marker
+    if (t == 0) *meta_of<K0P, H, NL>(smem, stage).count = -1;
+    mbar_arrive(&full[stage]);
+    int64_t nj = n_joined;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) nj += __shfl_down_sync(0xffffffffu, nj, o);
+    if (lane == 0) atomicAdd(reinterpret_cast<unsigned long long*>(&s_cnt[1]), (unsigned long long)nj);
+  } else if (warp == 4) {
+    // =============================== MMA ISSUER =============================================
+    if (lane == 0) {
+      constexpr uint32_t idesc = make_idesc_bf16(128, H);
+      const uint32_t x0 = smem_u32(smem + P::off_x);
+      const uint32_t w1 = smem_u32(smem + P::off_w1);
+      const uint32_t wh = smem_u32(smem + P::off_wh);
+      const uint32_t hb = smem_u32(smem + P::off_hb);
+      for (uint32_t tile = 0;; ++tile) {
+        const int s = tile % S;
+        const uint32_t ph = (tile / S) & 1;
+        mbar_wait(&full[s], ph, 10);
+        if (*meta_of<K0P, H, NL>(smem, s).count < 0) break;
+        tc_fence_after();
+        // layer 1: D0 = X[s] . W1^T     (M=128, N=H, K=K0P)
+        mbar_wait(&dempty[0], (tile & 1) ^ 1, 11);
+        tc_fence_after();
+#pragma unroll
+        for (int ks = 0; ks < K0P / 16; ++ks) {
+          const uint64_t ad = make_sdesc(x0 + s * P::XS + ks * 2 * (kTile * 16), kTile * 16, 128, kLayoutNone);
+          const uint64_t bd = make_sdesc(w1 + ks * 2 * (H * 16), H * 16, 128, kLayoutNone);
+          mma_bf16_ss(tmem_base, ad, bd, idesc, ks > 0);
+        }
+        mma_commit(&dfull[0]);
+        if constexpr (NL >= 2) {
+          // layer 2: D1 = Hbuf . W2^T   (M=128, N=H, K=H), both 128B-swizzled K-major
+          mbar_wait(hfull, tile & 1, 12);
+          mbar_wait(&dempty[1], (tile & 1) ^ 1, 13);
+          tc_fence_after();
+#pragma unroll 4
+          for (int ks = 0; ks < H / 16; ++ks) {
+            const uint32_t koff = (ks & 3) * 32;   // 16 bf16 = 32 B inside the 128 B swizzle row
+            const uint64_t ad = make_sdesc(hb + (ks >> 2) * (kTile * 128) + koff, 16, 1024, kLayoutSW128);
+            const uint64_t bd = make_sdesc(wh + (ks >> 2) * (H * 128) + koff, 16, 1024, kLayoutSW128);
+            mma_bf16_ss(tmem_base + H, ad, bd, idesc, ks > 0);
+          }
+          mma_commit(&dfull[1]);
+          mma_commit(hempty);
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp >= 8) {
+    // =============================== EPILOGUE =============================================
+    const int ew = warp - 8;                // 0..7
+    const int wg = ew >> 2;                 // column half
+    const int q = warp & 3;                 // TMEM lane quadrant (warp id % 4)
+    const int r = q * 32 + lane;            // tile row owned by this thread
+    constexpr int HC = H / 2;               // columns per warpgroup
+    const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+    const uint32_t hb = smem_u32(smem + P::off_hb);
+    for (uint32_t tile = 0;; ++tile) {
+      const int s = tile % S;
+      const uint32_t ph = (tile / S) & 1;
+      mbar_wait(&full[s], ph, 20);
+      const Meta m = meta_of<K0P, H, NL>(smem, s);
+      const int count = *m.count;
+      if (count < 0) break;
+      float part = 0.f;
+      // ---- layer 1 epilogue ----
+      mbar_wait(&dfull[0], tile & 1, 21);
+      tc_fence_after();
+      if constexpr (NL >= 2) {
+        mbar_wait(hempty, (tile & 1) ^ 1, 22);
+#pragma unroll 1
+        for (int c0 = wg * HC; c0 < wg * HC + HC; c0 += 32) {
+          uint32_t v[32];
+          tmem_ld32(tmem_base + lane_off + c0, v);
+          uint32_t pk[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i)
+            pk[i] = relu_bf16x2(__uint_as_float(v[2 * i]) + s_bias[c0 + 2 * i],
+                                __uint_as_float(v[2 * i + 1]) + s_bias[c0 + 2 * i + 1]);
+          // 128B-swizzled K-major: K block c0/64, chunk ((c0%64)/8 + j) ^ (r%8)
+          const uint32_t rowbase = hb + (c0 >> 6) * (kTile * 128) + (r >> 3) * 1024 + (r & 7) * 128;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const uint32_t chunk = (uint32_t)(((c0 & 63) >> 3) + j) ^ (uint32_t)(r & 7);
+            st_shared_v4(rowbase + chunk * 16, pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&dempty[0]);
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(hfull);
+        // ---- layer 2 epilogue: logit partial = sum_c relu(D1 + b2) * w_out ----
+        mbar_wait(&dfull[1], tile & 1, 23);
+        tc_fence_after();
+        float pa[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll 1
+        for (int c0 = wg * HC; c0 < wg * HC + HC; c0 += 32) {
+          uint32_t v[32];
+          tmem_ld32(tmem_base + H + lane_off + c0, v);
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            pa[i & 3] = fmaf(fmaxf(__uint_as_float(v[i]) + s_bias[H + c0 + i], 0.f), s_wout[c0 + i], pa[i & 3]);
+        }
+        part = (pa[0] + pa[1]) + (pa[2] + pa[3]);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&dempty[1]);
+      } else {
+        float pa[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll 1
+        for (int c0 = wg * HC; c0 < wg * HC + HC; c0 += 32) {
+          uint32_t v[32];
+          tmem_ld32(tmem_base + lane_off + c0, v);
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            pa[i & 3] = fmaf(fmaxf(__uint_as_float(v[i]) + s_bias[c0 + i], 0.f), s_wout[c0 + i], pa[i & 3]);
+        }
+        part = (pa[0] + pa[1]) + (pa[2] + pa[3]);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&dempty[0]);
+      }
+      // ---- combine the two column halves, predicate, aggregate ----
+      float* xb = xchg + (tile & 1) * kTile;
+      if (wg == 1) {
+        xb[r] = part;
+        named_bar_arrive(2, 256);
+      } else {
+        named_bar_sync(2, 256);
+        const float logit = part + xb[r] + p.bout;
+        const bool valid = r < count;
+        const bool sel = valid && (logit > p.thr_logit);
+        const int g = valid ? (int)m.grp[r] : 255;
+        const int32_t val = valid ? m.val[r] : 0;
+        if (valid && g == 255) atomicAdd(reinterpret_cast<unsigned long long*>(&s_cnt[3]), 1ull);
+        if (p.dbg_score && valid) p.dbg_score[m.rowid[r]] = 1.f / (1.f + __expf(-logit));
+        if (p.dbg_selected && sel) atomicOr(p.dbg_selected + (m.rowid[r] >> 5), 1u << (m.rowid[r] & 31));
+        // warp-level group-by: per present group, popc(ballot) rows and a split 16-bit sum
+        const int cls = sel ? 0 : 1;
+        const bool agg = valid && g != 255 && (sel || p.both_classes);
+        uint32_t pending = __ballot_sync(0xffffffffu, agg);
+        while (pending) {
+          const int leader = __ffs(pending) - 1;
+          const int lg = __shfl_sync(0xffffffffu, g, leader);
+          const int lc = __shfl_sync(0xffffffffu, cls, leader);
+          const bool mine = agg && g == lg && cls == lc;
+          const uint32_t mm = __ballot_sync(0xffffffffu, mine);
+          const int lo = __reduce_add_sync(0xffffffffu, mine ? (val & 0xFFFF) : 0);
+          const int hi = __reduce_add_sync(0xffffffffu, mine ? (val >> 16) : 0);
+          if (lane == leader) {
+            atomicAdd(&acc[lg * 4 + lc * 2 + 0], (unsigned long long)__popc(mm));
+            atomicAdd(&acc[lg * 4 + lc * 2 + 1], (unsigned long long)((long long)hi * 65536ll + (long long)lo));
+          }
+          pending &= ~mm;
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);   // stage (X + metadata) can be refilled
+      }
+    }
+  }
+
+  // ---- teardown: per-CTA partials, last CTA reduces ----
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 4) { tc_fence_after(); tmem_dealloc(tmem_base, kTmemCols); }
+  const int G = p.ngroups;
+  const int W = G * 4 + kCounters;
+  int64_t* mine = p.partials + (int64_t)blockIdx.x * W;
+  for (int i = tid; i < G * 4; i += kThreads) mine[i] = (int64_t)acc[i];
+  if (tid == 0) {
+    int64_t sel = 0;
+    for (int g = 0; g < G; ++g) sel += (int64_t)acc[g * 4 + 0];
+    mine[G * 4 + 0] = row_end > row_begin ? row_end - row_begin : 0;
+    mine[G * 4 + 1] = s_cnt[1];
+    mine[G * 4 + 2] = sel;
+    mine[G * 4 + 3] = s_cnt[3];
+    __threadfence();
+    const unsigned int prev = atomicAdd(p.ticket, 1u);
+    *s_is_last = (prev == gridDim.x - 1) ? 1u : 0u;
+  }
+  __syncthreads();
+  if (*s_is_last) {
+    __threadfence();
+    for (int i = tid; i < W; i += kThreads) {
+      int64_t t = 0;
+      for (int b = 0; b < (int)gridDim.x; ++b) t += *((volatile int64_t*)(p.partials + (int64_t)b * W + i));
+      if (i < G * 4) {
+        const int g = i / 4, cls = (i / 2) & 1, kind = i & 1;
+        if (cls == 0 || p.both_classes) {
+          int64_t* out = kind == 0 ? p.out_count : p.out_sum;
+          out[cls * G + g] = t;
+        }
+      } else {
+        p.out_counters[i - G * 4] = t;
+      }
+    }
+    if (tid == 0) *p.ticket = 0u;
+  }
+}
+
+}  // namespace flern

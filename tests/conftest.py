@@ -17,7 +17,8 @@ def pytest_configure(config):
 @pytest.fixture(scope="session", autouse=True)
 def _native_libs():
     """Build the in-tree native libraries if any is missing (make is incremental)."""
-    need = [os.path.join(ROOT, p) for p in ("datagen/libflern_gen.so", "oracle/liboracle.so")]
+    need = [os.path.join(ROOT, p) for p in ("datagen/libflern_gen.so", "oracle/liboracle.so",
+                                            "paper_2311_02781_b200/lib/libflern.so")]
     if not all(os.path.exists(p) for p in need):
         subprocess.run(["make", "-C", ROOT, "-j4"], check=True, stdout=subprocess.DEVNULL)
     yield

@@ -1,0 +1,64 @@
+"""The C-ABI library loads and exports every symbol include/flern.h declares (CPU-only), and
+refuses to run without an sm_100 GPU (no CPU fallback)."""
+import ctypes
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "flern.h")
+LIB = os.path.join(ROOT, "paper_2311_02781_b200", "lib", "libflern.so")
+
+
+def declared_functions():
+    src = open(HEADER).read()
+    return re.findall(r"FLERN_API\s+[\w\s\*]+?\b(flern_\w+)\s*\(", src)
+
+
+def test_header_declares_the_boundary():
+    fns = declared_functions()
+    for need in ("flern_load_table", "flern_load_model", "flern_build_hashtable", "flern_run_query",
+                 "flern_create", "flern_destroy", "flern_last_error"):
+        assert need in fns
+
+
+def test_library_exports_every_declared_symbol():
+    lib = ctypes.CDLL(LIB)
+    missing = [f for f in declared_functions() if not hasattr(lib, f)]
+    assert not missing, missing
+
+
+def test_binding_names_match_header():
+    from paper_2311_02781_b200 import flern as F
+    assert set(F.EXPORTED) == set(declared_functions())
+    for f in F.EXPORTED:
+        assert callable(getattr(F, f))
+
+
+def test_version_and_launch_count():
+    from paper_2311_02781_b200 import flern as F
+    assert "sm_100a" in F.flern_version()
+    assert F.flern_query_launches() == 1
+
+
+def test_kernels_are_sm100a_tcgen05():
+    """The library's SASS holds tcgen05 MMAs (UTCHMMA) and TMEM loads (LDTM): the MLP runs on
+    the 5th-generation tensor cores, not mma.sync (HMMA)."""
+    import shutil
+    import subprocess
+    if not shutil.which("cuobjdump"):
+        pytest.skip("cuobjdump not available")
+    sass = subprocess.run(["cuobjdump", "-sass", LIB], capture_output=True, text=True).stdout
+    assert "sm_100a" in subprocess.run(["cuobjdump", "-lelf", LIB], capture_output=True, text=True).stdout
+    assert "UTCHMMA" in sass and "LDTM" in sass
+    assert " HMMA" not in sass
+
+
+def test_no_gpu_means_error_not_fallback():
+    torch = pytest.importorskip("torch")
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    from paper_2311_02781_b200 import flern as F
+    with pytest.raises(F.FlernError):
+        F.flern_create(0)

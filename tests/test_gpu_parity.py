@@ -1,0 +1,211 @@
+"""CUDA path vs the oracle, through the C ABI, on the same seeded inputs (`-m gpu`)."""
+import math
+
+import numpy as np
+import pytest
+
+import datagen as D
+import oracle as O
+from tests import helpers as H
+from tests import parity
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_gpu():
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+
+
+# ---------------------------------------------------------------------------------- configs
+@pytest.mark.parametrize("match_rate", [1.0, 0.9])
+def test_c1_full_config(match_rate):
+    """Config 1 (SF0.01, L⋈O, 8-64-1) at its full size, with and without probe misses."""
+    cfg = D.with_sf(D.CONFIGS["c1"], 0.01, match_rate=match_rate)
+    db = D.make_database(cfg)
+    r = parity.check(cfg, db, D.make_model(cfg, db), emu_tol=3e-3)
+    assert r["scored"] > 0.85 * db.fact_n * match_rate
+
+
+@pytest.mark.parametrize("sf", [0.003, 0.02])
+def test_c2_mlp_small(sf):
+    """Config 2's query and 16-256-256-1 MLP at sizes the oracle finishes in seconds (many tiles
+    and a ragged tail), with probe misses."""
+    cfg = D.with_sf(D.CONFIGS["c2"], sf, match_rate=0.9)
+    db = D.make_database(cfg)
+    parity.check(cfg, db, D.make_model(cfg, db), emu_tol=3e-3)
+
+
+def test_c2_both_classes_conservation():
+    """The paper's two-class CASE WHEN query: selected + rejected == joined."""
+    cfg = D.with_sf(D.CONFIGS["c2"], 0.004, match_rate=0.9)
+    db = D.make_database(cfg)
+    parity.check(cfg, db, D.make_model(cfg, db), both=True)
+
+
+def test_c4p_prefilter_before_inference():
+    """Config 4's selective l_shipdate pre-filter (~2%) before inference, C2's MLP."""
+    cfg = D.with_sf(D.CONFIGS["c4p"], 0.1, match_rate=0.95)
+    db = D.make_database(cfg)
+    r = parity.check(cfg, db, D.make_model(cfg, db))
+    assert 0.015 * db.fact_n < r["scored"] < 0.03 * db.fact_n
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c4p"])
+def test_linear_threshold_model_bit_exact(name):
+    """Pin (iii): with the linear-threshold model the query is exactly `l_quantity >= 26`; no row
+    is in the band, so join, selection and aggregates must be bit-exact."""
+    sf = 0.1 if name == "c4p" else 0.01
+    cfg = D.with_sf(D.CONFIGS[name], sf, match_rate=0.9)
+    db = D.make_database(cfg)
+    model = H.linear_threshold_model(cfg)
+    r = parity.check(cfg, db, model)
+    assert r["band"] == 0
+    cnt, sm = H.brute_aggregate(cfg, db, db.fact["l_quantity"] >= 26)
+    assert r["gpu"]["count"].tolist() == cnt.tolist() and r["gpu"]["sum"].tolist() == sm.tolist()
+
+
+@pytest.mark.parametrize("t", [-math.inf, 0.0, math.inf, 1.0, 0.3])
+def test_threshold_extremes(t):
+    cfg = D.with_sf(D.CONFIGS["c1"], 0.004, match_rate=0.9)
+    db = D.make_database(cfg)
+    model = D.make_model(cfg, db)
+    r = parity.check(cfg, db, model, threshold=t)
+    if t <= 0:
+        assert r["gpu"]["rows_selected"] == r["gpu"]["rows_joined"]
+    if t >= 1:
+        assert r["gpu"]["rows_selected"] == 0
+
+
+# ---------------------------------------------------------------------------------- edge cases
+def _custom_db(cfg, nfact, seed=0, miss=0.2):
+    rng = np.random.default_rng(seed)
+    full = D.make_database(D.with_sf(cfg, 0.002))
+    bname, m, bcols = full.builds[0]
+    keys = bcols["o_orderkey"]
+    take = rng.integers(0, m, size=nfact)
+    fact = {}
+    src = D.make_database(D.with_sf(cfg, 0.002)).fact
+    rows = rng.integers(0, full.fact_n, size=nfact)
+    for c, v in src.items():
+        fact[c] = np.ascontiguousarray(v[rows]) if nfact else v[:0].copy()
+    fk = keys[take].copy()
+    fk[rng.random(nfact) < miss] = -7   # misses
+    fact["l_orderkey"] = fk.astype(np.int32)
+    return D.Database(cfg.sf, nfact, fact, full.builds)
+
+
+@pytest.mark.parametrize("nfact", [0, 1, 127, 128, 129, 255, 256, 257, 1000, 33_333])
+def test_ragged_sizes(nfact):
+    cfg = D.with_sf(D.CONFIGS["c1"], 0.002)
+    db = _custom_db(cfg, nfact, seed=nfact)
+    model = D.make_model(cfg, D.make_database(cfg))
+    r = parity.check(cfg, db, model)
+    assert r["gpu"]["rows_scanned"] == nfact
+
+
+def test_all_probes_miss():
+    cfg = D.with_sf(D.CONFIGS["c2"], 0.002)
+    db = _custom_db(cfg, 5000, miss=1.0)
+    r = parity.check(cfg, db, D.make_model(cfg, D.make_database(cfg)))
+    assert r["gpu"]["rows_joined"] == 0 and r["gpu"]["count"].sum() == 0
+
+
+def test_shuffled_fact_rows_same_aggregates():
+    """Permutation invariance on the GPU: shuffled lineitem gives bit-identical aggregates
+    (integer atomics; the tile decomposition changes, the result must not)."""
+    cfg = D.with_sf(D.CONFIGS["c1"], 0.01, match_rate=0.9)
+    db = D.make_database(cfg)
+    model = H.linear_threshold_model(cfg)
+    a = parity.run_gpu(cfg, db, model, debug=False)
+    b = parity.run_gpu(cfg, D.make_database(cfg, shuffle_seed=3), model, debug=False)
+    assert a["count"].tolist() == b["count"].tolist() and a["sum"].tolist() == b["sum"].tolist()
+
+
+def test_repeated_runs_deterministic():
+    cfg = D.with_sf(D.CONFIGS["c2"], 0.01, match_rate=0.9)
+    db = D.make_database(cfg)
+    model = D.make_model(cfg, db)
+    from paper_2311_02781_b200.session import GpuQuery
+    gq = GpuQuery(cfg, db, model)
+    try:
+        r1 = parity.run_gpu(cfg, db, model, gq=gq)
+        r2 = parity.run_gpu(cfg, db, model, gq=gq)
+        assert r1["count"].tolist() == r2["count"].tolist() and r1["sum"].tolist() == r2["sum"].tolist()
+        assert np.array_equal(r1["score"], r2["score"], equal_nan=True)
+    finally:
+        gq.close()
+
+
+# ---------------------------------------------------------------------------------- errors
+def test_errors_name_the_offender():
+    from paper_2311_02781_b200 import flern as F
+    from paper_2311_02781_b200.session import GpuQuery
+    cfg = D.with_sf(D.CONFIGS["c1"], 0.002)
+    db = D.make_database(cfg)
+    model = D.make_model(cfg, db)
+    gq = GpuQuery(cfg, db, model)
+    try:
+        with pytest.raises(F.FlernError, match="DUPLICATE.*fact"):
+            F.flern_load_table(gq.ctx, "fact", db.fact)
+        q = gq.make_query(gq.fact_id)
+        q.q.nfeat = 7
+        with pytest.raises(F.FlernError, match="ARITY"):
+            gq.run(q, count=np.zeros(5, np.int64), sum=np.zeros(5, np.int64))
+        q = gq.make_query(gq.fact_id, threshold=float("nan"))
+        with pytest.raises(F.FlernError, match="NaN"):
+            gq.run(q, count=np.zeros(5, np.int64), sum=np.zeros(5, np.int64))
+        dup = F.flern_load_table(gq.ctx, "dupdim", {"k": np.array([1, 2, 1], np.int32)})
+        with pytest.raises(F.FlernError, match="DUP_KEY"):
+            F.flern_build_hashtable(gq.ctx, dup, "k", [])
+        with pytest.raises(F.FlernError, match="NOT_FOUND.*nope"):
+            F.flern_build_hashtable(gq.ctx, dup, "nope", [])
+        with pytest.raises(F.FlernError, match="SHAPE"):
+            F.flern_load_model(gq.ctx, "bad", [8, 64, 2], [np.zeros((64, 8)), np.zeros((2, 64))],
+                               [np.zeros(64), np.zeros(2)], np.zeros(8), np.ones(8))
+        with pytest.raises(F.FlernError, match="UNSUPPORTED"):
+            F.flern_load_model(gq.ctx, "big", [8, 1024, 1], [np.zeros((1024, 8)), np.zeros((1, 1024))],
+                               [np.zeros(1024), np.zeros(1)], np.zeros(8), np.ones(8))
+        # the context is still usable after errors
+        r = parity.run_gpu(cfg, db, model, gq=gq, debug=False)
+        assert r["rows_joined"] > 0
+    finally:
+        gq.close()
+
+
+def test_bad_group_code_is_reported():
+    from paper_2311_02781_b200 import flern as F
+    cfg = D.with_sf(D.CONFIGS["c1"], 0.002)
+    db = D.make_database(cfg)
+    cfg.ngroups = 3   # o_orderpriority takes 5 values
+    with pytest.raises(F.FlernError, match="group code"):
+        parity.run_gpu(cfg, db, D.make_model(D.with_sf(D.CONFIGS["c1"], 0.002), db), debug=False)
+
+
+# ---------------------------------------------------------------------------------- full size
+@pytest.mark.slow
+def test_c2_full_size_sampled():
+    """Config 2 at its full size (SF1, 6.0M rows) in the launch configuration bench.py times:
+    join ids, scores and selection on sampled row ranges against the oracle; aggregates at
+    -INF and with the linear-threshold model exact at full size."""
+    from paper_2311_02781_b200.session import GpuQuery
+    cfg = D.CONFIGS["c2"]
+    db = D.make_database(cfg)
+    model = D.make_model(cfg, db)
+    gq = GpuQuery(cfg, db, model)
+    try:
+        n = db.fact_n
+        rng = np.random.default_rng(5)
+        starts = sorted(rng.integers(0, n - 2000, size=8).tolist()) + [n - 1500]
+        _, worst = parity.sample_check(cfg, db, model, gq, [(s, min(n, s + 1500)) for s in starts])
+        g = parity.run_gpu(cfg, db, model, threshold=-math.inf, gq=gq, debug=False)
+        cnt, sm = H.brute_aggregate(cfg, db, np.ones(n, bool))
+        assert g["count"].tolist() == cnt.tolist() and g["sum"].tolist() == sm.tolist()
+    finally:
+        gq.close()
+    lt = H.linear_threshold_model(cfg)
+    g = parity.run_gpu(cfg, db, lt, debug=False)
+    cnt, sm = H.brute_aggregate(cfg, db, db.fact["l_quantity"] >= 26)
+    assert g["count"].tolist() == cnt.tolist() and g["sum"].tolist() == sm.tolist()
