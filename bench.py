@@ -192,6 +192,7 @@ def main():
     ap.add_argument("--impl", default="flern", choices=["flern", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-model", action="store_true", help="diagnostic: FLERN_Q_NO_MODEL (scan/probe/gather/aggregate only)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -225,7 +226,8 @@ def main():
     out_sum = torch.zeros(G, dtype=torch.int64, device=f"cuda:{local}")
     counters = torch.zeros(4, dtype=torch.int64, device=f"cuda:{local}")
     partial = torch.zeros(2 * G, dtype=torch.int64, device=f"cuda:{local}")
-    q_async = gq.make_query(gq.fact_id, flags=F.FLERN_Q_RESULT_DEVICE | F.FLERN_Q_ASYNC)
+    q_async = gq.make_query(gq.fact_id, flags=F.FLERN_Q_RESULT_DEVICE | F.FLERN_Q_ASYNC |
+                            (F.FLERN_Q_NO_MODEL if args.no_model else 0))
 
     # rows scored by this rank (deterministic): one synchronous run
     r0 = gq.run(gq.make_query(gq.fact_id), count=np.zeros(G, np.int64), sum=np.zeros(G, np.int64))

@@ -152,8 +152,10 @@ enum {
   FLERN_Q_RESULT_DEVICE = 0x1, /* every result pointer is a device pointer (else host) */
   FLERN_Q_ASYNC = 0x2,         /* with RESULT_DEVICE: enqueue only, no host sync; the rows_* counters
                                   and elapsed_ms are not filled (read `counters` instead) */
-  FLERN_Q_BOTH_CLASSES = 0x4   /* count/sum hold [2][ngroups]: [0] score > t, [1] joined rows with score <= t
+  FLERN_Q_BOTH_CLASSES = 0x4,  /* count/sum hold [2][ngroups]: [0] score > t, [1] joined rows with score <= t
                                   (the CASE WHEN sentiment < 0.5 / >= 0.5 query of P:1346-1354) */
+  FLERN_Q_NO_MODEL = 0x8       /* diagnostic: skip the MLP and select every joined row (measures the
+                                  scan -> probe -> gather -> aggregate part alone) */
 };
 
 typedef struct {

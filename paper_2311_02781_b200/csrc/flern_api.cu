@@ -540,6 +540,7 @@ extern "C" FLERN_API flern_status flern_run_query(flern_ctx* ctx, const flern_qu
   }
   p.ngroups = q->ngroups;
   p.both_classes = both ? 1 : 0;
+  p.no_model = (q->flags & FLERN_Q_NO_MODEL) ? 1 : 0;
   const double t = (double)q->threshold;
   p.thr_logit = t <= 0.0 ? -INFINITY : (t >= 1.0 ? INFINITY : (float)std::log(t / (1.0 - t)));
   p.wimg = m.dbuf;

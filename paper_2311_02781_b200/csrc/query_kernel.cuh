@@ -69,6 +69,7 @@ struct QueryParams {
   int32_t ngroups;
   int32_t both_classes;
   float thr_logit;          // select logit > thr_logit  (score > t  <=>  logit > ln(t/(1-t)))
+  int32_t no_model;         // diagnostic: skip the MLP, select every joined row (scan/probe/gather only)
   const uint8_t* wimg;      // weight image: [Wh (SW128) | W1 (interleave)] bf16, exact SMEM layout
   const float* bias;        // [NL][H]
   const float* wout;        // [H]
@@ -142,10 +143,12 @@ __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_c
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + P::off_bar);
   uint64_t* full = bars;            // [S]   producers -> MMA/epilogue (128 arrivals)
   uint64_t* empty = bars + S;       // [S]   epilogue WG0 -> producers (4 arrivals)
-  uint64_t* dfull = bars + 2 * S;   // [2]   MMA commit -> epilogue
-  uint64_t* dempty = bars + 2 * S + 2;  // [2] epilogue (8 warps) -> MMA
-  uint64_t* hfull = bars + 2 * S + 4;   // epilogue (8 warps) -> MMA
-  uint64_t* hempty = bars + 2 * S + 5;  // MMA commit -> epilogue
+  uint64_t* d1full = bars + 8;      // NL=2: L1 commit -> warpgroup 0
+  uint64_t* d1empty = bars + 9;     // NL=2: warpgroup 0 (4 warps) drained D1 -> MMA
+  uint64_t* dfull = bars + 10;      // [2] NL=2: D2 halves; NL=1: ping-pong D buffers (commit)
+  uint64_t* dempty = bars + 12;     // [2] 4 warps drained it -> MMA
+  uint64_t* hfull = bars + 14;      // [4] NL=2: warpgroup 0 wrote H chunk c (4 warps)
+  uint64_t* hfree = bars + 18;      // [4] NL=2: L2b finished reading H chunk c (commit)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + P::off_misc);
   int32_t* wcnt = reinterpret_cast<int32_t*>(smem + P::off_misc + 16);     // [2][4] warp counts
   unsigned long long* acc = reinterpret_cast<unsigned long long*>(smem + P::off_acc);
@@ -153,7 +156,6 @@ __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_c
   float* s_wout = reinterpret_cast<float*>(smem + P::off_wout);
   float* s_shift = reinterpret_cast<float*>(smem + P::off_norm);
   float* s_scale = s_shift + kMaxFeat;
-  float* xchg = reinterpret_cast<float*>(smem + P::off_xchg);
   int64_t* s_cnt = reinterpret_cast<int64_t*>(smem + P::off_misc + 64);   // [kCounters]
   unsigned int* s_is_last = reinterpret_cast<unsigned int*>(smem + P::off_misc + 96);
 
@@ -174,14 +176,16 @@ __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_c
     if (tid < kCounters) s_cnt[tid] = 0;
     fence_proxy_async_smem();   // weights written by st.shared are read by the tensor core
   }
+  static_assert(S <= 4, "stage ring");
   if (tid == 0) {
     for (int s = 0; s < S; ++s) { mbar_init(&full[s], kProducerThreads); mbar_init(&empty[s], 4); }
-    for (int i = 0; i < 2; ++i) { mbar_init(&dfull[i], 1); mbar_init(&dempty[i], 8); }
-    mbar_init(hfull, 8);
-    mbar_init(hempty, 1);
+    mbar_init(d1full, 1);
+    mbar_init(d1empty, 4);
+    for (int i = 0; i < 2; ++i) { mbar_init(&dfull[i], 1); mbar_init(&dempty[i], 4); }
+    for (int c = 0; c < 4; ++c) { mbar_init(&hfull[c], 4); mbar_init(&hfree[c], 1); }
     fence_mbar_init();
   }
-  constexpr uint32_t kTmemCols = (NL >= 2) ? (2 * H <= 256 ? 256 : 512) : (H <= 32 ? 32 : (H <= 64 ? 64 : (H <= 128 ? 128 : 256)));
+  constexpr uint32_t kTmemCols = 2 * H <= 32 ? 32 : (2 * H <= 64 ? 64 : (2 * H <= 128 ? 128 : (2 * H <= 256 ? 256 : 512)));
   if (warp == 4) { tmem_alloc(tmem_slot, kTmemCols); tmem_relinquish(); }
   tc_fence_before();
   __syncthreads();
@@ -293,67 +297,77 @@ __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_c
       }
       buf ^= 1;
       n_joined += my_cnt;
-      // acquire every further stage this batch spills into
+      // Write surviving rows segment by segment (a segment = the part of the batch that lands in
+      // one stage). A completed stage is published before the next one is acquired, so the
+      // producer never holds more than one unpublished stage (no circular wait with consumers).
       const int end = fill + total;
-      const int nspill = (end - 1) / kTile;
-      for (int e = 1; e <= nspill && total > 0; ++e) {
-        mbar_wait(&empty[(stage + e) % S], ((acq / S) & 1) ^ 1, 2);
-        ++acq;
-      }
-      // normalise (fp32, two separately rounded ops: reading Q4) -> bf16 -> X tile + metadata
-      int pos = fill + woff + incl - my_cnt;
-#pragma unroll
-      for (int r = 0; r < R; ++r) {
-        if (!valid[r]) continue;
-        const int ts = (stage + pos / kTile) % S, tp = pos % kTile;
-        ++pos;
+      const int nseg = end > 0 ? (end + kTile - 1) / kTile : 1;
+      const int pos0 = fill + woff + incl - my_cnt;   // stream position of my first surviving row
+      for (int seg = 0; seg < nseg; ++seg) {
+        const int ts = (stage + seg) % S;
+        if (seg > 0) {
+          mbar_wait(&empty[ts], ((acq / S) & 1) ^ 1, 2);
+          ++acq;
+        }
         uint8_t* xs = smem + P::off_x + ts * P::XS;
         const Meta m = meta_of<K0P, H, NL>(smem, ts);
-        uint32_t packed[K0P / 2];
+        int pos = pos0;
 #pragma unroll
-        for (int k = 0; k < K0P; k += 2) {
-          float f[2];
+        for (int r = 0; r < R; ++r) {
+          if (!valid[r]) continue;
+          const int mypos = pos++;
+          if (mypos / kTile != seg) continue;
+          const int tp = mypos % kTile;
+          // normalise (fp32, two separately rounded ops: reading Q4) -> bf16 -> X tile
+          uint32_t packed[K0P / 2];
 #pragma unroll
-          for (int u = 0; u < 2; ++u) {
-            const int kk = k + u;
-            const float x = p.feat[kk].is_float ? __int_as_float(v[r][kk]) : (float)v[r][kk];
-            f[u] = kk < p.nfeat ? __fmul_rn(__fsub_rn(x, s_shift[kk]), s_scale[kk]) : 0.f;
+          for (int k = 0; k < K0P; k += 2) {
+            float f[2];
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+              const int kk = k + u;
+              const float x = p.feat[kk].is_float ? __int_as_float(v[r][kk]) : (float)v[r][kk];
+              f[u] = kk < p.nfeat ? __fmul_rn(__fsub_rn(x, s_shift[kk]), s_scale[kk]) : 0.f;
+            }
+            packed[k / 2] = bf16x2(f[0], f[1]);
           }
-          packed[k / 2] = bf16x2(f[0], f[1]);
-        }
-        // interleaved K-major layout: (k/8)*2048 + (row/8)*128 + (row%8)*16
+          // interleaved K-major layout: (k/8)*2048 + (row/8)*128 + (row%8)*16
 #pragma unroll
-        for (int c8 = 0; c8 < K0P / 8; ++c8)
-          st_shared_v4(smem_u32(xs + c8 * (kTile * 16) + (tp >> 3) * 128 + (tp & 7) * 16), packed[4 * c8],
-                       packed[4 * c8 + 1], packed[4 * c8 + 2], packed[4 * c8 + 3]);
-        m.rowid[tp] = (int32_t)row[r];
-        m.grp[tp] = (gv[r] >= 0 && gv[r] < p.ngroups) ? (uint8_t)gv[r] : (uint8_t)255;
-        m.val[tp] = sv[r];
+          for (int c8 = 0; c8 < K0P / 8; ++c8)
+            st_shared_v4(smem_u32(xs + c8 * (kTile * 16) + (tp >> 3) * 128 + (tp & 7) * 16), packed[4 * c8],
+                         packed[4 * c8 + 1], packed[4 * c8 + 2], packed[4 * c8 + 3]);
+          m.rowid[tp] = (int32_t)row[r];
+          m.grp[tp] = (gv[r] >= 0 && gv[r] < p.ngroups) ? (uint8_t)gv[r] : (uint8_t)255;
+          m.val[tp] = sv[r];
+        }
+        if ((seg + 1) * kTile <= end) {   // stage complete: publish
+          fence_proxy_async_smem();
+          if (t == 0) *m.count = kTile;
+          mbar_arrive(&full[ts]);
+        }
       }
-      fence_proxy_async_smem();
-      // publish completed stages
-      const int ncomplete = end / kTile;
-      for (int e = 0; e < ncomplete; ++e) {
-        const int ts = (stage + e) % S;
-        if (t == 0) *meta_of<K0P, H, NL>(smem, ts).count = kTile;
-        mbar_arrive(&full[ts]);
-      }
-      stage = (stage + ncomplete) % S;
+      stage = (stage + end / kTile) % S;
       fill = end % kTile;
-      if (ncomplete > 0 && fill == 0 && nspill < ncomplete) {
-        // the batch ended exactly on a tile boundary: acquire the next stage now
+      if (end > 0 && fill == 0) {   // every touched stage was published: acquire a fresh one
         mbar_wait(&empty[stage], ((acq / S) & 1) ^ 1, 3);
         ++acq;
       }
     }
     if (fill > 0) {   // flush the partial tile
+      fence_proxy_async_smem();
       if (t == 0) *meta_of<K0P, H, NL>(smem, stage).count = fill;
       mbar_arrive(&full[stage]);
       stage = (stage + 1) % S;
       mbar_wait(&empty[stage], ((acq / S) & 1) ^ 1, 4);
       ++acq;
     }
-    // end-of-stream marker
+    // end-of-stream marker, published on two consecutive stages (with NL == 1 the epilogue
+    // warpgroups take alternate tiles, so each must see one)
+    if (t == 0) *meta_of<K0P, H, NL>(smem, stage).count = -1;
+    mbar_arrive(&full[stage]);
+    stage = (stage + 1) % S;
+    mbar_wait(&empty[stage], ((acq / S) & 1) ^ 1, 5);
+    ++acq;
     if (t == 0) *meta_of<K0P, H, NL>(smem, stage).count = -1;
     mbar_arrive(&full[stage]);
     int64_t nj = n_joined;
@@ -362,157 +376,226 @@ __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_c
     if (lane == 0) atomicAdd(reinterpret_cast<unsigned long long*>(&s_cnt[1]), (unsigned long long)nj);
   } else if (warp == 4) {
     // =============================== MMA ISSUER =============================================
-    if (lane == 0) {
-      constexpr uint32_t idesc = make_idesc_bf16(128, H);
+    // NL == 2 issue order per tile t (steady state): L2a(t), L1(t+1), L2b(t). Layer 2 is split
+    // into two N-halves (D2a, D2b) so warpgroup 1 drains one half while the other is computed,
+    // and L1(t+1) sits between them so warpgroup 0 converts it into H chunk by chunk as L2b(t)
+    // releases each K-block of H (hfree[c]).
+    if (lane == 0 && !p.no_model) {
       const uint32_t x0 = smem_u32(smem + P::off_x);
       const uint32_t w1 = smem_u32(smem + P::off_w1);
-      const uint32_t wh = smem_u32(smem + P::off_wh);
-      const uint32_t hb = smem_u32(smem + P::off_hb);
-      for (uint32_t tile = 0;; ++tile) {
-        const int s = tile % S;
-        const uint32_t ph = (tile / S) & 1;
-        mbar_wait(&full[s], ph, 10);
-        if (*meta_of<K0P, H, NL>(smem, s).count < 0) break;
-        tc_fence_after();
-        // layer 1: D0 = X[s] . W1^T     (M=128, N=H, K=K0P)
-        mbar_wait(&dempty[0], (tile & 1) ^ 1, 11);
-        tc_fence_after();
+      auto issue_l1 = [&](int s, uint32_t dcol) {
+        constexpr uint32_t idesc1 = make_idesc_bf16(128, H);
 #pragma unroll
         for (int ks = 0; ks < K0P / 16; ++ks) {
           const uint64_t ad = make_sdesc(x0 + s * P::XS + ks * 2 * (kTile * 16), kTile * 16, 128, kLayoutNone);
           const uint64_t bd = make_sdesc(w1 + ks * 2 * (H * 16), H * 16, 128, kLayoutNone);
-          mma_bf16_ss(tmem_base, ad, bd, idesc, ks > 0);
+          mma_bf16_ss(tmem_base + dcol, ad, bd, idesc1, ks > 0);
         }
-        mma_commit(&dfull[0]);
-        if constexpr (NL >= 2) {
-          // layer 2: D1 = Hbuf . W2^T   (M=128, N=H, K=H), both 128B-swizzled K-major
-          mbar_wait(hfull, tile & 1, 12);
-          mbar_wait(&dempty[1], (tile & 1) ^ 1, 13);
-          tc_fence_after();
-#pragma unroll 4
-          for (int ks = 0; ks < H / 16; ++ks) {
-            const uint32_t koff = (ks & 3) * 32;   // 16 bf16 = 32 B inside the 128 B swizzle row
-            const uint64_t ad = make_sdesc(hb + (ks >> 2) * (kTile * 128) + koff, 16, 1024, kLayoutSW128);
-            const uint64_t bd = make_sdesc(wh + (ks >> 2) * (H * 128) + koff, 16, 1024, kLayoutSW128);
-            mma_bf16_ss(tmem_base + H, ad, bd, idesc, ks > 0);
+      };
+      if constexpr (NL >= 2) {
+        const uint32_t wh = smem_u32(smem + P::off_wh);
+        const uint32_t hb = smem_u32(smem + P::off_hb);
+        constexpr int NC = H / 64;
+        auto issue_l2_half = [&](int half, uint32_t tile) {
+          constexpr uint32_t idesc2 = make_idesc_bf16(128, H / 2);
+          for (int c = 0; c < NC; ++c) {
+            if (half == 0) { mbar_wait(&hfull[c], tile & 1, 12); tc_fence_after(); }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {   // 4 x K=16 inside one 64-column, 128B-swizzled K-block
+              const uint64_t ad = make_sdesc(hb + c * (kTile * 128) + j * 32, 16, 1024, kLayoutSW128);
+              const uint64_t bd = make_sdesc(wh + c * (H * 128) + half * (H / 16) * 1024 + j * 32, 16, 1024,
+                                             kLayoutSW128);
+              mma_bf16_ss(tmem_base + H + half * (H / 2), ad, bd, idesc2, (c | j) != 0);
+            }
+            if (half == 1) mma_commit(&hfree[c]);   // last reader of H chunk c for this tile
           }
-          mma_commit(&dfull[1]);
-          mma_commit(hempty);
+          mma_commit(&dfull[half]);
+        };
+        mbar_wait(&full[0], 0, 10);
+        if (*meta_of<K0P, H, NL>(smem, 0).count >= 0) {
+          tc_fence_after();
+          issue_l1(0, 0);
+          mma_commit(d1full);
+          for (uint32_t t = 0;; ++t) {
+            mbar_wait(&dempty[0], (t & 1) ^ 1, 13);
+            tc_fence_after();
+            issue_l2_half(0, t);
+            // L1(t+1) goes between the two halves when tile t+1 is already published (so that
+            // warpgroup 0 converts it while L2b(t) runs); otherwise after L2b(t) (never block the
+            // tile in flight on the producer)
+            const int s1 = (t + 1) % S;
+            const uint32_t ph1 = ((t + 1) / S) & 1;
+            bool have_next = mbar_test_wait(&full[s1], ph1);
+            bool next = false;
+            auto do_next = [&]() {
+              next = *meta_of<K0P, H, NL>(smem, s1).count >= 0;
+              if (next) {
+                mbar_wait(d1empty, ((t + 1) & 1) ^ 1, 11);
+                tc_fence_after();
+                issue_l1(s1, 0);
+                mma_commit(d1full);
+              }
+            };
+            if (have_next) do_next();
+            mbar_wait(&dempty[1], (t & 1) ^ 1, 14);
+            tc_fence_after();
+            issue_l2_half(1, t);
+            if (!have_next) {
+              mbar_wait(&full[s1], ph1, 10);
+              do_next();
+            }
+            if (!next) break;
+          }
+        }
+      } else {
+        // NL == 1: layer 1 is the only tensor-core layer; ping-pong TMEM buffers D[t&1]
+        for (uint32_t t = 0;; ++t) {
+          const int s = t % S;
+          mbar_wait(&full[s], (t / S) & 1, 10);
+          if (*meta_of<K0P, H, NL>(smem, s).count < 0) break;
+          const int b = t & 1;
+          mbar_wait(&dempty[b], ((t >> 1) & 1) ^ 1, 11);
+          tc_fence_after();
+          issue_l1(s, b * H);
+          mma_commit(&dfull[b]);
         }
       }
     }
     __syncwarp();
   } else if (warp >= 8) {
     // =============================== EPILOGUE =============================================
-    const int ew = warp - 8;                // 0..7
-    const int wg = ew >> 2;                 // column half
+    const int wg = (warp - 8) >> 2;         // warpgroup 0 / 1
     const int q = warp & 3;                 // TMEM lane quadrant (warp id % 4)
     const int r = q * 32 + lane;            // tile row owned by this thread
-    constexpr int HC = H / 2;               // columns per warpgroup
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
-    const uint32_t hb = smem_u32(smem + P::off_hb);
-    for (uint32_t tile = 0;; ++tile) {
-      const int s = tile % S;
-      const uint32_t ph = (tile / S) & 1;
-      mbar_wait(&full[s], ph, 20);
-      const Meta m = meta_of<K0P, H, NL>(smem, s);
-      const int count = *m.count;
-      if (count < 0) break;
-      float part = 0.f;
-      // ---- layer 1 epilogue ----
-      mbar_wait(&dfull[0], tile & 1, 21);
-      tc_fence_after();
-      if constexpr (NL >= 2) {
-        mbar_wait(hempty, (tile & 1) ^ 1, 22);
-#pragma unroll 1
-        for (int c0 = wg * HC; c0 < wg * HC + HC; c0 += 32) {
-          uint32_t v[32];
-          tmem_ld32(tmem_base + lane_off + c0, v);
-          uint32_t pk[16];
-#pragma unroll
-          for (int i = 0; i < 16; ++i)
-            pk[i] = relu_bf16x2(__uint_as_float(v[2 * i]) + s_bias[c0 + 2 * i],
-                                __uint_as_float(v[2 * i + 1]) + s_bias[c0 + 2 * i + 1]);
-          // 128B-swizzled K-major: K block c0/64, chunk ((c0%64)/8 + j) ^ (r%8)
-          const uint32_t rowbase = hb + (c0 >> 6) * (kTile * 128) + (r >> 3) * 1024 + (r & 7) * 128;
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const uint32_t chunk = (uint32_t)(((c0 & 63) >> 3) + j) ^ (uint32_t)(r & 7);
-            st_shared_v4(rowbase + chunk * 16, pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
-          }
+
+    // predicate + group-by of one tile's rows, then release the X stage (warpgroup-wide)
+    auto finish_tile = [&](const Meta& m, int count, int s, float logit) {
+      const bool valid = r < count;
+      const bool sel = valid && (p.no_model || logit > p.thr_logit);
+      const int g = valid ? (int)m.grp[r] : 255;
+      const int32_t val = valid ? m.val[r] : 0;
+      if (valid && g == 255) atomicAdd(reinterpret_cast<unsigned long long*>(&s_cnt[3]), 1ull);
+      if (p.dbg_score && valid) p.dbg_score[m.rowid[r]] = 1.f / (1.f + __expf(-logit));
+      if (p.dbg_selected && sel) atomicOr(p.dbg_selected + (m.rowid[r] >> 5), 1u << (m.rowid[r] & 31));
+      // warp-level group-by: per present (group, class), popc(ballot) rows and a split 16-bit sum
+      const int cls = sel ? 0 : 1;
+      const bool agg = valid && g != 255 && (sel || p.both_classes);
+      uint32_t pending = __ballot_sync(0xffffffffu, agg);
+      while (pending) {
+        const int leader = __ffs(pending) - 1;
+        const int lg = __shfl_sync(0xffffffffu, g, leader);
+        const int lc = __shfl_sync(0xffffffffu, cls, leader);
+        const bool mine = agg && g == lg && cls == lc;
+        const uint32_t mm = __ballot_sync(0xffffffffu, mine);
+        const int lo = __reduce_add_sync(0xffffffffu, mine ? (val & 0xFFFF) : 0);
+        const int hi = __reduce_add_sync(0xffffffffu, mine ? (val >> 16) : 0);
+        if (lane == leader) {
+          atomicAdd(&acc[lg * 4 + lc * 2 + 0], (unsigned long long)__popc(mm));
+          atomicAdd(&acc[lg * 4 + lc * 2 + 1], (unsigned long long)((long long)hi * 65536ll + (long long)lo));
         }
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&dempty[0]);
-        fence_proxy_async_smem();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(hfull);
-        // ---- layer 2 epilogue: logit partial = sum_c relu(D1 + b2) * w_out ----
-        mbar_wait(&dfull[1], tile & 1, 23);
-        tc_fence_after();
-        float pa[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll 1
-        for (int c0 = wg * HC; c0 < wg * HC + HC; c0 += 32) {
-          uint32_t v[32];
-          tmem_ld32(tmem_base + H + lane_off + c0, v);
-#pragma unroll
-          for (int i = 0; i < 32; ++i)
-            pa[i & 3] = fmaf(fmaxf(__uint_as_float(v[i]) + s_bias[H + c0 + i], 0.f), s_wout[c0 + i], pa[i & 3]);
-        }
-        part = (pa[0] + pa[1]) + (pa[2] + pa[3]);
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&dempty[1]);
-      } else {
-        float pa[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll 1
-        for (int c0 = wg * HC; c0 < wg * HC + HC; c0 += 32) {
-          uint32_t v[32];
-          tmem_ld32(tmem_base + lane_off + c0, v);
-#pragma unroll
-          for (int i = 0; i < 32; ++i)
-            pa[i & 3] = fmaf(fmaxf(__uint_as_float(v[i]) + s_bias[c0 + i], 0.f), s_wout[c0 + i], pa[i & 3]);
-        }
-        part = (pa[0] + pa[1]) + (pa[2] + pa[3]);
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&dempty[0]);
+        pending &= ~mm;
       }
-      // ---- combine the two column halves, predicate, aggregate ----
-      float* xb = xchg + (tile & 1) * kTile;
-      if (wg == 1) {
-        xb[r] = part;
-        named_bar_arrive(2, 256);
-      } else {
-        named_bar_sync(2, 256);
-        const float logit = part + xb[r] + p.bout;
-        const bool valid = r < count;
-        const bool sel = valid && (logit > p.thr_logit);
-        const int g = valid ? (int)m.grp[r] : 255;
-        const int32_t val = valid ? m.val[r] : 0;
-        if (valid && g == 255) atomicAdd(reinterpret_cast<unsigned long long*>(&s_cnt[3]), 1ull);
-        if (p.dbg_score && valid) p.dbg_score[m.rowid[r]] = 1.f / (1.f + __expf(-logit));
-        if (p.dbg_selected && sel) atomicOr(p.dbg_selected + (m.rowid[r] >> 5), 1u << (m.rowid[r] & 31));
-        // warp-level group-by: per present group, popc(ballot) rows and a split 16-bit sum
-        const int cls = sel ? 0 : 1;
-        const bool agg = valid && g != 255 && (sel || p.both_classes);
-        uint32_t pending = __ballot_sync(0xffffffffu, agg);
-        while (pending) {
-          const int leader = __ffs(pending) - 1;
-          const int lg = __shfl_sync(0xffffffffu, g, leader);
-          const int lc = __shfl_sync(0xffffffffu, cls, leader);
-          const bool mine = agg && g == lg && cls == lc;
-          const uint32_t mm = __ballot_sync(0xffffffffu, mine);
-          const int lo = __reduce_add_sync(0xffffffffu, mine ? (val & 0xFFFF) : 0);
-          const int hi = __reduce_add_sync(0xffffffffu, mine ? (val >> 16) : 0);
-          if (lane == leader) {
-            atomicAdd(&acc[lg * 4 + lc * 2 + 0], (unsigned long long)__popc(mm));
-            atomicAdd(&acc[lg * 4 + lc * 2 + 1], (unsigned long long)((long long)hi * 65536ll + (long long)lo));
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);   // stage (X + metadata) can be refilled
+    };
+    // relu(D + b) . w_out over `ncols` TMEM columns starting at `col` (bias/w offset `boff`)
+    auto dot_cols = [&](uint32_t col, int ncols, int boff, float (&pa)[4]) {
+#pragma unroll 1
+      for (int c0 = 0; c0 < ncols; c0 += 32) {
+        uint32_t v[32];
+        tmem_ld32(tmem_base + lane_off + col + c0, v);
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+          pa[i & 3] = fmaf(fmaxf(__uint_as_float(v[i]) + s_bias[boff + c0 + i], 0.f), s_wout[c0 + i + (boff % H)],
+                           pa[i & 3]);
+      }
+    };
+
+    if constexpr (NL >= 2) {
+      constexpr int NC = H / 64;
+      const uint32_t hb = smem_u32(smem + P::off_hb);
+      if (wg == 0) {
+        // ---- warpgroup 0: D1 -> bias + ReLU -> bf16 -> H (layer-2 A operand), chunk by chunk ----
+        for (uint32_t t = 0; !p.no_model; ++t) {
+          const int s = t % S;
+          mbar_wait(&full[s], (t / S) & 1, 20);
+          if (*meta_of<K0P, H, NL>(smem, s).count < 0) break;
+          mbar_wait(d1full, t & 1, 21);
+          tc_fence_after();
+          for (int c = 0; c < NC; ++c) {
+            uint32_t pk[32];
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+              uint32_t v[32];
+              const int c0 = c * 64 + j * 32;
+              tmem_ld32(tmem_base + lane_off + c0, v);
+#pragma unroll
+              for (int i = 0; i < 16; ++i)
+                pk[j * 16 + i] = relu_bf16x2(__uint_as_float(v[2 * i]) + s_bias[c0 + 2 * i],
+                                             __uint_as_float(v[2 * i + 1]) + s_bias[c0 + 2 * i + 1]);
+            }
+            if (c == NC - 1) {   // all of D1 is in registers: the MMA may overwrite it
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) mbar_arrive(d1empty);
+            }
+            mbar_wait(&hfree[c], (t & 1) ^ 1, 22);   // L2b(t-1) finished reading chunk c
+            const uint32_t rowbase = hb + c * (kTile * 128) + (r >> 3) * 1024 + (r & 7) * 128;
+#pragma unroll
+            for (int jj = 0; jj < 8; ++jj)   // 128B swizzle: chunk jj of the row goes to jj ^ (row % 8)
+              st_shared_v4(rowbase + ((uint32_t)(jj ^ (r & 7)) << 4), pk[4 * jj], pk[4 * jj + 1], pk[4 * jj + 2],
+                           pk[4 * jj + 3]);
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&hfull[c]);
           }
-          pending &= ~mm;
         }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[s]);   // stage (X + metadata) can be refilled
+      } else {
+        // ---- warpgroup 1: logit = relu(D2 + b2) . w_out + b_out, predicate, group-by ----
+        for (uint32_t t = 0;; ++t) {
+          const int s = t % S;
+          mbar_wait(&full[s], (t / S) & 1, 23);
+          const Meta m = meta_of<K0P, H, NL>(smem, s);
+          const int count = *m.count;
+          if (count < 0) break;
+          float logit = 0.f;
+          if (!p.no_model) {
+            float pa[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll 1
+            for (int h = 0; h < 2; ++h) {
+              mbar_wait(&dfull[h], t & 1, 24);
+              tc_fence_after();
+              dot_cols(H + h * (H / 2), H / 2, H + h * (H / 2), pa);
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) mbar_arrive(&dempty[h]);
+            }
+            logit = (pa[0] + pa[1]) + (pa[2] + pa[3]) + p.bout;
+          }
+          finish_tile(m, count, s, logit);
+        }
+      }
+    } else {
+      // ---- NL == 1: the two warpgroups take alternate tiles (TMEM buffer D[wg]) ----
+      for (uint32_t t = wg;; t += 2) {
+        const int s = t % S;
+        mbar_wait(&full[s], (t / S) & 1, 25);
+        const Meta m = meta_of<K0P, H, NL>(smem, s);
+        const int count = *m.count;
+        if (count < 0) break;
+        float logit = 0.f;
+        if (!p.no_model) {
+          mbar_wait(&dfull[wg], (t >> 1) & 1, 26);
+          tc_fence_after();
+          float pa[4] = {0.f, 0.f, 0.f, 0.f};
+          dot_cols(wg * H, H, 0, pa);
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&dempty[wg]);
+          logit = (pa[0] + pa[1]) + (pa[2] + pa[3]) + p.bout;
+        }
+        finish_tile(m, count, s, logit);
       }
     }
   }

@@ -26,7 +26,7 @@ ERRORS = {-1: "FLERN_E_INVALID_ARG", -2: "FLERN_E_NOT_FOUND", -3: "FLERN_E_DUPLI
           -10: "FLERN_E_UNSUPPORTED"}
 FLERN_I32, FLERN_F32, FLERN_DATE32, FLERN_DEC32, FLERN_DICT32 = 1, 2, 3, 4, 5
 FLERN_COPY_HOST, FLERN_COPY_DEVICE, FLERN_BORROW_DEVICE = 0x1, 0x2, 0x4
-FLERN_Q_RESULT_DEVICE, FLERN_Q_ASYNC, FLERN_Q_BOTH_CLASSES = 0x1, 0x2, 0x4
+FLERN_Q_RESULT_DEVICE, FLERN_Q_ASYNC, FLERN_Q_BOTH_CLASSES, FLERN_Q_NO_MODEL = 0x1, 0x2, 0x4, 0x8
 EXPORTED = ["flern_create", "flern_destroy", "flern_last_error", "flern_version", "flern_load_table",
             "flern_drop_table", "flern_load_model", "flern_build_hashtable", "flern_run_query",
             "flern_query_launches"]

@@ -209,3 +209,23 @@ def test_c2_full_size_sampled():
     g = parity.run_gpu(cfg, db, lt, debug=False)
     cnt, sm = H.brute_aggregate(cfg, db, db.fact["l_quantity"] >= 26)
     assert g["count"].tolist() == cnt.tolist() and g["sum"].tolist() == sm.tolist()
+
+
+def test_no_model_mode_is_join_aggregate():
+    """FLERN_Q_NO_MODEL (diagnostic used for the HBM roofline of scan/probe/gather): every joined
+    row is selected, so the aggregates equal the brute-force join aggregate."""
+    from paper_2311_02781_b200 import flern as F
+    from paper_2311_02781_b200.session import GpuQuery
+    for name in ("c1", "c2"):
+        cfg = D.with_sf(D.CONFIGS[name], 0.01, match_rate=0.9)
+        db = D.make_database(cfg)
+        gq = GpuQuery(cfg, db, D.make_model(cfg, db))
+        try:
+            cnt = np.zeros(cfg.ngroups, np.int64)
+            sm = np.zeros(cfg.ngroups, np.int64)
+            q = gq.make_query(gq.fact_id, flags=F.FLERN_Q_NO_MODEL)
+            gq.run(q, count=cnt, sum=sm)
+            c2, s2 = H.brute_aggregate(cfg, db, np.ones(db.fact_n, bool))
+            assert cnt.tolist() == c2.tolist() and sm.tolist() == s2.tolist()
+        finally:
+            gq.close()
