@@ -165,6 +165,8 @@ typedef struct {
   float* dbg_score;        /* optional [fact rows]: fp32 score of each row that reached the model, NaN otherwise */
   int32_t* dbg_match;      /* optional [fact rows * nprobes]: build row id of each probe, -1 = miss/not reached */
   uint32_t* dbg_selected;  /* optional bitmap [ceil(rows/32)]: bit set if selected */
+  uint64_t* dbg_trace;     /* optional [FLERN_TRACE_EVENTS * 256] (device if RESULT_DEVICE): clock64 stamps of
+                              the pipeline hand-offs of CTA 0 (diagnostic; zero = event not reached) */
   int64_t rows_scanned, rows_joined, rows_scored, rows_selected; /* filled unless FLERN_Q_ASYNC */
   float elapsed_ms;        /* device time of the query kernel (CUDA events), unless FLERN_Q_ASYNC */
 } flern_result;
@@ -173,6 +175,8 @@ typedef struct {
  * A group code outside [0, ngroups) is a data error: FLERN_E_INVALID_ARG after the run (sync mode)
  * and counted in counters[3]. */
 FLERN_API flern_status flern_run_query(flern_ctx* ctx, const flern_query* q, flern_result* res);
+
+#define FLERN_TRACE_EVENTS 20
 
 /* Number of CUDA kernels flern_run_query launches per call (for launch accounting): 1. */
 FLERN_API int32_t flern_query_launches(void);

@@ -14,21 +14,38 @@ __global__ void fill_slots_kernel(unsigned long long* slots, int64_t n) {
     slots[i] = kEmptySlot;
 }
 
-// flags[0]: duplicate key seen, flags[1]: reserved key (INT32_MIN) seen
+// key range of the build side: minmax[0] = min, minmax[1] = max (initialised to INT_MAX / INT_MIN)
+__global__ void key_minmax_kernel(const int32_t* __restrict__ keys, int64_t nrows, int32_t* __restrict__ minmax) {
+  int32_t lo = 0x7FFFFFFF, hi = (int32_t)0x80000000;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nrows; i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t k = keys[i];
+    lo = min(lo, k);
+    hi = max(hi, k);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+  }
+  if ((threadIdx.x & 31) == 0) { atomicMin(&minmax[0], lo); atomicMax(&minmax[1], hi); }
+}
+
+// flags[0]: duplicate key seen, flags[1]: reserved key (INT32_MIN) seen, flags[2]: max displacement
 __global__ void build_insert_kernel(const int32_t* __restrict__ keys, int64_t nrows,
-                                    unsigned long long* __restrict__ slots, uint32_t mask, uint32_t shift,
-                                    int32_t* __restrict__ flags) {
+                                    unsigned long long* __restrict__ slots, HashFn hf, int32_t* __restrict__ flags) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nrows; i += (int64_t)gridDim.x * blockDim.x) {
     const int32_t key = keys[i];
     if (key == kEmptyKey) { atomicExch(&flags[1], 1); continue; }
     const unsigned long long item = (unsigned long long)(uint32_t)key | ((unsigned long long)(uint32_t)i << 32);
-    uint32_t h = hash_key(key, shift);
+    uint32_t h = hash_slot(key, hf);
+    int32_t disp = 0;
     while (true) {
       const unsigned long long prev = atomicCAS(slots + h, kEmptySlot, item);
       if (prev == kEmptySlot) break;
       if ((int32_t)(uint32_t)prev == key) { atomicExch(&flags[0], 1); break; }
-      h = (h + 1) & mask;
+      h = (h + 1) & hf.mask;
+      ++disp;
     }
+    if (disp > 8) atomicMax(&flags[2], disp);
   }
 }
 

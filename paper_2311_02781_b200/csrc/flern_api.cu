@@ -4,7 +4,10 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
+#include <algorithm>
+#include <map>
 #include <memory>
 #include <string>
 #include <vector>
@@ -39,9 +42,12 @@ struct Model {
   std::string name;
   std::vector<int32_t> dims;
   int K0 = 0, K0P = 0, H = 0, NL = 0;
-  uint8_t* dbuf = nullptr;   // [wimg | bias | wout | shift | scale]
-  size_t wimg_bytes = 0, off_bias = 0, off_wout = 0, off_shift = 0, off_scale = 0;
+  uint8_t* dbuf = nullptr;   // [wimg | bias | wout | shift | scale], inputs in the model's order
+  size_t wimg_bytes = 0, off_bias = 0, off_wout = 0, off_shift = 0, off_scale = 0, total = 0;
   float bout = 0.f;
+  std::vector<std::vector<float>> W, b;      // host copies (fp32 as given)
+  std::vector<float> shift, scale;
+  std::map<std::vector<int>, uint8_t*> permuted;   // images with permuted inputs (see run_query)
 };
 struct HashTable {
   int32_t table_id = -1;
@@ -49,8 +55,10 @@ struct HashTable {
   flern_dtype key_type;
   int64_t nrows = 0;
   uint32_t log2cap = 0;
-  unsigned long long* slots = nullptr;
+  HashFn hf{};
+  unsigned long long* slots = nullptr;   // owns the allocation (payload follows the slots)
   int32_t* payload = nullptr;
+  size_t bytes = 0;
   int32_t pstride = 0;
   std::vector<std::string> pcols;
   std::vector<flern_dtype> ptypes;
@@ -71,6 +79,7 @@ struct flern_ctx {
   cudaStream_t stream = nullptr;
   bool own_stream = false;
   int num_sms = 148;
+  size_t persist_max = 0, window_max = 0;
   std::string err;
   std::vector<Table> tables;
   std::vector<Model> models;
@@ -80,6 +89,7 @@ struct flern_ctx {
   unsigned int* ticket = nullptr;
   int64_t* dres = nullptr;        // [2*kMaxGroups count | 2*kMaxGroups sum | kCounters]
   int32_t* dflags = nullptr;      // build flags
+  int32_t* dummy = nullptr;       // 64 zero bytes (kernel loads of unneeded values read here)
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
 };
 
@@ -173,6 +183,8 @@ extern "C" FLERN_API flern_status flern_create(int device, void* cuda_stream, fl
   std::unique_ptr<flern_ctx> ctx(new flern_ctx());
   ctx->device = device;
   ctx->num_sms = prop.multiProcessorCount;
+  ctx->persist_max = (size_t)prop.persistingL2CacheMaxSize;
+  ctx->window_max = (size_t)prop.accessPolicyMaxWindowSize;
   if (cudaSetDevice(device) != cudaSuccess) return FLERN_E_CUDA;
   if (cuda_stream) {
     ctx->stream = static_cast<cudaStream_t>(cuda_stream);
@@ -185,7 +197,11 @@ extern "C" FLERN_API flern_status flern_create(int device, void* cuda_stream, fl
   if (cudaMalloc(&ctx->ticket, 64) != cudaSuccess) return FLERN_E_OOM;
   if (cudaMalloc(&ctx->dres, (4 * kMaxGroups + kCounters) * sizeof(int64_t)) != cudaSuccess) return FLERN_E_OOM;
   if (cudaMalloc(&ctx->dflags, 64) != cudaSuccess) return FLERN_E_OOM;
+  if (cudaMalloc(&ctx->dummy, 256) != cudaSuccess) return FLERN_E_OOM;
+  if (cudaMemsetAsync(ctx->dummy, 0, 256, ctx->stream) != cudaSuccess) return FLERN_E_CUDA;
   if (cudaMemsetAsync(ctx->ticket, 0, 64, ctx->stream) != cudaSuccess) return FLERN_E_CUDA;
+  // let the build side of the join persist in L2 while the fact table streams through
+  if (ctx->persist_max > 0) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, ctx->persist_max);
   if (cudaEventCreate(&ctx->ev0) != cudaSuccess || cudaEventCreate(&ctx->ev1) != cudaSuccess) return FLERN_E_CUDA;
   if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) return FLERN_E_CUDA;
   *out = ctx.release();
@@ -199,12 +215,16 @@ extern "C" FLERN_API void flern_destroy(flern_ctx* ctx) {
   for (auto& t : ctx->tables)
     for (auto& c : t.cols)
       if (c.owned && c.dptr) cudaFree(c.dptr);
-  for (auto& m : ctx->models) cudaFree(m.dbuf);
-  for (auto& h : ctx->hts) { cudaFree(h.slots); cudaFree(h.payload); }
+  for (auto& m : ctx->models) {
+    cudaFree(m.dbuf);
+    for (auto& kv : m.permuted) cudaFree(kv.second);
+  }
+  for (auto& h : ctx->hts) cudaFree(h.slots);
   cudaFree(ctx->partials);
   cudaFree(ctx->ticket);
   cudaFree(ctx->dres);
   cudaFree(ctx->dflags);
+  cudaFree(ctx->dummy);
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
   if (ctx->ev1) cudaEventDestroy(ctx->ev1);
   if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
@@ -237,6 +257,9 @@ extern "C" FLERN_API flern_status flern_load_table(flern_ctx* ctx, const char* n
       return fail(ctx, FLERN_E_INVALID_ARG, "table '%s': column '%s' has no data", name, cols[i].name);
     if (reinterpret_cast<uintptr_t>(cols[i].data) % 4 != 0)
       return fail(ctx, FLERN_E_INVALID_ARG, "table '%s': column '%s' is not 4-byte aligned", name, cols[i].name);
+    if (mode == FLERN_BORROW_DEVICE && reinterpret_cast<uintptr_t>(cols[i].data) % 16 != 0)
+      return fail(ctx, FLERN_E_INVALID_ARG, "table '%s': borrowed column '%s' must be 16-byte aligned (vector scan)",
+                  name, cols[i].name);
     for (int32_t j = 0; j < i; ++j)
       if (std::strcmp(cols[i].name, cols[j].name) == 0)
         return fail(ctx, FLERN_E_DUPLICATE, "table '%s': column '%s' appears twice", name, cols[i].name);
@@ -298,6 +321,54 @@ extern "C" FLERN_API flern_status flern_drop_table(flern_ctx* ctx, int32_t table
 }
 
 // ================================================================================ models
+namespace {
+// Device image of a model with its inputs in kernel order: input kk of the kernel is the model's
+// input perm[kk] (the kernel wants fact-column features first; see flern_run_query).
+std::vector<uint8_t> model_image(Model& m, const std::vector<int>& perm) {
+  const int H = m.H, K0 = m.K0, K0P = m.K0P, NL = m.NL;
+  const size_t WH = NL >= 2 ? (size_t)H * H * 2 : 0;
+  const size_t W1 = (size_t)H * K0P * 2;
+  m.wimg_bytes = WH + W1;
+  m.off_bias = (m.wimg_bytes + 255) / 256 * 256;
+  m.off_wout = m.off_bias + (size_t)NL * H * 4;
+  m.off_shift = m.off_wout + (size_t)H * 4;
+  m.off_scale = m.off_shift + (size_t)K0P * 4;
+  m.total = m.off_scale + (size_t)K0P * 4;
+  std::vector<uint8_t> img(m.total, 0);
+  uint16_t* wh = reinterpret_cast<uint16_t*>(img.data());
+  uint16_t* w1 = reinterpret_cast<uint16_t*>(img.data() + WH);
+  // W1: [H x K0P] interleaved K-major: (k/8)*(H*16) + (n/8)*128 + (n%8)*16 + (k%8)*2 bytes
+  for (int n = 0; n < H; ++n)
+    for (int k = 0; k < K0P; ++k) {
+      const float v = k < K0 ? m.W[0][(size_t)n * K0 + perm[k]] : 0.f;
+      const size_t off = (size_t)(k / 8) * (H * 16) + (n / 8) * 128 + (n % 8) * 16 + (k % 8) * 2;
+      w1[off / 2] = bf16_rne_bits(v);
+    }
+  // W2: [H x H] 128B-swizzled K-major: (k/64)*(H*128) + (n/8)*1024 + (n%8)*128 + (((k%64)/8) ^ (n%8))*16 + (k%8)*2
+  if (NL >= 2)
+    for (int n = 0; n < H; ++n)
+      for (int k = 0; k < H; ++k) {
+        const size_t off = (size_t)(k / 64) * (H * 128) + (n / 8) * 1024 + (n % 8) * 128 +
+                           (size_t)((((k % 64) / 8) ^ (n % 8)) * 16) + (k % 8) * 2;
+        wh[off / 2] = bf16_rne_bits(m.W[1][(size_t)n * H + k]);
+      }
+  float* bias = reinterpret_cast<float*>(img.data() + m.off_bias);
+  for (int l = 0; l < NL; ++l)
+    for (int j = 0; j < H; ++j) bias[l * H + j] = m.b[l][j];
+  float* wout = reinterpret_cast<float*>(img.data() + m.off_wout);   // output layer stays fp32 (CUDA-core dot)
+  for (int j = 0; j < H; ++j) wout[j] = m.W[NL][j];
+  m.bout = m.b[NL][0];
+  float* sh = reinterpret_cast<float*>(img.data() + m.off_shift);
+  float* sc = reinterpret_cast<float*>(img.data() + m.off_scale);
+  // the gather computes fma(x, scale, c) with c = -shift * scale (rounded once to fp32)
+  for (int k = 0; k < K0; ++k) {
+    sh[k] = (float)(-(double)m.shift[perm[k]] * (double)m.scale[perm[k]]);
+    sc[k] = m.scale[perm[k]];
+  }
+  return img;
+}
+}  // namespace
+
 extern "C" FLERN_API flern_status flern_load_model(flern_ctx* ctx, const char* name, int32_t nlayers,
                                                    const int32_t* dims, const float* const* W, const float* const* b,
                                                    const float* in_shift, const float* in_scale, int32_t* model_id) {
@@ -337,41 +408,16 @@ extern "C" FLERN_API flern_status flern_load_model(flern_ctx* ctx, const char* n
   m.name = name;
   m.dims.assign(dims, dims + nlayers + 1);
   m.K0 = K0; m.K0P = K0P; m.H = H; m.NL = NL;
-  const size_t WH = NL >= 2 ? (size_t)H * H * 2 : 0;
-  const size_t W1 = (size_t)H * K0P * 2;
-  m.wimg_bytes = WH + W1;
-  m.off_bias = (m.wimg_bytes + 255) / 256 * 256;
-  m.off_wout = m.off_bias + (size_t)NL * H * 4;
-  m.off_shift = m.off_wout + (size_t)H * 4;
-  m.off_scale = m.off_shift + (size_t)K0P * 4;
-  const size_t total = m.off_scale + (size_t)K0P * 4;
-  std::vector<uint8_t> img(total, 0);
-  uint16_t* wh = reinterpret_cast<uint16_t*>(img.data());
-  uint16_t* w1 = reinterpret_cast<uint16_t*>(img.data() + WH);
-  // W1: [H x K0P] interleaved K-major: (k/8)*(H*16) + (n/8)*128 + (n%8)*16 + (k%8)*2 bytes
-  for (int n = 0; n < H; ++n)
-    for (int k = 0; k < K0P; ++k) {
-      const float v = k < K0 ? W[0][(int64_t)n * K0 + k] : 0.f;
-      const size_t off = (size_t)(k / 8) * (H * 16) + (n / 8) * 128 + (n % 8) * 16 + (k % 8) * 2;
-      w1[off / 2] = bf16_rne_bits(v);
-    }
-  // W2: [H x H] 128B-swizzled K-major: (k/64)*(H*128) + (n/8)*1024 + (n%8)*128 + (((k%64)/8) ^ (n%8))*16 + (k%8)*2
-  if (NL >= 2)
-    for (int n = 0; n < H; ++n)
-      for (int k = 0; k < H; ++k) {
-        const size_t off = (size_t)(k / 64) * (H * 128) + (n / 8) * 1024 + (n % 8) * 128 +
-                           (size_t)((((k % 64) / 8) ^ (n % 8)) * 16) + (k % 8) * 2;
-        wh[off / 2] = bf16_rne_bits(W[1][(int64_t)n * H + k]);
-      }
-  float* bias = reinterpret_cast<float*>(img.data() + m.off_bias);
-  for (int l = 0; l < NL; ++l)
-    for (int j = 0; j < H; ++j) bias[l * H + j] = b[l][j];
-  float* wout = reinterpret_cast<float*>(img.data() + m.off_wout);   // output layer stays fp32 (CUDA-core dot)
-  for (int j = 0; j < H; ++j) wout[j] = W[NL][j];
-  m.bout = b[NL][0];
-  float* sh = reinterpret_cast<float*>(img.data() + m.off_shift);
-  float* sc = reinterpret_cast<float*>(img.data() + m.off_scale);
-  for (int k = 0; k < K0; ++k) { sh[k] = in_shift[k]; sc[k] = in_scale[k]; }
+  for (int l = 0; l < nlayers; ++l) {
+    m.W.emplace_back(W[l], W[l] + (size_t)dims[l] * dims[l + 1]);
+    m.b.emplace_back(b[l], b[l] + dims[l + 1]);
+  }
+  m.shift.assign(in_shift, in_shift + K0);
+  m.scale.assign(in_scale, in_scale + K0);
+  std::vector<int> ident(K0);
+  for (int k = 0; k < K0; ++k) ident[k] = k;
+  std::vector<uint8_t> img = model_image(m, ident);
+  const size_t total = m.total;
   CUDA_TRY(ctx, cudaSetDevice(ctx->device));
   CUDA_TRY(ctx, cudaMalloc(&m.dbuf, total));
   CUDA_TRY(ctx, cudaMemcpyAsync(m.dbuf, img.data(), total, cudaMemcpyHostToDevice, ctx->stream));
@@ -409,30 +455,54 @@ extern "C" FLERN_API flern_status flern_build_hashtable(flern_ctx* ctx, int32_t 
     h.ptypes.push_back(c->dtype);
     pc.col[i] = static_cast<const int32_t*>(c->dptr);
   }
-  h.pstride = npayload <= 0 ? 1 : (npayload + 3) / 4 * 4;   // 16-byte rows
+  h.pstride = npayload <= 0 ? 1 : npayload;   // payload rows hold exactly the needed words
   uint32_t lg = 6;
   while (((int64_t)1 << lg) < 2 * t.nrows) ++lg;           // load factor <= 0.5
   h.log2cap = lg;
   const int64_t cap = (int64_t)1 << lg;
   CUDA_TRY(ctx, cudaSetDevice(ctx->device));
-  CUDA_TRY(ctx, cudaMalloc(&h.slots, cap * sizeof(unsigned long long)));
-  CUDA_TRY(ctx, cudaMalloc(&h.payload, std::max<int64_t>(1, t.nrows) * h.pstride * sizeof(int32_t)));
-  CUDA_TRY(ctx, cudaMemsetAsync(ctx->dflags, 0, 64, ctx->stream));
-  fill_slots_kernel<<<grid_for(cap), 256, 0, ctx->stream>>>(h.slots, cap);
+  // one allocation: slots then payload, so one L2 access-policy window can cover the build side
+  h.bytes = cap * sizeof(unsigned long long) + std::max<int64_t>(1, t.nrows) * h.pstride * sizeof(int32_t);
+  CUDA_TRY(ctx, cudaMalloc(&h.slots, h.bytes));
+  h.payload = reinterpret_cast<int32_t*>(h.slots + cap);
+  // Hash function: order-preserving range hash when the key range is dense enough (at most
+  // 16 key values per slot), Fibonacci hashing otherwise or when the range hash builds long probe
+  // chains (skewed keys): the build is retried with Fibonacci hashing.
+  int32_t mm[2] = {0x7FFFFFFF, (int32_t)0x80000000};
   if (t.nrows > 0) {
-    build_insert_kernel<<<grid_for(t.nrows), 256, 0, ctx->stream>>>(static_cast<const int32_t*>(kc->dptr), t.nrows,
-                                                                    h.slots, (uint32_t)(cap - 1), 32u - lg, ctx->dflags);
-    if (npayload > 0)
-      pack_payload_kernel<<<grid_for(t.nrows * h.pstride), 256, 0, ctx->stream>>>(pc, npayload, h.pstride, t.nrows,
-                                                                                  h.payload);
+    CUDA_TRY(ctx, cudaMemcpyAsync(ctx->dflags + 4, mm, sizeof(mm), cudaMemcpyHostToDevice, ctx->stream));
+    key_minmax_kernel<<<std::min(grid_for(t.nrows), 1024), 256, 0, ctx->stream>>>(
+        static_cast<const int32_t*>(kc->dptr), t.nrows, ctx->dflags + 4);
+    CUDA_TRY(ctx, cudaMemcpyAsync(mm, ctx->dflags + 4, sizeof(mm), cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
   }
+  const uint64_t range = t.nrows > 0 ? (uint64_t)((int64_t)mm[1] - (int64_t)mm[0]) + 1 : 1;
+  int32_t flags[3] = {0, 0, 0};
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    HashFn hf{};
+    hf.mask = (uint32_t)(cap - 1);
+    hf.shift = 32u - lg;
+    hf.kmin = mm[0];
+    hf.mode = (attempt == 0 && t.nrows > 0 && range <= 16ull * (uint64_t)cap && range < (1ull << 32)) ? 1u : 0u;
+    hf.mulc = hf.mode ? (uint32_t)std::min<uint64_t>(0xFFFFFFFFull, ((uint64_t)cap << 32) / range) : 0u;
+    CUDA_TRY(ctx, cudaMemsetAsync(ctx->dflags, 0, 16, ctx->stream));
+    fill_slots_kernel<<<grid_for(cap), 256, 0, ctx->stream>>>(h.slots, cap);
+    if (t.nrows > 0)
+      build_insert_kernel<<<grid_for(t.nrows), 256, 0, ctx->stream>>>(static_cast<const int32_t*>(kc->dptr), t.nrows,
+                                                                      h.slots, hf, ctx->dflags);
+    CUDA_TRY(ctx, cudaGetLastError());
+    CUDA_TRY(ctx, cudaMemcpyAsync(flags, ctx->dflags, sizeof(flags), cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    h.hf = hf;
+    if (!(hf.mode == 1 && flags[2] > 64 && !flags[0] && !flags[1])) break;   // long chains: retry
+  }
+  if (t.nrows > 0 && npayload > 0)
+    pack_payload_kernel<<<grid_for(t.nrows * h.pstride), 256, 0, ctx->stream>>>(pc, npayload, h.pstride, t.nrows,
+                                                                                h.payload);
   CUDA_TRY(ctx, cudaGetLastError());
-  int32_t flags[2] = {0, 0};
-  CUDA_TRY(ctx, cudaMemcpyAsync(flags, ctx->dflags, sizeof(flags), cudaMemcpyDeviceToHost, ctx->stream));
   CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
   if (flags[0] || flags[1]) {
     cudaFree(h.slots);
-    cudaFree(h.payload);
     if (flags[1]) return fail(ctx, FLERN_E_INVALID_ARG, "key column '%s' contains the reserved value INT32_MIN", key_col);
     return fail(ctx, FLERN_E_DUP_KEY, "key column '%s' of table '%s' is not unique", key_col, t.name.c_str());
   }
@@ -455,7 +525,7 @@ extern "C" FLERN_API flern_status flern_run_query(flern_ctx* ctx, const flern_qu
   const Table& fact = ctx->tables[q->fact_table];
   if (q->model_id < 0 || q->model_id >= (int32_t)ctx->models.size())
     return fail(ctx, FLERN_E_NOT_FOUND, "no model with id %d", q->model_id);
-  const Model& m = ctx->models[q->model_id];
+  Model& m = ctx->models[q->model_id];
   if (q->nfeat != m.K0)
     return fail(ctx, FLERN_E_ARITY, "UDF '%s' takes %d arguments, query passes %d", m.name.c_str(), m.K0, q->nfeat);
   if (q->nfeat > 0 && !q->feats) return fail(ctx, FLERN_E_INVALID_ARG, "null feature list");
@@ -480,8 +550,8 @@ extern "C" FLERN_API flern_status flern_run_query(flern_ctx* ctx, const flern_qu
       return fail(ctx, FLERN_E_UNSUPPORTED, "probe %d: the first probe is keyed by a fact column, the second by probe 0", i);
     ProbeDesc& d = p.probe[i];
     d.slots = reinterpret_cast<const int2*>(h.slots);
-    d.mask = (uint32_t)(((int64_t)1 << h.log2cap) - 1);
-    d.shift = 32u - h.log2cap;
+    d.hf = h.hf;
+    d.mask = h.hf.mask;
     d.payload = h.payload;
     d.pstride = h.pstride;
     d.src = pr.src;
@@ -518,16 +588,41 @@ extern "C" FLERN_API flern_status flern_run_query(flern_ctx* ctx, const flern_qu
     out->base = h.payload + w;
     out->stride = h.pstride;
     out->src = 1 + r.src;
+    out->word = w;
     out->is_float = h.ptypes[w] == FLERN_F32;
     return FLERN_OK;
   };
   flern_status st;
   p.nfeat = q->nfeat;
+  std::vector<ColDesc> fq(q->nfeat);
   for (int k = 0; k < q->nfeat; ++k) {
     char what[32];
     snprintf(what, sizeof(what), "feature %d", k);
-    if ((st = resolve(q->feats[k], &p.feat[k], false, what)) != FLERN_OK) return st;
+    if ((st = resolve(q->feats[k], &fq[k], false, what)) != FLERN_OK) return st;
   }
+  // kernel order: fact-column features first (one vector load per column before the probe),
+  // then build-payload features; the model image's W1 columns follow the same permutation
+  std::vector<int> perm;
+  for (int k = 0; k < q->nfeat; ++k) if (fq[k].src == 0) perm.push_back(k);
+  p.nfact = (int32_t)perm.size();
+  for (int k = 0; k < q->nfeat; ++k) if (fq[k].src != 0) perm.push_back(k);
+  bool ident = true;
+  const int32_t* any_fact_col = static_cast<const int32_t*>(fact.cols[0].dptr);
+  for (int k = 0; k < kMaxFeat; ++k) { p.fcol[k] = any_fact_col; p.dword[k] = 0; }
+  for (int k = 0; k < q->nfeat; ++k) {
+    p.feat[k] = fq[perm[k]];
+    ident = ident && perm[k] == k;
+    if (p.feat[k].src == 0) {
+      p.fcol[k] = p.feat[k].base;
+    } else {
+      p.dword[k] = (int32_t)(p.feat[k].base - ctx->hts[q->probes[p.feat[k].src - 1].ht_id].payload);
+      if (p.feat[k].src == 2) p.dprobe1 |= 1ull << k;
+    }
+    if (p.feat[k].is_float) p.fmask |= 1ull << k;
+  }
+  if (q->nprobes < 2) p.probe[1] = p.probe[0];   // valid pointers for unused address math
+  p.dummy = ctx->dummy;
+
   if ((st = resolve(q->group_col, &p.grp, true, "group column")) != FLERN_OK) return st;
   if ((st = resolve(q->sum_col, &p.sum, true, "sum column")) != FLERN_OK) return st;
   if (q->prefilter_col) {
@@ -543,12 +638,25 @@ extern "C" FLERN_API flern_status flern_run_query(flern_ctx* ctx, const flern_qu
   p.no_model = (q->flags & FLERN_Q_NO_MODEL) ? 1 : 0;
   const double t = (double)q->threshold;
   p.thr_logit = t <= 0.0 ? -INFINITY : (t >= 1.0 ? INFINITY : (float)std::log(t / (1.0 - t)));
-  p.wimg = m.dbuf;
-  p.bias = reinterpret_cast<const float*>(m.dbuf + m.off_bias);
-  p.wout = reinterpret_cast<const float*>(m.dbuf + m.off_wout);
+  uint8_t* img = m.dbuf;
+  if (!ident) {
+    auto it = m.permuted.find(perm);
+    if (it == m.permuted.end()) {
+      std::vector<uint8_t> h = model_image(m, perm);
+      uint8_t* d = nullptr;
+      CUDA_TRY(ctx, cudaMalloc(&d, h.size()));
+      CUDA_TRY(ctx, cudaMemcpyAsync(d, h.data(), h.size(), cudaMemcpyHostToDevice, ctx->stream));
+      CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+      it = m.permuted.emplace(perm, d).first;
+    }
+    img = it->second;
+  }
+  p.wimg = img;
+  p.bias = reinterpret_cast<const float*>(img + m.off_bias);
+  p.wout = reinterpret_cast<const float*>(img + m.off_wout);
   p.bout = m.bout;
-  p.shift = reinterpret_cast<const float*>(m.dbuf + m.off_shift);
-  p.scale = reinterpret_cast<const float*>(m.dbuf + m.off_scale);
+  p.shift = reinterpret_cast<const float*>(img + m.off_shift);
+  p.scale = reinterpret_cast<const float*>(img + m.off_scale);
   KernelEntry* ke = find_kernel(m.K0P, m.H, m.NL);
   if (!ke) return fail(ctx, FLERN_E_UNSUPPORTED, "no kernel for model '%s'", m.name.c_str());
 
@@ -593,6 +701,15 @@ extern "C" FLERN_API flern_status flern_run_query(flern_ctx* ctx, const flern_qu
     else if ((st = temp(nwords * 4, (void**)&d_sel)) != FLERN_OK) return st;
     CUDA_TRY(ctx, cudaMemsetAsync(d_sel, 0, nwords * 4, ctx->stream));
   }
+  unsigned long long* d_trace = nullptr;
+  const size_t trace_bytes = (size_t)kTraceEvents * kTraceTiles * 8;
+  static_assert(kTraceEvents == FLERN_TRACE_EVENTS, "trace events");
+  if (res->dbg_trace) {
+    if (dev_out) d_trace = reinterpret_cast<unsigned long long*>(res->dbg_trace);
+    else if ((st = temp(trace_bytes, (void**)&d_trace)) != FLERN_OK) return st;
+    CUDA_TRY(ctx, cudaMemsetAsync(d_trace, 0, trace_bytes, ctx->stream));
+  }
+  p.dbg_trace = d_trace;
   p.dbg_score = d_score;
   p.dbg_match = d_match;
   p.dbg_selected = d_sel;
@@ -608,8 +725,27 @@ extern "C" FLERN_API flern_status flern_run_query(flern_ctx* ctx, const flern_qu
     ke->attr_set = true;
   }
   if (!async) CUDA_TRY(ctx, cudaEventRecord(ctx->ev0, ctx->stream));
-  ke->fn<<<grid, kThreads, ke->smem, ctx->stream>>>(p);
-  CUDA_TRY(ctx, cudaGetLastError());
+  {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = ke->smem;
+    cfg.stream = ctx->stream;
+    cudaLaunchAttribute attr[1];
+    const HashTable& h0 = ctx->hts[q->probes[0].ht_id];
+    if (ctx->persist_max > 0 && ctx->window_max > 0 && !getenv("FLERN_NO_L2_WINDOW")) {   // build side persists in L2
+      attr[0].id = cudaLaunchAttributeAccessPolicyWindow;
+      attr[0].val.accessPolicyWindow.base_ptr = h0.slots;
+      attr[0].val.accessPolicyWindow.num_bytes = std::min(h0.bytes, ctx->window_max);
+      attr[0].val.accessPolicyWindow.hitRatio =
+          (float)std::min(1.0, (double)ctx->persist_max / (double)std::min(h0.bytes, ctx->window_max));
+      attr[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+      attr[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+    }
+    CUDA_TRY(ctx, cudaLaunchKernelEx(&cfg, ke->fn, p));
+  }
   if (async) return FLERN_OK;
   CUDA_TRY(ctx, cudaEventRecord(ctx->ev1, ctx->stream));
   int64_t hres[4 * kMaxGroups + kCounters];
@@ -622,6 +758,8 @@ extern "C" FLERN_API flern_status flern_run_query(flern_ctx* ctx, const flern_qu
       CUDA_TRY(ctx, cudaMemcpyAsync(res->dbg_match, d_match, n * q->nprobes * 4, cudaMemcpyDeviceToHost, ctx->stream));
     if (res->dbg_selected)
       CUDA_TRY(ctx, cudaMemcpyAsync(res->dbg_selected, d_sel, nwords * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    if (res->dbg_trace)
+      CUDA_TRY(ctx, cudaMemcpyAsync(res->dbg_trace, d_trace, trace_bytes, cudaMemcpyDeviceToHost, ctx->stream));
   }
   CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
   for (void* v : temps) cudaFree(v);

@@ -10,14 +10,15 @@
 // producer writing the joined row's features straight into the MMA operand tile (no HBM
 // intermediate). GROUP BY COUNT/SUM follows P:1346-1354.
 //
-// Warp roles (512 threads, 1 CTA per SM):
-//   warps 0-3  producers: 128 threads x ROWS rows per batch; scan, filter, probe, compact,
-//              gather+normalise+bf16 into X stage ring (S stages of 128 rows), row metadata
-//   warp  4    TMEM allocator + single-thread tcgen05.mma issuer
-//   warps 5-7  idle
-//   warps 8-15 epilogue: two warpgroups, each owns half of the hidden columns; TMEM -> regs ->
-//              bias+ReLU+bf16 -> SMEM (next layer's A operand) or bias+ReLU+dot(w_out) -> logit;
-//              warpgroup 0 then applies the predicate and aggregates.
+// Warp roles (416 threads = 13 warps, 1 CTA per SM):
+//   warps 0-3   producers: 128 threads x R consecutive rows per batch; scan, pre-filter, probe,
+//               compact, gather + normalise + bf16 into the X stage ring (S stages of 128 rows)
+//   warps 4-7   epilogue warpgroup 0 (NL=2): D1 -> bias + ReLU -> bf16 -> H (layer-2 operand),
+//               handed to the MMA in 64-column K-chunks
+//   warps 8-11  epilogue warpgroup 1: D2 -> bias + ReLU -> dot(w_out) -> logit -> predicate ->
+//               group-by (NL=1: both warpgroups do this on alternate tiles)
+//   warp  12    TMEM allocator + single-thread tcgen05.mma issuer
+// An epilogue warp w may only touch TMEM lanes 32*(w%4) .. +31, hence warpgroup-aligned roles.
 #pragma once
 #include "sm100.cuh"
 
@@ -27,21 +28,32 @@ constexpr int kMaxFeat = 48;
 constexpr int kMaxGroups = 64;
 constexpr int kMaxProbes = 2;
 constexpr int kTile = 128;
-constexpr int kThreads = 512;
+constexpr int kThreads = 416;   // 13 warps: producers 0-3, epilogue WG0 4-7, WG1 8-11, MMA 12
 constexpr int kProducerThreads = 128;
-// rows per producer thread per batch: 2 for narrow inputs (register budget)
+// consecutive fact rows per producer thread per batch (one 16/8/4-byte vector load per column);
+// fewer for wide inputs (register budget: R * K0P/2 packed bf16 pairs stay live)
 __host__ __device__ constexpr int rows_per_thread(int K0P) { return K0P <= 16 ? 2 : 1; }
 __host__ __device__ constexpr int batch_rows(int K0P) { return kProducerThreads * rows_per_thread(K0P); }
 constexpr int32_t kEmptyKey = (int32_t)0x80000000;         // INT32_MIN marks an empty slot
 constexpr int kCounters = 4;                               // scanned, joined(=scored), selected, bad_group
 
-__host__ __device__ constexpr uint32_t hash_key(int32_t key, uint32_t shift) {
-  return ((uint32_t)key * 0x9E3779B1u) >> shift;  // Fibonacci hashing, top log2(capacity) bits
+// Slot of `key`: mode 1 = order-preserving range hash (kmin..kmax spread linearly over the
+// capacity: consecutive keys land in neighbouring slots, so a fact table clustered by the join key
+// probes the table almost sequentially); mode 0 = Fibonacci hashing (top log2(capacity) bits).
+struct HashFn {
+  uint32_t mode, shift, mask, mulc;
+  int32_t kmin;
+};
+__host__ __device__ __forceinline__ uint32_t hash_slot(int32_t key, const HashFn& f) {
+  if (f.mode)
+    return (uint32_t)(((uint64_t)((uint32_t)key - (uint32_t)f.kmin) * (uint64_t)f.mulc) >> 32) & f.mask;
+  return ((uint32_t)key * 0x9E3779B1u) >> f.shift;
 }
 
 struct ProbeDesc {
   const int2* slots;        // {key, build row}, capacity = mask + 1
-  uint32_t mask, shift;     // shift = 32 - log2(capacity)
+  HashFn hf;
+  uint32_t mask;
   const int32_t* payload;   // row-major [build rows][pstride]
   int32_t pstride;
   int32_t src;              // -1: key from fact column `fact_key`; p: payload word `key_word` of probe p
@@ -54,6 +66,7 @@ struct ColDesc {            // a column reference resolved to base pointer + row
   int32_t stride;           // 1 for a fact column, the payload row stride otherwise
   int32_t src;              // 0 = fact row, 1 + p = build row of probe p
   int32_t is_float;
+  int32_t word;             // payload word (src > 0)
 };
 
 struct QueryParams {
@@ -64,7 +77,14 @@ struct QueryParams {
   const int32_t* pf_col;    // nullptr = no pre-filter
   int64_t pf_lo, pf_hi;
   int32_t nfeat;
+  int32_t nfact;            // features [0, nfact) are fact columns, [nfact, nfeat) build payload words
   ColDesc feat[kMaxFeat];
+  // compact views of feat[] for the producer's hot loop
+  const int32_t* fcol[kMaxFeat];   // fact column of feature k (k < nfact), else any valid pointer
+  int32_t dword[kMaxFeat];         // payload word of feature k (k >= nfact)
+  uint64_t dprobe1;                // bit k: feature k comes from probe 1's payload (else probe 0)
+  uint64_t fmask;                  // bit k: feature k is float32 (else int32)
+  const int32_t* dummy;            // 64 zero bytes: target of loads whose value is not needed
   ColDesc grp, sum;
   int32_t ngroups;
   int32_t both_classes;
@@ -74,7 +94,7 @@ struct QueryParams {
   const float* bias;        // [NL][H]
   const float* wout;        // [H]
   float bout;
-  const float* shift;       // [K0P]
+  const float* shift;       // [K0P]  c_k = -shift_k * scale_k (the gather computes fma(x, scale, c))
   const float* scale;       // [K0P]
   int64_t* partials;        // [gridDim.x][ngroups*4 + kCounters]
   unsigned int* ticket;     // zero between launches (the last CTA resets it)
@@ -84,7 +104,23 @@ struct QueryParams {
   float* dbg_score;         // optional
   int32_t* dbg_match;       // optional [nrows * nprobes]
   uint32_t* dbg_selected;   // optional bitmap
+  unsigned long long* dbg_trace;  // optional [kTraceEvents][kTraceTiles] clock64 stamps of CTA 0
 };
+
+// Pipeline trace (diagnostic): clock64() at each hand-off, CTA 0, first kTraceTiles tiles/batches.
+constexpr int kTraceTiles = 256;
+enum TraceEv {
+  TR_MMA_D2A_FREE, TR_MMA_L2A_DONE, TR_MMA_NEXT_READY, TR_MMA_L1_ISSUED, TR_MMA_D2B_FREE, TR_MMA_L2B_ISSUED,
+  TR_W0_FULL, TR_W0_D1FULL, TR_W0_HFREE0, TR_W0_DONE,
+  TR_W1_FULL, TR_W1_DFULL0, TR_W1_DOTA, TR_W1_DFULL1, TR_W1_DOTB, TR_W1_AGG,
+  TR_P_START, TR_P_PROBED, TR_P_GATHERED, TR_P_DONE,
+  kTraceEvents
+};
+#define FLERN_TRACE(ev, idx)                                                           \
+  do {                                                                                 \
+    if (p.dbg_trace && blockIdx.x == 0 && (idx) < kTraceTiles)                         \
+      p.dbg_trace[(ev) * kTraceTiles + (idx)] = (unsigned long long)clock64();         \
+  } while (0)
 
 // Shared-memory plan (byte offsets from a 1024-aligned base), identical on host and device.
 template <int K0P, int H, int NL>
@@ -168,9 +204,12 @@ __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_c
     for (uint32_t i = tid; i < P::wimg_bytes / 16; i += kThreads) dst[i] = ldg_nc(src + i);
     for (int i = tid; i < NL * H; i += kThreads) s_bias[i] = p.bias[i];
     for (int i = tid; i < H; i += kThreads) s_wout[i] = p.wout[i];
-    for (int i = tid; i < kMaxFeat; i += kThreads) {
-      s_shift[i] = i < K0P ? p.shift[i] : 0.f;
-      s_scale[i] = i < K0P ? p.scale[i] : 0.f;
+    for (int i = tid; i < kMaxFeat / 2; i += kThreads) {   // {scale_k, scale_k+1, c_k, c_k+1} per pair
+      const int k = 2 * i;
+      s_shift[4 * i + 0] = k < K0P ? p.scale[k] : 0.f;
+      s_shift[4 * i + 1] = k + 1 < K0P ? p.scale[k + 1] : 0.f;
+      s_shift[4 * i + 2] = k < K0P ? p.shift[k] : 0.f;
+      s_shift[4 * i + 3] = k + 1 < K0P ? p.shift[k + 1] : 0.f;
     }
     for (int i = tid; i < kMaxGroups * 4; i += kThreads) acc[i] = 0ull;
     if (tid < kCounters) s_cnt[tid] = 0;
@@ -186,7 +225,7 @@ __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_c
     fence_mbar_init();
   }
   constexpr uint32_t kTmemCols = 2 * H <= 32 ? 32 : (2 * H <= 64 ? 64 : (2 * H <= 128 ? 128 : (2 * H <= 256 ? 256 : 512)));
-  if (warp == 4) { tmem_alloc(tmem_slot, kTmemCols); tmem_relinquish(); }
+  if (warp == 12) { tmem_alloc(tmem_slot, kTmemCols); tmem_relinquish(); }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -197,6 +236,8 @@ __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_c
 
   if (warp < 4) {
     // =============================== PRODUCERS =============================================
+    // Each thread owns R consecutive fact rows of a 128*R-row batch: every fact column is read
+    // with one R-wide vector load per thread (coalesced, 16 B per lane for R = 4).
     constexpr int R = rows_per_thread(K0P);
     constexpr int kBatch = batch_rows(K0P);
     const int t = tid;                   // 0..127
@@ -205,77 +246,160 @@ __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_c
     int fill = 0;                        // rows already in `stage`
     int64_t n_joined = 0;
     int buf = 0;
+    // Loads are plain read-only loads whose ADDRESS is selected (a 64-byte zero dummy when the
+    // value is not needed): no predicates, no branches, so the compiler issues a batch's loads
+    // back to back and they overlap; the dummy stays in L1.
+    const int32_t* dz = p.dummy;
+    auto ld4 = [&](const int32_t* col, int64_t row0, bool need) -> int4 {
+      return ldg_nc(reinterpret_cast<const int4*>(need ? col + row0 : dz));
+    };
+    auto ld2 = [&](const int32_t* col, int64_t row0, bool need) -> int2 {
+      return ldg_nc(reinterpret_cast<const int2*>(need ? col + row0 : dz));
+    };
+    auto ld1 = [&](const int32_t* ptr, bool need) -> int32_t { return ldg_nc(need ? ptr : dz); };
+    // R rows of a column starting at row0 (vector path; the scalar tail handles a partial group)
+    auto loadR = [&](const int32_t* col, int64_t row0, bool whole, bool need, int32_t (&v)[R]) {
+      if (R == 1 || whole) {
+        if constexpr (R == 4) {
+          const int4 x = ld4(col, row0, need);
+          v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
+        } else if constexpr (R == 2) {
+          const int2 x = ld2(col, row0, need);
+          v[0] = x.x; v[1] = x.y;
+        } else {
+          v[0] = ld1(col + row0, need);
+        }
+      } else {
+#pragma unroll
+        for (int r = 0; r < R; ++r) v[r] = ld1(col + row0 + r, need && row0 + r < row_end);
+      }
+    };
+    const float4* s_norm = reinterpret_cast<const float4*>(s_shift);
+    auto cvt_pair = [&](int k, int32_t a, int32_t b) -> uint32_t {   // normalise + bf16-pack features k, k+1
+      const float4 nm = s_norm[k / 2];
+      const float fa = ((p.fmask >> k) & 1) ? __int_as_float(a) : (float)a;
+      const float fb = ((p.fmask >> (k + 1)) & 1) ? __int_as_float(b) : (float)b;
+      const float2 y = fma2(make_float2(fa, fb), make_float2(nm.x, nm.y), make_float2(nm.z, nm.w));
+      return bf16x2(y.x, y.y);
+    };
     mbar_wait(&empty[0], ((acq / S) & 1) ^ 1, 1);   // acquire the first stage
     acq = 1;
     for (int64_t base = row_begin; base < row_end; base += kBatch) {
-      int64_t row[R];
+      const int bidx = (int)((base - row_begin) / kBatch);
+      if (t == 0) FLERN_TRACE(TR_P_START, bidx);
+      const int64_t row0 = base + (int64_t)R * t;
+      const bool whole = row0 + R <= row_end;
       bool valid[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) valid[r] = row0 + r < row_end;
+      if (p.pf_col) {   // pre-filter on a fact column (config 4): before anything else
+        int32_t x[R];
+        loadR(p.pf_col, row0, whole, true, x);
+#pragma unroll
+        for (int r = 0; r < R; ++r) valid[r] = valid[r] && (p.pf_lo <= x[r]) && (x[r] < p.pf_hi);
+      }
+      bool any = false;
+#pragma unroll
+      for (int r = 0; r < R; ++r) any |= valid[r];
+      // 1. fact-side loads, all issued before any use: probe key, group/sum, features [0, nfact)
+      int32_t key[R], gv[R], sv[R];
+      int32_t v[K0P][R];
+      loadR(p.probe[0].fact_key, row0, whole, any, key);
+      loadR(p.grp.base, row0, whole, any && p.grp.src == 0, gv);
+      loadR(p.sum.base, row0, whole, any && p.sum.src == 0, sv);
+#pragma unroll
+      for (int k = 0; k < K0P; ++k) loadR(p.fcol[k], row0, whole, any && k < p.nfact, v[k]);
+      // 2. probes, bucketised linear probing: the aligned 4-slot bucket (a 32-byte
+      //    sector) holding the home slot is read with two 16-byte loads and resolved with selects;
+      //    only a row that meets neither its key nor an empty slot there continues (rare, warp-
+      //    uniform slow path); a miss drops the row
       int32_t brow[R][kMaxProbes];
-      int32_t v[R][K0P];
-      int32_t gv[R], sv[R], key[R];
-#pragma unroll
-      for (int r = 0; r < R; ++r) {
-        row[r] = base + r * kProducerThreads + t;
-        valid[r] = row[r] < row_end;
-        if (p.pf_col && valid[r]) {   // pre-filter on a fact column (config 4): before anything else
-          const int64_t x = ldg_nc(p.pf_col + row[r]);
-          valid[r] = (p.pf_lo <= x) && (x < p.pf_hi);
-        }
-      }
-      // fact-side loads of surviving rows, all independent: probe key, fact features, group/sum.
-      // Issued before the probe so their latency overlaps the probe's dependent loads.
-#pragma unroll
-      for (int r = 0; r < R; ++r) {
-        key[r] = valid[r] ? ldg_nc(p.probe[0].fact_key + row[r]) : 0;
-#pragma unroll
-        for (int k = 0; k < K0P; ++k) {
-          v[r][k] = 0;
-          if (k < p.nfeat && p.feat[k].src == 0 && valid[r]) v[r][k] = ldg_nc(p.feat[k].base + row[r]);
-        }
-        gv[r] = (p.grp.src == 0 && valid[r]) ? ldg_nc(p.grp.base + row[r]) : 0;
-        sv[r] = (p.sum.src == 0 && valid[r]) ? ldg_nc(p.sum.base + row[r]) : 0;
-      }
-      // probes: linear probing until the key or an empty slot; a miss drops the row
 #pragma unroll
       for (int q = 0; q < kMaxProbes; ++q) {
-        if (q >= p.nprobes) break;
+#pragma unroll
+        for (int r = 0; r < R; ++r) brow[r][q] = -1;
+        if (q >= p.nprobes) continue;
         const ProbeDesc& pd = p.probe[q];
+        int32_t kq[R];
+        uint32_t h[R];
+        int4 wa[R], wb[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r)   // probe 1 is keyed by a payload word of probe 0's build row
+          kq[r] = q == 0 ? key[r]
+                         : ld1(p.probe[0].payload + (int64_t)(valid[r] ? brow[r][0] : 0) * p.probe[0].pstride +
+                                   pd.key_word, valid[r]);
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-          brow[r][q] = -1;
-          if (!valid[r]) continue;
-          // probe 0 is keyed by a fact column; probe 1 by a payload word of probe 0's build row
-          const int32_t k = q == 0 ? key[r]
-                                   : ldg_nc(p.probe[0].payload + (int64_t)brow[r][0] * p.probe[0].pstride + pd.key_word);
-          uint32_t h = hash_key(k, pd.shift);
-          while (true) {
-            const int2 sl = ldg_nc(pd.slots + h);
-            if (sl.x == k) { brow[r][q] = sl.y; break; }
-            if (sl.x == kEmptyKey) break;
-            h = (h + 1) & pd.mask;
+          h[r] = hash_slot(kq[r], pd.hf);
+          const int4* bk = reinterpret_cast<const int4*>(valid[r] ? pd.slots + (h[r] & ~3u) : (const int2*)dz);
+          wa[r] = ldg_nc(bk);
+          wb[r] = ldg_nc(bk + 1);
+        }
+        bool undecided = false;
+        int res[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const uint32_t f = h[r] & 3u;
+          const int32_t sk[4] = {wa[r].x, wa[r].z, wb[r].x, wb[r].z};
+          const int32_t sr[4] = {wa[r].y, wa[r].w, wb[r].y, wb[r].w};
+          res[r] = -2;
+#pragma unroll
+          for (int j = 3; j >= 0; --j) {   // first qualifying slot wins: scan backwards with selects
+            const bool act = (uint32_t)j >= f;
+            res[r] = (act && sk[j] == kq[r]) ? sr[j] : ((act && sk[j] == kEmptyKey) ? -1 : res[r]);
           }
-          valid[r] = brow[r][q] >= 0;
+          if (!valid[r]) res[r] = -1;
+          undecided |= res[r] == -2;
+        }
+        if (__any_sync(0xffffffffu, undecided)) {
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+            uint32_t g = h[r] & ~3u;
+            while (res[r] == -2) {
+              g = (g + 4) & pd.mask;
+              const int4 x = ldg_nc(reinterpret_cast<const int4*>(pd.slots + g));
+              const int4 y = ldg_nc(reinterpret_cast<const int4*>(pd.slots + g) + 1);
+              const int32_t sk[4] = {x.x, x.z, y.x, y.z};
+              const int32_t sr[4] = {x.y, x.w, y.y, y.w};
+#pragma unroll
+              for (int j = 3; j >= 0; --j)
+                res[r] = sk[j] == kq[r] ? sr[j] : (sk[j] == kEmptyKey ? -1 : res[r]);
+            }
+          }
+        }
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          brow[r][q] = res[r];
+          valid[r] = res[r] >= 0;
         }
       }
+      if (t == 0) FLERN_TRACE(TR_P_PROBED, bidx);
       if (p.dbg_match) {
 #pragma unroll
         for (int r = 0; r < R; ++r)
-          if (row[r] < row_end)
-            for (int q = 0; q < p.nprobes; ++q) p.dbg_match[row[r] * p.nprobes + q] = brow[r][q];
+          if (row0 + r < row_end)
+            for (int q = 0; q < p.nprobes; ++q) p.dbg_match[(row0 + r) * p.nprobes + q] = brow[r][q];
       }
-      // dimension-side loads (payload rows of the matched build rows), all independent
+      // 3. build-side loads (payload words of the matched rows), all issued before any use
 #pragma unroll
       for (int r = 0; r < R; ++r) {
-        const int32_t b0 = brow[r][0], b1 = p.nprobes > 1 ? brow[r][1] : 0;
+        const int64_t b0 = valid[r] ? brow[r][0] : 0;
+        const int64_t b1 = (valid[r] && p.nprobes > 1) ? brow[r][1] : 0;
+        const int32_t* rb0 = p.probe[0].payload + b0 * p.probe[0].pstride;
+        const int32_t* rb1 = p.probe[1].payload + b1 * p.probe[1].pstride;
+        if (p.grp.src > 0) gv[r] = ld1((p.grp.src == 1 ? rb0 : rb1) + p.grp.word, valid[r]);
+        if (p.sum.src > 0) sv[r] = ld1((p.sum.src == 1 ? rb0 : rb1) + p.sum.word, valid[r]);
 #pragma unroll
-        for (int k = 0; k < K0P; ++k) {
-          const int fs = p.feat[k].src;
-          if (k < p.nfeat && fs > 0 && valid[r])
-            v[r][k] = ldg_nc(p.feat[k].base + (int64_t)(fs == 1 ? b0 : b1) * p.feat[k].stride);
-        }
-        if (p.grp.src > 0 && valid[r]) gv[r] = ldg_nc(p.grp.base + (int64_t)(p.grp.src == 1 ? b0 : b1) * p.grp.stride);
-        if (p.sum.src > 0 && valid[r]) sv[r] = ldg_nc(p.sum.base + (int64_t)(p.sum.src == 1 ? b0 : b1) * p.sum.stride);
+        for (int k = 0; k < K0P; ++k)
+          if (k >= p.nfact && k < p.nfeat) v[k][r] = ld1((((p.dprobe1 >> k) & 1) ? rb1 : rb0) + p.dword[k], valid[r]);
       }
+      // 4. normalise in fp32 (fma(x, scale, -shift*scale), reading Q4) -> packed bf16 pairs
+      uint32_t pk[R][K0P / 2];
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+#pragma unroll
+        for (int k = 0; k < K0P; k += 2) pk[r][k / 2] = cvt_pair(k, v[k][r], v[k + 1][r]);
+      if (t == 0) FLERN_TRACE(TR_P_GATHERED, bidx);
       // compaction: position of each surviving row in the batch (warp scan + per-warp counts)
       int my_cnt = 0;
 #pragma unroll
@@ -318,25 +442,12 @@ __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_c
           const int mypos = pos++;
           if (mypos / kTile != seg) continue;
           const int tp = mypos % kTile;
-          // normalise (fp32, two separately rounded ops: reading Q4) -> bf16 -> X tile
-          uint32_t packed[K0P / 2];
-#pragma unroll
-          for (int k = 0; k < K0P; k += 2) {
-            float f[2];
-#pragma unroll
-            for (int u = 0; u < 2; ++u) {
-              const int kk = k + u;
-              const float x = p.feat[kk].is_float ? __int_as_float(v[r][kk]) : (float)v[r][kk];
-              f[u] = kk < p.nfeat ? __fmul_rn(__fsub_rn(x, s_shift[kk]), s_scale[kk]) : 0.f;
-            }
-            packed[k / 2] = bf16x2(f[0], f[1]);
-          }
           // interleaved K-major layout: (k/8)*2048 + (row/8)*128 + (row%8)*16
 #pragma unroll
           for (int c8 = 0; c8 < K0P / 8; ++c8)
-            st_shared_v4(smem_u32(xs + c8 * (kTile * 16) + (tp >> 3) * 128 + (tp & 7) * 16), packed[4 * c8],
-                         packed[4 * c8 + 1], packed[4 * c8 + 2], packed[4 * c8 + 3]);
-          m.rowid[tp] = (int32_t)row[r];
+            st_shared_v4(smem_u32(xs + c8 * (kTile * 16) + (tp >> 3) * 128 + (tp & 7) * 16), pk[r][4 * c8],
+                         pk[r][4 * c8 + 1], pk[r][4 * c8 + 2], pk[r][4 * c8 + 3]);
+          m.rowid[tp] = (int32_t)(row0 + r);
           m.grp[tp] = (gv[r] >= 0 && gv[r] < p.ngroups) ? (uint8_t)gv[r] : (uint8_t)255;
           m.val[tp] = sv[r];
         }
@@ -346,6 +457,7 @@ __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_c
           mbar_arrive(&full[ts]);
         }
       }
+      if (t == 0) FLERN_TRACE(TR_P_DONE, bidx);
       stage = (stage + end / kTile) % S;
       fill = end % kTile;
       if (end > 0 && fill == 0) {   // every touched stage was published: acquire a fresh one
@@ -374,7 +486,7 @@ __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_c
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) nj += __shfl_down_sync(0xffffffffu, nj, o);
     if (lane == 0) atomicAdd(reinterpret_cast<unsigned long long*>(&s_cnt[1]), (unsigned long long)nj);
-  } else if (warp == 4) {
+  } else if (warp == 12) {
     // =============================== MMA ISSUER =============================================
     // NL == 2 issue order per tile t (steady state): L2a(t), L1(t+1), L2b(t). Layer 2 is split
     // into two N-halves (D2a, D2b) so warpgroup 1 drains one half while the other is computed,
@@ -418,8 +530,10 @@ __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_c
           mma_commit(d1full);
           for (uint32_t t = 0;; ++t) {
             mbar_wait(&dempty[0], (t & 1) ^ 1, 13);
+            FLERN_TRACE(TR_MMA_D2A_FREE, t);
             tc_fence_after();
             issue_l2_half(0, t);
+            FLERN_TRACE(TR_MMA_L2A_DONE, t);
             // L1(t+1) goes between the two halves when tile t+1 is already published (so that
             // warpgroup 0 converts it while L2b(t) runs); otherwise after L2b(t) (never block the
             // tile in flight on the producer)
@@ -428,18 +542,22 @@ __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_c
             bool have_next = mbar_test_wait(&full[s1], ph1);
             bool next = false;
             auto do_next = [&]() {
+              FLERN_TRACE(TR_MMA_NEXT_READY, t);
               next = *meta_of<K0P, H, NL>(smem, s1).count >= 0;
               if (next) {
                 mbar_wait(d1empty, ((t + 1) & 1) ^ 1, 11);
                 tc_fence_after();
                 issue_l1(s1, 0);
                 mma_commit(d1full);
+                FLERN_TRACE(TR_MMA_L1_ISSUED, t);
               }
             };
             if (have_next) do_next();
             mbar_wait(&dempty[1], (t & 1) ^ 1, 14);
+            FLERN_TRACE(TR_MMA_D2B_FREE, t);
             tc_fence_after();
             issue_l2_half(1, t);
+            FLERN_TRACE(TR_MMA_L2B_ISSUED, t);
             if (!have_next) {
               mbar_wait(&full[s1], ph1, 10);
               do_next();
@@ -462,13 +580,15 @@ __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_c
       }
     }
     __syncwarp();
-  } else if (warp >= 8) {
-    // =============================== EPILOGUE =============================================
-    const int wg = (warp - 8) >> 2;         // warpgroup 0 / 1
+  } else {
+    // =============================== EPILOGUE (warps 4-11) =============================================
+    const int wg = (warp - 4) >> 2;         // warpgroup 0 / 1
     const int q = warp & 3;                 // TMEM lane quadrant (warp id % 4)
     const int r = q * 32 + lane;            // tile row owned by this thread
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
 
+    // per-warp group-by accumulators in registers: lane l owns groups l and l+32, both classes
+    unsigned long long ac[2][2] = {{0ull, 0ull}, {0ull, 0ull}}, as[2][2] = {{0ull, 0ull}, {0ull, 0ull}};
     // predicate + group-by of one tile's rows, then release the X stage (warpgroup-wide)
     auto finish_tile = [&](const Meta& m, int count, int s, float logit) {
       const bool valid = r < count;
@@ -478,6 +598,8 @@ __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_c
       if (valid && g == 255) atomicAdd(reinterpret_cast<unsigned long long*>(&s_cnt[3]), 1ull);
       if (p.dbg_score && valid) p.dbg_score[m.rowid[r]] = 1.f / (1.f + __expf(-logit));
       if (p.dbg_selected && sel) atomicOr(p.dbg_selected + (m.rowid[r] >> 5), 1u << (m.rowid[r] & 31));
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);   // metadata read: the stage can be refilled
       // warp-level group-by: per present (group, class), popc(ballot) rows and a split 16-bit sum
       const int cls = sel ? 0 : 1;
       const bool agg = valid && g != 255 && (sel || p.both_classes);
@@ -490,25 +612,58 @@ __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_c
         const uint32_t mm = __ballot_sync(0xffffffffu, mine);
         const int lo = __reduce_add_sync(0xffffffffu, mine ? (val & 0xFFFF) : 0);
         const int hi = __reduce_add_sync(0xffffffffu, mine ? (val >> 16) : 0);
-        if (lane == leader) {
-          atomicAdd(&acc[lg * 4 + lc * 2 + 0], (unsigned long long)__popc(mm));
-          atomicAdd(&acc[lg * 4 + lc * 2 + 1], (unsigned long long)((long long)hi * 65536ll + (long long)lo));
+        if (lane == (lg & 31)) {
+          const unsigned long long dc = (unsigned long long)__popc(mm);
+          const unsigned long long ds = (unsigned long long)((long long)hi * 65536ll + (long long)lo);
+          const bool up = lg >= 32;
+          if (!up && lc == 0) { ac[0][0] += dc; as[0][0] += ds; }
+          if (!up && lc == 1) { ac[0][1] += dc; as[0][1] += ds; }
+          if (up && lc == 0) { ac[1][0] += dc; as[1][0] += ds; }
+          if (up && lc == 1) { ac[1][1] += dc; as[1][1] += ds; }
         }
         pending &= ~mm;
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);   // stage (X + metadata) can be refilled
     };
-    // relu(D + b) . w_out over `ncols` TMEM columns starting at `col` (bias/w offset `boff`)
-    auto dot_cols = [&](uint32_t col, int ncols, int boff, float (&pa)[4]) {
-#pragma unroll 1
-      for (int c0 = 0; c0 < ncols; c0 += 32) {
-        uint32_t v[32];
-        tmem_ld32(tmem_base + lane_off + col + c0, v);
+    auto flush_acc = [&]() {
 #pragma unroll
-        for (int i = 0; i < 32; ++i)
-          pa[i & 3] = fmaf(fmaxf(__uint_as_float(v[i]) + s_bias[boff + c0 + i], 0.f), s_wout[c0 + i + (boff % H)],
-                           pa[i & 3]);
+      for (int u = 0; u < 2; ++u) {
+        const int g = lane + 32 * u;
+        if (g < p.ngroups) {
+#pragma unroll
+          for (int c = 0; c < 2; ++c) {
+            if (ac[u][c]) atomicAdd(&acc[g * 4 + c * 2 + 0], ac[u][c]);
+            if (as[u][c]) atomicAdd(&acc[g * 4 + c * 2 + 1], as[u][c]);
+          }
+        }
+      }
+    };
+    // relu(D + b) . w_out over `ncols` TMEM columns at `col`; bias/w_out of neuron j at
+    // s_bias[boff + j], s_wout[woff + j]. TMEM loads are double-buffered: chunk c+1 is in flight
+    // while chunk c is reduced (packed fp32x2 add / fma).
+    auto dot_cols = [&](uint32_t col, int ncols, int boff, int woff, float2& acc2a, float2& acc2b) {
+      uint32_t v[2][32];
+      tmem_ld32_async(tmem_base + lane_off + col, v[0]);
+      tmem_ld_wait(v[0]);
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {   // up to 8 chunks of 32 columns (H <= 256)
+        if (c * 32 >= ncols) break;
+        const int cur = c & 1;
+        if ((c + 1) * 32 < ncols) tmem_ld32_async(tmem_base + lane_off + col + (c + 1) * 32, v[cur ^ 1]);
+        const float4* b4 = reinterpret_cast<const float4*>(s_bias + boff + c * 32);
+        const float4* w4 = reinterpret_cast<const float4*>(s_wout + woff + c * 32);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const float4 b = b4[i], w = w4[i];
+          float2 z0 = add2(make_float2(__uint_as_float(v[cur][4 * i]), __uint_as_float(v[cur][4 * i + 1])),
+                           make_float2(b.x, b.y));
+          float2 z1 = add2(make_float2(__uint_as_float(v[cur][4 * i + 2]), __uint_as_float(v[cur][4 * i + 3])),
+                           make_float2(b.z, b.w));
+          z0.x = fmaxf(z0.x, 0.f); z0.y = fmaxf(z0.y, 0.f);
+          z1.x = fmaxf(z1.x, 0.f); z1.y = fmaxf(z1.y, 0.f);
+          acc2a = fma2(z0, make_float2(w.x, w.y), acc2a);
+          acc2b = fma2(z1, make_float2(w.z, w.w), acc2b);
+        }
+        if ((c + 1) * 32 < ncols) tmem_ld_wait(v[cur ^ 1]);
       }
     };
 
@@ -521,7 +676,9 @@ __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_c
           const int s = t % S;
           mbar_wait(&full[s], (t / S) & 1, 20);
           if (*meta_of<K0P, H, NL>(smem, s).count < 0) break;
+          if (tid == 128) FLERN_TRACE(TR_W0_FULL, t);
           mbar_wait(d1full, t & 1, 21);
+          if (tid == 128) FLERN_TRACE(TR_W0_D1FULL, t);
           tc_fence_after();
           for (int c = 0; c < NC; ++c) {
             uint32_t pk[32];
@@ -530,10 +687,17 @@ __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_c
               uint32_t v[32];
               const int c0 = c * 64 + j * 32;
               tmem_ld32(tmem_base + lane_off + c0, v);
+              const float4* b4 = reinterpret_cast<const float4*>(s_bias + c0);
 #pragma unroll
-              for (int i = 0; i < 16; ++i)
-                pk[j * 16 + i] = relu_bf16x2(__uint_as_float(v[2 * i]) + s_bias[c0 + 2 * i],
-                                             __uint_as_float(v[2 * i + 1]) + s_bias[c0 + 2 * i + 1]);
+              for (int i = 0; i < 8; ++i) {
+                const float4 b = b4[i];
+                const float2 z0 = add2(make_float2(__uint_as_float(v[4 * i]), __uint_as_float(v[4 * i + 1])),
+                                       make_float2(b.x, b.y));
+                const float2 z1 = add2(make_float2(__uint_as_float(v[4 * i + 2]), __uint_as_float(v[4 * i + 3])),
+                                       make_float2(b.z, b.w));
+                pk[j * 16 + 2 * i] = relu_bf16x2(z0.x, z0.y);
+                pk[j * 16 + 2 * i + 1] = relu_bf16x2(z1.x, z1.y);
+              }
             }
             if (c == NC - 1) {   // all of D1 is in registers: the MMA may overwrite it
               tc_fence_before();
@@ -541,6 +705,7 @@ __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_c
               if (lane == 0) mbar_arrive(d1empty);
             }
             mbar_wait(&hfree[c], (t & 1) ^ 1, 22);   // L2b(t-1) finished reading chunk c
+            if (tid == 128 && c == 0) FLERN_TRACE(TR_W0_HFREE0, t);
             const uint32_t rowbase = hb + c * (kTile * 128) + (r >> 3) * 1024 + (r & 7) * 128;
 #pragma unroll
             for (int jj = 0; jj < 8; ++jj)   // 128B swizzle: chunk jj of the row goes to jj ^ (row % 8)
@@ -550,6 +715,7 @@ __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_c
             __syncwarp();
             if (lane == 0) mbar_arrive(&hfull[c]);
           }
+          if (tid == 128) FLERN_TRACE(TR_W0_DONE, t);
         }
       } else {
         // ---- warpgroup 1: logit = relu(D2 + b2) . w_out + b_out, predicate, group-by ----
@@ -559,22 +725,27 @@ __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_c
           const Meta m = meta_of<K0P, H, NL>(smem, s);
           const int count = *m.count;
           if (count < 0) break;
+          if (tid == 256) FLERN_TRACE(TR_W1_FULL, t);
           float logit = 0.f;
           if (!p.no_model) {
-            float pa[4] = {0.f, 0.f, 0.f, 0.f};
+            float2 pa = make_float2(0.f, 0.f), pb = make_float2(0.f, 0.f);
 #pragma unroll 1
             for (int h = 0; h < 2; ++h) {
               mbar_wait(&dfull[h], t & 1, 24);
+              if (tid == 256) FLERN_TRACE(h ? TR_W1_DFULL1 : TR_W1_DFULL0, t);
               tc_fence_after();
-              dot_cols(H + h * (H / 2), H / 2, H + h * (H / 2), pa);
+              dot_cols(H + h * (H / 2), H / 2, H + h * (H / 2), h * (H / 2), pa, pb);
+              if (tid == 256) FLERN_TRACE(h ? TR_W1_DOTB : TR_W1_DOTA, t);
               tc_fence_before();
               __syncwarp();
               if (lane == 0) mbar_arrive(&dempty[h]);
             }
-            logit = (pa[0] + pa[1]) + (pa[2] + pa[3]) + p.bout;
+            logit = ((pa.x + pa.y) + (pb.x + pb.y)) + p.bout;
           }
           finish_tile(m, count, s, logit);
+          if (tid == 256) FLERN_TRACE(TR_W1_AGG, t);
         }
+        flush_acc();
       }
     } else {
       // ---- NL == 1: the two warpgroups take alternate tiles (TMEM buffer D[wg]) ----
@@ -588,22 +759,23 @@ __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_c
         if (!p.no_model) {
           mbar_wait(&dfull[wg], (t >> 1) & 1, 26);
           tc_fence_after();
-          float pa[4] = {0.f, 0.f, 0.f, 0.f};
-          dot_cols(wg * H, H, 0, pa);
+          float2 pa = make_float2(0.f, 0.f), pb = make_float2(0.f, 0.f);
+          dot_cols(wg * H, H, 0, 0, pa, pb);
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&dempty[wg]);
-          logit = (pa[0] + pa[1]) + (pa[2] + pa[3]) + p.bout;
+          logit = ((pa.x + pa.y) + (pb.x + pb.y)) + p.bout;
         }
         finish_tile(m, count, s, logit);
       }
+      flush_acc();
     }
   }
 
   // ---- teardown: per-CTA partials, last CTA reduces ----
   tc_fence_before();
   __syncthreads();
-  if (warp == 4) { tc_fence_after(); tmem_dealloc(tmem_base, kTmemCols); }
+  if (warp == 12) { tc_fence_after(); tmem_dealloc(tmem_base, kTmemCols); }
   const int G = p.ngroups;
   const int W = G * 4 + kCounters;
   int64_t* mine = p.partials + (int64_t)blockIdx.x * W;

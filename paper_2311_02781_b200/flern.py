@@ -53,7 +53,7 @@ class FlernQuery(ctypes.Structure):
 
 class FlernResult(ctypes.Structure):
     _fields_ = [("count", c_p), ("sum", c_p), ("counters", c_p), ("dbg_score", c_p), ("dbg_match", c_p),
-                ("dbg_selected", c_p), ("rows_scanned", c_i64), ("rows_joined", c_i64), ("rows_scored", c_i64),
+                ("dbg_selected", c_p), ("dbg_trace", c_p), ("rows_scanned", c_i64), ("rows_joined", c_i64), ("rows_scored", c_i64),
                 ("rows_selected", c_i64), ("elapsed_ms", ctypes.c_float)]
 
 
@@ -204,14 +204,18 @@ class Query:
         self.ngroups = ngroups
 
 
+TRACE_EVENTS = 20
+TRACE_TILES = 256
+
+
 def flern_run_query(ctx, query: Query, count=None, sum=None, counters=None, dbg_score=None, dbg_match=None,
-                    dbg_selected=None, flags: int | None = None) -> FlernResult:
+                    dbg_selected=None, dbg_trace=None, flags: int | None = None) -> FlernResult:
     """Runs `query`. Output buffers: numpy host arrays (default) or device tensors with
     FLERN_Q_RESULT_DEVICE in flags. Returns the FlernResult (count/sum written in place)."""
     if flags is not None:
         query.q.flags = flags
     res = FlernResult(_ptr(count), _ptr(sum), _ptr(counters), _ptr(dbg_score), _ptr(dbg_match), _ptr(dbg_selected),
-                      0, 0, 0, 0, 0.0)
+                      _ptr(dbg_trace), 0, 0, 0, 0, 0.0)
     _check(ctx, _lib.flern_run_query(ctx, ctypes.byref(query.q), ctypes.byref(res)))
     return res
 

@@ -1,0 +1,44 @@
+"""Pipeline trace of CTA 0 (diagnostic): where does each role wait? Prints per-tile deltas."""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import datagen as D
+from paper_2311_02781_b200 import flern as F
+from paper_2311_02781_b200.session import GpuQuery
+
+EV = ["MMA_D2A_FREE", "MMA_L2A_DONE", "MMA_NEXT_READY", "MMA_L1_ISSUED", "MMA_D2B_FREE", "MMA_L2B_ISSUED",
+      "W0_FULL", "W0_D1FULL", "W0_HFREE0", "W0_DONE", "W1_FULL", "W1_DFULL0", "W1_DOTA", "W1_DFULL1", "W1_DOTB",
+      "W1_AGG", "P_START", "P_PROBED", "P_GATHERED", "P_DONE"]
+name = sys.argv[1] if len(sys.argv) > 1 else "c2"
+sf = float(sys.argv[2]) if len(sys.argv) > 2 else 1.0
+cfg = D.with_sf(D.CONFIGS[name], sf)
+db = D.make_database(cfg)
+gq = GpuQuery(cfg, db, D.make_model(cfg, db))
+G = cfg.ngroups
+for it in range(3):
+    tr = np.zeros(F.TRACE_EVENTS * F.TRACE_TILES, np.uint64)
+    r = gq.run(count=np.zeros(G, np.int64), sum=np.zeros(G, np.int64), dbg_trace=tr)
+tr = tr.reshape(F.TRACE_EVENTS, F.TRACE_TILES).astype(np.int64)
+t0 = tr[tr > 0].min()
+print("kernel ms", r.elapsed_ms)
+for t in list(range(0, 12)) + [100, 101, 102]:
+    row = " ".join(f"{EV[e][:12]}={(tr[e, t] - t0) if tr[e, t] else -1:>8d}" for e in range(16))
+    print(t, row)
+print("producer batches:")
+for b in list(range(0, 8)) + [100, 101]:
+    print(b, " ".join(f"{EV[e]}={(tr[e, b] - t0) if tr[e, b] else -1}" for e in range(16, 20)))
+# steady-state per-tile period and phase durations (tiles 20..200)
+sl = slice(20, 200)
+def d(a, b):
+    x = tr[b, sl] - tr[a, sl]
+    return float(np.median(x[(tr[a, sl] > 0) & (tr[b, sl] > 0)]))
+per = np.diff(tr[EV.index("MMA_L2B_ISSUED"), sl])
+print("median tile period (cycles):", float(np.median(per)))
+for a, b in [("MMA_D2A_FREE", "MMA_L2A_DONE"), ("MMA_L2A_DONE", "MMA_NEXT_READY"), ("MMA_NEXT_READY", "MMA_L1_ISSUED"),
+             ("MMA_L1_ISSUED", "MMA_D2B_FREE"), ("MMA_D2B_FREE", "MMA_L2B_ISSUED"), ("W0_FULL", "W0_D1FULL"),
+             ("W0_D1FULL", "W0_HFREE0"), ("W0_HFREE0", "W0_DONE"), ("W1_FULL", "W1_DFULL0"), ("W1_DFULL0", "W1_DOTA"),
+             ("W1_DOTA", "W1_DFULL1"), ("W1_DFULL1", "W1_DOTB"), ("W1_DOTB", "W1_AGG"), ("P_START", "P_PROBED"),
+             ("P_PROBED", "P_GATHERED"), ("P_GATHERED", "P_DONE")]:
+    print(f"  {a:>16s} -> {b:<16s} {d(EV.index(a), EV.index(b)):8.0f}")
+pd = np.diff(tr[EV.index("P_START"), 10:100])
+print("producer batch period (256 rows):", float(np.median(pd)))

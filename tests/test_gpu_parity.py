@@ -229,3 +229,32 @@ def test_no_model_mode_is_join_aggregate():
             assert cnt.tolist() == c2.tolist() and sm.tolist() == s2.tolist()
         finally:
             gq.close()
+
+
+@pytest.mark.parametrize("kind", ["skewed", "sparse", "negative"])
+def test_hash_build_key_distributions(kind):
+    """The build picks an order-preserving range hash for dense key ranges and falls back to
+    Fibonacci hashing for sparse or skewed ones; either way the join ids equal the oracle's,
+    including probe keys outside the build key range."""
+    rng = np.random.default_rng(11)
+    n = 20000
+    if kind == "skewed":     # a dense cluster plus a few far-away keys: long chains under the range hash
+        bkeys = np.concatenate([np.arange(5000, 5000 + n - 50), rng.choice(10**9, 50, replace=False) + 10**6])
+    elif kind == "sparse":   # range far larger than 16 x capacity
+        bkeys = rng.choice(2**31 - 2, n, replace=False) - 2**30
+    else:
+        bkeys = np.arange(-n, 0) * 3
+    bkeys = rng.permutation(bkeys).astype(np.int32)
+    cfg = D.QueryConfig("h", 0.0, [8, 64, 1], [("fact", f"f{k}") for k in range(8)],
+                        [("dim", "fact", "k", "dk")], group=(0, "dg"), ngroups=4, sum_col=("fact", "v"))
+    nf = 50000
+    fk = rng.choice(np.concatenate([bkeys, rng.integers(-2**31 + 1, 2**31 - 1, 5000).astype(np.int32)]), nf)
+    fact = {"k": fk.astype(np.int32), "v": rng.integers(0, 1000, nf).astype(np.int32)}
+    for k in range(8):
+        fact[f"f{k}"] = rng.normal(size=nf).astype(np.float32)
+    dim = {"dk": bkeys, "dg": rng.integers(0, 4, n).astype(np.int32)}
+    db = D.Database(0.0, nf, fact, [("dim", n, dim)])
+    model = H.SimpleModel([8, 64, 1], [rng.normal(size=(64, 8)) * 0.3, rng.normal(size=(1, 64)) * 0.2],
+                          [np.zeros(64), np.zeros(1)])
+    model.W = [D.bf16_round(w) for w in model.W]
+    parity.check(cfg, db, model)
