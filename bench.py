@@ -201,6 +201,7 @@ def main():
 
     import torch
     import torch.distributed as dist
+    from paper_2311_02781_b200 import dist as FD
     from paper_2311_02781_b200 import flern as F
     from paper_2311_02781_b200.session import GpuQuery
 
@@ -239,10 +240,8 @@ def main():
         F.flern_run_query(gq.ctx, q_async, count=out_count, sum=out_sum, counters=counters)
         if ev_pair:
             ev_pair[1].record(stream)
-        if world > 1:
-            partial[:G].copy_(out_count)
-            partial[G:].copy_(out_sum)
-            dist.reduce(partial, dst=0)
+        if world > 1:   # the one exchange step: NCCL reduce of the int64 group partials
+            FD.combine_partials(FD.pack_partials(out_count, out_sum, partial), dst=0)
 
     for _ in range(args.warmup):
         step()

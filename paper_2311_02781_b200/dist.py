@@ -1,0 +1,39 @@
+"""Cross-GPU combine of the per-group partials.
+
+The hot path shards the fact table across ranks (contiguous orderkey ranges) and replicates the
+build side and the weights, so every fact row's result depends only on replicated state: the only
+exchange is the sum of the per-rank int64 [count | sum] group partials (80 B for 5 groups), one
+NCCL reduce over NVLink/NVSwitch (torch.distributed is the plumbing; the partials stay on the GPU).
+"""
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+
+def pack_partials(count: torch.Tensor, sum_: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+    """[count | sum] into one contiguous int64 buffer (one collective instead of two)."""
+    g = count.numel()
+    if out is None:
+        out = torch.empty(2 * g, dtype=torch.int64, device=count.device)
+    out[:g].copy_(count)
+    out[g:].copy_(sum_)
+    return out
+
+
+def combine_partials(buf: torch.Tensor, dst: int | None = 0, group=None) -> torch.Tensor:
+    """Sum the packed partials over all ranks: to rank `dst` (reduce) or to every rank (dst=None).
+    Integer addition is exact and order-independent, so the result is bit-identical to a
+    single-rank run over the whole fact table."""
+    if not dist.is_available() or not dist.is_initialized() or dist.get_world_size(group) == 1:
+        return buf
+    if dst is None:
+        dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=group)
+    else:
+        dist.reduce(buf, dst=dst, op=dist.ReduceOp.SUM, group=group)
+    return buf
+
+
+def unpack_partials(buf: torch.Tensor):
+    g = buf.numel() // 2
+    return buf[:g], buf[g:]

@@ -258,3 +258,26 @@ def test_hash_build_key_distributions(kind):
                           [np.zeros(64), np.zeros(1)])
     model.W = [D.bf16_round(w) for w in model.W]
     parity.check(cfg, db, model)
+
+
+def _calibrated(cfg, db):
+    """Random model for `cfg`, output layer scaled (via the oracle) to std(logit) ~ 1."""
+    raw = D.make_model(cfg, db, out_scale=1.0, out_shift=0.0)
+    r = O.run(cfg, db, raw, per_row=True, threshold=-math.inf)
+    lg = r.logit[~np.isnan(r.logit)]
+    return D.make_model(cfg, db, out_scale=1.0 / float(lg.std()), out_shift=float(lg.mean()))
+
+
+@pytest.mark.parametrize("pf", [False, True])
+def test_two_probe_chain(pf):
+    """Config 3's join chain lineitem ⋈ orders ⋈ customer (two probes, the second keyed by a payload
+    word of the first) with its 32 features, on a 32-128-128-1 MLP this build supports; with and
+    without config 4's pre-filter."""
+    base = D.CONFIGS["c4" if pf else "c3"]
+    cfg = D.with_sf(base, 0.1 if pf else 0.01, match_rate=0.9, dims=[32, 128, 128, 1], name="c3s")
+    db = D.make_database(cfg)
+    r = parity.check(cfg, db, _calibrated(cfg, db))
+    assert r["scored"] > 0
+    lt = H.linear_threshold_model(cfg)
+    r = parity.check(cfg, db, lt)
+    assert r["band"] == 0
