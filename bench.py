@@ -36,6 +36,9 @@ WORKLOADS = {
           "o_orderpriority COUNT/SUM(l_extendedprice)",
     "c1x": "C1 query shape at SF10 per GPU (HBM-bound supplementary row), MLP 8-64-1",
     "c4p": "SF10 per GPU, l_shipdate pre-filter (~2%) before inference, lineitem⋈orders, MLP 16-256-256-1",
+    "c3": "TPC-H-shaped lineitem⋈orders⋈customer (two probes, SF10 per GPU), 32 features -> MLP "
+          "32-1024-1024-1024-1, score>0.5, GROUP BY o_orderpriority COUNT/SUM(l_extendedprice)",
+    "c4": "config 3 + l_shipdate pre-filter (~2%) before inference (SF10 per GPU), MLP 32-1024-1024-1024-1",
 }
 METRIC = "joined rows scored/sec (query+MLP, whole box)"
 
@@ -53,6 +56,10 @@ def workload_cfg(name, world):
         base, sf1 = D.CONFIGS["c1"], 10.0
     elif name == "c4p":
         base, sf1 = D.CONFIGS["c4p"], 10.0
+    elif name == "c3":
+        base, sf1 = D.CONFIGS["c3"], 10.0
+    elif name == "c4":
+        base, sf1 = D.CONFIGS["c4"], 10.0
     else:
         raise SystemExit(f"unknown workload {name}")
     return D.with_sf(base, sf1 * world), sf1

@@ -1,0 +1,232 @@
+// common.cuh — constants, parameter block, hashing, X-tile ring and group-by accumulators shared by
+// the fused query kernels (narrow: on-chip MLP; wide: streamed-weight MLP) and the build kernels.
+#pragma once
+#include "sm100.cuh"
+
+namespace flern {
+
+constexpr int kMaxFeat = 48;
+constexpr int kMaxGroups = 64;
+constexpr int kMaxProbes = 2;
+constexpr int kTile = 128;
+constexpr int kThreads = 416;   // 13 warps: producers 0-3, epilogue WG0 4-7, WG1 8-11, MMA 12
+constexpr int kProducerThreads = 128;
+// consecutive fact rows per producer thread per batch (one 16/8/4-byte vector load per column);
+// fewer for wide inputs (register budget: R * K0P/2 packed bf16 pairs stay live)
+__host__ __device__ constexpr int rows_per_thread(int K0P) { return K0P <= 16 ? 2 : 1; }
+__host__ __device__ constexpr int batch_rows(int K0P) { return kProducerThreads * rows_per_thread(K0P); }
+constexpr int32_t kEmptyKey = (int32_t)0x80000000;         // INT32_MIN marks an empty slot
+constexpr int kCounters = 4;                               // scanned, joined(=scored), selected, bad_group
+
+// Slot of `key`: mode 1 = order-preserving range hash (kmin..kmax spread linearly over the
+// capacity: consecutive keys land in neighbouring slots, so a fact table clustered by the join key
+// probes the table almost sequentially); mode 0 = Fibonacci hashing (top log2(capacity) bits).
+struct HashFn {
+  uint32_t mode, shift, mask, mulc;
+  int32_t kmin;
+};
+__host__ __device__ __forceinline__ uint32_t hash_slot(int32_t key, const HashFn& f) {
+  if (f.mode)
+    return (uint32_t)(((uint64_t)((uint32_t)key - (uint32_t)f.kmin) * (uint64_t)f.mulc) >> 32) & f.mask;
+  return ((uint32_t)key * 0x9E3779B1u) >> f.shift;
+}
+
+struct ProbeDesc {
+  const int2* slots;        // {key, build row}, capacity = mask + 1
+  HashFn hf;
+  uint32_t mask;
+  const int32_t* payload;   // row-major [build rows][pstride]
+  int32_t pstride;
+  int32_t src;              // -1: key from fact column `fact_key`; p: payload word `key_word` of probe p
+  const int32_t* fact_key;
+  int32_t key_word;
+};
+
+struct ColDesc {            // a column reference resolved to base pointer + row stride
+  const int32_t* base;      // fact column, or probe payload + word
+  int32_t stride;           // 1 for a fact column, the payload row stride otherwise
+  int32_t src;              // 0 = fact row, 1 + p = build row of probe p
+  int32_t is_float;
+  int32_t word;             // payload word (src > 0)
+};
+
+struct QueryParams {
+  int64_t nrows;            // fact rows (< 2^31)
+  int64_t rows_per_cta;     // multiple of batch_rows(K0P)
+  int32_t nprobes;
+  ProbeDesc probe[kMaxProbes];
+  const int32_t* pf_col;    // nullptr = no pre-filter
+  int64_t pf_lo, pf_hi;
+  int32_t nfeat;
+  int32_t nfact;            // features [0, nfact) are fact columns, [nfact, nfeat) build payload words
+  ColDesc feat[kMaxFeat];
+  // compact views of feat[] for the producer's hot loop
+  const int32_t* fcol[kMaxFeat];   // fact column of feature k (k < nfact), else any valid pointer
+  int32_t dword[kMaxFeat];         // payload word of feature k (k >= nfact)
+  uint64_t dprobe1;                // bit k: feature k comes from probe 1's payload (else probe 0)
+  uint64_t fmask;                  // bit k: feature k is float32 (else int32)
+  const int32_t* dummy;            // 64 zero bytes: target of loads whose value is not needed
+  uint8_t* scratch;                // wide kernel: per-CTA activation scratch
+  ColDesc grp, sum;
+  int32_t ngroups;
+  int32_t both_classes;
+  float thr_logit;          // select logit > thr_logit  (score > t  <=>  logit > ln(t/(1-t)))
+  int32_t no_model;         // diagnostic: skip the MLP, select every joined row (scan/probe/gather only)
+  const uint8_t* wimg;      // weight image: [Wh (SW128) | W1 (interleave)] bf16, exact SMEM layout
+  const float* bias;        // [NL][H]
+  const float* wout;        // [H]
+  float bout;
+  const float* shift;       // [K0P]  c_k = -shift_k * scale_k (the gather computes fma(x, scale, c))
+  const float* scale;       // [K0P]
+  int64_t* partials;        // [gridDim.x][ngroups*4 + kCounters]
+  unsigned int* ticket;     // zero between launches (the last CTA resets it)
+  int64_t* out_count;       // [ngroups] (x2 both classes)
+  int64_t* out_sum;
+  int64_t* out_counters;    // [kCounters]
+  float* dbg_score;         // optional
+  int32_t* dbg_match;       // optional [nrows * nprobes]
+  uint32_t* dbg_selected;   // optional bitmap
+  unsigned long long* dbg_trace;  // optional [kTraceEvents][kTraceTiles] clock64 stamps of CTA 0
+};
+
+// Pipeline trace (diagnostic): clock64() at each hand-off, CTA 0, first kTraceTiles tiles/batches.
+constexpr int kTraceTiles = 256;
+enum TraceEv {
+  TR_MMA_D2A_FREE, TR_MMA_L2A_DONE, TR_MMA_NEXT_READY, TR_MMA_L1_ISSUED, TR_MMA_D2B_FREE, TR_MMA_L2B_ISSUED,
+  TR_W0_FULL, TR_W0_D1FULL, TR_W0_HFREE0, TR_W0_DONE,
+  TR_W1_FULL, TR_W1_DFULL0, TR_W1_DOTA, TR_W1_DFULL1, TR_W1_DOTB, TR_W1_AGG,
+  TR_P_START, TR_P_PROBED, TR_P_GATHERED, TR_P_DONE,
+  kTraceEvents
+};
+#define FLERN_TRACE(ev, idx)                                                           \
+  do {                                                                                 \
+    if (p.dbg_trace && blockIdx.x == 0 && (idx) < kTraceTiles)                         \
+      p.dbg_trace[(ev) * kTraceTiles + (idx)] = (unsigned long long)clock64();         \
+  } while (0)
+
+// Shared-memory plan (byte offsets from a 1024-aligned base), identical on host and device.
+struct Meta {  // view of one stage's metadata block
+  int32_t* count;
+  int32_t* rowid;
+  int32_t* val;
+  uint8_t* grp;
+};
+
+// The ring of X stages the producer fills: S stages of [128 rows x K0P] bf16 (interleaved K-major)
+// plus a metadata block per stage (count, fact row id, sum value, group code).
+constexpr uint32_t kMetaBytes = 16 + 4 * kTile + 4 * kTile + kTile;
+struct XRing {
+  uint8_t* x;
+  uint32_t xs;       // bytes per X stage
+  uint8_t* meta;     // S blocks of kMetaBytes
+  uint64_t* full;    // [S] producers (128 arrivals) -> consumers
+  uint64_t* empty;   // [S] consumers (4 warps) -> producers
+};
+__device__ __forceinline__ Meta meta_at(uint8_t* meta, int s) {
+  uint8_t* m = meta + s * kMetaBytes;
+  return Meta{reinterpret_cast<int32_t*>(m), reinterpret_cast<int32_t*>(m + 16),
+              reinterpret_cast<int32_t*>(m + 16 + 4 * kTile), m + 16 + 8 * kTile};
+}
+
+// Predicate + group-by of one 128-row tile, one thread per row (a warpgroup covers the tile):
+// warp ballot per present (group, class), popc rows and a split 16-bit redux sum, accumulated in
+// registers (lane l owns groups l and l+32, both classes) and flushed to SMEM once per CTA.
+struct GroupAgg {
+  unsigned long long ac[2][2], as[2][2];
+  __device__ __forceinline__ void init() {
+#pragma unroll
+    for (int u = 0; u < 2; ++u)
+#pragma unroll
+      for (int c = 0; c < 2; ++c) { ac[u][c] = 0ull; as[u][c] = 0ull; }
+  }
+  // releases the X stage (empty barrier) as soon as the metadata has been read
+  __device__ __forceinline__ void tile(const QueryParams& p, const Meta& m, int count, int r, int lane, float logit,
+                                       int64_t* s_cnt, uint64_t* empty_bar) {
+    const bool valid = r < count;
+    const bool sel = valid && (p.no_model || logit > p.thr_logit);
+    const int g = valid ? (int)m.grp[r] : 255;
+    const int32_t val = valid ? m.val[r] : 0;
+    if (valid && g == 255) atomicAdd(reinterpret_cast<unsigned long long*>(&s_cnt[3]), 1ull);
+    if (p.dbg_score && valid) p.dbg_score[m.rowid[r]] = 1.f / (1.f + __expf(-logit));
+    if (p.dbg_selected && sel) atomicOr(p.dbg_selected + (m.rowid[r] >> 5), 1u << (m.rowid[r] & 31));
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty_bar);
+    const int cls = sel ? 0 : 1;
+    const bool agg = valid && g != 255 && (sel || p.both_classes);
+    uint32_t pending = __ballot_sync(0xffffffffu, agg);
+    while (pending) {
+      const int leader = __ffs(pending) - 1;
+      const int lg = __shfl_sync(0xffffffffu, g, leader);
+      const int lc = __shfl_sync(0xffffffffu, cls, leader);
+      const bool mine = agg && g == lg && cls == lc;
+      const uint32_t mm = __ballot_sync(0xffffffffu, mine);
+      const int lo = __reduce_add_sync(0xffffffffu, mine ? (val & 0xFFFF) : 0);
+      const int hi = __reduce_add_sync(0xffffffffu, mine ? (val >> 16) : 0);
+      if (lane == (lg & 31)) {
+        const unsigned long long dc = (unsigned long long)__popc(mm);
+        const unsigned long long ds = (unsigned long long)((long long)hi * 65536ll + (long long)lo);
+        const bool up = lg >= 32;
+        if (!up && lc == 0) { ac[0][0] += dc; as[0][0] += ds; }
+        if (!up && lc == 1) { ac[0][1] += dc; as[0][1] += ds; }
+        if (up && lc == 0) { ac[1][0] += dc; as[1][0] += ds; }
+        if (up && lc == 1) { ac[1][1] += dc; as[1][1] += ds; }
+      }
+      pending &= ~mm;
+    }
+  }
+  __device__ __forceinline__ void flush(unsigned long long* acc, int lane, int ngroups) {
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int g = lane + 32 * u;
+      if (g < ngroups) {
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          if (ac[u][c]) atomicAdd(&acc[g * 4 + c * 2 + 0], ac[u][c]);
+          if (as[u][c]) atomicAdd(&acc[g * 4 + c * 2 + 1], as[u][c]);
+        }
+      }
+    }
+  }
+};
+
+// Per-CTA partials -> global; the last CTA to finish (atomic ticket) reduces them in CTA order.
+__device__ __forceinline__ void write_partials_and_reduce(const QueryParams& p, unsigned long long* acc,
+                                                          int64_t* s_cnt, unsigned int* s_is_last,
+                                                          int64_t row_begin, int64_t row_end, int tid,
+                                                          int nthreads) {
+  const int G = p.ngroups;
+  const int W = G * 4 + kCounters;
+  int64_t* mine = p.partials + (int64_t)blockIdx.x * W;
+  for (int i = tid; i < G * 4; i += nthreads) mine[i] = (int64_t)acc[i];
+  if (tid == 0) {
+    int64_t sel = 0;
+    for (int g = 0; g < G; ++g) sel += (int64_t)acc[g * 4 + 0];
+    mine[G * 4 + 0] = row_end > row_begin ? row_end - row_begin : 0;
+    mine[G * 4 + 1] = s_cnt[1];
+    mine[G * 4 + 2] = sel;
+    mine[G * 4 + 3] = s_cnt[3];
+    __threadfence();
+    const unsigned int prev = atomicAdd(p.ticket, 1u);
+    *s_is_last = (prev == gridDim.x - 1) ? 1u : 0u;
+  }
+  __syncthreads();
+  if (*s_is_last) {
+    __threadfence();
+    for (int i = tid; i < W; i += nthreads) {
+      int64_t t = 0;
+      for (int b = 0; b < (int)gridDim.x; ++b) t += *((volatile int64_t*)(p.partials + (int64_t)b * W + i));
+      if (i < G * 4) {
+        const int g = i / 4, cls = (i / 2) & 1, kind = i & 1;
+        if (cls == 0 || p.both_classes) {
+          int64_t* out = kind == 0 ? p.out_count : p.out_sum;
+          out[cls * G + g] = t;
+        }
+      } else {
+        p.out_counters[i - G * 4] = t;
+      }
+    }
+    if (tid == 0) *p.ticket = 0u;
+  }
+}
+
+}  // namespace flern

