@@ -150,7 +150,7 @@ constexpr bool plan_fits() {
   constexpr uint32_t W1 = (uint32_t)H * K0P * 2;
   constexpr uint32_t XS = (uint32_t)kTile * K0P * 2;
   constexpr uint32_t META = 16 + 9 * kTile;
-  constexpr uint32_t FIXED = WH + HB + W1 + NL * H * 4 + H * 4 + kMaxGroups * 4 * 8 + 2 * kTile * 4 + kMaxFeat * 8 +
+  constexpr uint32_t FIXED = WH + HB + W1 + NL * H * 4 + H * 4 + kMaxGroups * 4 * 8 + kQueueBytes + kMaxFeat * 8 +
                              64 * 8 + 128;
   return FIXED + 3 * (XS + META) <= 232448;
 }
@@ -756,6 +756,7 @@ extern "C" FLERN_API flern_status flern_run_query(flern_ctx* ctx, const flern_qu
   if (res->dbg_match) {
     if (dev_out) d_match = res->dbg_match;
     else if ((st = temp(n * q->nprobes * 4, (void**)&d_match)) != FLERN_OK) return st;
+    CUDA_TRY(ctx, cudaMemsetAsync(d_match, 0xFF, n * q->nprobes * 4, ctx->stream));   // -1: not reached
   }
   if (res->dbg_selected) {
     if (dev_out) d_sel = res->dbg_selected;

@@ -2,26 +2,37 @@
 // kernels: fills a ring of 128-row X tiles (bf16, interleaved
 // K-major, the layer-1 MMA operand) plus row metadata, consumed by the MMA + epilogue roles.
 // Shared by the narrow (on-chip MLP) and wide (streamed-weight MLP) kernels.
+//
+// Two row sources feed the same batch body (produce_batch):
+//   - no pre-filter: each thread takes R consecutive rows of a 128*R-row batch (R-wide vector
+//     column loads);
+//   - pre-filter (config 4, ~2% selectivity): the group scans the pre-filter column 1024 rows at a
+//     time (two 16-byte loads per thread), ballot-compacts the survivors' row ids into an SMEM queue
+//     (SURVEY.md K-COMPACT), and runs the probe / gather body only on full 128-row batches of
+//     survivors (one row per thread), so rejected rows cost one 4-byte load and a compare.
 #pragma once
 #include "common.cuh"
 
 namespace flern {
 
-template <int K0P, int S>
-__device__ __forceinline__ void producer_loop(const QueryParams& p, const XRing& ring, int32_t* wcnt,
-                                              const float* s_normf, int64_t* s_cnt, int64_t row_begin,
-                                              int64_t row_end, int tid, int warp, int lane) {
-    // =============================== PRODUCERS =============================================
-    // Each thread owns R consecutive fact rows of a 128*R-row batch: every fact column is read
-    // with one R-wide vector load per thread (coalesced, 16 B per lane for R = 4).
-    constexpr int R = rows_per_thread(K0P);
-    constexpr int kBatch = batch_rows(K0P);
-    const int t = tid;                   // 0..127
-    int stage = 0;                       // stage currently being filled (acquired)
-    uint32_t acq = 0;                    // number of stages acquired so far
-    int fill = 0;                        // rows already in `stage`
-    int64_t n_joined = 0;
-    int buf = 0;
+constexpr int kScanChunk = 1024;                         // pre-filter scan: 8 rows per producer thread
+constexpr int kQueueCap = kScanChunk + kProducerThreads;  // survivors pending (< 128) + one chunk
+constexpr uint32_t kQueueBytes = kQueueCap * 4;
+
+struct ProdState {
+  int stage;          // stage currently being filled (acquired)
+  uint32_t acq;       // stages acquired so far
+  int fill;           // rows already in `stage`
+  int buf;            // warp-count double buffer
+  int64_t n_joined;
+};
+
+// One batch: rows [row0, row0 + R) of this thread (consecutive; with R == 1 any row id), in[r] =
+// the row takes part (inside the shard and past the pre-filter).
+template <int K0P, int S, int R>
+__device__ __forceinline__ void produce_batch(ProdState& st, const QueryParams& p, const XRing& ring, int32_t* wcnt,
+                                              const float* s_normf, int64_t row0, bool whole, const bool (&in)[R],
+                                              int bidx, int64_t row_end, int t, int warp, int lane) {
     // Loads are plain read-only loads whose ADDRESS is selected (a 64-byte zero dummy when the
     // value is not needed): no predicates, no branches, so the compiler issues a batch's loads
     // back to back and they overlap; the dummy stays in L1.
@@ -58,22 +69,9 @@ __device__ __forceinline__ void producer_loop(const QueryParams& p, const XRing&
       const float2 y = fma2(make_float2(fa, fb), make_float2(nm.x, nm.y), make_float2(nm.z, nm.w));
       return bf16x2(y.x, y.y);
     };
-    mbar_wait(&ring.empty[0], ((acq / S) & 1) ^ 1, 1);   // acquire the first stage
-    acq = 1;
-    for (int64_t base = row_begin; base < row_end; base += kBatch) {
-      const int bidx = (int)((base - row_begin) / kBatch);
-      if (t == 0) FLERN_TRACE(TR_P_START, bidx);
-      const int64_t row0 = base + (int64_t)R * t;
-      const bool whole = row0 + R <= row_end;
       bool valid[R];
 #pragma unroll
-      for (int r = 0; r < R; ++r) valid[r] = row0 + r < row_end;
-      if (p.pf_col) {   // pre-filter on a fact column (config 4): before anything else
-        int32_t x[R];
-        loadR(p.pf_col, row0, whole, true, x);
-#pragma unroll
-        for (int r = 0; r < R; ++r) valid[r] = valid[r] && (p.pf_lo <= x[r]) && (x[r] < p.pf_hi);
-      }
+      for (int r = 0; r < R; ++r) valid[r] = in[r];
       bool any = false;
 #pragma unroll
       for (int r = 0; r < R; ++r) any |= valid[r];
@@ -153,7 +151,7 @@ __device__ __forceinline__ void producer_loop(const QueryParams& p, const XRing&
       if (p.dbg_match) {
 #pragma unroll
         for (int r = 0; r < R; ++r)
-          if (row0 + r < row_end)
+          if (in[r])
             for (int q = 0; q < p.nprobes; ++q) p.dbg_match[(row0 + r) * p.nprobes + q] = brow[r][q];
       }
       // 3. build-side loads (payload words of the matched rows), all issued before any use
@@ -186,28 +184,28 @@ __device__ __forceinline__ void producer_loop(const QueryParams& p, const XRing&
         const int x = __shfl_up_sync(0xffffffffu, incl, o);
         if (lane >= o) incl += x;
       }
-      if (lane == 31) wcnt[buf * 4 + warp] = incl;
+      if (lane == 31) wcnt[st.buf * 4 + warp] = incl;
       named_bar_sync(1, kProducerThreads);
       int woff = 0, total = 0;
 #pragma unroll
       for (int w = 0; w < 4; ++w) {
-        const int c = wcnt[buf * 4 + w];
+        const int c = wcnt[st.buf * 4 + w];
         woff += (w < warp) ? c : 0;
         total += c;
       }
-      buf ^= 1;
-      n_joined += my_cnt;
+      st.buf ^= 1;
+      st.n_joined += my_cnt;
       // Write surviving rows segment by segment (a segment = the part of the batch that lands in
       // one stage). A completed stage is published before the next one is acquired, so the
       // producer never holds more than one unpublished stage (no circular wait with consumers).
-      const int end = fill + total;
+      const int end = st.fill + total;
       const int nseg = end > 0 ? (end + kTile - 1) / kTile : 1;
-      const int pos0 = fill + woff + incl - my_cnt;   // stream position of my first surviving row
+      const int pos0 = st.fill + woff + incl - my_cnt;   // stream position of my first surviving row
       for (int seg = 0; seg < nseg; ++seg) {
-        const int ts = (stage + seg) % S;
+        const int ts = (st.stage + seg) % S;
         if (seg > 0) {
-          mbar_wait(&ring.empty[ts], ((acq / S) & 1) ^ 1, 2);
-          ++acq;
+          mbar_wait(&ring.empty[ts], ((st.acq / S) & 1) ^ 1, 2);
+          ++st.acq;
         }
         uint8_t* xs = ring.x + ts * ring.xs;
         const Meta m = meta_at(ring.meta, ts);
@@ -234,31 +232,129 @@ __device__ __forceinline__ void producer_loop(const QueryParams& p, const XRing&
         }
       }
       if (t == 0) FLERN_TRACE(TR_P_DONE, bidx);
-      stage = (stage + end / kTile) % S;
-      fill = end % kTile;
-      if (end > 0 && fill == 0) {   // every touched stage was published: acquire a fresh one
-        mbar_wait(&ring.empty[stage], ((acq / S) & 1) ^ 1, 3);
-        ++acq;
+      st.stage = (st.stage + end / kTile) % S;
+      st.fill = end % kTile;
+      if (end > 0 && st.fill == 0) {   // every touched stage was published: acquire a fresh one
+        mbar_wait(&ring.empty[st.stage], ((st.acq / S) & 1) ^ 1, 3);
+        ++st.acq;
+      }
+}
+
+template <int K0P, int S>
+__device__ __forceinline__ void producer_loop(const QueryParams& p, const XRing& ring, int32_t* wcnt,
+                                              const float* s_normf, int64_t* s_cnt, int32_t* queue,
+                                              int64_t row_begin, int64_t row_end, int tid, int warp, int lane) {
+  constexpr int R = rows_per_thread(K0P);
+  constexpr int kBatch = batch_rows(K0P);
+  const int t = tid;   // 0..127
+  ProdState st{0, 0u, 0, 0, 0};
+  mbar_wait(&ring.empty[0], ((st.acq / S) & 1) ^ 1, 1);   // acquire the first stage
+  st.acq = 1;
+  if (!p.pf_col) {
+    for (int64_t base = row_begin; base < row_end; base += kBatch) {
+      const int bidx = (int)((base - row_begin) / kBatch);
+      if (t == 0) FLERN_TRACE(TR_P_START, bidx);
+      const int64_t row0 = base + (int64_t)R * t;
+      bool in[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) in[r] = row0 + r < row_end;
+      produce_batch<K0P, S, R>(st, p, ring, wcnt, s_normf, row0, row0 + R <= row_end, in, bidx, row_end, t, warp, lane);
+    }
+  } else {
+    int nq = 0;        // survivors queued (uniform across the producer group)
+    int bidx = 0;
+    // scan rows cb + 4t + 512j (j = 0, 1; each warp instruction covers 512 contiguous rows); the
+    // next chunk's loads are issued before this chunk is compacted (software pipeline)
+    auto scan_load = [&](int64_t cb, int32_t (&x)[8]) {
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int64_t r0 = cb + 4 * t + 512 * j;
+        if (r0 + 4 <= row_end) {
+          const int4 v = ldg_nc(reinterpret_cast<const int4*>(p.pf_col + r0));
+          x[4 * j] = v.x; x[4 * j + 1] = v.y; x[4 * j + 2] = v.z; x[4 * j + 3] = v.w;
+        } else {
+#pragma unroll
+          for (int u = 0; u < 4; ++u) x[4 * j + u] = r0 + u < row_end ? ldg_nc(p.pf_col + r0 + u) : 0;
+        }
+      }
+    };
+    int32_t xnext[8];
+    if (row_begin < row_end) scan_load(row_begin, xnext);
+    for (int64_t cb = row_begin; cb < row_end; cb += kScanChunk) {
+      int32_t x[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) x[u] = xnext[u];
+      if (cb + kScanChunk < row_end) scan_load(cb + kScanChunk, xnext);
+      uint32_t bits = 0;
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int64_t rr = cb + 4 * t + 512 * j + u;
+          if (rr < row_end && p.pf_lo <= x[4 * j + u] && x[4 * j + u] < p.pf_hi) bits |= 1u << (4 * j + u);
+        }
+      const int my = __popc(bits);
+      int incl = my;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int x = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += x;
+      }
+      if (lane == 31) wcnt[8 + warp] = incl;
+      named_bar_sync(1, kProducerThreads);
+      int woff = 0, total = 0;
+#pragma unroll
+      for (int w = 0; w < 4; ++w) {
+        const int c = wcnt[8 + w];
+        woff += (w < warp) ? c : 0;
+        total += c;
+      }
+      int pos = nq + woff + incl - my;
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (bits & (1u << (4 * j + u))) queue[pos++] = (int32_t)(cb + 4 * t + 512 * j + u);
+      nq += total;
+      named_bar_sync(1, kProducerThreads);   // queue written (and wcnt[8..] read) by all
+      const bool last = cb + kScanChunk >= row_end;
+      while (nq >= kProducerThreads || (last && nq > 0)) {
+        const bool in1[1] = {t < nq};
+        const int64_t row = in1[0] ? (int64_t)queue[t] : 0;
+        if (t == 0) FLERN_TRACE(TR_P_START, bidx);
+        produce_batch<K0P, S, 1>(st, p, ring, wcnt, s_normf, row, true, in1, bidx, row_end, t, warp, lane);
+        ++bidx;
+        const int taken = min(nq, kProducerThreads);
+        // shift the rest of the queue to the front
+        int32_t keep[kQueueCap / kProducerThreads + 1];
+        int nk = 0;
+        for (int i = taken + t; i < nq; i += kProducerThreads) keep[nk++] = queue[i];
+        named_bar_sync(1, kProducerThreads);
+        nk = 0;
+        for (int i = taken + t; i < nq; i += kProducerThreads) queue[i - taken] = keep[nk++];
+        nq -= taken;
+        named_bar_sync(1, kProducerThreads);
       }
     }
-    if (fill > 0) {   // flush the partial tile
+  }
+  if (st.fill > 0) {   // flush the partial tile
       fence_proxy_async_smem();
-      if (t == 0) *meta_at(ring.meta, stage).count = fill;
-      mbar_arrive(&ring.full[stage]);
-      stage = (stage + 1) % S;
-      mbar_wait(&ring.empty[stage], ((acq / S) & 1) ^ 1, 4);
-      ++acq;
+      if (t == 0) *meta_at(ring.meta, st.stage).count = st.fill;
+      mbar_arrive(&ring.full[st.stage]);
+      st.stage = (st.stage + 1) % S;
+      mbar_wait(&ring.empty[st.stage], ((st.acq / S) & 1) ^ 1, 4);
+      ++st.acq;
     }
     // end-of-stream marker, published on two consecutive stages (with NL == 1 the epilogue
     // warpgroups take alternate tiles, so each must see one)
-    if (t == 0) *meta_at(ring.meta, stage).count = -1;
-    mbar_arrive(&ring.full[stage]);
-    stage = (stage + 1) % S;
-    mbar_wait(&ring.empty[stage], ((acq / S) & 1) ^ 1, 5);
-    ++acq;
-    if (t == 0) *meta_at(ring.meta, stage).count = -1;
-    mbar_arrive(&ring.full[stage]);
-    int64_t nj = n_joined;
+    if (t == 0) *meta_at(ring.meta, st.stage).count = -1;
+    mbar_arrive(&ring.full[st.stage]);
+    st.stage = (st.stage + 1) % S;
+    mbar_wait(&ring.empty[st.stage], ((st.acq / S) & 1) ^ 1, 5);
+    ++st.acq;
+    if (t == 0) *meta_at(ring.meta, st.stage).count = -1;
+    mbar_arrive(&ring.full[st.stage]);
+    int64_t nj = st.n_joined;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) nj += __shfl_down_sync(0xffffffffu, nj, o);
     if (lane == 0) atomicAdd(reinterpret_cast<unsigned long long*>(&s_cnt[1]), (unsigned long long)nj);

@@ -31,7 +31,7 @@ struct SmemPlan {
   static constexpr uint32_t W1 = (uint32_t)H * K0P * 2;                       // layer-1 W, interleave
   static constexpr uint32_t XS = (uint32_t)kTile * K0P * 2;                   // one X stage, interleave
   static constexpr uint32_t META = 16 + 4 * kTile + 4 * kTile + kTile;        // count, rowid, val, grp
-  static constexpr uint32_t FIXED = WH + HB + W1 + NL * H * 4 + H * 4 + kMaxGroups * 4 * 8 + 2 * kTile * 4 +
+  static constexpr uint32_t FIXED = WH + HB + W1 + NL * H * 4 + H * 4 + kMaxGroups * 4 * 8 + kQueueBytes +
                                     kMaxFeat * 8 + 64 * 8 + 128;
   static constexpr int S = (FIXED + 4 * (XS + META) <= 232448) ? 4 : 3;
   static constexpr uint32_t off_wh = 0;                                       // [Wh | W1] = weight image
@@ -42,8 +42,8 @@ struct SmemPlan {
   static constexpr uint32_t off_bias = off_meta + S * META;
   static constexpr uint32_t off_wout = off_bias + NL * H * 4;
   static constexpr uint32_t off_acc = off_wout + H * 4;
-  static constexpr uint32_t off_xchg = off_acc + kMaxGroups * 4 * 8;
-  static constexpr uint32_t off_norm = off_xchg + 2 * kTile * 4;               // shift[48], scale[48]
+  static constexpr uint32_t off_queue = off_acc + kMaxGroups * 4 * 8;          // pre-filter survivor queue
+  static constexpr uint32_t off_norm = off_queue + kQueueBytes;                // shift[48], scale[48]
   static constexpr uint32_t off_bar = off_norm + kMaxFeat * 8;
   static constexpr uint32_t off_misc = off_bar + 64 * 8;    // tmem base, warp counts, counters
   static constexpr uint32_t total = off_misc + 128;
@@ -130,7 +130,7 @@ __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_c
 
   if (warp < 4) {
     producer_loop<K0P, S>(p, XRing{smem + P::off_x, P::XS, smem + P::off_meta, full, empty}, wcnt, s_shift, s_cnt,
-                          row_begin, row_end, tid, warp, lane);
+                          reinterpret_cast<int32_t*>(smem + P::off_queue), row_begin, row_end, tid, warp, lane);
   } else if (warp == 12) {
     // =============================== MMA ISSUER =============================================
     // NL == 2 issue order per tile t (steady state): L2a(t), L1(t+1), L2b(t). Layer 2 is split

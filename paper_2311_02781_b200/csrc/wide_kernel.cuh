@@ -42,7 +42,8 @@ struct WidePlan {
   static constexpr uint32_t off_wout = off_bias + NL * H * 4;
   static constexpr uint32_t off_acc = off_wout + H * 4;
   static constexpr uint32_t off_xchg = off_acc + kMaxGroups * 4 * 8;
-  static constexpr uint32_t off_norm = off_xchg + 2 * kTile * 4;
+  static constexpr uint32_t off_queue = off_xchg + 2 * kTile * 4;
+  static constexpr uint32_t off_norm = off_queue + kQueueBytes;
   static constexpr uint32_t off_bar = off_norm + kMaxFeat * 8;
   static constexpr uint32_t off_misc = off_bar + 64 * 8;
   static constexpr uint32_t total = off_misc + 128;
@@ -131,7 +132,7 @@ __global__ void __launch_bounds__(kThreadsWide, 1) flern_query_wide_kernel(const
 
   if (warp < 4) {
     producer_loop<K0P, S>(p, XRing{smem + P::off_x, P::XS, smem + P::off_meta, xfull, xempty}, wcnt, s_norm, s_cnt,
-                          row_begin, row_end, tid, warp, lane);
+                          reinterpret_cast<int32_t*>(smem + P::off_queue), row_begin, row_end, tid, warp, lane);
   } else if (warp == 13) {
     // =============================== LOADER (bulk copies into the operand ring) ==============
     if (lane == 0) {
