@@ -72,6 +72,7 @@ struct QueryParams {
   int32_t both_classes;
   float thr_logit;          // select logit > thr_logit  (score > t  <=>  logit > ln(t/(1-t)))
   int32_t no_model;         // diagnostic: skip the MLP, select every joined row (scan/probe/gather only)
+  int32_t dbg_mode;         // diagnostic (env FLERN_DBG_MODE): bit 0 = epilogues skip their math
   const uint8_t* wimg;      // weight image: [Wh (SW128) | W1 (interleave)] bf16, exact SMEM layout
   const float* bias;        // [NL][H]
   const float* wout;        // [H]
@@ -96,8 +97,30 @@ enum TraceEv {
   TR_W0_FULL, TR_W0_D1FULL, TR_W0_HFREE0, TR_W0_DONE,
   TR_W1_FULL, TR_W1_DFULL0, TR_W1_DOTA, TR_W1_DFULL1, TR_W1_DOTB, TR_W1_AGG,
   TR_P_START, TR_P_PROBED, TR_P_GATHERED, TR_P_DONE,
+  TR_WAITS,   // [category] accumulated wait cycles of CTA 0's role threads (see FLERN_WAIT)
   kTraceEvents
 };
+// wait categories for TR_WAITS
+enum WaitCat {
+  W_MMA_FULL, W_MMA_DEMPTY0, W_MMA_DEMPTY1, W_MMA_HFULL, W_MMA_D1EMPTY, W_WG0_FULL, W_WG0_D1FULL, W_WG0_HFREE,
+  W_WG1_FULL, W_WG1_DFULL, W_PROD_EMPTY, W_KERNEL
+};
+// mbar_wait that (when tracing, CTA 0, the role's first lane) adds its wait time to TR_WAITS[cat].
+// Compiled in only with -DFLERN_TRACE_WAITS (diagnostic builds): it costs registers in the hot loop.
+#ifndef FLERN_TRACE_WAITS
+#define FLERN_WAIT(cat, on, bar, parity, tag) mbar_wait(bar, parity, tag)
+#else
+#define FLERN_WAIT(cat, on, bar, parity, tag)                                                   \
+  do {                                                                                         \
+    if (p.dbg_trace && blockIdx.x == 0 && (on)) {                                               \
+      const unsigned long long t0_ = (unsigned long long)clock64();                            \
+      mbar_wait(bar, parity, tag);                                                             \
+      atomicAdd(&p.dbg_trace[TR_WAITS * kTraceTiles + (cat)], (unsigned long long)clock64() - t0_); \
+    } else {                                                                                   \
+      mbar_wait(bar, parity, tag);                                                             \
+    }                                                                                          \
+  } while (0)
+#endif
 #define FLERN_TRACE(ev, idx)                                                           \
   do {                                                                                 \
     if (p.dbg_trace && blockIdx.x == 0 && (idx) < kTraceTiles)                         \

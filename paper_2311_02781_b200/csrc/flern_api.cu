@@ -697,6 +697,7 @@ extern "C" FLERN_API flern_status flern_run_query(flern_ctx* ctx, const flern_qu
   p.ngroups = q->ngroups;
   p.both_classes = both ? 1 : 0;
   p.no_model = (q->flags & FLERN_Q_NO_MODEL) ? 1 : 0;
+  p.dbg_mode = getenv("FLERN_DBG_MODE") ? atoi(getenv("FLERN_DBG_MODE")) : 0;   // diagnostics only
   const double t = (double)q->threshold;
   p.thr_logit = t <= 0.0 ? -INFINITY : (t >= 1.0 ? INFINITY : (float)std::log(t / (1.0 - t)));
   uint8_t* img = m.dbuf;

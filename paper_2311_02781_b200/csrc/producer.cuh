@@ -204,7 +204,7 @@ __device__ __forceinline__ void produce_batch(ProdState& st, const QueryParams& 
       for (int seg = 0; seg < nseg; ++seg) {
         const int ts = (st.stage + seg) % S;
         if (seg > 0) {
-          mbar_wait(&ring.empty[ts], ((st.acq / S) & 1) ^ 1, 2);
+          FLERN_WAIT(W_PROD_EMPTY, t == 0, &ring.empty[ts], ((st.acq / S) & 1) ^ 1, 2);
           ++st.acq;
         }
         uint8_t* xs = ring.x + ts * ring.xs;
@@ -235,7 +235,7 @@ __device__ __forceinline__ void produce_batch(ProdState& st, const QueryParams& 
       st.stage = (st.stage + end / kTile) % S;
       st.fill = end % kTile;
       if (end > 0 && st.fill == 0) {   // every touched stage was published: acquire a fresh one
-        mbar_wait(&ring.empty[st.stage], ((st.acq / S) & 1) ^ 1, 3);
+        FLERN_WAIT(W_PROD_EMPTY, t == 0, &ring.empty[st.stage], ((st.acq / S) & 1) ^ 1, 3);
         ++st.acq;
       }
 }

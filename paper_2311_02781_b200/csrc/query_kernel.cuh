@@ -137,74 +137,78 @@ __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_c
     // into two N-halves (D2a, D2b) so warpgroup 1 drains one half while the other is computed,
     // and L1(t+1) sits between them so warpgroup 0 converts it into H chunk by chunk as L2b(t)
     // releases each K-block of H (hfree[c]).
-    if (lane == 0 && !p.no_model) {
-      const uint32_t x0 = smem_u32(smem + P::off_x);
-      const uint32_t w1 = smem_u32(smem + P::off_w1);
+    // Lane 0 issues every tcgen05.mma / tcgen05.commit. Descriptors are built once; a K-step or stage advances the 14-bit start-address field
+    // (byte offset >> 4, always < 2^14 for 228 KB of SMEM).
+    const unsigned long long k_t0 = (unsigned long long)clock64();
+    if (warp == 12 && lane == 0 && !p.no_model) {
+      const bool leader = true;
+      const uint64_t xdesc = make_sdesc(smem_u32(smem + P::off_x), kTile * 16, 128, kLayoutNone);
+      const uint64_t w1desc = make_sdesc(smem_u32(smem + P::off_w1), H * 16, 128, kLayoutNone);
       auto issue_l1 = [&](int s, uint32_t dcol) {
         constexpr uint32_t idesc1 = make_idesc_bf16(128, H);
 #pragma unroll
         for (int ks = 0; ks < K0P / 16; ++ks) {
-          const uint64_t ad = make_sdesc(x0 + s * P::XS + ks * 2 * (kTile * 16), kTile * 16, 128, kLayoutNone);
-          const uint64_t bd = make_sdesc(w1 + ks * 2 * (H * 16), H * 16, 128, kLayoutNone);
-          mma_bf16_ss(tmem_base + dcol, ad, bd, idesc1, ks > 0);
+          const uint64_t ad = xdesc + ((uint32_t)(s * P::XS + ks * 2 * (kTile * 16)) >> 4);
+          const uint64_t bd = w1desc + ((uint32_t)(ks * 2 * (H * 16)) >> 4);
+          if (leader) mma_bf16_ss(tmem_base + dcol, ad, bd, idesc1, ks > 0);
         }
       };
       if constexpr (NL >= 2) {
-        const uint32_t wh = smem_u32(smem + P::off_wh);
-        const uint32_t hb = smem_u32(smem + P::off_hb);
+        const uint64_t hdesc = make_sdesc(smem_u32(smem + P::off_hb), 16, 1024, kLayoutSW128);
+        const uint64_t whdesc = make_sdesc(smem_u32(smem + P::off_wh), 16, 1024, kLayoutSW128);
         constexpr int NC = H / 64;
         auto issue_l2_half = [&](int half, uint32_t tile) {
           constexpr uint32_t idesc2 = make_idesc_bf16(128, H / 2);
+#pragma unroll
           for (int c = 0; c < NC; ++c) {
-            if (half == 0) { mbar_wait(&hfull[c], tile & 1, 12); tc_fence_after(); }
+            if (half == 0) { FLERN_WAIT(W_MMA_HFULL, true, &hfull[c], tile & 1, 12); tc_fence_after(); }
 #pragma unroll
             for (int j = 0; j < 4; ++j) {   // 4 x K=16 inside one 64-column, 128B-swizzled K-block
-              const uint64_t ad = make_sdesc(hb + c * (kTile * 128) + j * 32, 16, 1024, kLayoutSW128);
-              const uint64_t bd = make_sdesc(wh + c * (H * 128) + half * (H / 16) * 1024 + j * 32, 16, 1024,
-                                             kLayoutSW128);
-              mma_bf16_ss(tmem_base + H + half * (H / 2), ad, bd, idesc2, (c | j) != 0);
+              const uint64_t ad = hdesc + ((uint32_t)(c * (kTile * 128) + j * 32) >> 4);
+              const uint64_t bd = whdesc + ((uint32_t)(c * (H * 128) + half * (H / 16) * 1024 + j * 32) >> 4);
+              if (leader) mma_bf16_ss(tmem_base + H + half * (H / 2), ad, bd, idesc2, (c | j) != 0);
             }
-            if (half == 1) mma_commit(&hfree[c]);   // last reader of H chunk c for this tile
+            if (half == 1 && leader) mma_commit(&hfree[c]);   // last reader of H chunk c for this tile
           }
-          mma_commit(&dfull[half]);
+          if (leader) mma_commit(&dfull[half]);
         };
-        mbar_wait(&full[0], 0, 10);
+        FLERN_WAIT(W_MMA_FULL, lane == 0, &full[0], 0, 10);
         if (*meta_of<K0P, H, NL>(smem, 0).count >= 0) {
           tc_fence_after();
           issue_l1(0, 0);
-          mma_commit(d1full);
+          if (leader) mma_commit(d1full);
           for (uint32_t t = 0;; ++t) {
-            mbar_wait(&dempty[0], (t & 1) ^ 1, 13);
-            FLERN_TRACE(TR_MMA_D2A_FREE, t);
+            FLERN_WAIT(W_MMA_DEMPTY0, lane == 0, &dempty[0], (t & 1) ^ 1, 13);
+            if (lane == 0) FLERN_TRACE(TR_MMA_D2A_FREE, t);
             tc_fence_after();
             issue_l2_half(0, t);
-            FLERN_TRACE(TR_MMA_L2A_DONE, t);
+            if (lane == 0) FLERN_TRACE(TR_MMA_L2A_DONE, t);
             // L1(t+1) goes between the two halves when tile t+1 is already published (so that
             // warpgroup 0 converts it while L2b(t) runs); otherwise after L2b(t) (never block the
             // tile in flight on the producer)
             const int s1 = (t + 1) % S;
             const uint32_t ph1 = ((t + 1) / S) & 1;
-            bool have_next = mbar_test_wait(&full[s1], ph1);
+            const bool have_next = mbar_test_wait(&full[s1], ph1);
             bool next = false;
             auto do_next = [&]() {
-              FLERN_TRACE(TR_MMA_NEXT_READY, t);
+              if (lane == 0) FLERN_TRACE(TR_MMA_NEXT_READY, t);
               next = *meta_of<K0P, H, NL>(smem, s1).count >= 0;
               if (next) {
-                mbar_wait(d1empty, ((t + 1) & 1) ^ 1, 11);
+                FLERN_WAIT(W_MMA_D1EMPTY, lane == 0, d1empty, ((t + 1) & 1) ^ 1, 11);
                 tc_fence_after();
                 issue_l1(s1, 0);
-                mma_commit(d1full);
+                if (leader) mma_commit(d1full);
                 FLERN_TRACE(TR_MMA_L1_ISSUED, t);
               }
             };
             if (have_next) do_next();
-            mbar_wait(&dempty[1], (t & 1) ^ 1, 14);
-            FLERN_TRACE(TR_MMA_D2B_FREE, t);
+            FLERN_WAIT(W_MMA_DEMPTY1, lane == 0, &dempty[1], (t & 1) ^ 1, 14);
+            if (lane == 0) FLERN_TRACE(TR_MMA_D2B_FREE, t);
             tc_fence_after();
             issue_l2_half(1, t);
-            FLERN_TRACE(TR_MMA_L2B_ISSUED, t);
+            if (lane == 0) FLERN_TRACE(TR_MMA_L2B_ISSUED, t);
             if (!have_next) {
-              mbar_wait(&full[s1], ph1, 10);
+              FLERN_WAIT(W_MMA_FULL, lane == 0, &full[s1], ph1, 10);
               do_next();
             }
             if (!next) break;
@@ -220,10 +224,12 @@ __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_c
           mbar_wait(&dempty[b], ((t >> 1) & 1) ^ 1, 11);
           tc_fence_after();
           issue_l1(s, b * H);
-          mma_commit(&dfull[b]);
+          if (leader) mma_commit(&dfull[b]);
         }
       }
     }
+    if (warp == 12 && lane == 0 && p.dbg_trace && blockIdx.x == 0)
+      p.dbg_trace[TR_WAITS * kTraceTiles + W_KERNEL] = (unsigned long long)clock64() - k_t0;
     __syncwarp();
   } else {
     // =============================== EPILOGUE (warps 4-11) =============================================
@@ -275,12 +281,22 @@ __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_c
         // ---- warpgroup 0: D1 -> bias + ReLU -> bf16 -> H (layer-2 A operand), chunk by chunk ----
         for (uint32_t t = 0; !p.no_model; ++t) {
           const int s = t % S;
-          mbar_wait(&full[s], (t / S) & 1, 20);
+          FLERN_WAIT(W_WG0_FULL, tid == 128, &full[s], (t / S) & 1, 20);
           if (*meta_of<K0P, H, NL>(smem, s).count < 0) break;
           if (tid == 128) FLERN_TRACE(TR_W0_FULL, t);
-          mbar_wait(d1full, t & 1, 21);
+          FLERN_WAIT(W_WG0_D1FULL, tid == 128, d1full, t & 1, 21);
           if (tid == 128) FLERN_TRACE(TR_W0_D1FULL, t);
           tc_fence_after();
+          if (p.dbg_mode & 1) {   // diagnostic: keep the protocol, skip the math
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(d1empty);
+            for (int c = 0; c < NC; ++c) {
+              mbar_wait(&hfree[c], (t & 1) ^ 1, 22);
+              __syncwarp();
+              if (lane == 0) mbar_arrive(&hfull[c]);
+            }
+          } else
           for (int c = 0; c < NC; ++c) {
             uint32_t pk[32];
 #pragma unroll
@@ -305,7 +321,7 @@ __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_c
               __syncwarp();
               if (lane == 0) mbar_arrive(d1empty);
             }
-            mbar_wait(&hfree[c], (t & 1) ^ 1, 22);   // L2b(t-1) finished reading chunk c
+            FLERN_WAIT(W_WG0_HFREE, tid == 128, &hfree[c], (t & 1) ^ 1, 22);   // L2b(t-1) done with chunk c
             if (tid == 128 && c == 0) FLERN_TRACE(TR_W0_HFREE0, t);
             const uint32_t rowbase = hb + c * (kTile * 128) + (r >> 3) * 1024 + (r & 7) * 128;
 #pragma unroll
@@ -322,7 +338,7 @@ __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_c
         // ---- warpgroup 1: logit = relu(D2 + b2) . w_out + b_out, predicate, group-by ----
         for (uint32_t t = 0;; ++t) {
           const int s = t % S;
-          mbar_wait(&full[s], (t / S) & 1, 23);
+          FLERN_WAIT(W_WG1_FULL, tid == 256, &full[s], (t / S) & 1, 23);
           const Meta m = meta_of<K0P, H, NL>(smem, s);
           const int count = *m.count;
           if (count < 0) break;
@@ -332,10 +348,10 @@ __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_c
             float2 pa = make_float2(0.f, 0.f), pb = make_float2(0.f, 0.f);
 #pragma unroll 1
             for (int h = 0; h < 2; ++h) {
-              mbar_wait(&dfull[h], t & 1, 24);
+              FLERN_WAIT(W_WG1_DFULL, tid == 256, &dfull[h], t & 1, 24);
               if (tid == 256) FLERN_TRACE(h ? TR_W1_DFULL1 : TR_W1_DFULL0, t);
               tc_fence_after();
-              dot_cols(H + h * (H / 2), H / 2, H + h * (H / 2), h * (H / 2), pa, pb);
+              if (!(p.dbg_mode & 1)) dot_cols(H + h * (H / 2), H / 2, H + h * (H / 2), h * (H / 2), pa, pb);
               if (tid == 256) FLERN_TRACE(h ? TR_W1_DOTB : TR_W1_DOTA, t);
               tc_fence_before();
               __syncwarp();

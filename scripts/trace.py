@@ -19,7 +19,7 @@ for it in range(3):
     tr = np.zeros(F.TRACE_EVENTS * F.TRACE_TILES, np.uint64)
     r = gq.run(count=np.zeros(G, np.int64), sum=np.zeros(G, np.int64), dbg_trace=tr)
 tr = tr.reshape(F.TRACE_EVENTS, F.TRACE_TILES).astype(np.int64)
-t0 = tr[tr > 0].min()
+t0 = tr[:20][tr[:20] > 0].min()
 print("kernel ms", r.elapsed_ms)
 for t in list(range(0, 12)) + [100, 101, 102]:
     row = " ".join(f"{EV[e][:12]}={(tr[e, t] - t0) if tr[e, t] else -1:>8d}" for e in range(16))
@@ -41,4 +41,11 @@ for a, b in [("MMA_D2A_FREE", "MMA_L2A_DONE"), ("MMA_L2A_DONE", "MMA_NEXT_READY"
              ("P_PROBED", "P_GATHERED"), ("P_GATHERED", "P_DONE")]:
     print(f"  {a:>16s} -> {b:<16s} {d(EV.index(a), EV.index(b)):8.0f}")
 pd = np.diff(tr[EV.index("P_START"), 10:100])
-print("producer batch period (256 rows):", float(np.median(pd)))
+print("producer batch period:", float(np.median(pd)))
+W = ["MMA<-producer(full)", "MMA<-WG1(dempty0)", "MMA<-WG1(dempty1)", "MMA<-WG0(hfull)", "MMA<-WG0(d1empty)",
+     "WG0<-producer(full)", "WG0<-MMA(d1full)", "WG0<-MMA(hfree)", "WG1<-producer(full)", "WG1<-MMA(dfull)",
+     "producer<-WG1(empty)", "kernel cycles (CTA0 MMA thread)"]
+w = tr[20]
+print("wait cycles, CTA 0 (fraction of kernel):")
+for i, nm in enumerate(W):
+    print(f"  {nm:34s} {int(w[i]):>10d}  {w[i] / max(1, w[11]):6.1%}")
