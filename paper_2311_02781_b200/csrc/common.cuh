@@ -135,6 +135,19 @@ struct Meta {  // view of one stage's metadata block
   uint8_t* grp;
 };
 
+// Query feature shape the producer is compiled for: NF fact-column features, ND0 / ND1 payload
+// features of probe 0 / 1 (in that order, kernel feature order), FM = float32 features bit mask.
+// GenericShape (NF = -1) reads all of it from QueryParams at run time.
+struct GenericShape {
+  static constexpr int NF = -1, ND0 = -1, ND1 = -1;
+  static constexpr uint64_t FM = 0;
+};
+template <int NF_, int ND0_, int ND1_, uint64_t FM_>
+struct FixedShape {
+  static constexpr int NF = NF_, ND0 = ND0_, ND1 = ND1_;
+  static constexpr uint64_t FM = FM_;
+};
+
 // The ring of X stages the producer fills: S stages of [128 rows x K0P] bf16 (interleaved K-major)
 // plus a metadata block per stage (count, fact row id, sum value, group code).
 constexpr uint32_t kMetaBytes = 16 + 4 * kTile + 4 * kTile + kTile;

@@ -136,6 +136,8 @@ int grid_for(int64_t n, int threads = 256) {
 using KernelFn = void (*)(const QueryParams);
 struct KernelEntry {
   int K0P, H, NL;
+  int nf, nd0, nd1;          // specialised feature shape (nf = -1: generic)
+  uint64_t fm;
   KernelFn fn;
   uint32_t smem;
   bool attr_set;
@@ -159,18 +161,34 @@ constexpr bool plan_fits() {
   X(16, 64, 1) X(16, 128, 1) X(16, 256, 1) X(32, 64, 1) X(32, 128, 1) X(32, 256, 1) X(48, 64, 1) X(48, 128, 1) \
   X(48, 256, 1) X(16, 64, 2) X(16, 128, 2) X(16, 256, 2) X(32, 64, 2) X(32, 128, 2) X(48, 64, 2) X(48, 128, 2)
 
-#define FLERN_ENTRY(a, b, c) {a, b, c, flern_query_kernel<a, b, c>, SmemPlan<a, b, c>::total, false},
+#define FLERN_ENTRY(a, b, c) {a, b, c, -1, -1, -1, 0, flern_query_kernel<a, b, c, GenericShape>, SmemPlan<a, b, c>::total, false},
 #define FLERN_WIDE_KERNELS(X) X(16, 512, 2) X(16, 1024, 2) X(16, 1024, 3) X(32, 512, 2) X(32, 1024, 2) X(32, 1024, 3) \
   X(48, 1024, 2) X(48, 1024, 3)
 #define FLERN_WIDE_ENTRY(a, b, c) \
-  {a, b, c, flern_query_wide_kernel<a, b, c>, WidePlan<a, b, c>::total, false, kThreadsWide, WidePlan<a, b, c>::scratch_per_cta},
-KernelEntry g_kernels[] = {FLERN_KERNELS(FLERN_ENTRY) FLERN_WIDE_KERNELS(FLERN_WIDE_ENTRY)};
+  {a, b, c, -1, -1, -1, 0, flern_query_wide_kernel<a, b, c, GenericShape>, WidePlan<a, b, c>::total, false, \
+   kThreadsWide, WidePlan<a, b, c>::scratch_per_cta},
+// Producer specialised for the benchmark query shapes (SURVEY.md §8(d) feature lists, kernel order
+// fact-first): C1 = 6 fact + 2 orders; C2 = 12 fact + 4 orders (o_f0 float); C3/C4 = 20 fact
+// (l_f0..5 float) + 8 orders (o_f0..4 float) + 4 customer (c_f0 float).
+#define FLERN_SPEC(a, b, c, nf, n0, n1, fm) {a, b, c, nf, n0, n1, fm, flern_query_kernel<a, b, c, FixedShape<nf, n0, n1, fm>>, \
+   SmemPlan<a, b, c>::total, false},
+#define FLERN_WSPEC(a, b, c, nf, n0, n1, fm) {a, b, c, nf, n0, n1, fm, \
+   flern_query_wide_kernel<a, b, c, FixedShape<nf, n0, n1, fm>>, WidePlan<a, b, c>::total, false, kThreadsWide, \
+   WidePlan<a, b, c>::scratch_per_cta},
+constexpr uint64_t kC2Mask = 1ull << 15;
+constexpr uint64_t kC3Mask = (0x3Full << 14) | (0x1Full << 23) | (1ull << 31);
+KernelEntry g_kernels[] = {FLERN_KERNELS(FLERN_ENTRY) FLERN_WIDE_KERNELS(FLERN_WIDE_ENTRY)
+                           FLERN_SPEC(16, 64, 1, 6, 2, 0, 0ull) FLERN_SPEC(16, 256, 2, 12, 4, 0, kC2Mask)
+                           FLERN_WSPEC(32, 1024, 3, 20, 8, 4, kC3Mask)};
 #define FLERN_FITS(a, b, c) static_assert(plan_fits<a, b, c>(), "plan");
 FLERN_KERNELS(FLERN_FITS)
 
-KernelEntry* find_kernel(int K0P, int H, int NL) {
+KernelEntry* find_kernel(int K0P, int H, int NL, int nf = -1, int nd0 = -1, int nd1 = -1, uint64_t fm = 0) {
+  if (nf >= 0 && !getenv("FLERN_GENERIC_ONLY"))
+    for (auto& e : g_kernels)   // a producer specialised for exactly this feature shape
+      if (e.K0P == K0P && e.H == H && e.NL == NL && e.nf == nf && e.nd0 == nd0 && e.nd1 == nd1 && e.fm == fm) return &e;
   for (auto& e : g_kernels)
-    if (e.K0P == K0P && e.H == H && e.NL == NL) return &e;
+    if (e.K0P == K0P && e.H == H && e.NL == NL && e.nf < 0) return &e;
   return nullptr;
 }
 
@@ -664,9 +682,11 @@ extern "C" FLERN_API flern_status flern_run_query(flern_ctx* ctx, const flern_qu
   // kernel order: fact-column features first (one vector load per column before the probe),
   // then build-payload features; the model image's W1 columns follow the same permutation
   std::vector<int> perm;
-  for (int k = 0; k < q->nfeat; ++k) if (fq[k].src == 0) perm.push_back(k);
-  p.nfact = (int32_t)perm.size();
-  for (int k = 0; k < q->nfeat; ++k) if (fq[k].src != 0) perm.push_back(k);
+  int nsrc[3] = {0, 0, 0};
+  for (int src = 0; src < 3; ++src)
+    for (int k = 0; k < q->nfeat; ++k)
+      if (fq[k].src == src) { perm.push_back(k); ++nsrc[src]; }
+  p.nfact = nsrc[0];
   bool ident = true;
   const int32_t* any_fact_col = static_cast<const int32_t*>(fact.cols[0].dptr);
   for (int k = 0; k < kMaxFeat; ++k) { p.fcol[k] = any_fact_col; p.dword[k] = 0; }
@@ -719,7 +739,7 @@ extern "C" FLERN_API flern_status flern_run_query(flern_ctx* ctx, const flern_qu
   p.bout = m.bout;
   p.shift = reinterpret_cast<const float*>(img + m.off_shift);
   p.scale = reinterpret_cast<const float*>(img + m.off_scale);
-  KernelEntry* ke = find_kernel(m.K0P, m.H, m.NL);
+  KernelEntry* ke = find_kernel(m.K0P, m.H, m.NL, nsrc[0], nsrc[1], nsrc[2], p.fmask);
   if (!ke) return fail(ctx, FLERN_E_UNSUPPORTED, "no kernel for model '%s'", m.name.c_str());
 
   CUDA_TRY(ctx, cudaSetDevice(ctx->device));

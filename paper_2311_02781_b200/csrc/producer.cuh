@@ -29,10 +29,15 @@ struct ProdState {
 
 // One batch: rows [row0, row0 + R) of this thread (consecutive; with R == 1 any row id), in[r] =
 // the row takes part (inside the shard and past the pre-filter).
-template <int K0P, int S, int R>
+template <int K0P, int S, int R, class SH>
 __device__ __forceinline__ void produce_batch(ProdState& st, const QueryParams& p, const XRing& ring, int32_t* wcnt,
                                               const float* s_normf, int64_t row0, bool whole, const bool (&in)[R],
                                               int bidx, int64_t row_end, int t, int warp, int lane) {
+  constexpr bool kSpec = SH::NF >= 0;   // feature shape known at compile time
+  const int nfact = kSpec ? SH::NF : p.nfact;
+  const int nfeat = kSpec ? SH::NF + SH::ND0 + SH::ND1 : p.nfeat;
+  const uint64_t fmask = kSpec ? SH::FM : p.fmask;
+  const uint64_t dprobe1 = kSpec ? ((SH::ND1 > 0 ? ((1ull << SH::ND1) - 1) : 0ull) << (SH::NF + SH::ND0)) : p.dprobe1;
     // Loads are plain read-only loads whose ADDRESS is selected (a 64-byte zero dummy when the
     // value is not needed): no predicates, no branches, so the compiler issues a batch's loads
     // back to back and they overlap; the dummy stays in L1.
@@ -64,8 +69,8 @@ __device__ __forceinline__ void produce_batch(ProdState& st, const QueryParams& 
     const float4* s_norm = reinterpret_cast<const float4*>(s_normf);
     auto cvt_pair = [&](int k, int32_t a, int32_t b) -> uint32_t {   // normalise + bf16-pack features k, k+1
       const float4 nm = s_norm[k / 2];
-      const float fa = ((p.fmask >> k) & 1) ? __int_as_float(a) : (float)a;
-      const float fb = ((p.fmask >> (k + 1)) & 1) ? __int_as_float(b) : (float)b;
+      const float fa = ((fmask >> k) & 1) ? __int_as_float(a) : (float)a;
+      const float fb = ((fmask >> (k + 1)) & 1) ? __int_as_float(b) : (float)b;
       const float2 y = fma2(make_float2(fa, fb), make_float2(nm.x, nm.y), make_float2(nm.z, nm.w));
       return bf16x2(y.x, y.y);
     };
@@ -82,7 +87,7 @@ __device__ __forceinline__ void produce_batch(ProdState& st, const QueryParams& 
       loadR(p.grp.base, row0, whole, any && p.grp.src == 0, gv);
       loadR(p.sum.base, row0, whole, any && p.sum.src == 0, sv);
 #pragma unroll
-      for (int k = 0; k < K0P; ++k) loadR(p.fcol[k], row0, whole, any && k < p.nfact, v[k]);
+      for (int k = 0; k < K0P; ++k) loadR(p.fcol[k], row0, whole, any && k < nfact, v[k]);
       // 2. probes, bucketised linear probing: the aligned 4-slot bucket (a 32-byte
       //    sector) holding the home slot is read with two 16-byte loads and resolved with selects;
       //    only a row that meets neither its key nor an empty slot there continues (rare, warp-
@@ -165,7 +170,7 @@ __device__ __forceinline__ void produce_batch(ProdState& st, const QueryParams& 
         if (p.sum.src > 0) sv[r] = ld1((p.sum.src == 1 ? rb0 : rb1) + p.sum.word, valid[r]);
 #pragma unroll
         for (int k = 0; k < K0P; ++k)
-          if (k >= p.nfact && k < p.nfeat) v[k][r] = ld1((((p.dprobe1 >> k) & 1) ? rb1 : rb0) + p.dword[k], valid[r]);
+          if (k >= nfact && k < nfeat) v[k][r] = ld1((((dprobe1 >> k) & 1) ? rb1 : rb0) + p.dword[k], valid[r]);
       }
       // 4. normalise in fp32 (fma(x, scale, -shift*scale), reading Q4) -> packed bf16 pairs
       uint32_t pk[R][K0P / 2];
@@ -240,7 +245,7 @@ __device__ __forceinline__ void produce_batch(ProdState& st, const QueryParams& 
       }
 }
 
-template <int K0P, int S>
+template <int K0P, int S, class SH>
 __device__ __forceinline__ void producer_loop(const QueryParams& p, const XRing& ring, int32_t* wcnt,
                                               const float* s_normf, int64_t* s_cnt, int32_t* queue,
                                               int64_t row_begin, int64_t row_end, int tid, int warp, int lane) {
@@ -258,7 +263,7 @@ __device__ __forceinline__ void producer_loop(const QueryParams& p, const XRing&
       bool in[R];
 #pragma unroll
       for (int r = 0; r < R; ++r) in[r] = row0 + r < row_end;
-      produce_batch<K0P, S, R>(st, p, ring, wcnt, s_normf, row0, row0 + R <= row_end, in, bidx, row_end, t, warp, lane);
+      produce_batch<K0P, S, R, SH>(st, p, ring, wcnt, s_normf, row0, row0 + R <= row_end, in, bidx, row_end, t, warp, lane);
     }
   } else {
     int nq = 0;        // survivors queued (uniform across the producer group)
@@ -322,7 +327,7 @@ __device__ __forceinline__ void producer_loop(const QueryParams& p, const XRing&
         const bool in1[1] = {t < nq};
         const int64_t row = in1[0] ? (int64_t)queue[t] : 0;
         if (t == 0) FLERN_TRACE(TR_P_START, bidx);
-        produce_batch<K0P, S, 1>(st, p, ring, wcnt, s_normf, row, true, in1, bidx, row_end, t, warp, lane);
+        produce_batch<K0P, S, 1, SH>(st, p, ring, wcnt, s_normf, row, true, in1, bidx, row_end, t, warp, lane);
         ++bidx;
         const int taken = min(nq, kProducerThreads);
         // shift the rest of the queue to the front

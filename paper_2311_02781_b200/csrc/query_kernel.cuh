@@ -62,7 +62,7 @@ __device__ __forceinline__ Meta meta_of(uint8_t* base, int s) {
               reinterpret_cast<int32_t*>(m + 16 + 4 * kTile), m + 16 + 8 * kTile};
 }
 
-template <int K0P, int H, int NL>
+template <int K0P, int H, int NL, class SH>
 __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_constant__ QueryParams p) {
   using P = SmemPlan<K0P, H, NL>;
   constexpr int S = P::S;
@@ -129,7 +129,7 @@ __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_c
   const int64_t row_end = min(p.nrows, row_begin + p.rows_per_cta);
 
   if (warp < 4) {
-    producer_loop<K0P, S>(p, XRing{smem + P::off_x, P::XS, smem + P::off_meta, full, empty}, wcnt, s_shift, s_cnt,
+    producer_loop<K0P, S, SH>(p, XRing{smem + P::off_x, P::XS, smem + P::off_meta, full, empty}, wcnt, s_shift, s_cnt,
                           reinterpret_cast<int32_t*>(smem + P::off_queue), row_begin, row_end, tid, warp, lane);
   } else if (warp == 12) {
     // =============================== MMA ISSUER =============================================

@@ -75,7 +75,7 @@ __device__ __forceinline__ void st_global_v4(void* ptr, uint32_t a, uint32_t b, 
   asm volatile("st.global.v4.b32 [%0], {%1,%2,%3,%4};" ::"l"(ptr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
 }
 
-template <int K0P, int H, int NL>
+template <int K0P, int H, int NL, class SH>
 __global__ void __launch_bounds__(kThreadsWide, 1) flern_query_wide_kernel(const __grid_constant__ QueryParams p) {
   using P = WidePlan<K0P, H, NL>;
   constexpr int S = P::S, RS = P::RS, NCH = P::NCH, KB = P::KB;
@@ -131,7 +131,7 @@ __global__ void __launch_bounds__(kThreadsWide, 1) flern_query_wide_kernel(const
   const uint8_t* img_wh = p.wimg + P::img_w1;
 
   if (warp < 4) {
-    producer_loop<K0P, S>(p, XRing{smem + P::off_x, P::XS, smem + P::off_meta, xfull, xempty}, wcnt, s_norm, s_cnt,
+    producer_loop<K0P, S, SH>(p, XRing{smem + P::off_x, P::XS, smem + P::off_meta, xfull, xempty}, wcnt, s_norm, s_cnt,
                           reinterpret_cast<int32_t*>(smem + P::off_queue), row_begin, row_end, tid, warp, lane);
   } else if (warp == 13) {
     // =============================== LOADER (bulk copies into the operand ring) ==============

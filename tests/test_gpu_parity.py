@@ -293,3 +293,14 @@ def test_wide_mlp_configs(name, sf):
     assert r["scored"] > 0
     lt = H.linear_threshold_model(cfg)
     assert parity.check(cfg, db, lt)["band"] == 0
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c4p"])
+def test_generic_producer_path(name, monkeypatch):
+    """The benchmark shapes run a producer specialised for their feature layout; the same queries
+    through the generic (run-time shape) producer must give the same parity results."""
+    monkeypatch.setenv("FLERN_GENERIC_ONLY", "1")
+    sf = 0.1 if name == "c4p" else 0.004
+    cfg = D.with_sf(D.CONFIGS[name], sf, match_rate=0.9)
+    db = D.make_database(cfg)
+    parity.check(cfg, db, D.make_model(cfg, db))
