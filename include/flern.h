@@ -166,7 +166,8 @@ typedef struct {
   int32_t* dbg_match;      /* optional [fact rows * nprobes]: build row id of each probe, -1 = miss/not reached */
   uint32_t* dbg_selected;  /* optional bitmap [ceil(rows/32)]: bit set if selected */
   uint64_t* dbg_trace;     /* optional [FLERN_TRACE_EVENTS * 256] (device if RESULT_DEVICE): clock64 stamps of
-                              the pipeline hand-offs of CTA 0 (diagnostic; zero = event not reached) */
+                              the pipeline hand-offs of CTA 0, wait-cycle totals, and %globaltimer (ns) at
+                              start / setup done / loop end / exit of every CTA (diagnostic; zero = event not reached) */
   int64_t rows_scanned, rows_joined, rows_scored, rows_selected; /* filled unless FLERN_Q_ASYNC */
   float elapsed_ms;        /* device time of the query kernel (CUDA events), unless FLERN_Q_ASYNC */
 } flern_result;
@@ -176,7 +177,7 @@ typedef struct {
  * and counted in counters[3]. */
 FLERN_API flern_status flern_run_query(flern_ctx* ctx, const flern_query* q, flern_result* res);
 
-#define FLERN_TRACE_EVENTS 21
+#define FLERN_TRACE_EVENTS 25
 
 /* Number of CUDA kernels flern_run_query launches per call (for launch accounting): 1. */
 FLERN_API int32_t flern_query_launches(void);

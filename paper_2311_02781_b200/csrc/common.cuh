@@ -16,6 +16,7 @@ constexpr int kProducerThreads = 128;
 __host__ __device__ constexpr int rows_per_thread(int K0P) { return K0P <= 16 ? 2 : 1; }
 __host__ __device__ constexpr int batch_rows(int K0P) { return kProducerThreads * rows_per_thread(K0P); }
 constexpr int32_t kEmptyKey = (int32_t)0x80000000;         // INT32_MIN marks an empty slot
+constexpr int kScanChunkRows = 1024;                       // pre-filter scan chunk (4 rows x 2 x 128 threads)
 constexpr int kCounters = 4;                               // scanned, joined(=scored), selected, bad_group
 
 // Slot of `key`: mode 1 = order-preserving range hash (kmin..kmax spread linearly over the
@@ -52,7 +53,10 @@ struct ColDesc {            // a column reference resolved to base pointer + row
 
 struct QueryParams {
   int64_t nrows;            // fact rows (< 2^31)
-  int64_t rows_per_cta;     // multiple of batch_rows(K0P)
+  unsigned long long* work; // chunk-claim counter (guided distribution, see chunk_rows); zero between launches
+  int64_t claim_big;        // rows per "big" chunk (multiple of claim_small); chunks [0, claim_nbig) are big
+  int64_t claim_nbig;       // 2 x grid, or 0 for small inputs
+  int64_t claim_small;      // rows per later chunk: batch_rows(K0P), or kScanChunkRows with a pre-filter
   int32_t nprobes;
   ProbeDesc probe[kMaxProbes];
   const int32_t* pf_col;    // nullptr = no pre-filter
@@ -79,8 +83,8 @@ struct QueryParams {
   float bout;
   const float* shift;       // [K0P]  c_k = -shift_k * scale_k (the gather computes fma(x, scale, c))
   const float* scale;       // [K0P]
-  int64_t* partials;        // [gridDim.x][ngroups*4 + kCounters]
-  unsigned int* ticket;     // zero between launches (the last CTA resets it)
+  unsigned long long* partials;  // [ngroups*4 + kCounters] atomic accumulators; zero between launches
+  unsigned int* ticket;     // zero between launches (the last CTA resets it, with work and partials)
   int64_t* out_count;       // [ngroups] (x2 both classes)
   int64_t* out_sum;
   int64_t* out_counters;    // [kCounters]
@@ -98,6 +102,7 @@ enum TraceEv {
   TR_W1_FULL, TR_W1_DFULL0, TR_W1_DOTA, TR_W1_DFULL1, TR_W1_DOTB, TR_W1_AGG,
   TR_P_START, TR_P_PROBED, TR_P_GATHERED, TR_P_DONE,
   TR_WAITS,   // [category] accumulated wait cycles of CTA 0's role threads (see FLERN_WAIT)
+  TR_CTA_START, TR_CTA_SETUP, TR_CTA_LOOP_END, TR_CTA_EXIT,   // [cta]: %globaltimer (ns) of every CTA < kTraceTiles
   kTraceEvents
 };
 // wait categories for TR_WAITS
@@ -105,6 +110,12 @@ enum WaitCat {
   W_MMA_FULL, W_MMA_DEMPTY0, W_MMA_DEMPTY1, W_MMA_HFULL, W_MMA_D1EMPTY, W_WG0_FULL, W_WG0_D1FULL, W_WG0_HFREE,
   W_WG1_FULL, W_WG1_DFULL, W_PROD_EMPTY, W_KERNEL
 };
+#define FLERN_CTA_STAMP(ev)                                                                       \
+  do {                                                                                           \
+    if (p.dbg_trace && threadIdx.x == 0 && blockIdx.x < kTraceTiles)                             \
+      p.dbg_trace[(ev) * kTraceTiles + blockIdx.x] = globaltimer_ns();                            \
+  } while (0)
+
 // mbar_wait that (when tracing, CTA 0, the role's first lane) adds its wait time to TR_WAITS[cat].
 // Compiled in only with -DFLERN_TRACE_WAITS (diagnostic builds): it costs registers in the hot loop.
 #ifndef FLERN_TRACE_WAITS
@@ -164,16 +175,26 @@ __device__ __forceinline__ Meta meta_at(uint8_t* meta, int s) {
               reinterpret_cast<int32_t*>(m + 16 + 4 * kTile), m + 16 + 8 * kTile};
 }
 
-// Predicate + group-by of one 128-row tile, one thread per row (a warpgroup covers the tile):
-// warp ballot per present (group, class), popc rows and a split 16-bit redux sum, accumulated in
-// registers (lane l owns groups l and l+32, both classes) and flushed to SMEM once per CTA.
+// Predicate + group-by of one 128-row tile, one thread per row (a warpgroup covers the tile).
+// Small group domains (ngroups <= kFastGroups, e.g. the 5 order priorities): every thread keeps
+// per-group count/sum registers for the rows it owns across all tiles (predicated adds, no
+// cross-lane traffic in the per-tile path) and the warp reduces them once per CTA. Larger domains:
+// a warp ballot per present (group, class) with popc rows and a split 16-bit redux sum, into
+// registers of the owning lane (lane l owns groups l and l+32).
+constexpr int kFastGroups = 8;
 struct GroupAgg {
-  unsigned long long ac[2][2], as[2][2];
+  unsigned long long ac[2][2], as[2][2];      // ballot path
+  uint32_t fc[2][kFastGroups];                // fast path: [class][group] row counts (this thread)
+  long long fs[2][kFastGroups];               // fast path: sums
   __device__ __forceinline__ void init() {
 #pragma unroll
     for (int u = 0; u < 2; ++u)
 #pragma unroll
       for (int c = 0; c < 2; ++c) { ac[u][c] = 0ull; as[u][c] = 0ull; }
+#pragma unroll
+    for (int c = 0; c < 2; ++c)
+#pragma unroll
+      for (int g = 0; g < kFastGroups; ++g) { fc[c][g] = 0u; fs[c][g] = 0ll; }
   }
   // releases the X stage (empty barrier) as soon as the metadata has been read
   __device__ __forceinline__ void tile(const QueryParams& p, const Meta& m, int count, int r, int lane, float logit,
@@ -189,6 +210,17 @@ struct GroupAgg {
     if (lane == 0) mbar_arrive(empty_bar);
     const int cls = sel ? 0 : 1;
     const bool agg = valid && g != 255 && (sel || p.both_classes);
+    if (p.ngroups <= kFastGroups) {
+#pragma unroll
+      for (int gg = 0; gg < kFastGroups; ++gg) {
+        const bool h0 = agg && g == gg && cls == 0, h1 = agg && g == gg && cls == 1;
+        fc[0][gg] += h0 ? 1u : 0u;
+        fs[0][gg] += h0 ? (long long)val : 0ll;
+        fc[1][gg] += h1 ? 1u : 0u;
+        fs[1][gg] += h1 ? (long long)val : 0ll;
+      }
+      return;
+    }
     uint32_t pending = __ballot_sync(0xffffffffu, agg);
     while (pending) {
       const int leader = __ffs(pending) - 1;
@@ -211,6 +243,25 @@ struct GroupAgg {
     }
   }
   __device__ __forceinline__ void flush(unsigned long long* acc, int lane, int ngroups) {
+    if (ngroups <= kFastGroups) {
+#pragma unroll
+      for (int c = 0; c < 2; ++c)
+#pragma unroll
+        for (int g = 0; g < kFastGroups; ++g) {
+          unsigned long long n = fc[c][g];
+          long long v = fs[c][g];
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) {
+            n += __shfl_xor_sync(0xffffffffu, n, o);
+            v += __shfl_xor_sync(0xffffffffu, v, o);
+          }
+          if (lane == 0 && g < ngroups && n) {
+            atomicAdd(&acc[g * 4 + c * 2 + 0], n);
+            atomicAdd(&acc[g * 4 + c * 2 + 1], (unsigned long long)v);
+          }
+        }
+      return;
+    }
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
       const int g = lane + 32 * u;
@@ -225,22 +276,47 @@ struct GroupAgg {
   }
 };
 
-// Per-CTA partials -> global; the last CTA to finish (atomic ticket) reduces them in CTA order.
+// Guided work distribution. Rows are handed out as numbered chunks from the global counter
+// p.work. Chunks [0, 2*grid) split the first ~85% of the rows into contiguous halves of one static
+// share per CTA (each CTA claims two adjacent ones at setup, so it streams one contiguous range);
+// later chunks are small (one producer batch, or one pre-filter scan chunk) and go to whichever CTA
+// asks first, so CTAs that run slower (e.g. farther from the L2 slices holding the hash table) take
+// fewer of them instead of setting the kernel's tail. Each claim is one atomicAdd, issued a chunk
+// ahead so its latency hides under the chunk in flight. Chunk starts are multiples of claim_small,
+// which keeps the vector loads aligned.
+struct RowChunk { int64_t lo, hi; };
+__device__ __forceinline__ RowChunk chunk_rows(const QueryParams& p, int64_t i) {
+  int64_t lo, hi;
+  if (i < p.claim_nbig) {
+    lo = i * p.claim_big;
+    hi = lo + p.claim_big;
+  } else {
+    lo = p.claim_nbig * p.claim_big + (i - p.claim_nbig) * p.claim_small;
+    hi = lo + p.claim_small;
+  }
+  return RowChunk{min(lo, p.nrows), min(hi, p.nrows)};
+}
+__device__ __forceinline__ int64_t claim_chunk(const QueryParams& p, int64_t k) {
+  return (int64_t)atomicAdd(p.work, (unsigned long long)k);
+}
+
+// Per-CTA totals -> global atomic accumulators (a few dozen atomics per CTA); the last CTA to
+// finish (atomic ticket) copies them out and zeroes them, the ticket and the work counter for the
+// next launch. Integer sums, so the result does not depend on the order of CTAs.
 __device__ __forceinline__ void write_partials_and_reduce(const QueryParams& p, unsigned long long* acc,
-                                                          int64_t* s_cnt, unsigned int* s_is_last,
-                                                          int64_t row_begin, int64_t row_end, int tid,
+                                                          int64_t* s_cnt, unsigned int* s_is_last, int tid,
                                                           int nthreads) {
   const int G = p.ngroups;
   const int W = G * 4 + kCounters;
-  int64_t* mine = p.partials + (int64_t)blockIdx.x * W;
-  for (int i = tid; i < G * 4; i += nthreads) mine[i] = (int64_t)acc[i];
+  for (int i = tid; i < G * 4; i += nthreads)
+    if (acc[i]) atomicAdd(&p.partials[i], acc[i]);
   if (tid == 0) {
-    int64_t sel = 0;
-    for (int g = 0; g < G; ++g) sel += (int64_t)acc[g * 4 + 0];
-    mine[G * 4 + 0] = row_end > row_begin ? row_end - row_begin : 0;
-    mine[G * 4 + 1] = s_cnt[1];
-    mine[G * 4 + 2] = sel;
-    mine[G * 4 + 3] = s_cnt[3];
+    unsigned long long sel = 0;
+    for (int g = 0; g < G; ++g) sel += acc[g * 4 + 0];
+    const unsigned long long c[kCounters] = {(unsigned long long)s_cnt[0], (unsigned long long)s_cnt[1], sel,
+                                             (unsigned long long)s_cnt[3]};
+    for (int i = 0; i < kCounters; ++i)
+      if (c[i]) atomicAdd(&p.partials[G * 4 + i], c[i]);
     __threadfence();
     const unsigned int prev = atomicAdd(p.ticket, 1u);
     *s_is_last = (prev == gridDim.x - 1) ? 1u : 0u;
@@ -249,8 +325,7 @@ __device__ __forceinline__ void write_partials_and_reduce(const QueryParams& p, 
   if (*s_is_last) {
     __threadfence();
     for (int i = tid; i < W; i += nthreads) {
-      int64_t t = 0;
-      for (int b = 0; b < (int)gridDim.x; ++b) t += *((volatile int64_t*)(p.partials + (int64_t)b * W + i));
+      const int64_t t = (int64_t)atomicExch(&p.partials[i], 0ull);
       if (i < G * 4) {
         const int g = i / 4, cls = (i / 2) & 1, kind = i & 1;
         if (cls == 0 || p.both_classes) {
@@ -261,8 +336,9 @@ __device__ __forceinline__ void write_partials_and_reduce(const QueryParams& p, 
         p.out_counters[i - G * 4] = t;
       }
     }
-    if (tid == 0) *p.ticket = 0u;
+    if (tid == 0) { *p.ticket = 0u; *p.work = 0ull; }
   }
+  FLERN_CTA_STAMP(TR_CTA_EXIT);
 }
 
 }  // namespace flern

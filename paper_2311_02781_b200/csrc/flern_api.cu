@@ -86,7 +86,7 @@ struct flern_ctx {
   std::vector<Model> models;
   std::vector<HashTable> hts;
   // query scratch
-  int64_t* partials = nullptr;
+  int64_t* partials = nullptr;   // [kMaxGroups*4 + kCounters] global accumulators (zero between launches)
   unsigned int* ticket = nullptr;
   int64_t* dres = nullptr;        // [2*kMaxGroups count | 2*kMaxGroups sum | kCounters]
   int32_t* dflags = nullptr;      // build flags
@@ -220,7 +220,8 @@ extern "C" FLERN_API flern_status flern_create(int device, void* cuda_stream, fl
     ctx->own_stream = true;
   }
   const size_t W = (size_t)kMaxGroups * 4 + kCounters;
-  if (cudaMalloc(&ctx->partials, (size_t)ctx->num_sms * W * sizeof(int64_t)) != cudaSuccess) return FLERN_E_OOM;
+  if (cudaMalloc(&ctx->partials, W * sizeof(int64_t)) != cudaSuccess) return FLERN_E_OOM;
+  if (cudaMemsetAsync(ctx->partials, 0, W * sizeof(int64_t), ctx->stream) != cudaSuccess) return FLERN_E_CUDA;
   if (cudaMalloc(&ctx->ticket, 64) != cudaSuccess) return FLERN_E_OOM;
   if (cudaMalloc(&ctx->dres, (4 * kMaxGroups + kCounters) * sizeof(int64_t)) != cudaSuccess) return FLERN_E_OOM;
   if (cudaMalloc(&ctx->dflags, 64) != cudaSuccess) return FLERN_E_OOM;
@@ -751,8 +752,9 @@ extern "C" FLERN_API flern_status flern_run_query(flern_ctx* ctx, const flern_qu
   p.out_count = d_count;
   p.out_sum = d_sum;
   p.out_counters = d_counters;
-  p.partials = ctx->partials;
+  p.partials = reinterpret_cast<unsigned long long*>(ctx->partials);
   p.ticket = ctx->ticket;
+  p.work = reinterpret_cast<unsigned long long*>(ctx->ticket) + 1;
   // debug exports: device pointers as given, or temporary device buffers copied back
   const int64_t n = fact.nrows;
   float* d_score = nullptr;
@@ -797,12 +799,13 @@ extern "C" FLERN_API flern_status flern_run_query(flern_ctx* ctx, const flern_qu
   p.dbg_match = d_match;
   p.dbg_selected = d_sel;
 
-  const int64_t batch = batch_rows(m.K0P);
-  int grid = (int)std::min<int64_t>(ctx->num_sms, std::max<int64_t>(1, (n + batch - 1) / batch));
-  int64_t per = (n + grid - 1) / grid;
-  per = (per + batch - 1) / batch * batch;
-  if (per < batch) per = batch;
-  p.rows_per_cta = per;
+  // one persistent CTA per SM; rows are claimed as chunks (guided schedule, chunk_rows in common.cuh):
+  // 2*grid contiguous halves of an 85% static share, then small chunks on demand
+  const int64_t chunk = p.pf_col ? (int64_t)kScanChunkRows : (int64_t)batch_rows(m.K0P);
+  const int grid = (int)std::min<int64_t>(ctx->num_sms, std::max<int64_t>(1, (n + chunk - 1) / chunk));
+  p.claim_small = chunk;
+  p.claim_big = (int64_t)(0.85 * (double)n / (2.0 * grid)) / chunk * chunk;
+  p.claim_nbig = p.claim_big > 0 ? 2 * (int64_t)grid : 0;
   if (ke->scratch_per_cta) {   // wide kernel: per-CTA activation scratch
     const size_t need = (size_t)grid * ke->scratch_per_cta;
     if (ctx->scratch_bytes < need) {

@@ -248,29 +248,49 @@ __device__ __forceinline__ void produce_batch(ProdState& st, const QueryParams& 
 template <int K0P, int S, class SH>
 __device__ __forceinline__ void producer_loop(const QueryParams& p, const XRing& ring, int32_t* wcnt,
                                               const float* s_normf, int64_t* s_cnt, int32_t* queue,
-                                              int64_t row_begin, int64_t row_end, int tid, int warp, int lane) {
+                                              int64_t* s_claim, int tid, int warp, int lane) {
   constexpr int R = rows_per_thread(K0P);
   constexpr int kBatch = batch_rows(K0P);
   const int t = tid;   // 0..127
+  const int64_t n = p.nrows;
+  // claims (chunk indices, see chunk_rows): the CTA setup took chunks s_claim[0], s_claim[1]; chunk
+  // k+2 is claimed while chunk k is processed and published through s_claim[k & 1] (every chunk
+  // passes a producer barrier before its slot is rewritten)
+  RowChunk cur = chunk_rows(p, s_claim[0]), nxt = chunk_rows(p, s_claim[1]);
+  int k = 0;
+  auto advance = [&](int64_t a) {
+    if (t == 0) s_claim[k & 1] = a;
+    named_bar_sync(1, kProducerThreads);
+    cur = nxt;
+    nxt = chunk_rows(p, s_claim[k & 1]);
+    ++k;
+  };
   ProdState st{0, 0u, 0, 0, 0};
   mbar_wait(&ring.empty[0], ((st.acq / S) & 1) ^ 1, 1);   // acquire the first stage
   st.acq = 1;
+  int bidx = 0;
   if (!p.pf_col) {
-    for (int64_t base = row_begin; base < row_end; base += kBatch) {
-      const int bidx = (int)((base - row_begin) / kBatch);
-      if (t == 0) FLERN_TRACE(TR_P_START, bidx);
-      const int64_t row0 = base + (int64_t)R * t;
-      bool in[R];
+    while (cur.lo < n) {
+      int64_t a = 0;
+      if (t == 0) a = claim_chunk(p, 1);
+      const int64_t row_end = cur.hi;
+      if (t == 0) s_cnt[0] += row_end - cur.lo;   // rows scanned by this CTA
+      for (int64_t base = cur.lo; base < row_end; base += kBatch, ++bidx) {
+        if (t == 0) FLERN_TRACE(TR_P_START, bidx);
+        const int64_t row0 = base + (int64_t)R * t;
+        bool in[R];
 #pragma unroll
-      for (int r = 0; r < R; ++r) in[r] = row0 + r < row_end;
-      produce_batch<K0P, S, R, SH>(st, p, ring, wcnt, s_normf, row0, row0 + R <= row_end, in, bidx, row_end, t, warp, lane);
+        for (int r = 0; r < R; ++r) in[r] = row0 + r < row_end;
+        produce_batch<K0P, S, R, SH>(st, p, ring, wcnt, s_normf, row0, row0 + R <= row_end, in, bidx, row_end, t, warp, lane);
+      }
+      advance(a);
     }
   } else {
+    static_assert(kScanChunk == kScanChunkRows, "scan chunk");
     int nq = 0;        // survivors queued (uniform across the producer group)
-    int bidx = 0;
     // scan rows cb + 4t + 512j (j = 0, 1; each warp instruction covers 512 contiguous rows); the
     // next chunk's loads are issued before this chunk is compacted (software pipeline)
-    auto scan_load = [&](int64_t cb, int32_t (&x)[8]) {
+    auto scan_load = [&](int64_t cb, int64_t row_end, int32_t (&x)[8]) {
 #pragma unroll
       for (int j = 0; j < 2; ++j) {
         const int64_t r0 = cb + 4 * t + 512 * j;
@@ -284,62 +304,71 @@ __device__ __forceinline__ void producer_loop(const QueryParams& p, const XRing&
       }
     };
     int32_t xnext[8];
-    if (row_begin < row_end) scan_load(row_begin, xnext);
-    for (int64_t cb = row_begin; cb < row_end; cb += kScanChunk) {
-      int32_t x[8];
+    if (cur.lo < n) scan_load(cur.lo, cur.hi, xnext);
+    while (cur.lo < n) {
+      int64_t a = 0;
+      if (t == 0) a = claim_chunk(p, 1);
+      if (t == 0) s_cnt[0] += cur.hi - cur.lo;   // rows scanned by this CTA
+      for (int64_t cb = cur.lo; cb < cur.hi; cb += kScanChunk) {
+        const int64_t row_end = cur.hi;
+        const bool last_block = cb + kScanChunk >= cur.hi;
+        int32_t x[8];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) x[u] = xnext[u];
-      if (cb + kScanChunk < row_end) scan_load(cb + kScanChunk, xnext);
-      uint32_t bits = 0;
+        for (int u = 0; u < 8; ++u) x[u] = xnext[u];
+        if (!last_block) scan_load(cb + kScanChunk, cur.hi, xnext);
+        else if (nxt.lo < n) scan_load(nxt.lo, nxt.hi, xnext);
+        uint32_t bits = 0;
 #pragma unroll
-      for (int j = 0; j < 2; ++j)
+        for (int j = 0; j < 2; ++j)
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int64_t rr = cb + 4 * t + 512 * j + u;
-          if (rr < row_end && p.pf_lo <= x[4 * j + u] && x[4 * j + u] < p.pf_hi) bits |= 1u << (4 * j + u);
+          for (int u = 0; u < 4; ++u) {
+            const int64_t rr = cb + 4 * t + 512 * j + u;
+            if (rr < row_end && p.pf_lo <= x[4 * j + u] && x[4 * j + u] < p.pf_hi) bits |= 1u << (4 * j + u);
+          }
+        const int my = __popc(bits);
+        int incl = my;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int x = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += x;
         }
-      const int my = __popc(bits);
-      int incl = my;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int x = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += x;
-      }
-      if (lane == 31) wcnt[8 + warp] = incl;
-      named_bar_sync(1, kProducerThreads);
-      int woff = 0, total = 0;
-#pragma unroll
-      for (int w = 0; w < 4; ++w) {
-        const int c = wcnt[8 + w];
-        woff += (w < warp) ? c : 0;
-        total += c;
-      }
-      int pos = nq + woff + incl - my;
-#pragma unroll
-      for (int j = 0; j < 2; ++j)
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-          if (bits & (1u << (4 * j + u))) queue[pos++] = (int32_t)(cb + 4 * t + 512 * j + u);
-      nq += total;
-      named_bar_sync(1, kProducerThreads);   // queue written (and wcnt[8..] read) by all
-      const bool last = cb + kScanChunk >= row_end;
-      while (nq >= kProducerThreads || (last && nq > 0)) {
-        const bool in1[1] = {t < nq};
-        const int64_t row = in1[0] ? (int64_t)queue[t] : 0;
-        if (t == 0) FLERN_TRACE(TR_P_START, bidx);
-        produce_batch<K0P, S, 1, SH>(st, p, ring, wcnt, s_normf, row, true, in1, bidx, row_end, t, warp, lane);
-        ++bidx;
-        const int taken = min(nq, kProducerThreads);
-        // shift the rest of the queue to the front
-        int32_t keep[kQueueCap / kProducerThreads + 1];
-        int nk = 0;
-        for (int i = taken + t; i < nq; i += kProducerThreads) keep[nk++] = queue[i];
+        if (lane == 31) wcnt[8 + warp] = incl;
         named_bar_sync(1, kProducerThreads);
-        nk = 0;
-        for (int i = taken + t; i < nq; i += kProducerThreads) queue[i - taken] = keep[nk++];
-        nq -= taken;
-        named_bar_sync(1, kProducerThreads);
+        int woff = 0, total = 0;
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+          const int c = wcnt[8 + w];
+          woff += (w < warp) ? c : 0;
+          total += c;
+        }
+        int pos = nq + woff + incl - my;
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (bits & (1u << (4 * j + u))) queue[pos++] = (int32_t)(cb + 4 * t + 512 * j + u);
+        nq += total;
+        named_bar_sync(1, kProducerThreads);   // queue written (and wcnt[8..] read) by all
+        const bool last = last_block && nxt.lo >= n;
+        while (nq >= kProducerThreads || (last && nq > 0)) {
+          const bool in1[1] = {t < nq};
+          const int64_t row = in1[0] ? (int64_t)queue[t] : 0;
+          if (t == 0) FLERN_TRACE(TR_P_START, bidx);
+          produce_batch<K0P, S, 1, SH>(st, p, ring, wcnt, s_normf, row, true, in1, bidx, n, t, warp, lane);
+          ++bidx;
+          const int taken = min(nq, kProducerThreads);
+          // shift the rest of the queue to the front
+          int32_t keep[kQueueCap / kProducerThreads + 1];
+          int nk = 0;
+          for (int i = taken + t; i < nq; i += kProducerThreads) keep[nk++] = queue[i];
+          named_bar_sync(1, kProducerThreads);
+          nk = 0;
+          for (int i = taken + t; i < nq; i += kProducerThreads) queue[i - taken] = keep[nk++];
+          nq -= taken;
+          named_bar_sync(1, kProducerThreads);
+        }
       }
+      advance(a);
     }
   }
   if (st.fill > 0) {   // flush the partial tile

@@ -69,6 +69,10 @@ __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_c
   extern __shared__ __align__(1024) uint8_t smem[];
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
+  FLERN_CTA_STAMP(TR_CTA_START);
+  // first two row chunks (guided distribution, see chunk_rows); the atomic's latency hides under the setup
+  int64_t claim0 = 0;
+  if (tid == 0) claim0 = claim_chunk(p, 2);
 
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + P::off_bar);
   uint64_t* full = bars;            // [S]   producers -> MMA/epilogue (128 arrivals)
@@ -88,6 +92,7 @@ __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_c
   float* s_scale = s_shift + kMaxFeat;
   int64_t* s_cnt = reinterpret_cast<int64_t*>(smem + P::off_misc + 64);   // [kCounters]
   unsigned int* s_is_last = reinterpret_cast<unsigned int*>(smem + P::off_misc + 96);
+  int64_t* s_claim = reinterpret_cast<int64_t*>(smem + P::off_misc + 104);   // [2] row-chunk claims
 
   if ((smem_u32(smem) & 1023u) != 0) __trap();  // SW128 operands need a 1024-aligned base
 
@@ -107,6 +112,7 @@ __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_c
     }
     for (int i = tid; i < kMaxGroups * 4; i += kThreads) acc[i] = 0ull;
     if (tid < kCounters) s_cnt[tid] = 0;
+    if (tid == 0) { s_claim[0] = claim0; s_claim[1] = claim0 + 1; }
     fence_proxy_async_smem();   // weights written by st.shared are read by the tensor core
   }
   static_assert(S <= 4, "stage ring");
@@ -124,13 +130,12 @@ __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_c
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  FLERN_CTA_STAMP(TR_CTA_SETUP);
 
-  const int64_t row_begin = (int64_t)blockIdx.x * p.rows_per_cta;
-  const int64_t row_end = min(p.nrows, row_begin + p.rows_per_cta);
 
   if (warp < 4) {
     producer_loop<K0P, S, SH>(p, XRing{smem + P::off_x, P::XS, smem + P::off_meta, full, empty}, wcnt, s_shift, s_cnt,
-                          reinterpret_cast<int32_t*>(smem + P::off_queue), row_begin, row_end, tid, warp, lane);
+                          reinterpret_cast<int32_t*>(smem + P::off_queue), s_claim, tid, warp, lane);
   } else if (warp == 12) {
     // =============================== MMA ISSUER =============================================
     // NL == 2 issue order per tile t (steady state): L2a(t), L1(t+1), L2b(t). Layer 2 is split
@@ -392,8 +397,9 @@ __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_c
   // ---- teardown: per-CTA partials, last CTA reduces ----
   tc_fence_before();
   __syncthreads();
+  FLERN_CTA_STAMP(TR_CTA_LOOP_END);
   if (warp == 12) { tc_fence_after(); tmem_dealloc(tmem_base, kTmemCols); }
-  write_partials_and_reduce(p, acc, s_cnt, s_is_last, row_begin, row_end, tid, kThreads);
+  write_partials_and_reduce(p, acc, s_cnt, s_is_last, tid, kThreads);
 }
 
 }  // namespace flern

@@ -82,6 +82,10 @@ __global__ void __launch_bounds__(kThreadsWide, 1) flern_query_wide_kernel(const
   extern __shared__ __align__(1024) uint8_t smem[];
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
+  FLERN_CTA_STAMP(TR_CTA_START);
+  // first two row chunks (guided distribution, see chunk_rows); the atomic's latency hides under the setup
+  int64_t claim0 = 0;
+  if (tid == 0) claim0 = claim_chunk(p, 2);
 
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + P::off_bar);
   uint64_t* xfull = bars;             // [S] producers -> consumers (128)
@@ -95,6 +99,7 @@ __global__ void __launch_bounds__(kThreadsWide, 1) flern_query_wide_kernel(const
   int32_t* wcnt = reinterpret_cast<int32_t*>(smem + P::off_misc + 16);
   int64_t* s_cnt = reinterpret_cast<int64_t*>(smem + P::off_misc + 64);
   unsigned int* s_is_last = reinterpret_cast<unsigned int*>(smem + P::off_misc + 96);
+  int64_t* s_claim = reinterpret_cast<int64_t*>(smem + P::off_misc + 104);   // [2] row-chunk claims
   unsigned long long* acc = reinterpret_cast<unsigned long long*>(smem + P::off_acc);
   float* s_bias = reinterpret_cast<float*>(smem + P::off_bias);
   float* s_wout = reinterpret_cast<float*>(smem + P::off_wout);
@@ -113,6 +118,7 @@ __global__ void __launch_bounds__(kThreadsWide, 1) flern_query_wide_kernel(const
   }
   for (int i = tid; i < kMaxGroups * 4; i += kThreadsWide) acc[i] = 0ull;
   if (tid < kCounters) s_cnt[tid] = 0;
+  if (tid == 0) { s_claim[0] = claim0; s_claim[1] = claim0 + 1; }
   if (tid == 0) {
     for (int s = 0; s < S; ++s) { mbar_init(&xfull[s], kProducerThreads); mbar_init(&xempty[s], 4); }
     for (int s = 0; s < RS; ++s) { mbar_init(&rfull[s], 1); mbar_init(&rempty[s], 1); }
@@ -124,15 +130,14 @@ __global__ void __launch_bounds__(kThreadsWide, 1) flern_query_wide_kernel(const
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  const int64_t row_begin = (int64_t)blockIdx.x * p.rows_per_cta;
-  const int64_t row_end = min(p.nrows, row_begin + p.rows_per_cta);
+  FLERN_CTA_STAMP(TR_CTA_SETUP);
   uint8_t* scratch = p.scratch + (size_t)blockIdx.x * P::scratch_per_cta;   // act[0] | act[1]
   const uint8_t* img_w1 = p.wimg;
   const uint8_t* img_wh = p.wimg + P::img_w1;
 
   if (warp < 4) {
     producer_loop<K0P, S, SH>(p, XRing{smem + P::off_x, P::XS, smem + P::off_meta, xfull, xempty}, wcnt, s_norm, s_cnt,
-                          reinterpret_cast<int32_t*>(smem + P::off_queue), row_begin, row_end, tid, warp, lane);
+                          reinterpret_cast<int32_t*>(smem + P::off_queue), s_claim, tid, warp, lane);
   } else if (warp == 13) {
     // =============================== LOADER (bulk copies into the operand ring) ==============
     if (lane == 0) {
@@ -318,8 +323,9 @@ __global__ void __launch_bounds__(kThreadsWide, 1) flern_query_wide_kernel(const
 
   tc_fence_before();
   __syncthreads();
+  FLERN_CTA_STAMP(TR_CTA_LOOP_END);
   if (warp == 12) { tc_fence_after(); tmem_dealloc(tmem_base, 512); }
-  write_partials_and_reduce(p, acc, s_cnt, s_is_last, row_begin, row_end, tid, kThreadsWide);
+  write_partials_and_reduce(p, acc, s_cnt, s_is_last, tid, kThreadsWide);
 }
 
 }  // namespace flern

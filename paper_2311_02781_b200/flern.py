@@ -204,7 +204,7 @@ class Query:
         self.ngroups = ngroups
 
 
-TRACE_EVENTS = 21
+TRACE_EVENTS = 25
 TRACE_TILES = 256
 
 

@@ -49,3 +49,16 @@ w = tr[20]
 print("wait cycles, CTA 0 (fraction of kernel):")
 for i, nm in enumerate(W):
     print(f"  {nm:34s} {int(w[i]):>10d}  {w[i] / max(1, w[11]):6.1%}")
+# per-CTA timeline (%globaltimer, ns): start skew, loop-end spread (imbalance), final reduce
+st, su, le, ex = (tr[F.TRACE_EVENTS - 4], tr[F.TRACE_EVENTS - 3], tr[F.TRACE_EVENTS - 2], tr[F.TRACE_EVENTS - 1])
+n = int((st > 0).sum())
+if n:
+    st, su, le, ex = st[:n], su[:n], le[:n], ex[:n]
+    z = st.min()
+    print(f"CTAs {n}: start skew {(st.max() - z) / 1e3:.1f} us; setup median/max {np.median(su - st) / 1e3:.1f}/"
+          f"{(su - st).max() / 1e3:.1f} us; loop end min/median/max "
+          f"{(le.min() - z) / 1e3:.1f}/{np.median(le - z) / 1e3:.1f}/{(le.max() - z) / 1e3:.1f} us; "
+          f"last exit {(ex.max() - z) / 1e3:.1f} us; kernel (events) {r.elapsed_ms * 1e3:.1f} us")
+    order = np.argsort(le - st)
+    print("  slowest CTAs (loop us):", [(int(i), round(float(le[i] - st[i]) / 1e3, 1)) for i in order[-6:]])
+    print("  fastest CTAs (loop us):", [(int(i), round(float(le[i] - st[i]) / 1e3, 1)) for i in order[:6]])
