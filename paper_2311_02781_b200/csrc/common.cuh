@@ -16,6 +16,24 @@ constexpr int kProducerThreads = 128;
 __host__ __device__ constexpr int rows_per_thread(int K0P) { return K0P <= 16 ? 2 : 1; }
 __host__ __device__ constexpr int batch_rows(int K0P) { return kProducerThreads * rows_per_thread(K0P); }
 constexpr int32_t kEmptyKey = (int32_t)0x80000000;         // INT32_MIN marks an empty slot
+// Biases on the tensor core: every layer's accumulator is initialised by one extra K=16 MMA,
+// D = ONES x BIAS^T (accumulate off), before the layer's own MMAs accumulate onto it, so no
+// epilogue adds a bias. ONES (A, K-major, no swizzle) is one 16-byte row [1, 1, 0 x 6] that every
+// row of the 128-row tile aliases (SBO = 16 B), then a zero K-block (LBO = kOnesHalf). BIAS (B,
+// MN-major, no swizzle) keeps, per block of 8 neurons, the bf16 high parts then the bf16 low
+// parts (b - hi) of their biases (32 B per block, SBO = 32 B): rows k = 2..7 of each 128-byte
+// core matrix overlap the next blocks and the K = 8..15 block aliases the first (LBO = 0); both
+// only meet zeros of ONES, and the 96-byte zero tail keeps every byte read finite. hi + lo
+// carries the fp32 bias to ~2^-17 relative.
+constexpr uint32_t kOnesHalf = 16 * 16 + 112;                  // 16 aliased row blocks x 16 B + 7 rows
+constexpr uint32_t kOnesBytes = 2 * kOnesHalf;
+__host__ __device__ constexpr uint32_t bias_operand_bytes(int n) { return (uint32_t)(n / 8) * 32u + 96u; }
+__device__ __forceinline__ void fill_ones_operand(uint8_t* dst, int tid, int nthreads) {
+  uint32_t* w = reinterpret_cast<uint32_t*>(dst);
+  for (int i = tid; i < (int)kOnesBytes / 4; i += nthreads)
+    w[i] = (i * 4 < (int)kOnesHalf && (i & 3) == 0) ? 0x3F803F80u : 0u;   // bf16 1.0 at k = 0, 1
+}
+
 constexpr int kScanChunkRows = 1024;                       // pre-filter scan chunk (4 rows x 2 x 128 threads)
 constexpr int kCounters = 4;                               // scanned, joined(=scored), selected, bad_group
 

@@ -125,6 +125,13 @@ uint16_t bf16_rne_bits(float f) {
   return (uint16_t)(u >> 16);
 }
 
+float bf16_bits_to_float(uint16_t h) {
+  const uint32_t u = (uint32_t)h << 16;
+  float f;
+  std::memcpy(&f, &u, 4);
+  return f;
+}
+
 int grid_for(int64_t n, int threads = 256) {
   int64_t g = (n + threads - 1) / threads;
   if (g < 1) g = 1;
@@ -360,7 +367,8 @@ std::vector<uint8_t> model_image(Model& m, const std::vector<int>& perm) {
   const int H = m.H, K0 = m.K0, K0P = m.K0P, NL = m.NL;
   const size_t WH = NL >= 2 ? (size_t)H * H * 2 : 0;
   const size_t W1 = (size_t)H * K0P * 2;
-  m.wimg_bytes = WH + W1;
+  const size_t BB = bias_operand_bytes(H);
+  m.wimg_bytes = WH + W1 + (size_t)NL * BB;   // [Wh | W1 | bias B operands], see kOnesBytes
   m.off_bias = (m.wimg_bytes + 255) / 256 * 256;
   m.off_wout = m.off_bias + (size_t)NL * H * 4;
   m.off_shift = m.off_wout + (size_t)H * 4;
@@ -384,6 +392,17 @@ std::vector<uint8_t> model_image(Model& m, const std::vector<int>& perm) {
                            (size_t)((((k % 64) / 8) ^ (n % 8)) * 16) + (k % 8) * 2;
         wh[off / 2] = bf16_rne_bits(m.W[1][(size_t)n * H + k]);
       }
+  // bias B operands (MN-major): per 8-neuron block, 8 bf16 high parts then 8 bf16 low parts
+  for (int l = 0; l < NL; ++l) {
+    uint16_t* bb = reinterpret_cast<uint16_t*>(img.data() + WH + W1 + (size_t)l * BB);
+    for (int j = 0; j < H; ++j) {
+      const float b = m.b[l][j];
+      const uint16_t hi = bf16_rne_bits(b);
+      const float hif = bf16_bits_to_float(hi);
+      bb[(j / 8) * 16 + (j % 8)] = hi;
+      bb[(j / 8) * 16 + 8 + (j % 8)] = bf16_rne_bits(b - hif);
+    }
+  }
   float* bias = reinterpret_cast<float*>(img.data() + m.off_bias);
   for (int l = 0; l < NL; ++l)
     for (int j = 0; j < H; ++j) bias[l * H + j] = m.b[l][j];

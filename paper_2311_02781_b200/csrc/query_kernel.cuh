@@ -13,9 +13,9 @@
 // Warp roles (416 threads = 13 warps, 1 CTA per SM):
 //   warps 0-3   producers: 128 threads x R consecutive rows per batch; scan, pre-filter, probe,
 //               compact, gather + normalise + bf16 into the X stage ring (S stages of 128 rows)
-//   warps 4-7   epilogue warpgroup 0 (NL=2): D1 -> bias + ReLU -> bf16 -> H (layer-2 operand),
+//   warps 4-7   epilogue warpgroup 0 (NL=2): D1 (bias folded in by the MMA) -> ReLU -> bf16 -> H,
 //               handed to the MMA in 64-column K-chunks
-//   warps 8-11  epilogue warpgroup 1: D2 -> bias + ReLU -> dot(w_out) -> logit -> predicate ->
+//   warps 8-11  epilogue warpgroup 1: D2 -> ReLU -> dot(w_out) -> logit -> predicate ->
 //               group-by (NL=1: both warpgroups do this on alternate tiles)
 //   warp  12    TMEM allocator + single-thread tcgen05.mma issuer
 // An epilogue warp w may only touch TMEM lanes 32*(w%4) .. +31, hence warpgroup-aligned roles.
@@ -31,16 +31,18 @@ struct SmemPlan {
   static constexpr uint32_t W1 = (uint32_t)H * K0P * 2;                       // layer-1 W, interleave
   static constexpr uint32_t XS = (uint32_t)kTile * K0P * 2;                   // one X stage, interleave
   static constexpr uint32_t META = 16 + 4 * kTile + 4 * kTile + kTile;        // count, rowid, val, grp
-  static constexpr uint32_t FIXED = WH + HB + W1 + NL * H * 4 + H * 4 + kMaxGroups * 4 * 8 + kQueueBytes +
-                                    kMaxFeat * 8 + 64 * 8 + 128;
+  static constexpr uint32_t BB = bias_operand_bytes(H);                       // one layer's bias B operand
+  static constexpr uint32_t FIXED = WH + HB + W1 + kOnesBytes + NL * BB + H * 4 + kMaxGroups * 4 * 8 +
+                                    kQueueBytes + kMaxFeat * 8 + 64 * 8 + 128;
   static constexpr int S = (FIXED + 4 * (XS + META) <= 232448) ? 4 : 3;
   static constexpr uint32_t off_wh = 0;                                       // [Wh | W1] = weight image
   static constexpr uint32_t off_w1 = off_wh + WH;
   static constexpr uint32_t off_hb = off_w1 + W1;
   static constexpr uint32_t off_x = off_hb + HB;
   static constexpr uint32_t off_meta = off_x + S * XS;
-  static constexpr uint32_t off_bias = off_meta + S * META;
-  static constexpr uint32_t off_wout = off_bias + NL * H * 4;
+  static constexpr uint32_t off_ones = off_meta + S * META;                   // bias-MMA A operand
+  static constexpr uint32_t off_bb = off_ones + kOnesBytes;                   // [NL] bias B operands
+  static constexpr uint32_t off_wout = off_bb + NL * BB;
   static constexpr uint32_t off_acc = off_wout + H * 4;
   static constexpr uint32_t off_queue = off_acc + kMaxGroups * 4 * 8;          // pre-filter survivor queue
   static constexpr uint32_t off_norm = off_queue + kQueueBytes;                // shift[48], scale[48]
@@ -48,10 +50,12 @@ struct SmemPlan {
   static constexpr uint32_t off_misc = off_bar + 64 * 8;    // tmem base, warp counts, counters
   static constexpr uint32_t total = off_misc + 128;
   static constexpr uint32_t wimg_bytes = WH + W1;                              // contiguous [Wh | W1]
+  static constexpr uint32_t bimg_bytes = NL * BB;                              // follows it in the image
   static_assert(total <= 232448, "shared-memory plan exceeds 227 KB");
   static_assert(K0P % 16 == 0 && K0P <= kMaxFeat, "K0P");
   static_assert(H % 64 == 0 && H >= 64 && H <= 256, "hidden width");
   static_assert(NL == 1 || NL == 2, "hidden layers");
+  static_assert(off_ones % 16 == 0 && BB % 16 == 0, "operand alignment");
 };
 
 template <int K0P, int H, int NL>
@@ -86,7 +90,6 @@ __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_c
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + P::off_misc);
   int32_t* wcnt = reinterpret_cast<int32_t*>(smem + P::off_misc + 16);     // [2][4] warp counts
   unsigned long long* acc = reinterpret_cast<unsigned long long*>(smem + P::off_acc);
-  float* s_bias = reinterpret_cast<float*>(smem + P::off_bias);
   float* s_wout = reinterpret_cast<float*>(smem + P::off_wout);
   float* s_shift = reinterpret_cast<float*>(smem + P::off_norm);
   float* s_scale = s_shift + kMaxFeat;
@@ -101,7 +104,9 @@ __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_c
     const int4* src = reinterpret_cast<const int4*>(p.wimg);
     int4* dst = reinterpret_cast<int4*>(smem + P::off_wh);   // [Wh | W1] contiguous, same layout
     for (uint32_t i = tid; i < P::wimg_bytes / 16; i += kThreads) dst[i] = ldg_nc(src + i);
-    for (int i = tid; i < NL * H; i += kThreads) s_bias[i] = p.bias[i];
+    int4* bdst = reinterpret_cast<int4*>(smem + P::off_bb);   // bias B operands (see bias_operand_bytes)
+    for (uint32_t i = tid; i < P::bimg_bytes / 16; i += kThreads) bdst[i] = ldg_nc(src + P::wimg_bytes / 16 + i);
+    fill_ones_operand(smem + P::off_ones, tid, kThreads);
     for (int i = tid; i < H; i += kThreads) s_wout[i] = p.wout[i];
     for (int i = tid; i < kMaxFeat / 2; i += kThreads) {   // {scale_k, scale_k+1, c_k, c_k+1} per pair
       const int k = 2 * i;
@@ -149,21 +154,30 @@ __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_c
       const bool leader = true;
       const uint64_t xdesc = make_sdesc(smem_u32(smem + P::off_x), kTile * 16, 128, kLayoutNone);
       const uint64_t w1desc = make_sdesc(smem_u32(smem + P::off_w1), H * 16, 128, kLayoutNone);
+      // bias MMAs (see kOnesBytes): A = ONES (rows alias, SBO 16 B), B = MN-major hi/lo bias rows
+      const uint64_t onesdesc = make_sdesc(smem_u32(smem + P::off_ones), kOnesHalf, 16, kLayoutNone);
+      const uint64_t bb1desc = make_sdesc(smem_u32(smem + P::off_bb), 0, 32, kLayoutNone);
       auto issue_l1 = [&](int s, uint32_t dcol) {
         constexpr uint32_t idesc1 = make_idesc_bf16(128, H);
+        if (leader) mma_bf16_ss(tmem_base + dcol, onesdesc, bb1desc, idesc1 | kIdescBMajorMN, 0);
 #pragma unroll
         for (int ks = 0; ks < K0P / 16; ++ks) {
           const uint64_t ad = xdesc + ((uint32_t)(s * P::XS + ks * 2 * (kTile * 16)) >> 4);
           const uint64_t bd = w1desc + ((uint32_t)(ks * 2 * (H * 16)) >> 4);
-          if (leader) mma_bf16_ss(tmem_base + dcol, ad, bd, idesc1, ks > 0);
+          if (leader) mma_bf16_ss(tmem_base + dcol, ad, bd, idesc1, 1);
         }
       };
       if constexpr (NL >= 2) {
         const uint64_t hdesc = make_sdesc(smem_u32(smem + P::off_hb), 16, 1024, kLayoutSW128);
         const uint64_t whdesc = make_sdesc(smem_u32(smem + P::off_wh), 16, 1024, kLayoutSW128);
         constexpr int NC = H / 64;
+        const uint64_t bb2desc = make_sdesc(smem_u32(smem + P::off_bb + P::BB), 0, 32, kLayoutNone);
         auto issue_l2_half = [&](int half, uint32_t tile) {
           constexpr uint32_t idesc2 = make_idesc_bf16(128, H / 2);
+          // bias first (needs no H chunk): neurons [half*H/2, +H/2) = bias blocks from half*H/16
+          if (leader)
+            mma_bf16_ss(tmem_base + H + half * (H / 2), onesdesc, bb2desc + ((uint32_t)(half * (H / 16) * 32) >> 4),
+                        idesc2 | kIdescBMajorMN, 0);
 #pragma unroll
           for (int c = 0; c < NC; ++c) {
             if (half == 0) { FLERN_WAIT(W_MMA_HFULL, true, &hfull[c], tile & 1, 12); tc_fence_after(); }
@@ -171,7 +185,7 @@ __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_c
             for (int j = 0; j < 4; ++j) {   // 4 x K=16 inside one 64-column, 128B-swizzled K-block
               const uint64_t ad = hdesc + ((uint32_t)(c * (kTile * 128) + j * 32) >> 4);
               const uint64_t bd = whdesc + ((uint32_t)(c * (H * 128) + half * (H / 16) * 1024 + j * 32) >> 4);
-              if (leader) mma_bf16_ss(tmem_base + H + half * (H / 2), ad, bd, idesc2, (c | j) != 0);
+              if (leader) mma_bf16_ss(tmem_base + H + half * (H / 2), ad, bd, idesc2, 1);
             }
             if (half == 1 && leader) mma_commit(&hfree[c]);   // last reader of H chunk c for this tile
           }
@@ -249,10 +263,10 @@ __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_c
       agg.tile(p, m, count, r, lane, logit, s_cnt, &empty[s]);
     };
     auto flush_acc = [&]() { agg.flush(acc, lane, p.ngroups); };
-    // relu(D + b) . w_out over `ncols` TMEM columns at `col`; bias/w_out of neuron j at
-    // s_bias[boff + j], s_wout[woff + j]. TMEM loads are double-buffered: chunk c+1 is in flight
-    // while chunk c is reduced (packed fp32x2 add / fma).
-    auto dot_cols = [&](uint32_t col, int ncols, int boff, int woff, float2& acc2a, float2& acc2b) {
+    // relu(D) . w_out over `ncols` TMEM columns at `col` (D already holds the bias, see
+    // kOnesBytes); w_out of neuron j at s_wout[woff + j]. TMEM loads are double-buffered: chunk
+    // c+1 is in flight while chunk c is reduced (packed fp32x2 fma).
+    auto dot_cols = [&](uint32_t col, int ncols, int woff, float2& acc2a, float2& acc2b) {
       uint32_t v[2][32];
       tmem_ld32_async(tmem_base + lane_off + col, v[0]);
       tmem_ld_wait(v[0]);
@@ -261,17 +275,14 @@ __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_c
         if (c * 32 >= ncols) break;
         const int cur = c & 1;
         if ((c + 1) * 32 < ncols) tmem_ld32_async(tmem_base + lane_off + col + (c + 1) * 32, v[cur ^ 1]);
-        const float4* b4 = reinterpret_cast<const float4*>(s_bias + boff + c * 32);
         const float4* w4 = reinterpret_cast<const float4*>(s_wout + woff + c * 32);
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-          const float4 b = b4[i], w = w4[i];
-          float2 z0 = add2(make_float2(__uint_as_float(v[cur][4 * i]), __uint_as_float(v[cur][4 * i + 1])),
-                           make_float2(b.x, b.y));
-          float2 z1 = add2(make_float2(__uint_as_float(v[cur][4 * i + 2]), __uint_as_float(v[cur][4 * i + 3])),
-                           make_float2(b.z, b.w));
-          z0.x = fmaxf(z0.x, 0.f); z0.y = fmaxf(z0.y, 0.f);
-          z1.x = fmaxf(z1.x, 0.f); z1.y = fmaxf(z1.y, 0.f);
+          const float4 w = w4[i];
+          const float2 z0 = make_float2(fmaxf(__uint_as_float(v[cur][4 * i]), 0.f),
+                                        fmaxf(__uint_as_float(v[cur][4 * i + 1]), 0.f));
+          const float2 z1 = make_float2(fmaxf(__uint_as_float(v[cur][4 * i + 2]), 0.f),
+                                        fmaxf(__uint_as_float(v[cur][4 * i + 3]), 0.f));
           acc2a = fma2(z0, make_float2(w.x, w.y), acc2a);
           acc2b = fma2(z1, make_float2(w.z, w.w), acc2b);
         }
@@ -283,7 +294,7 @@ __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_c
       constexpr int NC = H / 64;
       const uint32_t hb = smem_u32(smem + P::off_hb);
       if (wg == 0) {
-        // ---- warpgroup 0: D1 -> bias + ReLU -> bf16 -> H (layer-2 A operand), chunk by chunk ----
+        // ---- warpgroup 0: D1 -> ReLU -> bf16 -> H (layer-2 A operand), chunk by chunk ----
         for (uint32_t t = 0; !p.no_model; ++t) {
           const int s = t % S;
           FLERN_WAIT(W_WG0_FULL, tid == 128, &full[s], (t / S) & 1, 20);
@@ -309,17 +320,9 @@ __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_c
               uint32_t v[32];
               const int c0 = c * 64 + j * 32;
               tmem_ld32(tmem_base + lane_off + c0, v);
-              const float4* b4 = reinterpret_cast<const float4*>(s_bias + c0);
 #pragma unroll
-              for (int i = 0; i < 8; ++i) {
-                const float4 b = b4[i];
-                const float2 z0 = add2(make_float2(__uint_as_float(v[4 * i]), __uint_as_float(v[4 * i + 1])),
-                                       make_float2(b.x, b.y));
-                const float2 z1 = add2(make_float2(__uint_as_float(v[4 * i + 2]), __uint_as_float(v[4 * i + 3])),
-                                       make_float2(b.z, b.w));
-                pk[j * 16 + 2 * i] = relu_bf16x2(z0.x, z0.y);
-                pk[j * 16 + 2 * i + 1] = relu_bf16x2(z1.x, z1.y);
-              }
+              for (int i = 0; i < 16; ++i)   // D1 already holds the bias (kOnesBytes)
+                pk[j * 16 + i] = relu_bf16x2(__uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1]));
             }
             if (c == NC - 1) {   // all of D1 is in registers: the MMA may overwrite it
               tc_fence_before();
@@ -340,7 +343,7 @@ __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_c
           if (tid == 128) FLERN_TRACE(TR_W0_DONE, t);
         }
       } else {
-        // ---- warpgroup 1: logit = relu(D2 + b2) . w_out + b_out, predicate, group-by ----
+        // ---- warpgroup 1: logit = relu(D2) . w_out + b_out, predicate, group-by ----
         for (uint32_t t = 0;; ++t) {
           const int s = t % S;
           FLERN_WAIT(W_WG1_FULL, tid == 256, &full[s], (t / S) & 1, 23);
@@ -356,7 +359,7 @@ __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_c
               FLERN_WAIT(W_WG1_DFULL, tid == 256, &dfull[h], t & 1, 24);
               if (tid == 256) FLERN_TRACE(h ? TR_W1_DFULL1 : TR_W1_DFULL0, t);
               tc_fence_after();
-              if (!(p.dbg_mode & 1)) dot_cols(H + h * (H / 2), H / 2, H + h * (H / 2), h * (H / 2), pa, pb);
+              if (!(p.dbg_mode & 1)) dot_cols(H + h * (H / 2), H / 2, h * (H / 2), pa, pb);
               if (tid == 256) FLERN_TRACE(h ? TR_W1_DOTB : TR_W1_DOTA, t);
               tc_fence_before();
               __syncwarp();
@@ -382,7 +385,7 @@ __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_c
           mbar_wait(&dfull[wg], (t >> 1) & 1, 26);
           tc_fence_after();
           float2 pa = make_float2(0.f, 0.f), pb = make_float2(0.f, 0.f);
-          dot_cols(wg * H, H, 0, 0, pa, pb);
+          dot_cols(wg * H, H, 0, pa, pb);
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&dempty[wg]);

@@ -134,6 +134,8 @@ __host__ __device__ constexpr uint32_t make_idesc_bf16(uint32_t M, uint32_t N) {
   return (1u << 4) | (1u << 7) | (1u << 10) | ((N >> 3) << 17) | ((M >> 4) << 24);
 }
 
+constexpr uint32_t kIdescBMajorMN = 1u << 16;   // instruction descriptor: B operand MN-major
+
 // D[tmem] (+)= A[smem] * B[smem]^T, M=128, K=16, single CTA. Issued by ONE thread.
 __device__ __forceinline__ void mma_bf16_ss(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
                                             uint32_t accumulate) {
