@@ -44,8 +44,11 @@ struct HashFn {
   uint32_t mode, shift, mask, mulc;
   int32_t kmin;
 };
+// mode 2: direct addressing (capacity >= key range, every unique key owns its home slot);
+// mode 1: order-preserving range hash; mode 0: Fibonacci hashing
 __host__ __device__ __forceinline__ uint32_t hash_slot(int32_t key, const HashFn& f) {
-  if (f.mode)
+  if (f.mode == 2) return ((uint32_t)key - (uint32_t)f.kmin) & f.mask;
+  if (f.mode == 1)
     return (uint32_t)(((uint64_t)((uint32_t)key - (uint32_t)f.kmin) * (uint64_t)f.mulc) >> 32) & f.mask;
   return ((uint32_t)key * 0x9E3779B1u) >> f.shift;
 }

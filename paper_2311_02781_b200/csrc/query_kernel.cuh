@@ -315,14 +315,17 @@ __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_c
           } else
           for (int c = 0; c < NC; ++c) {
             uint32_t pk[32];
+            {
+              uint32_t va[32], vb[32];   // both halves of the chunk in flight, one wait
+              tmem_ld32_async(tmem_base + lane_off + c * 64, va);
+              tmem_ld32_async(tmem_base + lane_off + c * 64 + 32, vb);
+              tmem_ld_wait(va);
+              tmem_ld_wait(vb);
 #pragma unroll
-            for (int j = 0; j < 2; ++j) {
-              uint32_t v[32];
-              const int c0 = c * 64 + j * 32;
-              tmem_ld32(tmem_base + lane_off + c0, v);
-#pragma unroll
-              for (int i = 0; i < 16; ++i)   // D1 already holds the bias (kOnesBytes)
-                pk[j * 16 + i] = relu_bf16x2(__uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1]));
+              for (int i = 0; i < 16; ++i) {   // D1 already holds the bias (kOnesBytes)
+                pk[i] = relu_bf16x2(__uint_as_float(va[2 * i]), __uint_as_float(va[2 * i + 1]));
+                pk[16 + i] = relu_bf16x2(__uint_as_float(vb[2 * i]), __uint_as_float(vb[2 * i + 1]));
+              }
             }
             if (c == NC - 1) {   // all of D1 is in registers: the MMA may overwrite it
               tc_fence_before();
