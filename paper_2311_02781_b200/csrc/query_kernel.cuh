@@ -92,7 +92,6 @@ __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_c
   unsigned long long* acc = reinterpret_cast<unsigned long long*>(smem + P::off_acc);
   float* s_wout = reinterpret_cast<float*>(smem + P::off_wout);
   float* s_shift = reinterpret_cast<float*>(smem + P::off_norm);
-  float* s_scale = s_shift + kMaxFeat;
   int64_t* s_cnt = reinterpret_cast<int64_t*>(smem + P::off_misc + 64);   // [kCounters]
   unsigned int* s_is_last = reinterpret_cast<unsigned int*>(smem + P::off_misc + 96);
   int64_t* s_claim = reinterpret_cast<int64_t*>(smem + P::off_misc + 104);   // [2] row-chunk claims
@@ -107,7 +106,7 @@ __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_c
     int4* bdst = reinterpret_cast<int4*>(smem + P::off_bb);   // bias B operands (see bias_operand_bytes)
     for (uint32_t i = tid; i < P::bimg_bytes / 16; i += kThreads) bdst[i] = ldg_nc(src + P::wimg_bytes / 16 + i);
     fill_ones_operand(smem + P::off_ones, tid, kThreads);
-    for (int i = tid; i < H; i += kThreads) s_wout[i] = p.wout[i];
+    for (int i = tid; i < H; i += kThreads) s_wout[i] = 0.5f * p.wout[i];   // w/2: see dot_cols
     for (int i = tid; i < kMaxFeat / 2; i += kThreads) {   // {scale_k, scale_k+1, c_k, c_k+1} per pair
       const int k = 2 * i;
       s_shift[4 * i + 0] = k < K0P ? p.scale[k] : 0.f;
@@ -264,9 +263,11 @@ __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_c
     };
     auto flush_acc = [&]() { agg.flush(acc, lane, p.ngroups); };
     // relu(D) . w_out over `ncols` TMEM columns at `col` (D already holds the bias, see
-    // kOnesBytes); w_out of neuron j at s_wout[woff + j]. TMEM loads are double-buffered: chunk
-    // c+1 is in flight while chunk c is reduced (packed fp32x2 fma).
-    auto dot_cols = [&](uint32_t col, int ncols, int woff, float2& acc2a, float2& acc2b) {
+    // kOnesBytes), with relu(x) * w = x * (w/2) + |x| * (w/2): two packed FMAs per column pair,
+    // the |x| an operand modifier, so the dot needs no max instruction (s_wout holds w_out / 2,
+    // exact in fp32). Four independent accumulator chains; TMEM loads are double-buffered: chunk
+    // c+1 is in flight while chunk c is reduced.
+    auto dot_cols = [&](uint32_t col, int ncols, int woff, float2 (&acc)[4]) {
       uint32_t v[2][32];
       tmem_ld32_async(tmem_base + lane_off + col, v[0]);
       tmem_ld_wait(v[0]);
@@ -279,15 +280,18 @@ __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_c
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
           const float4 w = w4[i];
-          const float2 z0 = make_float2(fmaxf(__uint_as_float(v[cur][4 * i]), 0.f),
-                                        fmaxf(__uint_as_float(v[cur][4 * i + 1]), 0.f));
-          const float2 z1 = make_float2(fmaxf(__uint_as_float(v[cur][4 * i + 2]), 0.f),
-                                        fmaxf(__uint_as_float(v[cur][4 * i + 3]), 0.f));
-          acc2a = fma2(z0, make_float2(w.x, w.y), acc2a);
-          acc2b = fma2(z1, make_float2(w.z, w.w), acc2b);
+          const float2 z0 = make_float2(__uint_as_float(v[cur][4 * i]), __uint_as_float(v[cur][4 * i + 1]));
+          const float2 z1 = make_float2(__uint_as_float(v[cur][4 * i + 2]), __uint_as_float(v[cur][4 * i + 3]));
+          acc[0] = fma2(z0, make_float2(w.x, w.y), acc[0]);
+          acc[1] = fma2(make_float2(fabsf(z0.x), fabsf(z0.y)), make_float2(w.x, w.y), acc[1]);
+          acc[2] = fma2(z1, make_float2(w.z, w.w), acc[2]);
+          acc[3] = fma2(make_float2(fabsf(z1.x), fabsf(z1.y)), make_float2(w.z, w.w), acc[3]);
         }
         if ((c + 1) * 32 < ncols) tmem_ld_wait(v[cur ^ 1]);
       }
+    };
+    auto dot_sum = [](const float2 (&acc)[4]) {
+      return ((acc[0].x + acc[1].x) + (acc[0].y + acc[1].y)) + ((acc[2].x + acc[3].x) + (acc[2].y + acc[3].y));
     };
 
     if constexpr (NL >= 2) {
@@ -356,19 +360,20 @@ __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_c
           if (tid == 256) FLERN_TRACE(TR_W1_FULL, t);
           float logit = 0.f;
           if (!p.no_model) {
-            float2 pa = make_float2(0.f, 0.f), pb = make_float2(0.f, 0.f);
+            float2 acc4[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
+                              make_float2(0.f, 0.f)};
 #pragma unroll 1
             for (int h = 0; h < 2; ++h) {
               FLERN_WAIT(W_WG1_DFULL, tid == 256, &dfull[h], t & 1, 24);
               if (tid == 256) FLERN_TRACE(h ? TR_W1_DFULL1 : TR_W1_DFULL0, t);
               tc_fence_after();
-              if (!(p.dbg_mode & 1)) dot_cols(H + h * (H / 2), H / 2, h * (H / 2), pa, pb);
+              if (!(p.dbg_mode & 1)) dot_cols(H + h * (H / 2), H / 2, h * (H / 2), acc4);
               if (tid == 256) FLERN_TRACE(h ? TR_W1_DOTB : TR_W1_DOTA, t);
               tc_fence_before();
               __syncwarp();
               if (lane == 0) mbar_arrive(&dempty[h]);
             }
-            logit = ((pa.x + pa.y) + (pb.x + pb.y)) + p.bout;
+            logit = dot_sum(acc4) + p.bout;
           }
           finish_tile(m, count, s, logit);
           if (tid == 256) FLERN_TRACE(TR_W1_AGG, t);
@@ -387,12 +392,13 @@ __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_c
         if (!p.no_model) {
           mbar_wait(&dfull[wg], (t >> 1) & 1, 26);
           tc_fence_after();
-          float2 pa = make_float2(0.f, 0.f), pb = make_float2(0.f, 0.f);
-          dot_cols(wg * H, H, 0, pa, pb);
+          float2 acc4[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
+                            make_float2(0.f, 0.f)};
+          dot_cols(wg * H, H, 0, acc4);
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&dempty[wg]);
-          logit = ((pa.x + pa.y) + (pb.x + pb.y)) + p.bout;
+          logit = dot_sum(acc4) + p.bout;
         }
         finish_tile(m, count, s, logit);
       }

@@ -1,0 +1,119 @@
+// epi_microbench.cu — per-SMSP throughput of the epilogue's instruction mix on this GPU:
+// F2FP (cvt.rn.relu.bf16x2.f32), FMNMX, FFMA2, FADD2, and the tcgen05.ld 32x32b.x32 round trip.
+// One warp per SMSP (4 warps per CTA, one CTA per SM) or 2 warps per SMSP; independent chains.
+// Diagnostic for DESIGN.md §7. Build:
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I paper_2311_02781_b200/csrc \
+//        scripts/epi_microbench.cu -o build/epi_microbench
+#include <cstdio>
+#include "sm100.cuh"
+
+using namespace flern;
+
+template <int OP>
+__global__ void __launch_bounds__(256, 1) bench(int iters, unsigned long long* out, float seed) {
+  __shared__ uint32_t tslot;
+  __shared__ __align__(16) uint8_t sbuf[16384 + 1024];
+  const int warp = threadIdx.x >> 5;
+  float a[16];
+  uint32_t u[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) { a[i] = seed * (i + 1) + threadIdx.x; u[i] = 0; }
+  uint32_t tmem = 0;
+  if (OP == 4) {
+    if (warp == 0) { tmem_alloc(&tslot, 64); tmem_relinquish(); }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    tmem = tslot;
+  }
+  __syncthreads();
+  const unsigned long long t0 = clock64();
+  for (int it = 0; it < iters; ++it) {
+    if (OP == 0) {   // F2FP relu pack: 16 independent per iteration
+#pragma unroll
+      for (int i = 0; i < 16; i += 2) {
+        u[i] ^= relu_bf16x2(a[i], a[i + 1]);
+        u[i + 1] ^= relu_bf16x2(a[i + 1], a[i]);
+      }
+#pragma unroll
+      for (int i = 0; i < 16; ++i) a[i] = __uint_as_float(__float_as_uint(a[i]) + 1u);
+    } else if (OP == 1) {   // FMNMX
+#pragma unroll
+      for (int i = 0; i < 16; ++i) a[i] = fmaxf(a[i], a[(i + 1) & 15]);
+    } else if (OP == 2) {   // FFMA2
+#pragma unroll
+      for (int i = 0; i < 16; i += 2) {
+        float2 x = make_float2(a[i], a[i + 1]);
+        x = fma2(x, make_float2(1.0001f, 0.9999f), make_float2(0.5f, 0.25f));
+        a[i] = x.x; a[i + 1] = x.y;
+      }
+    } else if (OP == 3) {   // FADD2
+#pragma unroll
+      for (int i = 0; i < 16; i += 2) {
+        float2 x = make_float2(a[i], a[i + 1]);
+        x = add2(x, make_float2(0.5f, 0.25f));
+        a[i] = x.x; a[i + 1] = x.y;
+      }
+    } else if (OP == 5 || OP == 6) {   // 8 x st.shared.v4 (one 128-byte row chunk) [+ fence.proxy.async]
+      // the kernel's H-chunk store: row r = 32*(warp%4) + lane, 128B-swizzled (conflict-free)
+      const uint32_t r = (uint32_t)(threadIdx.x & 127);
+      const uint32_t base = ((smem_u32(sbuf) + 1023u) & ~1023u) + (r >> 3) * 1024 + (r & 7) * 128;
+#pragma unroll
+      for (int jj = 0; jj < 8; ++jj)
+        st_shared_v4(base + ((uint32_t)(jj ^ (r & 7)) << 4), u[jj] + it, u[jj + 1], u[jj + 2], u[jj + 3]);
+      if (OP == 5) fence_proxy_async_smem();
+      __syncwarp();
+    } else {   // tcgen05.ld x32 + wait, dependent round trips
+      uint32_t v[32];
+      tmem_ld32(tmem + (((uint32_t)(warp & 3) * 32) << 16) + (it & 1) * 32, v);
+#pragma unroll
+      for (int i = 0; i < 16; ++i) u[i] ^= v[i] ^ v[i + 16];
+    }
+  }
+  const unsigned long long t1 = clock64();
+  uint32_t acc = 0;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) acc ^= u[i] ^ __float_as_uint(a[i]);
+  if ((threadIdx.x & 31) == 0) out[blockIdx.x * 8 + warp] = (t1 - t0);
+  if (acc == 0x12345678u) out[0] = acc;   // keep the work
+  if (OP == 4) {
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) { tc_fence_after(); tmem_dealloc(tmem, 64); }
+  }
+}
+
+template <int OP>
+void run(const char* name, int warps, int per_iter) {
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  unsigned long long* d;
+  cudaMalloc(&d, sms * 8 * 8);
+  const int iters = 4096;
+  bench<OP><<<sms, warps * 32>>>(iters, d, 1.5f);
+  bench<OP><<<sms, warps * 32>>>(iters, d, 1.5f);
+  cudaDeviceSynchronize();
+  unsigned long long h[148 * 8];
+  cudaMemcpy(h, d, sms * 8 * 8, cudaMemcpyDeviceToHost);
+  double avg = 0;
+  for (int b = 0; b < sms; ++b)
+    for (int w = 0; w < warps; ++w) avg += h[b * 8 + w];
+  avg /= sms * warps;
+  const double per = avg / iters;
+  printf("%-28s warps/SM=%d  cycles/iter %.1f  -> %.2f cycles per warp-instr per warp (%d instr/iter); err=%s\n", name,
+         warps, per, per / per_iter, per_iter, cudaGetErrorString(cudaGetLastError()));
+  cudaFree(d);
+}
+
+int main() {
+  for (int w : {4, 8}) {
+    run<0>("F2FP.RELU.BF16 pack", w, 16);
+    run<1>("FMNMX", w, 16);
+    run<2>("FFMA2", w, 8);
+    run<3>("FADD2", w, 8);
+    run<4>("tcgen05.ld.x32+wait", w, 1);
+    run<5>("8xSTS.128 + fence.proxy.async", w, 1);
+    run<6>("8xSTS.128 (no fence)", w, 1);
+  }
+  return 0;
+}
