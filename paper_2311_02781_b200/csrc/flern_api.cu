@@ -155,7 +155,7 @@ struct KernelEntry {
 template <int K0P, int H, int NL>
 constexpr bool plan_fits() {
   constexpr uint32_t WH = (NL >= 2) ? (uint32_t)H * H * 2 : 0;
-  constexpr uint32_t HB = (NL >= 2) ? (uint32_t)kTile * H * 2 : 0;
+  constexpr uint32_t HB = 0;   // H lives in TMEM
   constexpr uint32_t W1 = (uint32_t)H * K0P * 2;
   constexpr uint32_t XS = (uint32_t)kTile * K0P * 2;
   constexpr uint32_t META = 16 + 9 * kTile;
@@ -237,6 +237,10 @@ extern "C" FLERN_API flern_status flern_create(int device, void* cuda_stream, fl
   if (cudaMemsetAsync(ctx->ticket, 0, 64, ctx->stream) != cudaSuccess) return FLERN_E_CUDA;
   // let the build side of the join persist in L2 while the fact table streams through
   if (ctx->persist_max > 0) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, ctx->persist_max);
+  if (const char* wh = getenv("FLERN_WAIT_HINT")) {   // tuning knob (see c_wait_hint)
+    const uint32_t v = (uint32_t)strtoul(wh, nullptr, 0);
+    if (cudaMemcpyToSymbol(c_wait_hint, &v, sizeof(v)) != cudaSuccess) return FLERN_E_CUDA;
+  }
   if (cudaEventCreate(&ctx->ev0) != cudaSuccess || cudaEventCreate(&ctx->ev1) != cudaSuccess) return FLERN_E_CUDA;
   if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) return FLERN_E_CUDA;
   *out = ctx.release();
@@ -749,6 +753,7 @@ extern "C" FLERN_API flern_status flern_run_query(flern_ctx* ctx, const flern_qu
   p.both_classes = both ? 1 : 0;
   p.no_model = (q->flags & FLERN_Q_NO_MODEL) ? 1 : 0;
   p.dbg_mode = getenv("FLERN_DBG_MODE") ? atoi(getenv("FLERN_DBG_MODE")) : 0;   // diagnostics only
+  p.l2_ahead = getenv("FLERN_L2_AHEAD") ? atoi(getenv("FLERN_L2_AHEAD")) : 0;    // tuning knob
   const double t = (double)q->threshold;
   p.thr_logit = t <= 0.0 ? -INFINITY : (t >= 1.0 ? INFINITY : (float)std::log(t / (1.0 - t)));
   uint8_t* img = m.dbuf;

@@ -74,20 +74,24 @@ __device__ __forceinline__ void produce_batch(ProdState& st, const QueryParams& 
       const float2 y = fma2(make_float2(fa, fb), make_float2(nm.x, nm.y), make_float2(nm.z, nm.w));
       return bf16x2(y.x, y.y);
     };
+      // diagnostic (FLERN_DBG_MODE bit 1): no global loads at all, every row joins build row 0 -- the
+      // consumer side's ceiling with an infinitely fast producer
+      const bool synth = (p.dbg_mode & 2) != 0;
       bool valid[R];
 #pragma unroll
       for (int r = 0; r < R; ++r) valid[r] = in[r];
       bool any = false;
 #pragma unroll
       for (int r = 0; r < R; ++r) any |= valid[r];
+      const bool anyld = any && !synth;
       // 1. fact-side loads, all issued before any use: probe key, group/sum, features [0, nfact)
       int32_t key[R], gv[R], sv[R];
       int32_t v[K0P][R];
-      loadR(p.probe[0].fact_key, row0, whole, any, key);
-      loadR(p.grp.base, row0, whole, any && p.grp.src == 0, gv);
-      loadR(p.sum.base, row0, whole, any && p.sum.src == 0, sv);
+      loadR(p.probe[0].fact_key, row0, whole, anyld, key);
+      loadR(p.grp.base, row0, whole, anyld && p.grp.src == 0, gv);
+      loadR(p.sum.base, row0, whole, anyld && p.sum.src == 0, sv);
 #pragma unroll
-      for (int k = 0; k < K0P; ++k) loadR(p.fcol[k], row0, whole, any && k < nfact, v[k]);
+      for (int k = 0; k < K0P; ++k) loadR(p.fcol[k], row0, whole, anyld && k < nfact, v[k]);
       // 2. probes, bucketised linear probing: the aligned 4-slot bucket (a 32-byte
       //    sector) holding the home slot is read with two 16-byte loads and resolved with selects;
       //    only a row that meets neither its key nor an empty slot there continues (rare, warp-
@@ -110,7 +114,7 @@ __device__ __forceinline__ void produce_batch(ProdState& st, const QueryParams& 
 #pragma unroll
         for (int r = 0; r < R; ++r) {
           h[r] = hash_slot(kq[r], pd.hf);
-          const int4* bk = reinterpret_cast<const int4*>(valid[r] ? pd.slots + (h[r] & ~3u) : (const int2*)dz);
+          const int4* bk = reinterpret_cast<const int4*>(valid[r] && !synth ? pd.slots + (h[r] & ~3u) : (const int2*)dz);
           wa[r] = ldg_nc(bk);
           wb[r] = ldg_nc(bk + 1);
         }
@@ -128,6 +132,7 @@ __device__ __forceinline__ void produce_batch(ProdState& st, const QueryParams& 
             res[r] = (act && sk[j] == kq[r]) ? sr[j] : ((act && sk[j] == kEmptyKey) ? -1 : res[r]);
           }
           if (!valid[r]) res[r] = -1;
+          if (synth && valid[r]) res[r] = 0;
           undecided |= res[r] == -2;
         }
         if (__any_sync(0xffffffffu, undecided)) {
@@ -166,11 +171,11 @@ __device__ __forceinline__ void produce_batch(ProdState& st, const QueryParams& 
         const int64_t b1 = (valid[r] && p.nprobes > 1) ? brow[r][1] : 0;
         const int32_t* rb0 = p.probe[0].payload + b0 * p.probe[0].pstride;
         const int32_t* rb1 = p.probe[1].payload + b1 * p.probe[1].pstride;
-        if (p.grp.src > 0) gv[r] = ld1((p.grp.src == 1 ? rb0 : rb1) + p.grp.word, valid[r]);
-        if (p.sum.src > 0) sv[r] = ld1((p.sum.src == 1 ? rb0 : rb1) + p.sum.word, valid[r]);
+        if (p.grp.src > 0) gv[r] = ld1((p.grp.src == 1 ? rb0 : rb1) + p.grp.word, valid[r] && !synth);
+        if (p.sum.src > 0) sv[r] = ld1((p.sum.src == 1 ? rb0 : rb1) + p.sum.word, valid[r] && !synth);
 #pragma unroll
         for (int k = 0; k < K0P; ++k)
-          if (k >= nfact && k < nfeat) v[k][r] = ld1((((dprobe1 >> k) & 1) ? rb1 : rb0) + p.dword[k], valid[r]);
+          if (k >= nfact && k < nfeat) v[k][r] = ld1((((dprobe1 >> k) & 1) ? rb1 : rb0) + p.dword[k], valid[r] && !synth);
       }
       // 4. normalise in fp32 (fma(x, scale, -shift*scale), reading Q4) -> packed bf16 pairs
       uint32_t pk[R][K0P / 2];
@@ -269,13 +274,39 @@ __device__ __forceinline__ void producer_loop(const QueryParams& p, const XRing&
   mbar_wait(&ring.empty[0], ((st.acq / S) & 1) ^ 1, 1);   // acquire the first stage
   st.acq = 1;
   int bidx = 0;
+  // L2 prefetch (p.l2_ahead > 0): the fact columns a batch reads are requested into L2 ahead of use,
+  // so the batch's column loads hit L2 instead of HBM; that shortens the dependent chain
+  // fact load -> probe -> payload load which bounds a batch, and keeps HBM busy without holding
+  // registers or shared memory for the bytes in flight.
+  constexpr bool kSpecP = SH::NF >= 0;
+  const int ncolpf = 3 + (kSpecP ? SH::NF : p.nfact);
+  auto pf_col_ptr = [&](int c) -> const int32_t* {
+    return c == 0 ? p.probe[0].fact_key
+                  : (c == 1 ? (p.sum.src == 0 ? p.sum.base : nullptr)
+                            : (c == 2 ? (p.grp.src == 0 ? p.grp.base : nullptr) : p.fcol[c - 3]));
+  };
+  const int ahead = p.l2_ahead;
   if (!p.pf_col) {
+    // one bulk prefetch per column and batch, spread over the first threads
+    auto prefetch_rows = [&](int64_t lo, int64_t hi) {   // rows [lo, hi) of every fact column read
+      if (t < ncolpf && lo < hi) {
+        const int32_t* c = pf_col_ptr(t);
+        const int64_t a = lo & ~3ll, b = (hi + 3) & ~3ll;
+        if (c) prefetch_l2_bulk(c + a, (uint32_t)(b - a) * 4u);
+      }
+    };
+    if (ahead > 0) prefetch_rows(cur.lo, min(cur.hi, cur.lo + (int64_t)ahead * kBatch));
     while (cur.lo < n) {
       int64_t a = 0;
       if (t == 0) a = claim_chunk(p, 1);
       const int64_t row_end = cur.hi;
       if (t == 0) s_cnt[0] += row_end - cur.lo;   // rows scanned by this CTA
+      if (ahead > 0 && nxt.lo < n) prefetch_rows(nxt.lo, min(nxt.hi, nxt.lo + (int64_t)ahead * kBatch));
       for (int64_t base = cur.lo; base < row_end; base += kBatch, ++bidx) {
+        if (ahead > 0) {
+          const int64_t pl = base + (int64_t)ahead * kBatch;
+          prefetch_rows(pl, min(row_end, pl + kBatch));
+        }
         if (t == 0) FLERN_TRACE(TR_P_START, bidx);
         const int64_t row0 = base + (int64_t)R * t;
         bool in[R];
@@ -303,14 +334,25 @@ __device__ __forceinline__ void producer_loop(const QueryParams& p, const XRing&
         }
       }
     };
+    // the filter column is bulk-prefetched 2*ahead scan chunks ahead (4 KB each, thread 0)
+    auto prefetch_scan = [&](int64_t lo, int64_t hi) {
+      if (t == 0 && lo < hi) {
+        const int64_t a = lo & ~3ll, b = (hi + 3) & ~3ll;
+        prefetch_l2_bulk(p.pf_col + a, (uint32_t)(b - a) * 4u);
+      }
+    };
+    const int64_t pf_span = 2 * (int64_t)ahead * kScanChunk;
+    if (ahead > 0 && cur.lo < n) prefetch_scan(cur.lo, min(cur.hi, cur.lo + pf_span));
     int32_t xnext[8];
     if (cur.lo < n) scan_load(cur.lo, cur.hi, xnext);
     while (cur.lo < n) {
       int64_t a = 0;
       if (t == 0) a = claim_chunk(p, 1);
       if (t == 0) s_cnt[0] += cur.hi - cur.lo;   // rows scanned by this CTA
+      if (ahead > 0 && nxt.lo < n) prefetch_scan(nxt.lo, min(nxt.hi, nxt.lo + pf_span));
       for (int64_t cb = cur.lo; cb < cur.hi; cb += kScanChunk) {
         const int64_t row_end = cur.hi;
+        if (ahead > 0) prefetch_scan(cb + pf_span, min(row_end, cb + pf_span + kScanChunk));
         const bool last_block = cb + kScanChunk >= cur.hi;
         int32_t x[8];
 #pragma unroll
@@ -346,7 +388,15 @@ __device__ __forceinline__ void producer_loop(const QueryParams& p, const XRing&
         for (int j = 0; j < 2; ++j)
 #pragma unroll
           for (int u = 0; u < 4; ++u)
-            if (bits & (1u << (4 * j + u))) queue[pos++] = (int32_t)(cb + 4 * t + 512 * j + u);
+            if (bits & (1u << (4 * j + u))) {
+              const int64_t row = cb + 4 * t + 512 * j + u;
+              queue[pos++] = (int32_t)row;
+              if (ahead > 0)   // the survivor's fact columns: in L2 by the time its batch runs
+                for (int c = 0; c < ncolpf; ++c) {
+                  const int32_t* cp = pf_col_ptr(c);
+                  if (cp) prefetch_l2(cp + row);
+                }
+            }
         nq += total;
         named_bar_sync(1, kProducerThreads);   // queue written (and wcnt[8..] read) by all
         const bool last = last_block && nxt.lo >= n;

@@ -13,8 +13,8 @@
 // Warp roles (416 threads = 13 warps, 1 CTA per SM):
 //   warps 0-3   producers: 128 threads x R consecutive rows per batch; scan, pre-filter, probe,
 //               compact, gather + normalise + bf16 into the X stage ring (S stages of 128 rows)
-//   warps 4-7   epilogue warpgroup 0 (NL=2): D1 (bias folded in by the MMA) -> ReLU -> bf16 -> H,
-//               handed to the MMA in 64-column K-chunks
+//   warps 4-7   epilogue warpgroup 0 (NL=2): D1 (bias folded in by the MMA) -> ReLU -> bf16 -> H
+//               in TMEM (the A operand of layer 2, "ts" MMA), handed over in 64-wide K-chunks
 //   warps 8-11  epilogue warpgroup 1: D2 -> ReLU -> dot(w_out) -> logit -> predicate ->
 //               group-by (NL=1: both warpgroups do this on alternate tiles)
 //   warp  12    TMEM allocator + single-thread tcgen05.mma issuer
@@ -27,7 +27,7 @@ namespace flern {
 template <int K0P, int H, int NL>
 struct SmemPlan {
   static constexpr uint32_t WH = (NL >= 2) ? (uint32_t)H * H * 2 : 0;         // hidden->hidden W, SW128
-  static constexpr uint32_t HB = (NL >= 2) ? (uint32_t)kTile * H * 2 : 0;     // hidden activation, SW128
+  static constexpr uint32_t HB = 0;   // the hidden activation lives in TMEM (TmemPlan::HT)
   static constexpr uint32_t W1 = (uint32_t)H * K0P * 2;                       // layer-1 W, interleave
   static constexpr uint32_t XS = (uint32_t)kTile * K0P * 2;                   // one X stage, interleave
   static constexpr uint32_t META = 16 + 4 * kTile + 4 * kTile + kTile;        // count, rowid, val, grp
@@ -58,6 +58,21 @@ struct SmemPlan {
   static_assert(off_ones % 16 == 0 && BB % 16 == 0, "operand alignment");
 };
 
+// TMEM columns (NL >= 2). Layer 1 runs as NH1 N-pieces into R1; warpgroup 0 turns each piece
+// into bf16 H (packed two per column, the A operand of layer 2) at HT; layer 2 runs as two N-halves
+// into D2 (drained by warpgroup 1 while the other half computes). H at 256: 128 + 128 + 256 = 512.
+// NL == 1: ping-pong D buffers at 0 and H.
+template <int H, int NL>
+struct TmemPlan {
+  static constexpr int NH1 = (NL >= 2 && H >= 128) ? 2 : 1;
+  static constexpr uint32_t R1W = (uint32_t)H / NH1;
+  static constexpr uint32_t HT = R1W;
+  static constexpr uint32_t D2C = (NL >= 2) ? R1W + H / 2 : 0;
+  static constexpr uint32_t used = (NL >= 2) ? R1W + H / 2 + H : 2 * H;
+  static constexpr uint32_t cols = used <= 32 ? 32 : (used <= 64 ? 64 : (used <= 128 ? 128 : (used <= 256 ? 256 : 512)));
+  static_assert(used <= 512, "TMEM plan");
+};
+
 template <int K0P, int H, int NL>
 __device__ __forceinline__ Meta meta_of(uint8_t* base, int s) {
   using P = SmemPlan<K0P, H, NL>;
@@ -81,11 +96,11 @@ __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_c
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + P::off_bar);
   uint64_t* full = bars;            // [S]   producers -> MMA/epilogue (128 arrivals)
   uint64_t* empty = bars + S;       // [S]   epilogue WG0 -> producers (4 arrivals)
-  uint64_t* d1full = bars + 8;      // NL=2: L1 commit -> warpgroup 0
-  uint64_t* d1empty = bars + 9;     // NL=2: warpgroup 0 (4 warps) drained D1 -> MMA
+  uint64_t* d1full = bars + 8;      // NL=2: L1 piece commit -> warpgroup 0
+  uint64_t* d1empty = bars + 9;     // NL=2: warpgroup 0 (4 warps) read the L1 piece out of R1 -> MMA
   uint64_t* dfull = bars + 10;      // [2] NL=2: D2 halves; NL=1: ping-pong D buffers (commit)
   uint64_t* dempty = bars + 12;     // [2] 4 warps drained it -> MMA
-  uint64_t* hfull = bars + 14;      // [4] NL=2: warpgroup 0 wrote H chunk c (4 warps)
+  uint64_t* hfull = bars + 14;      // [4] NL=2: warpgroup 0 stored H chunk c in TMEM (4 warps)
   uint64_t* hfree = bars + 18;      // [4] NL=2: L2b finished reading H chunk c (commit)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + P::off_misc);
   int32_t* wcnt = reinterpret_cast<int32_t*>(smem + P::off_misc + 16);     // [2][4] warp counts
@@ -128,7 +143,8 @@ __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_c
     for (int c = 0; c < 4; ++c) { mbar_init(&hfull[c], 4); mbar_init(&hfree[c], 1); }
     fence_mbar_init();
   }
-  constexpr uint32_t kTmemCols = 2 * H <= 32 ? 32 : (2 * H <= 64 ? 64 : (2 * H <= 128 ? 128 : (2 * H <= 256 ? 256 : 512)));
+  using TP = TmemPlan<H, NL>;
+  constexpr uint32_t kTmemCols = TP::cols;
   if (warp == 12) { tmem_alloc(tmem_slot, kTmemCols); tmem_relinquish(); }
   tc_fence_before();
   __syncthreads();
@@ -167,24 +183,41 @@ __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_c
         }
       };
       if constexpr (NL >= 2) {
-        const uint64_t hdesc = make_sdesc(smem_u32(smem + P::off_hb), 16, 1024, kLayoutSW128);
+        // Layer 2 takes A (= H) from TMEM and B (= W2) from SMEM: the tensor core reads 4 KB of
+        // SMEM per K=16 step instead of 8, and no epilogue writes H through shared memory.
         const uint64_t whdesc = make_sdesc(smem_u32(smem + P::off_wh), 16, 1024, kLayoutSW128);
-        constexpr int NC = H / 64;
+        constexpr int NC = H / 64;                 // 64-wide K-chunks of H (32 TMEM columns each)
         const uint64_t bb2desc = make_sdesc(smem_u32(smem + P::off_bb + P::BB), 0, 32, kLayoutNone);
+        uint32_t pc = 0;   // L1 pieces issued
+        auto issue_l1_piece = [&](int s, int piece) {
+          constexpr uint32_t NP = (uint32_t)H / TP::NH1;
+          constexpr uint32_t idesc1 = make_idesc_bf16(128, NP);
+          FLERN_WAIT(W_MMA_D1EMPTY, lane == 0, d1empty, (pc & 1) ^ 1, 11);   // R1 read out by warpgroup 0
+          tc_fence_after();
+          if (leader)
+            mma_bf16_ss(tmem_base, onesdesc, bb1desc + ((uint32_t)(piece * (NP / 8) * 32) >> 4), idesc1 | kIdescBMajorMN, 0);
+#pragma unroll
+          for (int ks = 0; ks < K0P / 16; ++ks) {
+            const uint64_t ad = xdesc + ((uint32_t)(s * P::XS + ks * 2 * (kTile * 16)) >> 4);
+            const uint64_t bd = w1desc + ((uint32_t)(ks * 2 * (H * 16) + piece * NP * 16) >> 4);
+            if (leader) mma_bf16_ss(tmem_base, ad, bd, idesc1, 1);
+          }
+          if (leader) mma_commit(d1full);
+          ++pc;
+        };
         auto issue_l2_half = [&](int half, uint32_t tile) {
           constexpr uint32_t idesc2 = make_idesc_bf16(128, H / 2);
+          const uint32_t dcol = tmem_base + TP::D2C + half * (H / 2);
           // bias first (needs no H chunk): neurons [half*H/2, +H/2) = bias blocks from half*H/16
           if (leader)
-            mma_bf16_ss(tmem_base + H + half * (H / 2), onesdesc, bb2desc + ((uint32_t)(half * (H / 16) * 32) >> 4),
-                        idesc2 | kIdescBMajorMN, 0);
+            mma_bf16_ss(dcol, onesdesc, bb2desc + ((uint32_t)(half * (H / 16) * 32) >> 4), idesc2 | kIdescBMajorMN, 0);
 #pragma unroll
           for (int c = 0; c < NC; ++c) {
             if (half == 0) { FLERN_WAIT(W_MMA_HFULL, true, &hfull[c], tile & 1, 12); tc_fence_after(); }
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {   // 4 x K=16 inside one 64-column, 128B-swizzled K-block
-              const uint64_t ad = hdesc + ((uint32_t)(c * (kTile * 128) + j * 32) >> 4);
+            for (int j = 0; j < 4; ++j) {   // 4 x K=16 inside one 64-wide K-chunk (8 TMEM columns each)
               const uint64_t bd = whdesc + ((uint32_t)(c * (H * 128) + half * (H / 16) * 1024 + j * 32) >> 4);
-              if (leader) mma_bf16_ss(tmem_base + H + half * (H / 2), ad, bd, idesc2, 1);
+              if (leader) mma_bf16_ts(dcol, tmem_base + TP::HT + c * 32 + j * 8, bd, idesc2, 1);
             }
             if (half == 1 && leader) mma_commit(&hfree[c]);   // last reader of H chunk c for this tile
           }
@@ -193,17 +226,16 @@ __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_c
         FLERN_WAIT(W_MMA_FULL, lane == 0, &full[0], 0, 10);
         if (*meta_of<K0P, H, NL>(smem, 0).count >= 0) {
           tc_fence_after();
-          issue_l1(0, 0);
-          if (leader) mma_commit(d1full);
+          for (int piece = 0; piece < TP::NH1; ++piece) issue_l1_piece(0, piece);
           for (uint32_t t = 0;; ++t) {
             FLERN_WAIT(W_MMA_DEMPTY0, lane == 0, &dempty[0], (t & 1) ^ 1, 13);
             if (lane == 0) FLERN_TRACE(TR_MMA_D2A_FREE, t);
             tc_fence_after();
             issue_l2_half(0, t);
             if (lane == 0) FLERN_TRACE(TR_MMA_L2A_DONE, t);
-            // L1(t+1) goes between the two halves when tile t+1 is already published (so that
-            // warpgroup 0 converts it while L2b(t) runs); otherwise after L2b(t) (never block the
-            // tile in flight on the producer)
+            // L1 piece 0 of tile t+1 goes between the two halves when tile t+1 is already published
+            // (warpgroup 0 converts it while L2b(t) runs); otherwise after L2b(t) (never block the
+            // tile in flight on the producer). Piece 1 follows L2b(t).
             const int s1 = (t + 1) % S;
             const uint32_t ph1 = ((t + 1) / S) & 1;
             const bool have_next = mbar_test_wait(&full[s1], ph1);
@@ -212,10 +244,7 @@ __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_c
               if (lane == 0) FLERN_TRACE(TR_MMA_NEXT_READY, t);
               next = *meta_of<K0P, H, NL>(smem, s1).count >= 0;
               if (next) {
-                FLERN_WAIT(W_MMA_D1EMPTY, lane == 0, d1empty, ((t + 1) & 1) ^ 1, 11);
-                tc_fence_after();
-                issue_l1(s1, 0);
-                if (leader) mma_commit(d1full);
+                issue_l1_piece(s1, 0);
                 FLERN_TRACE(TR_MMA_L1_ISSUED, t);
               }
             };
@@ -230,6 +259,7 @@ __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_c
               do_next();
             }
             if (!next) break;
+            for (int piece = 1; piece < TP::NH1; ++piece) issue_l1_piece(s1, piece);
           }
         }
       } else {
@@ -296,56 +326,60 @@ __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_c
 
     if constexpr (NL >= 2) {
       constexpr int NC = H / 64;
-      const uint32_t hb = smem_u32(smem + P::off_hb);
       if (wg == 0) {
-        // ---- warpgroup 0: D1 -> ReLU -> bf16 -> H (layer-2 A operand), chunk by chunk ----
+        // ---- warpgroup 0: D1 -> ReLU -> bf16 -> H in TMEM (layer-2 A operand), chunk by chunk ----
+        constexpr int CPP = NC / TP::NH1;   // 64-wide chunks per L1 piece
         for (uint32_t t = 0; !p.no_model; ++t) {
           const int s = t % S;
           FLERN_WAIT(W_WG0_FULL, tid == 128, &full[s], (t / S) & 1, 20);
           if (*meta_of<K0P, H, NL>(smem, s).count < 0) break;
           if (tid == 128) FLERN_TRACE(TR_W0_FULL, t);
-          FLERN_WAIT(W_WG0_D1FULL, tid == 128, d1full, t & 1, 21);
-          if (tid == 128) FLERN_TRACE(TR_W0_D1FULL, t);
-          tc_fence_after();
-          if (p.dbg_mode & 1) {   // diagnostic: keep the protocol, skip the math
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(d1empty);
-            for (int c = 0; c < NC; ++c) {
-              mbar_wait(&hfree[c], (t & 1) ^ 1, 22);
-              __syncwarp();
-              if (lane == 0) mbar_arrive(&hfull[c]);
-            }
-          } else
-          for (int c = 0; c < NC; ++c) {
-            uint32_t pk[32];
-            {
-              uint32_t va[32], vb[32];   // both halves of the chunk in flight, one wait
-              tmem_ld32_async(tmem_base + lane_off + c * 64, va);
-              tmem_ld32_async(tmem_base + lane_off + c * 64 + 32, vb);
-              tmem_ld_wait(va);
-              tmem_ld_wait(vb);
-#pragma unroll
-              for (int i = 0; i < 16; ++i) {   // D1 already holds the bias (kOnesBytes)
-                pk[i] = relu_bf16x2(__uint_as_float(va[2 * i]), __uint_as_float(va[2 * i + 1]));
-                pk[16 + i] = relu_bf16x2(__uint_as_float(vb[2 * i]), __uint_as_float(vb[2 * i + 1]));
-              }
-            }
-            if (c == NC - 1) {   // all of D1 is in registers: the MMA may overwrite it
+#pragma unroll 1
+          for (int piece = 0; piece < TP::NH1; ++piece) {
+            FLERN_WAIT(W_WG0_D1FULL, tid == 128, d1full, (t * TP::NH1 + piece) & 1, 21);
+            if (tid == 128 && piece == 0) FLERN_TRACE(TR_W0_D1FULL, t);
+            tc_fence_after();
+            if (p.dbg_mode & 1) {   // diagnostic: keep the protocol, skip the math
               tc_fence_before();
               __syncwarp();
               if (lane == 0) mbar_arrive(d1empty);
+              for (int cc = 0; cc < CPP; ++cc) {
+                const int c = piece * CPP + cc;
+                mbar_wait(&hfree[c], (t & 1) ^ 1, 22);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&hfull[c]);
+              }
+              continue;
             }
-            FLERN_WAIT(W_WG0_HFREE, tid == 128, &hfree[c], (t & 1) ^ 1, 22);   // L2b(t-1) done with chunk c
-            if (tid == 128 && c == 0) FLERN_TRACE(TR_W0_HFREE0, t);
-            const uint32_t rowbase = hb + c * (kTile * 128) + (r >> 3) * 1024 + (r & 7) * 128;
 #pragma unroll
-            for (int jj = 0; jj < 8; ++jj)   // 128B swizzle: chunk jj of the row goes to jj ^ (row % 8)
-              st_shared_v4(rowbase + ((uint32_t)(jj ^ (r & 7)) << 4), pk[4 * jj], pk[4 * jj + 1], pk[4 * jj + 2],
-                           pk[4 * jj + 3]);
-            fence_proxy_async_smem();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&hfull[c]);
+            for (int cc = 0; cc < CPP; ++cc) {
+              const int c = piece * CPP + cc;
+              uint32_t pk[32];
+              {
+                uint32_t va[32], vb[32];   // both halves of the chunk in flight, one wait
+                tmem_ld32_async(tmem_base + lane_off + cc * 64, va);
+                tmem_ld32_async(tmem_base + lane_off + cc * 64 + 32, vb);
+                tmem_ld_wait(va);
+                tmem_ld_wait(vb);
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {   // D1 already holds the bias (kOnesBytes)
+                  pk[i] = relu_bf16x2(__uint_as_float(va[2 * i]), __uint_as_float(va[2 * i + 1]));
+                  pk[16 + i] = relu_bf16x2(__uint_as_float(vb[2 * i]), __uint_as_float(vb[2 * i + 1]));
+                }
+              }
+              if (cc == CPP - 1) {   // the whole L1 piece is in registers: the MMA may overwrite R1
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(d1empty);
+              }
+              FLERN_WAIT(W_WG0_HFREE, tid == 128, &hfree[c], (t & 1) ^ 1, 22);   // L2b(t-1) done with chunk c
+              if (tid == 128 && c == 0) FLERN_TRACE(TR_W0_HFREE0, t);
+              tc_fence_after();
+              tmem_st32(tmem_base + lane_off + TP::HT + c * 32, pk);   // K = 64c .. 64c+63, packed pairs
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) mbar_arrive(&hfull[c]);
+            }
           }
           if (tid == 128) FLERN_TRACE(TR_W0_DONE, t);
         }
@@ -367,7 +401,7 @@ __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_c
               FLERN_WAIT(W_WG1_DFULL, tid == 256, &dfull[h], t & 1, 24);
               if (tid == 256) FLERN_TRACE(h ? TR_W1_DFULL1 : TR_W1_DFULL0, t);
               tc_fence_after();
-              if (!(p.dbg_mode & 1)) dot_cols(H + h * (H / 2), H / 2, h * (H / 2), acc4);
+              if (!(p.dbg_mode & 1)) dot_cols(TP::D2C + h * (H / 2), H / 2, h * (H / 2), acc4);
               if (tid == 256) FLERN_TRACE(h ? TR_W1_DOTB : TR_W1_DOTA, t);
               tc_fence_before();
               __syncwarp();

@@ -13,7 +13,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libflern.so")
+# FLERN_LIB: diagnostic builds of the same library (e.g. -DFLERN_TRACE_WAITS) under lib/
+LIB_PATH = os.path.join(_HERE, "lib", os.environ.get("FLERN_LIB", "libflern.so"))
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is missing: build it with `make` or __graft_entry__.build()")
 _lib = ctypes.CDLL(LIB_PATH)

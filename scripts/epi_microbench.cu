@@ -19,8 +19,8 @@ __global__ void __launch_bounds__(256, 1) bench(int iters, unsigned long long* o
 #pragma unroll
   for (int i = 0; i < 16; ++i) { a[i] = seed * (i + 1) + threadIdx.x; u[i] = 0; }
   uint32_t tmem = 0;
-  if (OP == 4) {
-    if (warp == 0) { tmem_alloc(&tslot, 64); tmem_relinquish(); }
+  if (OP == 4 || OP == 7) {
+    if (warp == 0) { tmem_alloc(&tslot, 128); tmem_relinquish(); }
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -63,6 +63,19 @@ __global__ void __launch_bounds__(256, 1) bench(int iters, unsigned long long* o
         st_shared_v4(base + ((uint32_t)(jj ^ (r & 7)) << 4), u[jj] + it, u[jj + 1], u[jj + 2], u[jj + 3]);
       if (OP == 5) fence_proxy_async_smem();
       __syncwarp();
+    } else if (OP == 7) {   // 4 x tcgen05.ld x32 in flight (128 columns = 16 KB per warp), one wait
+      uint32_t v0[32], v1[32], v2[32], v3[32];
+      const uint32_t ta = tmem + (((uint32_t)(warp & 3) * 32) << 16);
+      tmem_ld32_async(ta + 0, v0);
+      tmem_ld32_async(ta + 32, v1);
+      tmem_ld32_async(ta + 64, v2);
+      tmem_ld32_async(ta + 96, v3);
+      tmem_ld_wait(v0);
+      tmem_ld_wait(v1);
+      tmem_ld_wait(v2);
+      tmem_ld_wait(v3);
+#pragma unroll
+      for (int i = 0; i < 16; ++i) u[i] ^= v0[i] ^ v1[i + 16] ^ v2[i] ^ v3[i + 16];
     } else {   // tcgen05.ld x32 + wait, dependent round trips
       uint32_t v[32];
       tmem_ld32(tmem + (((uint32_t)(warp & 3) * 32) << 16) + (it & 1) * 32, v);
@@ -76,10 +89,10 @@ __global__ void __launch_bounds__(256, 1) bench(int iters, unsigned long long* o
   for (int i = 0; i < 16; ++i) acc ^= u[i] ^ __float_as_uint(a[i]);
   if ((threadIdx.x & 31) == 0) out[blockIdx.x * 8 + warp] = (t1 - t0);
   if (acc == 0x12345678u) out[0] = acc;   // keep the work
-  if (OP == 4) {
+  if (OP == 4 || OP == 7) {
     tc_fence_before();
     __syncthreads();
-    if (warp == 0) { tc_fence_after(); tmem_dealloc(tmem, 64); }
+    if (warp == 0) { tc_fence_after(); tmem_dealloc(tmem, 128); }
   }
 }
 
@@ -112,6 +125,7 @@ int main() {
     run<2>("FFMA2", w, 8);
     run<3>("FADD2", w, 8);
     run<4>("tcgen05.ld.x32+wait", w, 1);
+    run<7>("4x tcgen05.ld.x32, 1 wait", w, 1);
     run<5>("8xSTS.128 + fence.proxy.async", w, 1);
     run<6>("8xSTS.128 (no fence)", w, 1);
   }

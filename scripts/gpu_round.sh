@@ -1,0 +1,23 @@
+#!/bin/bash
+# One GPU round trip: parity tests, bench lines for every workload, launch list and a full ncu
+# capture of the query kernel (C2). usage: scripts/gpu_round.sh TAG [skip_tests]
+TAG=${1:-run}
+mkdir -p gpurun_out
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.limit --format=csv,noheader | tee gpurun_out/smi_$TAG.txt
+nproc >> gpurun_out/smi_$TAG.txt
+if [ -z "$2" ]; then
+  timeout 1500 python -m pytest tests -m gpu -q --timeout 900 2>&1 | tail -30 | tee gpurun_out/pytest_$TAG.log
+fi
+timeout 600 python bench.py 2>&1 | tail -2 | tee gpurun_out/bench_c2_$TAG.json
+for w in c1 c1x c4p c3 c4; do
+  timeout 900 python bench.py --workload $w --no-cpu-baseline --steps 20 --warmup 3 --e2e-steps 2 2>&1 | tail -2 | tee gpurun_out/bench_${w}_$TAG.json
+done
+timeout 600 python bench.py --workload c2 --no-model --no-cpu-baseline --steps 50 --e2e-steps 1 2>&1 | tail -1 | tee gpurun_out/bench_c2nomodel_$TAG.json
+timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -c 200 --csv --log-file gpurun_out/launches_c2_$TAG.csv \
+  python bench.py --steps 20 --warmup 3 --no-cpu-baseline --e2e-steps 1 > /dev/null 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:flern_query -s 6 -c 1 -o gpurun_out/prof_c2_$TAG -f \
+  python bench.py --steps 5 --warmup 3 --no-cpu-baseline --e2e-steps 1 > gpurun_out/ncu_c2_$TAG.log 2>&1
+tail -2 gpurun_out/ncu_c2_$TAG.log
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:flern_query_wide -s 4 -c 1 -o gpurun_out/prof_c3_$TAG -f \
+  python bench.py --workload c3 --steps 3 --warmup 3 --no-cpu-baseline --e2e-steps 1 > gpurun_out/ncu_c3_$TAG.log 2>&1
+tail -2 gpurun_out/ncu_c3_$TAG.log

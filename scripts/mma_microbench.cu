@@ -10,7 +10,8 @@ using namespace flern;
 
 // COMMIT: tcgen05.commit to an mbarrier after every 4 MMAs (as the fused kernel's per-K-chunk
 // hfree commits); SPREAD: A/B walk over a 64 KB / 128 KB operand region like layer 2 of the kernel
-template <int N, bool COMMIT, bool SPREAD>
+// TS: A from TMEM (columns 256.. of the allocation) instead of SMEM
+template <int N, bool COMMIT, bool SPREAD, bool TS = false>
 __global__ void __launch_bounds__(128, 1) mma_bench(int iters, unsigned long long* out) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t bar;
@@ -21,7 +22,7 @@ __global__ void __launch_bounds__(128, 1) mma_bench(int iters, unsigned long lon
   __shared__ uint64_t cbar[4];
   fence_proxy_async_smem();
   if (threadIdx.x == 0) { mbar_init(&bar, 1); for (int i = 0; i < 4; ++i) mbar_init(&cbar[i], 1); fence_mbar_init(); }
-  if (warp == 0) { tmem_alloc(&tslot, 256); tmem_relinquish(); }
+  if (warp == 0) { tmem_alloc(&tslot, 512); tmem_relinquish(); }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -34,9 +35,14 @@ __global__ void __launch_bounds__(128, 1) mma_bench(int iters, unsigned long lon
     for (int it = 0; it < iters; ++it) {
       const uint32_t kb = SPREAD ? (it & 3) : 0;
 #pragma unroll
-      for (int j = 0; j < 4; ++j)
-        mma_bf16_ss(tmem, ad0 + ((kb * 16384) >> 4) + j * 2, bd0 + ((kb * (uint32_t)N * 128) >> 4) + j * 2, idesc,
-                    (it | j) != 0);
+      for (int j = 0; j < 4; ++j) {
+        if (TS)
+          mma_bf16_ts(tmem, tmem + 256 + kb * 32 + j * 8, bd0 + ((kb * (uint32_t)N * 128) >> 4) + j * 2, idesc,
+                      (it | j) != 0);
+        else
+          mma_bf16_ss(tmem, ad0 + ((kb * 16384) >> 4) + j * 2, bd0 + ((kb * (uint32_t)N * 128) >> 4) + j * 2, idesc,
+                      (it | j) != 0);
+      }
       if (COMMIT) mma_commit(&cbar[it & 3]);
     }
     mma_commit(&bar);
@@ -46,18 +52,18 @@ __global__ void __launch_bounds__(128, 1) mma_bench(int iters, unsigned long lon
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 0) { tc_fence_after(); tmem_dealloc(tmem, 256); }
+  if (warp == 0) { tc_fence_after(); tmem_dealloc(tmem, 512); }
 }
 
-template <int N, bool COMMIT, bool SPREAD>
+template <int N, bool COMMIT, bool SPREAD, bool TS = false>
 void run(int sms) {
   const int iters = 4096;
   unsigned long long* d;
   cudaMalloc(&d, sms * 8);
   const int smem = (SPREAD ? 65536 + N * 512 : 16384 + N * 128) + 1024;
-  cudaFuncSetAttribute(mma_bench<N, COMMIT, SPREAD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  mma_bench<N, COMMIT, SPREAD><<<sms, 128, smem>>>(iters, d);   // warm-up
-  mma_bench<N, COMMIT, SPREAD><<<sms, 128, smem>>>(iters, d);
+  cudaFuncSetAttribute(mma_bench<N, COMMIT, SPREAD, TS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  mma_bench<N, COMMIT, SPREAD, TS><<<sms, 128, smem>>>(iters, d);   // warm-up
+  mma_bench<N, COMMIT, SPREAD, TS><<<sms, 128, smem>>>(iters, d);
   cudaDeviceSynchronize();
   unsigned long long h[256];
   cudaMemcpy(h, d, sms * 8, cudaMemcpyDeviceToHost);
@@ -66,7 +72,7 @@ void run(int sms) {
   avg /= sms;
   const double per = avg / (iters * 4.0);
   const double ideal = 128.0 * N / 256.0;
-  printf("commit=%d spread=%d N=%3d  grid=%3d  cycles/MMA %.1f  (ideal %.1f at 8192 flop/clk/SM)  -> %.0f%% of per-SM peak; err=%s\n", (int)COMMIT, (int)SPREAD, N, sms,
+  printf("ts=%d commit=%d spread=%d N=%3d  grid=%3d  cycles/MMA %.1f  (ideal %.1f at 8192 flop/clk/SM)  -> %.0f%% of per-SM peak; err=%s\n", (int)TS, (int)COMMIT, (int)SPREAD, N, sms,
          per, ideal, 100.0 * ideal / per, cudaGetErrorString(cudaGetLastError()));
   cudaFree(d);
 }
@@ -82,5 +88,8 @@ int main() {
   run<256, false, true>(sms);
   run<128, true, true>(sms);
   run<256, true, true>(sms);
+  run<128, true, true, true>(sms);
+  run<256, true, true, true>(sms);
+  run<128, false, true, true>(sms);
   return 0;
 }

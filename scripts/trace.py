@@ -9,15 +9,18 @@ from paper_2311_02781_b200.session import GpuQuery
 EV = ["MMA_D2A_FREE", "MMA_L2A_DONE", "MMA_NEXT_READY", "MMA_L1_ISSUED", "MMA_D2B_FREE", "MMA_L2B_ISSUED",
       "W0_FULL", "W0_D1FULL", "W0_HFREE0", "W0_DONE", "W1_FULL", "W1_DFULL0", "W1_DOTA", "W1_DFULL1", "W1_DOTB",
       "W1_AGG", "P_START", "P_PROBED", "P_GATHERED", "P_DONE"]
-name = sys.argv[1] if len(sys.argv) > 1 else "c2"
-sf = float(sys.argv[2]) if len(sys.argv) > 2 else 1.0
+args = [a for a in sys.argv[1:] if not a.startswith("--")]
+name = args[0] if args else "c2"
+sf = float(args[1]) if len(args) > 1 else 1.0
+flags = F.FLERN_Q_NO_MODEL if "--no-model" in sys.argv else 0
 cfg = D.with_sf(D.CONFIGS[name], sf)
 db = D.make_database(cfg)
 gq = GpuQuery(cfg, db, D.make_model(cfg, db))
 G = cfg.ngroups
 for it in range(3):
     tr = np.zeros(F.TRACE_EVENTS * F.TRACE_TILES, np.uint64)
-    r = gq.run(count=np.zeros(G, np.int64), sum=np.zeros(G, np.int64), dbg_trace=tr)
+    r = gq.run(gq.make_query(gq.fact_id, flags=flags), count=np.zeros(G, np.int64), sum=np.zeros(G, np.int64),
+               dbg_trace=tr)
 tr = tr.reshape(F.TRACE_EVENTS, F.TRACE_TILES).astype(np.int64)
 t0 = tr[:20][tr[:20] > 0].min()
 print("kernel ms", r.elapsed_ms)
