@@ -31,6 +31,10 @@ $(PKG)/lib/libflern_tw.so: $(KERNEL_SRCS) $(KERNEL_HDRS)
 	@mkdir -p $(PKG)/lib build
 	$(NVCC) $(NVFLAGS) -DFLERN_TRACE_WAITS -shared -o $@ $(KERNEL_SRCS) 2> build/ptxas_tw.log || (cat build/ptxas_tw.log; exit 1)
 
+$(PKG)/lib/libflern_seq.so: $(KERNEL_SRCS) $(KERNEL_HDRS)
+	@mkdir -p $(PKG)/lib build
+	$(NVCC) $(NVFLAGS) -DFLERN_SEQ_TRACE -shared -o $@ $(KERNEL_SRCS) 2> build/ptxas_seq.log || (cat build/ptxas_seq.log; exit 1)
+
 clean:
 	rm -f datagen/libflern_gen.so oracle/liboracle.so $(PKG)/lib/libflern.so
 

@@ -177,7 +177,7 @@ typedef struct {
  * and counted in counters[3]. */
 FLERN_API flern_status flern_run_query(flern_ctx* ctx, const flern_query* q, flern_result* res);
 
-#define FLERN_TRACE_EVENTS 25
+#define FLERN_TRACE_EVENTS 26
 
 /* Number of CUDA kernels flern_run_query launches per call (for launch accounting): 1. */
 FLERN_API int32_t flern_query_launches(void);

@@ -9,12 +9,25 @@ constexpr int kMaxFeat = 48;
 constexpr int kMaxGroups = 64;
 constexpr int kMaxProbes = 2;
 constexpr int kTile = 128;
-constexpr int kThreads = 416;   // 13 warps: producers 0-3, epilogue WG0 4-7, WG1 8-11, MMA 12
-constexpr int kProducerThreads = 128;
+// Narrow kernel: 16 warps. SMSP k runs warps k, k+4, k+8, k+12. The MMA issuer (warp 12) shares
+// SMSP 0 only with the two quadrant-0 epilogue warps: the six producer warps (1, 2, 3, 13, 14, 15)
+// sit on SMSPs 1-3, so the issuing thread is not starved of issue slots by warps with deep ILP
+// (scripts/tile_mma_bench.cu: three busy warps on its SMSP stretch a 2.4K-cycle tile to 5.7K).
+constexpr int kThreads = 512;
+constexpr int kProdWarps = 6;                              // narrow kernel producer warps
+constexpr int kProdWarpsWide = 4;                          // wide kernel producer warps (0-3)
+__host__ __device__ constexpr int prod_warp_index(int warp) { return warp < 4 ? warp - 1 : warp - 10; }
+__host__ __device__ constexpr bool is_prod_warp(int warp) { return (warp >= 1 && warp <= 3) || warp >= 13; }
 // consecutive fact rows per producer thread per batch (one 16/8/4-byte vector load per column);
 // fewer for wide inputs (register budget: R * K0P/2 packed bf16 pairs stay live)
 __host__ __device__ constexpr int rows_per_thread(int K0P) { return K0P <= 16 ? 2 : 1; }
-__host__ __device__ constexpr int batch_rows(int K0P) { return kProducerThreads * rows_per_thread(K0P); }
+__host__ __device__ constexpr int batch_rows(int K0P, int npt) { return npt * rows_per_thread(K0P); }
+// pre-filter scan chunk: 8 rows per producer thread (two 16-byte loads)
+__host__ __device__ constexpr int scan_rows(int npt) { return 8 * npt; }
+// survivor queue: pending (< one batch) + one scan chunk
+__host__ __device__ constexpr uint32_t queue_bytes(int npt) { return (uint32_t)(scan_rows(npt) + npt) * 4u; }
+// misc block: tmem slot @0, warp counts [3][8] @16, counters [4] @112, last-CTA flag @144, claims [2] @152
+constexpr uint32_t kMiscBytes = 192;
 constexpr int32_t kEmptyKey = (int32_t)0x80000000;         // INT32_MIN marks an empty slot
 // Biases on the tensor core: every layer's accumulator is initialised by one extra K=16 MMA,
 // D = ONES x BIAS^T (accumulate off), before the layer's own MMAs accumulate onto it, so no
@@ -34,7 +47,6 @@ __device__ __forceinline__ void fill_ones_operand(uint8_t* dst, int tid, int nth
     w[i] = (i * 4 < (int)kOnesHalf && (i & 3) == 0) ? 0x3F803F80u : 0u;   // bf16 1.0 at k = 0, 1
 }
 
-constexpr int kScanChunkRows = 1024;                       // pre-filter scan chunk (4 rows x 2 x 128 threads)
 constexpr int kCounters = 4;                               // scanned, joined(=scored), selected, bad_group
 
 // Slot of `key`: mode 1 = order-preserving range hash (kmin..kmax spread linearly over the
@@ -77,7 +89,7 @@ struct QueryParams {
   unsigned long long* work; // chunk-claim counter (guided distribution, see chunk_rows); zero between launches
   int64_t claim_big;        // rows per "big" chunk (multiple of claim_small); chunks [0, claim_nbig) are big
   int64_t claim_nbig;       // 2 x grid, or 0 for small inputs
-  int64_t claim_small;      // rows per later chunk: batch_rows(K0P), or kScanChunkRows with a pre-filter
+  int64_t claim_small;      // rows per later chunk: batch_rows(K0P, npt), or scan_rows(npt) with a pre-filter
   int32_t nprobes;
   ProbeDesc probe[kMaxProbes];
   const int32_t* pf_col;    // nullptr = no pre-filter
@@ -98,6 +110,7 @@ struct QueryParams {
   float thr_logit;          // select logit > thr_logit  (score > t  <=>  logit > ln(t/(1-t)))
   int32_t no_model;         // diagnostic: skip the MLP, select every joined row (scan/probe/gather only)
   int32_t dbg_mode;         // diagnostic (env FLERN_DBG_MODE): bit 0 = epilogues skip their math, bit 1 = producer issues no global loads
+  int32_t sched;            // MMA issue order variant (env FLERN_SCHED; tuning)
   int32_t l2_ahead;         // producer: fact rows are bulk-prefetched into L2 this many batches ahead (0 = off)
   const uint8_t* wimg;      // weight image: [Wh (SW128) | W1 (interleave)] bf16, exact SMEM layout
   const float* bias;        // [NL][H]
@@ -125,8 +138,14 @@ enum TraceEv {
   TR_P_START, TR_P_PROBED, TR_P_GATHERED, TR_P_DONE,
   TR_WAITS,   // [category] accumulated wait cycles of CTA 0's role threads (see FLERN_WAIT)
   TR_CTA_START, TR_CTA_SETUP, TR_CTA_LOOP_END, TR_CTA_EXIT,   // [cta]: %globaltimer (ns) of every CTA < kTraceTiles
+  TR_MMA_SEQ,   // [i]: (clock64 << 8) | tag of the MMA thread's i-th event during tiles kSeqTile.. (CTA 0)
   kTraceEvents
 };
+constexpr uint32_t kSeqTile = 100;   // first tile of the TR_MMA_SEQ window
+// TR_MMA_SEQ tags: 1 L2a MMA, 2 L2b MMA, 3 L1 MMA, 4 bias MMA; waits (begin, end): 10/11 hfull,
+// 12/13 dempty0, 14/15 dempty1, 16/17 d1empty, 18/19 full; 30 tile start
+enum SeqTag { SQ_L2A = 1, SQ_L2B, SQ_L1, SQ_BIAS, SQ_HFULL = 10, SQ_DEMPTY0 = 12, SQ_DEMPTY1 = 14, SQ_D1EMPTY = 16,
+              SQ_FULL = 18, SQ_TILE = 30 };
 // wait categories for TR_WAITS
 enum WaitCat {
   W_MMA_FULL, W_MMA_DEMPTY0, W_MMA_DEMPTY1, W_MMA_HFULL, W_MMA_D1EMPTY, W_WG0_FULL, W_WG0_D1FULL, W_WG0_HFREE,

@@ -159,7 +159,7 @@ constexpr bool plan_fits() {
   constexpr uint32_t W1 = (uint32_t)H * K0P * 2;
   constexpr uint32_t XS = (uint32_t)kTile * K0P * 2;
   constexpr uint32_t META = 16 + 9 * kTile;
-  constexpr uint32_t FIXED = WH + HB + W1 + NL * H * 4 + H * 4 + kMaxGroups * 4 * 8 + kQueueBytes + kMaxFeat * 8 +
+  constexpr uint32_t FIXED = WH + HB + W1 + NL * H * 4 + H * 4 + kMaxGroups * 4 * 8 + queue_bytes(32 * kProdWarps) + kMaxFeat * 8 +
                              64 * 8 + 128;
   return FIXED + 3 * (XS + META) <= 232448;
 }
@@ -753,6 +753,7 @@ extern "C" FLERN_API flern_status flern_run_query(flern_ctx* ctx, const flern_qu
   p.both_classes = both ? 1 : 0;
   p.no_model = (q->flags & FLERN_Q_NO_MODEL) ? 1 : 0;
   p.dbg_mode = getenv("FLERN_DBG_MODE") ? atoi(getenv("FLERN_DBG_MODE")) : 0;   // diagnostics only
+  p.sched = getenv("FLERN_SCHED") ? atoi(getenv("FLERN_SCHED")) : 1;              // tuning knob
   p.l2_ahead = getenv("FLERN_L2_AHEAD") ? atoi(getenv("FLERN_L2_AHEAD")) : 0;    // tuning knob
   const double t = (double)q->threshold;
   p.thr_logit = t <= 0.0 ? -INFINITY : (t >= 1.0 ? INFINITY : (float)std::log(t / (1.0 - t)));
@@ -836,7 +837,8 @@ extern "C" FLERN_API flern_status flern_run_query(flern_ctx* ctx, const flern_qu
 
   // one persistent CTA per SM; rows are claimed as chunks (guided schedule, chunk_rows in common.cuh):
   // 2*grid contiguous halves of an 85% static share, then small chunks on demand
-  const int64_t chunk = p.pf_col ? (int64_t)kScanChunkRows : (int64_t)batch_rows(m.K0P);
+  const int npt = 32 * (ke->threads == kThreads ? kProdWarps : kProdWarpsWide);   // producer threads
+  const int64_t chunk = p.pf_col ? (int64_t)scan_rows(npt) : (int64_t)batch_rows(m.K0P, npt);
   const int grid = (int)std::min<int64_t>(ctx->num_sms, std::max<int64_t>(1, (n + chunk - 1) / chunk));
   p.claim_small = chunk;
   p.claim_big = (int64_t)(0.85 * (double)n / (2.0 * grid)) / chunk * chunk;

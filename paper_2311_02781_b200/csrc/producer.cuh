@@ -15,9 +15,6 @@
 
 namespace flern {
 
-constexpr int kScanChunk = 1024;                         // pre-filter scan: 8 rows per producer thread
-constexpr int kQueueCap = kScanChunk + kProducerThreads;  // survivors pending (< 128) + one chunk
-constexpr uint32_t kQueueBytes = kQueueCap * 4;
 
 struct ProdState {
   int stage;          // stage currently being filled (acquired)
@@ -29,7 +26,7 @@ struct ProdState {
 
 // One batch: rows [row0, row0 + R) of this thread (consecutive; with R == 1 any row id), in[r] =
 // the row takes part (inside the shard and past the pre-filter).
-template <int K0P, int S, int R, class SH>
+template <int K0P, int S, int R, class SH, int NPW>
 __device__ __forceinline__ void produce_batch(ProdState& st, const QueryParams& p, const XRing& ring, int32_t* wcnt,
                                               const float* s_normf, int64_t row0, bool whole, const bool (&in)[R],
                                               int bidx, int64_t row_end, int t, int warp, int lane) {
@@ -194,12 +191,12 @@ __device__ __forceinline__ void produce_batch(ProdState& st, const QueryParams& 
         const int x = __shfl_up_sync(0xffffffffu, incl, o);
         if (lane >= o) incl += x;
       }
-      if (lane == 31) wcnt[st.buf * 4 + warp] = incl;
-      named_bar_sync(1, kProducerThreads);
+      if (lane == 31) wcnt[st.buf * 8 + warp] = incl;
+      named_bar_sync(1, 32 * NPW);
       int woff = 0, total = 0;
 #pragma unroll
-      for (int w = 0; w < 4; ++w) {
-        const int c = wcnt[st.buf * 4 + w];
+      for (int w = 0; w < NPW; ++w) {
+        const int c = wcnt[st.buf * 8 + w];
         woff += (w < warp) ? c : 0;
         total += c;
       }
@@ -250,12 +247,16 @@ __device__ __forceinline__ void produce_batch(ProdState& st, const QueryParams& 
       }
 }
 
-template <int K0P, int S, class SH>
+// `tid` is the thread's index in the producer group [0, 32*NPW), `warp` its warp in the group.
+template <int K0P, int S, class SH, int NPW>
 __device__ __forceinline__ void producer_loop(const QueryParams& p, const XRing& ring, int32_t* wcnt,
                                               const float* s_normf, int64_t* s_cnt, int32_t* queue,
                                               int64_t* s_claim, int tid, int warp, int lane) {
+  constexpr int NPT = 32 * NPW;
   constexpr int R = rows_per_thread(K0P);
-  constexpr int kBatch = batch_rows(K0P);
+  constexpr int kBatch = batch_rows(K0P, NPT);
+  constexpr int kScanChunk = scan_rows(NPT);
+  constexpr int kQueueCap = (int)queue_bytes(NPT) / 4;
   const int t = tid;   // 0..127
   const int64_t n = p.nrows;
   // claims (chunk indices, see chunk_rows): the CTA setup took chunks s_claim[0], s_claim[1]; chunk
@@ -265,7 +266,7 @@ __device__ __forceinline__ void producer_loop(const QueryParams& p, const XRing&
   int k = 0;
   auto advance = [&](int64_t a) {
     if (t == 0) s_claim[k & 1] = a;
-    named_bar_sync(1, kProducerThreads);
+    named_bar_sync(1, NPT);
     cur = nxt;
     nxt = chunk_rows(p, s_claim[k & 1]);
     ++k;
@@ -312,19 +313,18 @@ __device__ __forceinline__ void producer_loop(const QueryParams& p, const XRing&
         bool in[R];
 #pragma unroll
         for (int r = 0; r < R; ++r) in[r] = row0 + r < row_end;
-        produce_batch<K0P, S, R, SH>(st, p, ring, wcnt, s_normf, row0, row0 + R <= row_end, in, bidx, row_end, t, warp, lane);
+        produce_batch<K0P, S, R, SH, NPW>(st, p, ring, wcnt, s_normf, row0, row0 + R <= row_end, in, bidx, row_end, t, warp, lane);
       }
       advance(a);
     }
   } else {
-    static_assert(kScanChunk == kScanChunkRows, "scan chunk");
     int nq = 0;        // survivors queued (uniform across the producer group)
-    // scan rows cb + 4t + 512j (j = 0, 1; each warp instruction covers 512 contiguous rows); the
+    // scan rows cb + 4t + 4*NPT*j (j = 0, 1; each warp instruction covers 128 contiguous rows); the
     // next chunk's loads are issued before this chunk is compacted (software pipeline)
     auto scan_load = [&](int64_t cb, int64_t row_end, int32_t (&x)[8]) {
 #pragma unroll
       for (int j = 0; j < 2; ++j) {
-        const int64_t r0 = cb + 4 * t + 512 * j;
+        const int64_t r0 = cb + 4 * t + 4 * NPT * j;
         if (r0 + 4 <= row_end) {
           const int4 v = ldg_nc(reinterpret_cast<const int4*>(p.pf_col + r0));
           x[4 * j] = v.x; x[4 * j + 1] = v.y; x[4 * j + 2] = v.z; x[4 * j + 3] = v.w;
@@ -364,7 +364,7 @@ __device__ __forceinline__ void producer_loop(const QueryParams& p, const XRing&
         for (int j = 0; j < 2; ++j)
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
-            const int64_t rr = cb + 4 * t + 512 * j + u;
+            const int64_t rr = cb + 4 * t + 4 * NPT * j + u;
             if (rr < row_end && p.pf_lo <= x[4 * j + u] && x[4 * j + u] < p.pf_hi) bits |= 1u << (4 * j + u);
           }
         const int my = __popc(bits);
@@ -374,12 +374,12 @@ __device__ __forceinline__ void producer_loop(const QueryParams& p, const XRing&
           const int x = __shfl_up_sync(0xffffffffu, incl, o);
           if (lane >= o) incl += x;
         }
-        if (lane == 31) wcnt[8 + warp] = incl;
-        named_bar_sync(1, kProducerThreads);
+        if (lane == 31) wcnt[16 + warp] = incl;
+        named_bar_sync(1, NPT);
         int woff = 0, total = 0;
 #pragma unroll
-        for (int w = 0; w < 4; ++w) {
-          const int c = wcnt[8 + w];
+        for (int w = 0; w < NPW; ++w) {
+          const int c = wcnt[16 + w];
           woff += (w < warp) ? c : 0;
           total += c;
         }
@@ -389,7 +389,7 @@ __device__ __forceinline__ void producer_loop(const QueryParams& p, const XRing&
 #pragma unroll
           for (int u = 0; u < 4; ++u)
             if (bits & (1u << (4 * j + u))) {
-              const int64_t row = cb + 4 * t + 512 * j + u;
+              const int64_t row = cb + 4 * t + 4 * NPT * j + u;
               queue[pos++] = (int32_t)row;
               if (ahead > 0)   // the survivor's fact columns: in L2 by the time its batch runs
                 for (int c = 0; c < ncolpf; ++c) {
@@ -398,24 +398,24 @@ __device__ __forceinline__ void producer_loop(const QueryParams& p, const XRing&
                 }
             }
         nq += total;
-        named_bar_sync(1, kProducerThreads);   // queue written (and wcnt[8..] read) by all
+        named_bar_sync(1, NPT);   // queue written (and wcnt[16..] read) by all
         const bool last = last_block && nxt.lo >= n;
-        while (nq >= kProducerThreads || (last && nq > 0)) {
+        while (nq >= NPT || (last && nq > 0)) {
           const bool in1[1] = {t < nq};
           const int64_t row = in1[0] ? (int64_t)queue[t] : 0;
           if (t == 0) FLERN_TRACE(TR_P_START, bidx);
-          produce_batch<K0P, S, 1, SH>(st, p, ring, wcnt, s_normf, row, true, in1, bidx, n, t, warp, lane);
+          produce_batch<K0P, S, 1, SH, NPW>(st, p, ring, wcnt, s_normf, row, true, in1, bidx, n, t, warp, lane);
           ++bidx;
-          const int taken = min(nq, kProducerThreads);
+          const int taken = min(nq, NPT);
           // shift the rest of the queue to the front
-          int32_t keep[kQueueCap / kProducerThreads + 1];
+          int32_t keep[kQueueCap / NPT + 1];
           int nk = 0;
-          for (int i = taken + t; i < nq; i += kProducerThreads) keep[nk++] = queue[i];
-          named_bar_sync(1, kProducerThreads);
+          for (int i = taken + t; i < nq; i += NPT) keep[nk++] = queue[i];
+          named_bar_sync(1, NPT);
           nk = 0;
-          for (int i = taken + t; i < nq; i += kProducerThreads) queue[i - taken] = keep[nk++];
+          for (int i = taken + t; i < nq; i += NPT) queue[i - taken] = keep[nk++];
           nq -= taken;
-          named_bar_sync(1, kProducerThreads);
+          named_bar_sync(1, NPT);
         }
       }
       advance(a);

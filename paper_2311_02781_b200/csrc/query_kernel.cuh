@@ -33,7 +33,7 @@ struct SmemPlan {
   static constexpr uint32_t META = 16 + 4 * kTile + 4 * kTile + kTile;        // count, rowid, val, grp
   static constexpr uint32_t BB = bias_operand_bytes(H);                       // one layer's bias B operand
   static constexpr uint32_t FIXED = WH + HB + W1 + kOnesBytes + NL * BB + H * 4 + kMaxGroups * 4 * 8 +
-                                    kQueueBytes + kMaxFeat * 8 + 64 * 8 + 128;
+                                    queue_bytes(32 * kProdWarps) + kMaxFeat * 8 + 64 * 8 + kMiscBytes;
   static constexpr int S = (FIXED + 4 * (XS + META) <= 232448) ? 4 : 3;
   static constexpr uint32_t off_wh = 0;                                       // [Wh | W1] = weight image
   static constexpr uint32_t off_w1 = off_wh + WH;
@@ -45,10 +45,17 @@ struct SmemPlan {
   static constexpr uint32_t off_wout = off_bb + NL * BB;
   static constexpr uint32_t off_acc = off_wout + H * 4;
   static constexpr uint32_t off_queue = off_acc + kMaxGroups * 4 * 8;          // pre-filter survivor queue
-  static constexpr uint32_t off_norm = off_queue + kQueueBytes;                // shift[48], scale[48]
+  static constexpr uint32_t off_norm = off_queue + queue_bytes(32 * kProdWarps);   // shift[48], scale[48]
   static constexpr uint32_t off_bar = off_norm + kMaxFeat * 8;
   static constexpr uint32_t off_misc = off_bar + 64 * 8;    // tmem base, warp counts, counters
-  static constexpr uint32_t total = off_misc + 128;
+#ifdef FLERN_SEQ_TRACE
+  static constexpr uint32_t SEQB = 256 * 8;   // diagnostic MMA-thread event log (TR_MMA_SEQ)
+#else
+  static constexpr uint32_t SEQB = 0;
+#endif
+  static constexpr uint32_t off_part = off_misc + kMiscBytes;                 // [2][128] fp32 partial logits
+  static constexpr uint32_t off_seq = off_part + 2 * kTile * 4;
+  static constexpr uint32_t total = off_seq + SEQB;
   static constexpr uint32_t wimg_bytes = WH + W1;                              // contiguous [Wh | W1]
   static constexpr uint32_t bimg_bytes = NL * BB;                              // follows it in the image
   static_assert(total <= 232448, "shared-memory plan exceeds 227 KB");
@@ -59,8 +66,10 @@ struct SmemPlan {
 };
 
 // TMEM columns (NL >= 2). Layer 1 runs as NH1 N-pieces into R1; warpgroup 0 turns each piece
-// into bf16 H (packed two per column, the A operand of layer 2) at HT; layer 2 runs as two N-halves
-// into D2 (drained by warpgroup 1 while the other half computes). H at 256: 128 + 128 + 256 = 512.
+// into bf16 H (packed two per column: the A operand of layer 2, "ts" MMA) at HT; layer 2 runs as
+// ONE N = H accumulation into D2 (tcgen05 reaches full rate only at N >= 128, and the wide MMA
+// halves the instructions the single issuing thread must keep ahead of the tensor core), drained
+// by both epilogue warpgroups (lower / upper half of the columns). H = 256: 128 + 128 + 256 = 512.
 // NL == 1: ping-pong D buffers at 0 and H.
 template <int H, int NL>
 struct TmemPlan {
@@ -87,7 +96,9 @@ __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_c
   constexpr int S = P::S;
   extern __shared__ __align__(1024) uint8_t smem[];
   const int tid = threadIdx.x;
-  const int warp = tid >> 5, lane = tid & 31;
+  // warp index through a shuffle from lane 0: ptxas then knows it is warp-uniform, so role branches
+  // are uniform and the MMA warp keeps descriptors and addresses in uniform registers (no R2UR)
+  const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0), lane = tid & 31;
   FLERN_CTA_STAMP(TR_CTA_START);
   // first two row chunks (guided distribution, see chunk_rows); the atomic's latency hides under the setup
   int64_t claim0 = 0;
@@ -98,18 +109,19 @@ __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_c
   uint64_t* empty = bars + S;       // [S]   epilogue WG0 -> producers (4 arrivals)
   uint64_t* d1full = bars + 8;      // NL=2: L1 piece commit -> warpgroup 0
   uint64_t* d1empty = bars + 9;     // NL=2: warpgroup 0 (4 warps) read the L1 piece out of R1 -> MMA
-  uint64_t* dfull = bars + 10;      // [2] NL=2: D2 halves; NL=1: ping-pong D buffers (commit)
-  uint64_t* dempty = bars + 12;     // [2] 4 warps drained it -> MMA
+  uint64_t* dfull = bars + 10;      // NL=2: [0] layer 2 done (commit); NL=1: [2] ping-pong D buffers
+  uint64_t* dempty = bars + 12;     // NL=2: [0] both warpgroups drained D2 (8 warps); NL=1: [2] (4 warps)
+  uint64_t* pready = bars + 24;     // NL=2: warpgroup 0's partial logits of the tile are in SMEM (4 warps)
   uint64_t* hfull = bars + 14;      // [4] NL=2: warpgroup 0 stored H chunk c in TMEM (4 warps)
   uint64_t* hfree = bars + 18;      // [4] NL=2: L2b finished reading H chunk c (commit)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + P::off_misc);
-  int32_t* wcnt = reinterpret_cast<int32_t*>(smem + P::off_misc + 16);     // [2][4] warp counts
+  int32_t* wcnt = reinterpret_cast<int32_t*>(smem + P::off_misc + 16);     // [3][8] warp counts
   unsigned long long* acc = reinterpret_cast<unsigned long long*>(smem + P::off_acc);
   float* s_wout = reinterpret_cast<float*>(smem + P::off_wout);
   float* s_shift = reinterpret_cast<float*>(smem + P::off_norm);
-  int64_t* s_cnt = reinterpret_cast<int64_t*>(smem + P::off_misc + 64);   // [kCounters]
-  unsigned int* s_is_last = reinterpret_cast<unsigned int*>(smem + P::off_misc + 96);
-  int64_t* s_claim = reinterpret_cast<int64_t*>(smem + P::off_misc + 104);   // [2] row-chunk claims
+  int64_t* s_cnt = reinterpret_cast<int64_t*>(smem + P::off_misc + 112);  // [kCounters]
+  unsigned int* s_is_last = reinterpret_cast<unsigned int*>(smem + P::off_misc + 144);
+  int64_t* s_claim = reinterpret_cast<int64_t*>(smem + P::off_misc + 152);   // [2] row-chunk claims
 
   if ((smem_u32(smem) & 1023u) != 0) __trap();  // SW128 operands need a 1024-aligned base
 
@@ -136,10 +148,11 @@ __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_c
   }
   static_assert(S <= 4, "stage ring");
   if (tid == 0) {
-    for (int s = 0; s < S; ++s) { mbar_init(&full[s], kProducerThreads); mbar_init(&empty[s], 4); }
+    for (int s = 0; s < S; ++s) { mbar_init(&full[s], 32 * kProdWarps); mbar_init(&empty[s], 4); }
     mbar_init(d1full, 1);
     mbar_init(d1empty, 4);
-    for (int i = 0; i < 2; ++i) { mbar_init(&dfull[i], 1); mbar_init(&dempty[i], 4); }
+    for (int i = 0; i < 2; ++i) { mbar_init(&dfull[i], 1); mbar_init(&dempty[i], (NL >= 2 && i == 0) ? 8 : 4); }
+    mbar_init(pready, 4);
     for (int c = 0; c < 4; ++c) { mbar_init(&hfull[c], 4); mbar_init(&hfree[c], 1); }
     fence_mbar_init();
   }
@@ -149,13 +162,21 @@ __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_c
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem_base = *tmem_slot;
+  // One CTA per SM allocates the whole TMEM plan, so the allocation starts at lane 0, column 0.
+  // Using the constant (checked) lets every TMEM operand address be an immediate in the MMA issue
+  // loop instead of a value moved through R2UR per instruction.
+  if (*tmem_slot != 0u) __trap();
+  constexpr uint32_t tmem_base = 0;
   FLERN_CTA_STAMP(TR_CTA_SETUP);
 
 
-  if (warp < 4) {
-    producer_loop<K0P, S, SH>(p, XRing{smem + P::off_x, P::XS, smem + P::off_meta, full, empty}, wcnt, s_shift, s_cnt,
-                          reinterpret_cast<int32_t*>(smem + P::off_queue), s_claim, tid, warp, lane);
+  if (warp == 0) {
+    // setup only: keeps SMSP 0 free for the MMA issuer
+  } else if (is_prod_warp(warp)) {
+    const int pw = prod_warp_index(warp);
+    producer_loop<K0P, S, SH, kProdWarps>(p, XRing{smem + P::off_x, P::XS, smem + P::off_meta, full, empty}, wcnt,
+                                          s_shift, s_cnt, reinterpret_cast<int32_t*>(smem + P::off_queue), s_claim,
+                                          pw * 32 + lane, pw, lane);
   } else if (warp == 12) {
     // =============================== MMA ISSUER =============================================
     // NL == 2 issue order per tile t (steady state): L2a(t), L1(t+1), L2b(t). Layer 2 is split
@@ -165,8 +186,11 @@ __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_c
     // Lane 0 issues every tcgen05.mma / tcgen05.commit. Descriptors are built once; a K-step or stage advances the 14-bit start-address field
     // (byte offset >> 4, always < 2^14 for 228 KB of SMEM).
     const unsigned long long k_t0 = (unsigned long long)clock64();
-    if (warp == 12 && lane == 0 && !p.no_model) {
-      const bool leader = true;
+    // The whole warp runs the issue loop (warp-uniform control flow, so descriptors and TMEM
+    // addresses live in uniform registers) and elect.sync picks the lane that issues each
+    // tcgen05.mma / commit: a single-lane loop makes ptxas move every operand through R2UR and wrap
+    // each MMA in a waterfall loop, which made issue, not the tensor core, the limit.
+    if (warp == 12 && !p.no_model) {
       const uint64_t xdesc = make_sdesc(smem_u32(smem + P::off_x), kTile * 16, 128, kLayoutNone);
       const uint64_t w1desc = make_sdesc(smem_u32(smem + P::off_w1), H * 16, 128, kLayoutNone);
       // bias MMAs (see kOnesBytes): A = ONES (rows alias, SBO 16 B), B = MN-major hi/lo bias rows
@@ -174,92 +198,102 @@ __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_c
       const uint64_t bb1desc = make_sdesc(smem_u32(smem + P::off_bb), 0, 32, kLayoutNone);
       auto issue_l1 = [&](int s, uint32_t dcol) {
         constexpr uint32_t idesc1 = make_idesc_bf16(128, H);
-        if (leader) mma_bf16_ss(tmem_base + dcol, onesdesc, bb1desc, idesc1 | kIdescBMajorMN, 0);
+        if (elect_one_sync()) mma_bf16_ss(tmem_base + dcol, onesdesc, bb1desc, idesc1 | kIdescBMajorMN, 0);
 #pragma unroll
         for (int ks = 0; ks < K0P / 16; ++ks) {
           const uint64_t ad = xdesc + ((uint32_t)(s * P::XS + ks * 2 * (kTile * 16)) >> 4);
           const uint64_t bd = w1desc + ((uint32_t)(ks * 2 * (H * 16)) >> 4);
-          if (leader) mma_bf16_ss(tmem_base + dcol, ad, bd, idesc1, 1);
+          if (elect_one_sync()) mma_bf16_ss(tmem_base + dcol, ad, bd, idesc1, 1);
         }
       };
       if constexpr (NL >= 2) {
-        // Layer 2 takes A (= H) from TMEM and B (= W2) from SMEM: the tensor core reads 4 KB of
-        // SMEM per K=16 step instead of 8, and no epilogue writes H through shared memory.
+        // Layer 2 takes A (= H) from TMEM and B (= W2) from SMEM, N = H in one accumulation.
+        // Pipe order per tile t: L2(t) chunks 0..NC/2-1, L1 piece 0 (t+1), L2(t) chunks NC/2..,
+        // L1 piece 1 (t+1), then L2(t+1) once both warpgroups drained D2(t). Warpgroup 0 converts
+        // piece 0 (t+1) into H chunks 0.. while L2(t) finishes (hfree[c] commits release H chunk by
+        // chunk), helps drain D2(t), then converts piece 1 (t+1).
         const uint64_t whdesc = make_sdesc(smem_u32(smem + P::off_wh), 16, 1024, kLayoutSW128);
         constexpr int NC = H / 64;                 // 64-wide K-chunks of H (32 TMEM columns each)
         const uint64_t bb2desc = make_sdesc(smem_u32(smem + P::off_bb + P::BB), 0, 32, kLayoutNone);
         uint32_t pc = 0;   // L1 pieces issued
+        uint32_t cur_tile = 0;
+#ifdef FLERN_SEQ_TRACE
+        uint32_t mseq = 0;
+        unsigned long long* seqbuf = reinterpret_cast<unsigned long long*>(smem + P::off_seq);
+        auto SEQ = [&](uint32_t tag) {   // SMEM log, copied out at teardown (one st.shared per event)
+          if (cur_tile >= kSeqTile && mseq < 256u) {
+            if (lane == 0) seqbuf[mseq] = ((unsigned long long)clock64() << 8) | tag;
+            ++mseq;
+          }
+        };
+#else
+        auto SEQ = [](uint32_t) {};
+#endif
+        auto WAITQ = [&](uint32_t tag, uint64_t* bar, uint32_t par, int code) {
+          SEQ(tag);
+          mbar_wait(bar, par, code);
+          SEQ(tag + 1);
+        };
         auto issue_l1_piece = [&](int s, int piece) {
           constexpr uint32_t NP = (uint32_t)H / TP::NH1;
           constexpr uint32_t idesc1 = make_idesc_bf16(128, NP);
-          FLERN_WAIT(W_MMA_D1EMPTY, lane == 0, d1empty, (pc & 1) ^ 1, 11);   // R1 read out by warpgroup 0
+          WAITQ(SQ_D1EMPTY, d1empty, (pc & 1) ^ 1, 11);   // R1 read out by warpgroup 0
           tc_fence_after();
-          if (leader)
+          if (elect_one_sync())
             mma_bf16_ss(tmem_base, onesdesc, bb1desc + ((uint32_t)(piece * (NP / 8) * 32) >> 4), idesc1 | kIdescBMajorMN, 0);
 #pragma unroll
           for (int ks = 0; ks < K0P / 16; ++ks) {
             const uint64_t ad = xdesc + ((uint32_t)(s * P::XS + ks * 2 * (kTile * 16)) >> 4);
             const uint64_t bd = w1desc + ((uint32_t)(ks * 2 * (H * 16) + piece * NP * 16) >> 4);
-            if (leader) mma_bf16_ss(tmem_base, ad, bd, idesc1, 1);
+            if (elect_one_sync()) mma_bf16_ss(tmem_base, ad, bd, idesc1, 1);
           }
-          if (leader) mma_commit(d1full);
+          if (elect_one_sync()) mma_commit(d1full);
+          SEQ(SQ_L1);
           ++pc;
-        };
-        auto issue_l2_half = [&](int half, uint32_t tile) {
-          constexpr uint32_t idesc2 = make_idesc_bf16(128, H / 2);
-          const uint32_t dcol = tmem_base + TP::D2C + half * (H / 2);
-          // bias first (needs no H chunk): neurons [half*H/2, +H/2) = bias blocks from half*H/16
-          if (leader)
-            mma_bf16_ss(dcol, onesdesc, bb2desc + ((uint32_t)(half * (H / 16) * 32) >> 4), idesc2 | kIdescBMajorMN, 0);
-#pragma unroll
-          for (int c = 0; c < NC; ++c) {
-            if (half == 0) { FLERN_WAIT(W_MMA_HFULL, true, &hfull[c], tile & 1, 12); tc_fence_after(); }
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {   // 4 x K=16 inside one 64-wide K-chunk (8 TMEM columns each)
-              const uint64_t bd = whdesc + ((uint32_t)(c * (H * 128) + half * (H / 16) * 1024 + j * 32) >> 4);
-              if (leader) mma_bf16_ts(dcol, tmem_base + TP::HT + c * 32 + j * 8, bd, idesc2, 1);
-            }
-            if (half == 1 && leader) mma_commit(&hfree[c]);   // last reader of H chunk c for this tile
-          }
-          if (leader) mma_commit(&dfull[half]);
         };
         FLERN_WAIT(W_MMA_FULL, lane == 0, &full[0], 0, 10);
         if (*meta_of<K0P, H, NL>(smem, 0).count >= 0) {
           tc_fence_after();
           for (int piece = 0; piece < TP::NH1; ++piece) issue_l1_piece(0, piece);
+          constexpr uint32_t idesc2 = make_idesc_bf16(128, H);
+          const uint32_t dcol = tmem_base + TP::D2C;
           for (uint32_t t = 0;; ++t) {
-            FLERN_WAIT(W_MMA_DEMPTY0, lane == 0, &dempty[0], (t & 1) ^ 1, 13);
+            cur_tile = t;
+            SEQ(SQ_TILE);
+            WAITQ(SQ_DEMPTY0, &dempty[0], (t & 1) ^ 1, 13);   // D2(t-1) drained by both warpgroups
             if (lane == 0) FLERN_TRACE(TR_MMA_D2A_FREE, t);
             tc_fence_after();
-            issue_l2_half(0, t);
-            if (lane == 0) FLERN_TRACE(TR_MMA_L2A_DONE, t);
-            // L1 piece 0 of tile t+1 goes between the two halves when tile t+1 is already published
-            // (warpgroup 0 converts it while L2b(t) runs); otherwise after L2b(t) (never block the
-            // tile in flight on the producer). Piece 1 follows L2b(t).
+            if (elect_one_sync()) mma_bf16_ss(dcol, onesdesc, bb2desc, idesc2 | kIdescBMajorMN, 0);   // bias
             const int s1 = (t + 1) % S;
             const uint32_t ph1 = ((t + 1) / S) & 1;
-            const bool have_next = mbar_test_wait(&full[s1], ph1);
-            bool next = false;
-            auto do_next = [&]() {
-              if (lane == 0) FLERN_TRACE(TR_MMA_NEXT_READY, t);
-              next = *meta_of<K0P, H, NL>(smem, s1).count >= 0;
-              if (next) {
-                issue_l1_piece(s1, 0);
-                FLERN_TRACE(TR_MMA_L1_ISSUED, t);
+            int next = -1;   // tile t+1: -1 not yet known, 0 none (end of stream), 1 published
+            int pieces = 0;
+#pragma unroll
+            for (int c = 0; c < NC; ++c) {
+              WAITQ(SQ_HFULL, &hfull[c], t & 1, 12);
+              tc_fence_after();
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {   // 4 x K=16 inside one 64-wide K-chunk (8 TMEM columns each)
+                const uint64_t bd = whdesc + ((uint32_t)(c * (H * 128) + j * 32) >> 4);
+                if (elect_one_sync()) mma_bf16_ts(dcol, tmem_base + TP::HT + c * 32 + j * 8, bd, idesc2, 1);
               }
-            };
-            if (have_next) do_next();
-            FLERN_WAIT(W_MMA_DEMPTY1, lane == 0, &dempty[1], (t & 1) ^ 1, 14);
-            if (lane == 0) FLERN_TRACE(TR_MMA_D2B_FREE, t);
-            tc_fence_after();
-            issue_l2_half(1, t);
-            if (lane == 0) FLERN_TRACE(TR_MMA_L2B_ISSUED, t);
-            if (!have_next) {
-              FLERN_WAIT(W_MMA_FULL, lane == 0, &full[s1], ph1, 10);
-              do_next();
+              if (elect_one_sync()) mma_commit(&hfree[c]);   // last reader of H chunk c for this tile
+              SEQ(SQ_L2A);
+              if (c == NC / 2 - 1 || (NC == 1 && c == 0)) {   // L1 piece 0 of tile t+1, if published
+                if (__shfl_sync(0xffffffffu, (int)mbar_test_wait(&full[s1], ph1), 0)) {
+                  next = *meta_of<K0P, H, NL>(smem, s1).count >= 0 ? 1 : 0;
+                  if (next == 1) issue_l1_piece(s1, pieces++);
+                }
+              }
             }
-            if (!next) break;
-            for (int piece = 1; piece < TP::NH1; ++piece) issue_l1_piece(s1, piece);
+            if (elect_one_sync()) mma_commit(&dfull[0]);
+            if (lane == 0) FLERN_TRACE(TR_MMA_L2B_ISSUED, t);
+            if (next < 0) {
+              WAITQ(SQ_FULL, &full[s1], ph1, 10);
+              next = *meta_of<K0P, H, NL>(smem, s1).count >= 0 ? 1 : 0;
+            }
+            if (next == 0) break;
+            while (pieces < TP::NH1) issue_l1_piece(s1, pieces++);
           }
         }
       } else {
@@ -272,7 +306,7 @@ __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_c
           mbar_wait(&dempty[b], ((t >> 1) & 1) ^ 1, 11);
           tc_fence_after();
           issue_l1(s, b * H);
-          if (leader) mma_commit(&dfull[b]);
+          if (elect_one_sync()) mma_commit(&dfull[b]);
         }
       }
     }
@@ -297,10 +331,13 @@ __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_c
     // the |x| an operand modifier, so the dot needs no max instruction (s_wout holds w_out / 2,
     // exact in fp32). Four independent accumulator chains; TMEM loads are double-buffered: chunk
     // c+1 is in flight while chunk c is reduced.
-    auto dot_cols = [&](uint32_t col, int ncols, int woff, float2 (&acc)[4]) {
+    // loaded() runs once every column has been read out of TMEM (before the last chunk's math), so
+    // the caller can release the accumulator early.
+    auto dot_cols = [&](uint32_t col, int ncols, int woff, float2 (&acc)[4], auto&& loaded) {
       uint32_t v[2][32];
       tmem_ld32_async(tmem_base + lane_off + col, v[0]);
       tmem_ld_wait(v[0]);
+      if (ncols <= 32) loaded();
 #pragma unroll
       for (int c = 0; c < 8; ++c) {   // up to 8 chunks of 32 columns (H <= 256)
         if (c * 32 >= ncols) break;
@@ -317,8 +354,18 @@ __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_c
           acc[2] = fma2(z1, make_float2(w.z, w.w), acc[2]);
           acc[3] = fma2(make_float2(fabsf(z1.x), fabsf(z1.y)), make_float2(w.z, w.w), acc[3]);
         }
-        if ((c + 1) * 32 < ncols) tmem_ld_wait(v[cur ^ 1]);
+        if ((c + 1) * 32 < ncols) {
+          tmem_ld_wait(v[cur ^ 1]);
+          if ((c + 2) * 32 >= ncols) loaded();
+        }
       }
+    };
+    auto release = [&](uint64_t* bar) {   // this warp's TMEM reads are complete -> MMA may overwrite
+      return [&, bar] {
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(bar);
+      };
     };
     auto dot_sum = [](const float2 (&acc)[4]) {
       return ((acc[0].x + acc[1].x) + (acc[0].y + acc[1].y)) + ((acc[2].x + acc[3].x) + (acc[2].y + acc[3].y));
@@ -326,65 +373,83 @@ __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_c
 
     if constexpr (NL >= 2) {
       constexpr int NC = H / 64;
+      constexpr int CPP = NC / TP::NH1;   // 64-wide chunks per L1 piece
+      float* s_part = reinterpret_cast<float*>(smem + P::off_part);   // [2][128] warpgroup-0 partial logits
       if (wg == 0) {
-        // ---- warpgroup 0: D1 -> ReLU -> bf16 -> H in TMEM (layer-2 A operand), chunk by chunk ----
-        constexpr int CPP = NC / TP::NH1;   // 64-wide chunks per L1 piece
-        for (uint32_t t = 0; !p.no_model; ++t) {
-          const int s = t % S;
-          FLERN_WAIT(W_WG0_FULL, tid == 128, &full[s], (t / S) & 1, 20);
-          if (*meta_of<K0P, H, NL>(smem, s).count < 0) break;
-          if (tid == 128) FLERN_TRACE(TR_W0_FULL, t);
-#pragma unroll 1
-          for (int piece = 0; piece < TP::NH1; ++piece) {
-            FLERN_WAIT(W_WG0_D1FULL, tid == 128, d1full, (t * TP::NH1 + piece) & 1, 21);
-            if (tid == 128 && piece == 0) FLERN_TRACE(TR_W0_D1FULL, t);
-            tc_fence_after();
-            if (p.dbg_mode & 1) {   // diagnostic: keep the protocol, skip the math
-              tc_fence_before();
-              __syncwarp();
-              if (lane == 0) mbar_arrive(d1empty);
-              for (int cc = 0; cc < CPP; ++cc) {
-                const int c = piece * CPP + cc;
-                mbar_wait(&hfree[c], (t & 1) ^ 1, 22);
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&hfull[c]);
-              }
-              continue;
-            }
-#pragma unroll
+        // ---- warpgroup 0: L1 pieces -> ReLU -> bf16 -> H in TMEM; upper half of the D2 drain ----
+        uint32_t pcs = 0;   // L1 pieces consumed
+        // one L1 piece of tile tt into H chunks [piece*CPP, +CPP); waits for layer 2 of tile tt-1 to
+        // release each chunk (hfree)
+        auto convert_piece = [&](uint32_t tt, int piece) {
+          FLERN_WAIT(W_WG0_D1FULL, tid == 128, d1full, pcs & 1, 21);
+          ++pcs;
+          tc_fence_after();
+          if (p.dbg_mode & 1) {   // diagnostic: keep the protocol, skip the math
+            release(d1empty)();
             for (int cc = 0; cc < CPP; ++cc) {
               const int c = piece * CPP + cc;
-              uint32_t pk[32];
-              {
-                uint32_t va[32], vb[32];   // both halves of the chunk in flight, one wait
-                tmem_ld32_async(tmem_base + lane_off + cc * 64, va);
-                tmem_ld32_async(tmem_base + lane_off + cc * 64 + 32, vb);
-                tmem_ld_wait(va);
-                tmem_ld_wait(vb);
-#pragma unroll
-                for (int i = 0; i < 16; ++i) {   // D1 already holds the bias (kOnesBytes)
-                  pk[i] = relu_bf16x2(__uint_as_float(va[2 * i]), __uint_as_float(va[2 * i + 1]));
-                  pk[16 + i] = relu_bf16x2(__uint_as_float(vb[2 * i]), __uint_as_float(vb[2 * i + 1]));
-                }
-              }
-              if (cc == CPP - 1) {   // the whole L1 piece is in registers: the MMA may overwrite R1
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(d1empty);
-              }
-              FLERN_WAIT(W_WG0_HFREE, tid == 128, &hfree[c], (t & 1) ^ 1, 22);   // L2b(t-1) done with chunk c
-              if (tid == 128 && c == 0) FLERN_TRACE(TR_W0_HFREE0, t);
-              tc_fence_after();
-              tmem_st32(tmem_base + lane_off + TP::HT + c * 32, pk);   // K = 64c .. 64c+63, packed pairs
-              tc_fence_before();
+              mbar_wait(&hfree[c], (tt & 1) ^ 1, 22);
               __syncwarp();
               if (lane == 0) mbar_arrive(&hfull[c]);
             }
+            return;
           }
-          if (tid == 128) FLERN_TRACE(TR_W0_DONE, t);
+#pragma unroll
+          for (int cc = 0; cc < CPP; ++cc) {
+            const int c = piece * CPP + cc;
+            uint32_t pk[32];
+            {
+              uint32_t va[32], vb[32];   // both halves of the chunk in flight, one wait
+              tmem_ld32_async(tmem_base + lane_off + cc * 64, va);
+              tmem_ld32_async(tmem_base + lane_off + cc * 64 + 32, vb);
+              tmem_ld_wait(va);
+              tmem_ld_wait(vb);
+#pragma unroll
+              for (int i = 0; i < 16; ++i) {   // D1 already holds the bias (kOnesBytes)
+                pk[i] = relu_bf16x2(__uint_as_float(va[2 * i]), __uint_as_float(va[2 * i + 1]));
+                pk[16 + i] = relu_bf16x2(__uint_as_float(vb[2 * i]), __uint_as_float(vb[2 * i + 1]));
+              }
+            }
+            if (cc == CPP - 1) release(d1empty)();   // the whole piece is in registers: R1 is free
+            FLERN_WAIT(W_WG0_HFREE, tid == 128, &hfree[c], (tt & 1) ^ 1, 22);   // L2(tt-1) done with chunk c
+            tc_fence_after();
+            tmem_st32(tmem_base + lane_off + TP::HT + c * 32, pk);   // K = 64c .. 64c+63, packed pairs
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&hfull[c]);
+          }
+        };
+        // does tile tt exist (published and not the end marker)?
+        auto has_tile = [&](uint32_t tt) {
+          const int s = tt % S;
+          FLERN_WAIT(W_WG0_FULL, tid == 128, &full[s], (tt / S) & 1, 20);
+          return *meta_of<K0P, H, NL>(smem, s).count >= 0;
+        };
+        if (!p.no_model && has_tile(0)) {
+          for (int piece = 0; piece < TP::NH1; ++piece) convert_piece(0, piece);
+          for (uint32_t t = 0;; ++t) {
+            if (tid == 128) FLERN_TRACE(TR_W0_FULL, t);
+            const bool more = has_tile(t + 1);
+            if (more) convert_piece(t + 1, 0);
+            if (tid == 128) FLERN_TRACE(TR_W0_D1FULL, t);
+            // upper half of D2(t): relu(D2) . w_out partial -> SMEM for warpgroup 1
+            FLERN_WAIT(W_WG0_D1FULL, tid == 128, &dfull[0], t & 1, 21);
+            tc_fence_after();
+            float2 acc4[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
+                              make_float2(0.f, 0.f)};
+            if (!(p.dbg_mode & 1)) dot_cols(TP::D2C + H / 2, H / 2, H / 2, acc4, release(&dempty[0]));
+            else release(&dempty[0])();
+            s_part[(t & 1) * kTile + r] = dot_sum(acc4);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(pready);
+            if (tid == 128) FLERN_TRACE(TR_W0_HFREE0, t);
+            if (!more) break;
+            for (int piece = 1; piece < TP::NH1; ++piece) convert_piece(t + 1, piece);
+            if (tid == 128) FLERN_TRACE(TR_W0_DONE, t);
+          }
         }
       } else {
-        // ---- warpgroup 1: logit = relu(D2) . w_out + b_out, predicate, group-by ----
+        // ---- warpgroup 1: lower half of the D2 drain, logit = both halves + b_out, predicate, group-by ----
         for (uint32_t t = 0;; ++t) {
           const int s = t % S;
           FLERN_WAIT(W_WG1_FULL, tid == 256, &full[s], (t / S) & 1, 23);
@@ -396,18 +461,16 @@ __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_c
           if (!p.no_model) {
             float2 acc4[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
                               make_float2(0.f, 0.f)};
-#pragma unroll 1
-            for (int h = 0; h < 2; ++h) {
-              FLERN_WAIT(W_WG1_DFULL, tid == 256, &dfull[h], t & 1, 24);
-              if (tid == 256) FLERN_TRACE(h ? TR_W1_DFULL1 : TR_W1_DFULL0, t);
-              tc_fence_after();
-              if (!(p.dbg_mode & 1)) dot_cols(TP::D2C + h * (H / 2), H / 2, h * (H / 2), acc4);
-              if (tid == 256) FLERN_TRACE(h ? TR_W1_DOTB : TR_W1_DOTA, t);
-              tc_fence_before();
-              __syncwarp();
-              if (lane == 0) mbar_arrive(&dempty[h]);
-            }
-            logit = dot_sum(acc4) + p.bout;
+            FLERN_WAIT(W_WG1_DFULL, tid == 256, &dfull[0], t & 1, 24);
+            if (tid == 256) FLERN_TRACE(TR_W1_DFULL0, t);
+            tc_fence_after();
+            if (!(p.dbg_mode & 1)) dot_cols(TP::D2C, H / 2, 0, acc4, release(&dempty[0]));
+            else release(&dempty[0])();
+            if (tid == 256) FLERN_TRACE(TR_W1_DOTA, t);
+            const float mine = dot_sum(acc4);
+            FLERN_WAIT(W_WG1_DFULL, tid == 256, pready, t & 1, 26);   // warpgroup 0's half
+            logit = (mine + s_part[(t & 1) * kTile + r]) + p.bout;
+            if (tid == 256) FLERN_TRACE(TR_W1_DOTB, t);
           }
           finish_tile(m, count, s, logit);
           if (tid == 256) FLERN_TRACE(TR_W1_AGG, t);
@@ -428,7 +491,7 @@ __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_c
           tc_fence_after();
           float2 acc4[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
                             make_float2(0.f, 0.f)};
-          dot_cols(wg * H, H, 0, acc4);
+          dot_cols(wg * H, H, 0, acc4, [] {});
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&dempty[wg]);
@@ -444,6 +507,11 @@ __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_c
   tc_fence_before();
   __syncthreads();
   FLERN_CTA_STAMP(TR_CTA_LOOP_END);
+#ifdef FLERN_SEQ_TRACE
+  if (p.dbg_trace && blockIdx.x == 0)
+    for (int i = tid; i < 256; i += kThreads)
+      p.dbg_trace[TR_MMA_SEQ * kTraceTiles + i] = reinterpret_cast<unsigned long long*>(smem + P::off_seq)[i];
+#endif
   if (warp == 12) { tc_fence_after(); tmem_dealloc(tmem_base, kTmemCols); }
   write_partials_and_reduce(p, acc, s_cnt, s_is_last, tid, kThreads);
 }

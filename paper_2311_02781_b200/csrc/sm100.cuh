@@ -26,7 +26,7 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 // Suspend-time hint of mbarrier waits in ns (host-set from FLERN_WAIT_HINT; 0 = the instruction's
 // default, no explicit hint). A waiting thread sleeps in hardware until the phase completes or the
 // hint expires instead of spinning through issue slots the working warps need.
-__constant__ uint32_t c_wait_hint = 0x100000u;
+__constant__ uint32_t c_wait_hint = 0u;
 __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
   uint32_t ok;
   const uint32_t hint = c_wait_hint;
@@ -77,6 +77,21 @@ __device__ __noinline__ void mbar_wait_slow(uint64_t* bar, uint32_t parity, int 
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity, int tag) {
   if (!mbar_try_wait(bar, parity)) mbar_wait_slow(bar, parity, tag);
+}
+
+// Spin on the non-blocking test_wait (for the MMA issue warp: a try_wait there costs the tensor pipe
+// far more than its own latency; same watchdog as mbar_wait).
+__device__ __forceinline__ void mbar_spin(uint64_t* bar, uint32_t parity, int tag) {
+  if (mbar_test_wait(bar, parity)) return;
+  uint64_t t0 = globaltimer_ns();
+  uint32_t n = 0;
+  while (!mbar_test_wait(bar, parity)) {
+    if ((++n & 65535u) == 0 && globaltimer_ns() - t0 > 4000000000ull) {
+      printf("flern: mbarrier watchdog (spin, tag %d) block %d thread %d parity %u\n", tag, (int)blockIdx.x,
+             (int)threadIdx.x, parity);
+      __trap();
+    }
+  }
 }
 
 // Named barrier among `nthreads` threads (id 1..15; 0 is __syncthreads).

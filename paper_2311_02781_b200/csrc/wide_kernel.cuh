@@ -43,10 +43,10 @@ struct WidePlan {
   static constexpr uint32_t off_acc = off_wout + H * 4;
   static constexpr uint32_t off_xchg = off_acc + kMaxGroups * 4 * 8;
   static constexpr uint32_t off_queue = off_xchg + 2 * kTile * 4;
-  static constexpr uint32_t off_norm = off_queue + kQueueBytes;
+  static constexpr uint32_t off_norm = off_queue + queue_bytes(32 * kProdWarpsWide);
   static constexpr uint32_t off_bar = off_norm + kMaxFeat * 8;
   static constexpr uint32_t off_misc = off_bar + 64 * 8;
-  static constexpr uint32_t total = off_misc + 128;
+  static constexpr uint32_t total = off_misc + kMiscBytes;
   // global weight image: [W1: NCH x W1C][W_2..W_NL: (NL-1) x NCH x KB x kBBlock]
   static constexpr size_t img_w1 = (size_t)NCH * W1C;
   static constexpr size_t img_wh = (size_t)(NL - 1) * NCH * KB * kBBlock;
@@ -97,9 +97,9 @@ __global__ void __launch_bounds__(kThreadsWide, 1) flern_query_wide_kernel(const
   uint64_t* actrdy = bars + 20;       // [2] a hidden layer's activations are in the scratch (NCH*4)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + P::off_misc);
   int32_t* wcnt = reinterpret_cast<int32_t*>(smem + P::off_misc + 16);
-  int64_t* s_cnt = reinterpret_cast<int64_t*>(smem + P::off_misc + 64);
-  unsigned int* s_is_last = reinterpret_cast<unsigned int*>(smem + P::off_misc + 96);
-  int64_t* s_claim = reinterpret_cast<int64_t*>(smem + P::off_misc + 104);   // [2] row-chunk claims
+  int64_t* s_cnt = reinterpret_cast<int64_t*>(smem + P::off_misc + 112);
+  unsigned int* s_is_last = reinterpret_cast<unsigned int*>(smem + P::off_misc + 144);
+  int64_t* s_claim = reinterpret_cast<int64_t*>(smem + P::off_misc + 152);   // [2] row-chunk claims
   unsigned long long* acc = reinterpret_cast<unsigned long long*>(smem + P::off_acc);
   float* s_bias = reinterpret_cast<float*>(smem + P::off_bias);
   float* s_wout = reinterpret_cast<float*>(smem + P::off_wout);
@@ -120,7 +120,7 @@ __global__ void __launch_bounds__(kThreadsWide, 1) flern_query_wide_kernel(const
   if (tid < kCounters) s_cnt[tid] = 0;
   if (tid == 0) { s_claim[0] = claim0; s_claim[1] = claim0 + 1; }
   if (tid == 0) {
-    for (int s = 0; s < S; ++s) { mbar_init(&xfull[s], kProducerThreads); mbar_init(&xempty[s], 4); }
+    for (int s = 0; s < S; ++s) { mbar_init(&xfull[s], 32 * kProdWarpsWide); mbar_init(&xempty[s], 4); }
     for (int s = 0; s < RS; ++s) { mbar_init(&rfull[s], 1); mbar_init(&rempty[s], 1); }
     for (int i = 0; i < 2; ++i) { mbar_init(&dfull[i], 1); mbar_init(&dempty[i], 4); mbar_init(&actrdy[i], NCH * 4); }
     fence_mbar_init();
@@ -136,7 +136,7 @@ __global__ void __launch_bounds__(kThreadsWide, 1) flern_query_wide_kernel(const
   const uint8_t* img_wh = p.wimg + P::img_w1;
 
   if (warp < 4) {
-    producer_loop<K0P, S, SH>(p, XRing{smem + P::off_x, P::XS, smem + P::off_meta, xfull, xempty}, wcnt, s_norm, s_cnt,
+    producer_loop<K0P, S, SH, kProdWarpsWide>(p, XRing{smem + P::off_x, P::XS, smem + P::off_meta, xfull, xempty}, wcnt, s_norm, s_cnt,
                           reinterpret_cast<int32_t*>(smem + P::off_queue), s_claim, tid, warp, lane);
   } else if (warp == 13) {
     // =============================== LOADER (bulk copies into the operand ring) ==============

@@ -205,7 +205,7 @@ class Query:
         self.ngroups = ngroups
 
 
-TRACE_EVENTS = 25
+TRACE_EVENTS = 26
 TRACE_TILES = 256
 
 

@@ -91,5 +91,9 @@ int main() {
   run<128, true, true, true>(sms);
   run<256, true, true, true>(sms);
   run<128, false, true, true>(sms);
+  run<64, true, true, true>(sms);
+  run<64, true, true, false>(sms);
+  run<32, true, true, true>(sms);
+  run<32, true, true, false>(sms);
   return 0;
 }

@@ -53,7 +53,7 @@ print("wait cycles, CTA 0 (fraction of kernel):")
 for i, nm in enumerate(W):
     print(f"  {nm:34s} {int(w[i]):>10d}  {w[i] / max(1, w[11]):6.1%}")
 # per-CTA timeline (%globaltimer, ns): start skew, loop-end spread (imbalance), final reduce
-st, su, le, ex = (tr[F.TRACE_EVENTS - 4], tr[F.TRACE_EVENTS - 3], tr[F.TRACE_EVENTS - 2], tr[F.TRACE_EVENTS - 1])
+st, su, le, ex = tr[21], tr[22], tr[23], tr[24]
 n = int((st > 0).sum())
 if n:
     st, su, le, ex = st[:n], su[:n], le[:n], ex[:n]
@@ -65,3 +65,29 @@ if n:
     order = np.argsort(le - st)
     print("  slowest CTAs (loop us):", [(int(i), round(float(le[i] - st[i]) / 1e3, 1)) for i in order[-6:]])
     print("  fastest CTAs (loop us):", [(int(i), round(float(le[i] - st[i]) / 1e3, 1)) for i in order[:6]])
+
+# MMA thread event sequence from tile 100 (TR_MMA_SEQ): clock deltas and tags
+TAGS = {1: "L2a", 2: "L2b", 3: "L1", 4: "bias", 10: "hfull>", 11: "<hfull", 12: "dempty0>", 13: "<dempty0",
+        14: "dempty1>", 15: "<dempty1", 16: "d1empty>", 17: "<d1empty", 18: "full>", 19: "<full", 30: "TILE"}
+seq = tr[25]
+seq = seq[seq != 0]
+if len(seq):
+    clk = (seq.astype(np.uint64) >> np.uint64(8)).astype(np.int64)
+    tag = (seq & 255).astype(np.int64)
+    c0 = clk[0]
+    line = []
+    for i in range(len(seq)):
+        d = clk[i] - (clk[i - 1] if i else c0)
+        line.append(f"{TAGS.get(int(tag[i]), tag[i])}+{d}")
+    print("MMA sequence (event+cycles since previous):")
+    for i in range(0, min(len(line), 96), 12):
+        print("   ", " ".join(line[i:i + 12]))
+    import collections
+    agg = collections.defaultdict(list)
+    for i in range(1, len(seq)):
+        agg[TAGS.get(int(tag[i]), int(tag[i]))].append(int(clk[i] - clk[i - 1]))
+    nt = max(1, int((tag == 30).sum()) - 1)
+    span = int(clk[np.where(tag == 30)[0][-1]] - clk[np.where(tag == 30)[0][0]]) if (tag == 30).sum() > 1 else 0
+    print(f"per tile ({nt} tiles, {span / nt:.0f} cycles/tile): total cycles attributed to each event (time since previous)")
+    for k, v in sorted(agg.items(), key=lambda kv: -sum(kv[1])):
+        print(f"   {k:>10s}: n/tile {len(v) / nt:5.1f}  mean {np.mean(v):7.1f}  total/tile {sum(v) / nt:8.1f}")
