@@ -111,7 +111,6 @@ struct QueryParams {
   int32_t no_model;         // diagnostic: skip the MLP, select every joined row (scan/probe/gather only)
   int32_t dbg_mode;         // diagnostic (env FLERN_DBG_MODE): bit 0 = epilogues skip their math, bit 1 = producer issues no global loads
   int32_t sched;            // MMA issue order variant (env FLERN_SCHED; tuning)
-  int32_t l2_ahead;         // producer: fact rows are bulk-prefetched into L2 this many batches ahead (0 = off)
   const uint8_t* wimg;      // weight image: [Wh (SW128) | W1 (interleave)] bf16, exact SMEM layout
   const float* bias;        // [NL][H]
   const float* wout;        // [H]
@@ -214,6 +213,27 @@ __device__ __forceinline__ Meta meta_at(uint8_t* meta, int s) {
   uint8_t* m = meta + s * kMetaBytes;
   return Meta{reinterpret_cast<int32_t*>(m), reinterpret_cast<int32_t*>(m + 16),
               reinterpret_cast<int32_t*>(m + 16 + 4 * kTile), m + 16 + 8 * kTile};
+}
+
+// Fact-column ring (narrow kernel, producer shapes fixed at compile time): the loader warp copies
+// every fact column a batch reads into shared memory with 1D bulk copies (one per column and batch,
+// the whole HBM stream in flight without registers), the producer warps read their rows from it.
+// Stage f: column c at base + f * stage_bytes + c * rows * 4; header hdr[f]: {row0, nrows}
+// (nrows < 0 = end of stream). Columns: 0 probe key, 1 sum, 2 group (when on the fact side),
+// 3 + k fact feature k.
+constexpr int kFactStages = 2;
+__host__ __device__ constexpr int fact_cols(int nf) { return 3 + nf; }
+struct FactRing {
+  uint8_t* base = nullptr;
+  uint32_t stage_bytes = 0;
+  int64_t* hdr = nullptr;      // [kFactStages][2]
+  uint64_t* full = nullptr;    // [kFactStages] loader (1 arrival + tx bytes) -> producers
+  uint64_t* empty = nullptr;   // [kFactStages] producer warps -> loader
+};
+__device__ __forceinline__ const int32_t* fact_col_ptr(const QueryParams& p, int c) {
+  return c == 0 ? p.probe[0].fact_key
+                : (c == 1 ? (p.sum.src == 0 ? p.sum.base : nullptr)
+                          : (c == 2 ? (p.grp.src == 0 ? p.grp.base : nullptr) : p.fcol[c - 3]));
 }
 
 // Predicate + group-by of one 128-row tile, one thread per row (a warpgroup covers the tile).

@@ -178,7 +178,7 @@ constexpr bool plan_fits() {
 // fact-first): C1 = 6 fact + 2 orders; C2 = 12 fact + 4 orders (o_f0 float); C3/C4 = 20 fact
 // (l_f0..5 float) + 8 orders (o_f0..4 float) + 4 customer (c_f0 float).
 #define FLERN_SPEC(a, b, c, nf, n0, n1, fm) {a, b, c, nf, n0, n1, fm, flern_query_kernel<a, b, c, FixedShape<nf, n0, n1, fm>>, \
-   SmemPlan<a, b, c>::total, false},
+   SmemPlan<a, b, c, fact_cols(nf)>::total, false},
 #define FLERN_WSPEC(a, b, c, nf, n0, n1, fm) {a, b, c, nf, n0, n1, fm, \
    flern_query_wide_kernel<a, b, c, FixedShape<nf, n0, n1, fm>>, WidePlan<a, b, c>::total, false, kThreadsWide, \
    WidePlan<a, b, c>::scratch_per_cta},
@@ -754,7 +754,6 @@ extern "C" FLERN_API flern_status flern_run_query(flern_ctx* ctx, const flern_qu
   p.no_model = (q->flags & FLERN_Q_NO_MODEL) ? 1 : 0;
   p.dbg_mode = getenv("FLERN_DBG_MODE") ? atoi(getenv("FLERN_DBG_MODE")) : 0;   // diagnostics only
   p.sched = getenv("FLERN_SCHED") ? atoi(getenv("FLERN_SCHED")) : 1;              // tuning knob
-  p.l2_ahead = getenv("FLERN_L2_AHEAD") ? atoi(getenv("FLERN_L2_AHEAD")) : 0;    // tuning knob
   const double t = (double)q->threshold;
   p.thr_logit = t <= 0.0 ? -INFINITY : (t >= 1.0 ? INFINITY : (float)std::log(t / (1.0 - t)));
   uint8_t* img = m.dbuf;

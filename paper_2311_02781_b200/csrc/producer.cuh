@@ -26,10 +26,16 @@ struct ProdState {
 
 // One batch: rows [row0, row0 + R) of this thread (consecutive; with R == 1 any row id), in[r] =
 // the row takes part (inside the shard and past the pre-filter).
-template <int K0P, int S, int R, class SH, int NPW>
+// BULK: the fact columns of this batch are in the shared-memory fact stage at sfa (rows [0, nfull) of
+// the batch, column stride kBR rows; see FactRing); my rows are [rel, rel + R) of the batch. The
+// few tail rows past nfull (table end, not a whole 16-byte granule) are read from global memory.
+// features_read() runs once every fact-stage read of this batch has completed.
+template <int K0P, int S, int R, class SH, int NPW, bool BULK = false, class FR = void (*)()>
 __device__ __forceinline__ void produce_batch(ProdState& st, const QueryParams& p, const XRing& ring, int32_t* wcnt,
                                               const float* s_normf, int64_t row0, bool whole, const bool (&in)[R],
-                                              int bidx, int64_t row_end, int t, int warp, int lane) {
+                                              int bidx, int64_t row_end, int t, int warp, int lane,
+                                              uint32_t sfa = 0, int rel = 0, int nfull = 0, FR&& features_read = nullptr) {
+  constexpr int kBR = batch_rows(K0P, 32 * NPW);
   constexpr bool kSpec = SH::NF >= 0;   // feature shape known at compile time
   const int nfact = kSpec ? SH::NF : p.nfact;
   const int nfeat = kSpec ? SH::NF + SH::ND0 + SH::ND1 : p.nfeat;
@@ -81,14 +87,34 @@ __device__ __forceinline__ void produce_batch(ProdState& st, const QueryParams& 
 #pragma unroll
       for (int r = 0; r < R; ++r) any |= valid[r];
       const bool anyld = any && !synth;
+      // fact column c of my R rows from the fact stage (BULK)
+      auto loadF = [&](int c, int32_t (&v)[R]) {
+        const uint32_t a = sfa + (uint32_t)(c * kBR + rel) * 4u;
+        if (R == 2 && rel + R <= nfull) {
+          const int2 x = lds64(a);
+          v[0] = x.x;
+          v[R - 1] = x.y;
+        } else {
+#pragma unroll
+          for (int r = 0; r < R; ++r)
+            v[r] = rel + r < nfull ? lds32(a + 4 * r) : ld1(fact_col_ptr(p, c) + row0 + r, in[r]);
+        }
+      };
       // 1. fact-side loads, all issued before any use: probe key, group/sum, features [0, nfact)
+      //    (BULK: features come from the fact stage after the probes, so no registers wait on them)
       int32_t key[R], gv[R], sv[R];
       int32_t v[K0P][R];
-      loadR(p.probe[0].fact_key, row0, whole, anyld, key);
-      loadR(p.grp.base, row0, whole, anyld && p.grp.src == 0, gv);
-      loadR(p.sum.base, row0, whole, anyld && p.sum.src == 0, sv);
+      if constexpr (BULK) {
+        loadF(0, key);
+        if (p.grp.src == 0) loadF(2, gv);
+        if (p.sum.src == 0) loadF(1, sv);
+      } else {
+        loadR(p.probe[0].fact_key, row0, whole, anyld, key);
+        loadR(p.grp.base, row0, whole, anyld && p.grp.src == 0, gv);
+        loadR(p.sum.base, row0, whole, anyld && p.sum.src == 0, sv);
 #pragma unroll
-      for (int k = 0; k < K0P; ++k) loadR(p.fcol[k], row0, whole, anyld && k < nfact, v[k]);
+        for (int k = 0; k < K0P; ++k) loadR(p.fcol[k], row0, whole, anyld && k < nfact, v[k]);
+      }
       // 2. probes, bucketised linear probing: the aligned 4-slot bucket (a 32-byte
       //    sector) holding the home slot is read with two 16-byte loads and resolved with selects;
       //    only a row that meets neither its key nor an empty slot there continues (rare, warp-
@@ -174,12 +200,18 @@ __device__ __forceinline__ void produce_batch(ProdState& st, const QueryParams& 
         for (int k = 0; k < K0P; ++k)
           if (k >= nfact && k < nfeat) v[k][r] = ld1((((dprobe1 >> k) & 1) ? rb1 : rb0) + p.dword[k], valid[r] && !synth);
       }
+      if constexpr (BULK) {
+#pragma unroll
+        for (int k = 0; k < K0P; ++k)
+          if (k < nfact) loadF(3 + k, v[k]);
+      }
       // 4. normalise in fp32 (fma(x, scale, -shift*scale), reading Q4) -> packed bf16 pairs
       uint32_t pk[R][K0P / 2];
 #pragma unroll
       for (int r = 0; r < R; ++r)
 #pragma unroll
         for (int k = 0; k < K0P; k += 2) pk[r][k / 2] = cvt_pair(k, v[k][r], v[k + 1][r]);
+      if constexpr (BULK) features_read();
       if (t == 0) FLERN_TRACE(TR_P_GATHERED, bidx);
       // compaction: position of each surviving row in the batch (warp scan + per-warp counts)
       int my_cnt = 0;
@@ -248,10 +280,10 @@ __device__ __forceinline__ void produce_batch(ProdState& st, const QueryParams& 
 }
 
 // `tid` is the thread's index in the producer group [0, 32*NPW), `warp` its warp in the group.
-template <int K0P, int S, class SH, int NPW>
+template <int K0P, int S, class SH, int NPW, bool BULK>
 __device__ __forceinline__ void producer_loop(const QueryParams& p, const XRing& ring, int32_t* wcnt,
                                               const float* s_normf, int64_t* s_cnt, int32_t* queue,
-                                              int64_t* s_claim, int tid, int warp, int lane) {
+                                              int64_t* s_claim, const FactRing& fr, int tid, int warp, int lane) {
   constexpr int NPT = 32 * NPW;
   constexpr int R = rows_per_thread(K0P);
   constexpr int kBatch = batch_rows(K0P, NPT);
@@ -275,39 +307,41 @@ __device__ __forceinline__ void producer_loop(const QueryParams& p, const XRing&
   mbar_wait(&ring.empty[0], ((st.acq / S) & 1) ^ 1, 1);   // acquire the first stage
   st.acq = 1;
   int bidx = 0;
-  // L2 prefetch (p.l2_ahead > 0): the fact columns a batch reads are requested into L2 ahead of use,
-  // so the batch's column loads hit L2 instead of HBM; that shortens the dependent chain
-  // fact load -> probe -> payload load which bounds a batch, and keeps HBM busy without holding
-  // registers or shared memory for the bytes in flight.
-  constexpr bool kSpecP = SH::NF >= 0;
-  const int ncolpf = 3 + (kSpecP ? SH::NF : p.nfact);
-  auto pf_col_ptr = [&](int c) -> const int32_t* {
+  // staged fact column c: 0 = probe key, 1 = sum column, 2 = group column (null when they come from
+  // the build side), 3 + k = fact feature k
+  auto fact_col = [&](int c) -> const int32_t* {
     return c == 0 ? p.probe[0].fact_key
                   : (c == 1 ? (p.sum.src == 0 ? p.sum.base : nullptr)
                             : (c == 2 ? (p.grp.src == 0 ? p.grp.base : nullptr) : p.fcol[c - 3]));
   };
-  const int ahead = p.l2_ahead;
-  if (!p.pf_col) {
-    // one bulk prefetch per column and batch, spread over the first threads
-    auto prefetch_rows = [&](int64_t lo, int64_t hi) {   // rows [lo, hi) of every fact column read
-      if (t < ncolpf && lo < hi) {
-        const int32_t* c = pf_col_ptr(t);
-        const int64_t a = lo & ~3ll, b = (hi + 3) & ~3ll;
-        if (c) prefetch_l2_bulk(c + a, (uint32_t)(b - a) * 4u);
-      }
-    };
-    if (ahead > 0) prefetch_rows(cur.lo, min(cur.hi, cur.lo + (int64_t)ahead * kBatch));
+  if (BULK && !p.pf_col) {
+    // batches come from the loader warp's fact ring (loader_loop), which also claims the row chunks
+    for (uint32_t b = 0;; ++b, ++bidx) {
+      const int f = b % kFactStages;
+      mbar_wait(&fr.full[f], (b / kFactStages) & 1, 6);
+      const int64_t srow0 = fr.hdr[2 * f];
+      const int nrows = (int)fr.hdr[2 * f + 1];
+      if (nrows < 0) break;
+      if (t == 0) FLERN_TRACE(TR_P_START, bidx);
+      const int rel = R * t;
+      bool in[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) in[r] = rel + r < nrows;
+      auto release = [&] {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&fr.empty[f]);
+      };
+      produce_batch<K0P, S, R, SH, NPW, true>(st, p, ring, wcnt, s_normf, srow0 + rel, rel + R <= nrows, in, bidx,
+                                              srow0 + nrows, t, warp, lane,
+                                              smem_u32(fr.base + f * fr.stage_bytes), rel, nrows & ~3, release);
+    }
+  } else if (!p.pf_col) {
     while (cur.lo < n) {
       int64_t a = 0;
       if (t == 0) a = claim_chunk(p, 1);
       const int64_t row_end = cur.hi;
       if (t == 0) s_cnt[0] += row_end - cur.lo;   // rows scanned by this CTA
-      if (ahead > 0 && nxt.lo < n) prefetch_rows(nxt.lo, min(nxt.hi, nxt.lo + (int64_t)ahead * kBatch));
       for (int64_t base = cur.lo; base < row_end; base += kBatch, ++bidx) {
-        if (ahead > 0) {
-          const int64_t pl = base + (int64_t)ahead * kBatch;
-          prefetch_rows(pl, min(row_end, pl + kBatch));
-        }
         if (t == 0) FLERN_TRACE(TR_P_START, bidx);
         const int64_t row0 = base + (int64_t)R * t;
         bool in[R];
@@ -334,25 +368,14 @@ __device__ __forceinline__ void producer_loop(const QueryParams& p, const XRing&
         }
       }
     };
-    // the filter column is bulk-prefetched 2*ahead scan chunks ahead (4 KB each, thread 0)
-    auto prefetch_scan = [&](int64_t lo, int64_t hi) {
-      if (t == 0 && lo < hi) {
-        const int64_t a = lo & ~3ll, b = (hi + 3) & ~3ll;
-        prefetch_l2_bulk(p.pf_col + a, (uint32_t)(b - a) * 4u);
-      }
-    };
-    const int64_t pf_span = 2 * (int64_t)ahead * kScanChunk;
-    if (ahead > 0 && cur.lo < n) prefetch_scan(cur.lo, min(cur.hi, cur.lo + pf_span));
     int32_t xnext[8];
     if (cur.lo < n) scan_load(cur.lo, cur.hi, xnext);
     while (cur.lo < n) {
       int64_t a = 0;
       if (t == 0) a = claim_chunk(p, 1);
       if (t == 0) s_cnt[0] += cur.hi - cur.lo;   // rows scanned by this CTA
-      if (ahead > 0 && nxt.lo < n) prefetch_scan(nxt.lo, min(nxt.hi, nxt.lo + pf_span));
       for (int64_t cb = cur.lo; cb < cur.hi; cb += kScanChunk) {
         const int64_t row_end = cur.hi;
-        if (ahead > 0) prefetch_scan(cb + pf_span, min(row_end, cb + pf_span + kScanChunk));
         const bool last_block = cb + kScanChunk >= cur.hi;
         int32_t x[8];
 #pragma unroll
@@ -388,15 +411,7 @@ __device__ __forceinline__ void producer_loop(const QueryParams& p, const XRing&
         for (int j = 0; j < 2; ++j)
 #pragma unroll
           for (int u = 0; u < 4; ++u)
-            if (bits & (1u << (4 * j + u))) {
-              const int64_t row = cb + 4 * t + 4 * NPT * j + u;
-              queue[pos++] = (int32_t)row;
-              if (ahead > 0)   // the survivor's fact columns: in L2 by the time its batch runs
-                for (int c = 0; c < ncolpf; ++c) {
-                  const int32_t* cp = pf_col_ptr(c);
-                  if (cp) prefetch_l2(cp + row);
-                }
-            }
+            if (bits & (1u << (4 * j + u))) queue[pos++] = (int32_t)(cb + 4 * t + 4 * NPT * j + u);
         nq += total;
         named_bar_sync(1, NPT);   // queue written (and wcnt[16..] read) by all
         const bool last = last_block && nxt.lo >= n;
@@ -442,6 +457,55 @@ __device__ __forceinline__ void producer_loop(const QueryParams& p, const XRing&
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) nj += __shfl_down_sync(0xffffffffu, nj, o);
     if (lane == 0) atomicAdd(reinterpret_cast<unsigned long long*>(&s_cnt[1]), (unsigned long long)nj);
+}
+
+// The fact loader (one warp, BULK kernels without a pre-filter): claims row chunks (guided
+// distribution, chunk_rows) and streams each batch's fact columns into the fact ring with one 1D
+// bulk copy per column; the copies complete on the stage's full barrier (expect_tx).
+template <int K0P, class SH, int NPW>
+__device__ __forceinline__ void loader_loop(const QueryParams& p, const FactRing& fr, int64_t* s_claim, int64_t* s_cnt,
+                                            int lane) {
+  constexpr int kBR = batch_rows(K0P, 32 * NPW);
+  constexpr int NCS = fact_cols(SH::NF);
+  const int64_t n = p.nrows;
+  RowChunk cur = chunk_rows(p, s_claim[0]), nxt = chunk_rows(p, s_claim[1]);
+  uint32_t b = 0;
+  auto publish = [&](int64_t row0, int nrows) {
+    const int f = b % kFactStages;
+    mbar_wait(&fr.empty[f], ((b / kFactStages) & 1) ^ 1, 7);
+    if (lane == 0) {
+      fr.hdr[2 * f] = row0;
+      fr.hdr[2 * f + 1] = nrows;
+      const int n4 = nrows > 0 ? (nrows & ~3) : 0;   // whole 16-byte granules; the producers read the rest
+      uint32_t bytes = 0;
+#pragma unroll
+      for (int c = 0; c < NCS; ++c)
+        if (fact_col_ptr(p, c)) bytes += (uint32_t)n4 * 4u;
+      mbar_arrive_expect_tx(&fr.full[f], bytes);
+      if (n4 > 0) {
+        uint8_t* dst = fr.base + f * fr.stage_bytes;
+#pragma unroll
+        for (int c = 0; c < NCS; ++c) {
+          const int32_t* src = fact_col_ptr(p, c);
+          if (src) bulk_g2s(dst + c * kBR * 4, src + row0, (uint32_t)n4 * 4u, &fr.full[f]);
+        }
+      }
+    }
+    __syncwarp();
+    ++b;
+  };
+  while (cur.lo < n) {
+    int64_t a = 0;
+    if (lane == 0) {
+      a = claim_chunk(p, 1);
+      s_cnt[0] += cur.hi - cur.lo;   // rows scanned by this CTA
+    }
+    a = __shfl_sync(0xffffffffu, a, 0);
+    for (int64_t base = cur.lo; base < cur.hi; base += kBR) publish(base, (int)min((int64_t)kBR, cur.hi - base));
+    cur = nxt;
+    nxt = chunk_rows(p, a);
+  }
+  publish(0, -1);   // end of stream
 }
 
 }  // namespace flern

@@ -24,8 +24,11 @@
 
 namespace flern {
 
-template <int K0P, int H, int NL>
+// NCS > 0: a fact-column ring of kFactStages stages x NCS columns x one batch (FactRing)
+template <int K0P, int H, int NL, int NCS = 0>
 struct SmemPlan {
+  static constexpr uint32_t FSB = (uint32_t)NCS * batch_rows(K0P, 32 * kProdWarps) * 4;   // one fact stage
+  static constexpr uint32_t FR = kFactStages * FSB + (NCS > 0 ? 64 : 0);                  // stages + headers
   static constexpr uint32_t WH = (NL >= 2) ? (uint32_t)H * H * 2 : 0;         // hidden->hidden W, SW128
   static constexpr uint32_t HB = 0;   // the hidden activation lives in TMEM (TmemPlan::HT)
   static constexpr uint32_t W1 = (uint32_t)H * K0P * 2;                       // layer-1 W, interleave
@@ -33,7 +36,8 @@ struct SmemPlan {
   static constexpr uint32_t META = 16 + 4 * kTile + 4 * kTile + kTile;        // count, rowid, val, grp
   static constexpr uint32_t BB = bias_operand_bytes(H);                       // one layer's bias B operand
   static constexpr uint32_t FIXED = WH + HB + W1 + kOnesBytes + NL * BB + H * 4 + kMaxGroups * 4 * 8 +
-                                    queue_bytes(32 * kProdWarps) + kMaxFeat * 8 + 64 * 8 + kMiscBytes;
+                                    queue_bytes(32 * kProdWarps) + kMaxFeat * 8 + 64 * 8 + kMiscBytes +
+                                    2 * kTile * 4 + FR;
   static constexpr int S = (FIXED + 4 * (XS + META) <= 232448) ? 4 : 3;
   static constexpr uint32_t off_wh = 0;                                       // [Wh | W1] = weight image
   static constexpr uint32_t off_w1 = off_wh + WH;
@@ -54,7 +58,9 @@ struct SmemPlan {
   static constexpr uint32_t SEQB = 0;
 #endif
   static constexpr uint32_t off_part = off_misc + kMiscBytes;                 // [2][128] fp32 partial logits
-  static constexpr uint32_t off_seq = off_part + 2 * kTile * 4;
+  static constexpr uint32_t off_fring = off_part + 2 * kTile * 4;             // fact ring (NCS > 0), 128-aligned
+  static constexpr uint32_t off_fhdr = off_fring + kFactStages * FSB;
+  static constexpr uint32_t off_seq = off_fring + FR;
   static constexpr uint32_t total = off_seq + SEQB;
   static constexpr uint32_t wimg_bytes = WH + W1;                              // contiguous [Wh | W1]
   static constexpr uint32_t bimg_bytes = NL * BB;                              // follows it in the image
@@ -63,13 +69,13 @@ struct SmemPlan {
   static_assert(H % 64 == 0 && H >= 64 && H <= 256, "hidden width");
   static_assert(NL == 1 || NL == 2, "hidden layers");
   static_assert(off_ones % 16 == 0 && BB % 16 == 0, "operand alignment");
+  static_assert(off_fring % 16 == 0 && FSB % 16 == 0, "fact ring alignment");
 };
 
 // TMEM columns (NL >= 2). Layer 1 runs as NH1 N-pieces into R1; warpgroup 0 turns each piece
-// into bf16 H (packed two per column: the A operand of layer 2, "ts" MMA) at HT; layer 2 runs as
-// ONE N = H accumulation into D2 (tcgen05 reaches full rate only at N >= 128, and the wide MMA
-// halves the instructions the single issuing thread must keep ahead of the tensor core), drained
-// by both epilogue warpgroups (lower / upper half of the columns). H = 256: 128 + 128 + 256 = 512.
+// into bf16 H (packed two per column: the A operand of layer 2, "ts" MMA) at HT; layer 2 runs as two
+// N = H/2 halves into D2 (D2a, D2b), so warpgroup 1 drains one half while the other computes
+// (tcgen05 runs at full rate from N = 128 up). H = 256: 128 + 128 + 2 x 128 = 512.
 // NL == 1: ping-pong D buffers at 0 and H.
 template <int H, int NL>
 struct TmemPlan {
@@ -82,9 +88,8 @@ struct TmemPlan {
   static_assert(used <= 512, "TMEM plan");
 };
 
-template <int K0P, int H, int NL>
+template <class P>
 __device__ __forceinline__ Meta meta_of(uint8_t* base, int s) {
-  using P = SmemPlan<K0P, H, NL>;
   uint8_t* m = base + P::off_meta + s * P::META;
   return Meta{reinterpret_cast<int32_t*>(m), reinterpret_cast<int32_t*>(m + 16),
               reinterpret_cast<int32_t*>(m + 16 + 4 * kTile), m + 16 + 8 * kTile};
@@ -92,7 +97,9 @@ __device__ __forceinline__ Meta meta_of(uint8_t* base, int s) {
 
 template <int K0P, int H, int NL, class SH>
 __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_constant__ QueryParams p) {
-  using P = SmemPlan<K0P, H, NL>;
+  // producer shape fixed at compile time -> fact columns staged by the loader warp (FactRing)
+  constexpr bool kBulk = SH::NF >= 0;
+  using P = SmemPlan<K0P, H, NL, kBulk ? fact_cols(SH::NF) : 0>;
   constexpr int S = P::S;
   extern __shared__ __align__(1024) uint8_t smem[];
   const int tid = threadIdx.x;
@@ -109,9 +116,11 @@ __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_c
   uint64_t* empty = bars + S;       // [S]   epilogue WG0 -> producers (4 arrivals)
   uint64_t* d1full = bars + 8;      // NL=2: L1 piece commit -> warpgroup 0
   uint64_t* d1empty = bars + 9;     // NL=2: warpgroup 0 (4 warps) read the L1 piece out of R1 -> MMA
-  uint64_t* dfull = bars + 10;      // NL=2: [0] layer 2 done (commit); NL=1: [2] ping-pong D buffers
-  uint64_t* dempty = bars + 12;     // NL=2: [0] both warpgroups drained D2 (8 warps); NL=1: [2] (4 warps)
+  uint64_t* dfull = bars + 10;      // [2] NL=2: layer-2 N-halves D2a/D2b (commit); NL=1: ping-pong D buffers
+  uint64_t* dempty = bars + 12;     // [2] warpgroup 1 (4 warps) drained it -> MMA
   uint64_t* pready = bars + 24;     // NL=2: warpgroup 0's partial logits of the tile are in SMEM (4 warps)
+  uint64_t* ffull = bars + 26;      // [kFactStages] fact ring: loader -> producers
+  uint64_t* fempty = bars + 28;     // [kFactStages] fact ring: producer warps -> loader
   uint64_t* hfull = bars + 14;      // [4] NL=2: warpgroup 0 stored H chunk c in TMEM (4 warps)
   uint64_t* hfree = bars + 18;      // [4] NL=2: L2b finished reading H chunk c (commit)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + P::off_misc);
@@ -151,8 +160,9 @@ __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_c
     for (int s = 0; s < S; ++s) { mbar_init(&full[s], 32 * kProdWarps); mbar_init(&empty[s], 4); }
     mbar_init(d1full, 1);
     mbar_init(d1empty, 4);
-    for (int i = 0; i < 2; ++i) { mbar_init(&dfull[i], 1); mbar_init(&dempty[i], (NL >= 2 && i == 0) ? 8 : 4); }
+    for (int i = 0; i < 2; ++i) { mbar_init(&dfull[i], 1); mbar_init(&dempty[i], 4); }
     mbar_init(pready, 4);
+    for (int f = 0; f < kFactStages; ++f) { mbar_init(&ffull[f], 1); mbar_init(&fempty[f], kProdWarps); }
     for (int c = 0; c < 4; ++c) { mbar_init(&hfull[c], 4); mbar_init(&hfree[c], 1); }
     fence_mbar_init();
   }
@@ -170,13 +180,17 @@ __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_c
   FLERN_CTA_STAMP(TR_CTA_SETUP);
 
 
+  const FactRing fr{smem + P::off_fring, P::FSB, reinterpret_cast<int64_t*>(smem + P::off_fhdr), ffull, fempty};
   if (warp == 0) {
-    // setup only: keeps SMSP 0 free for the MMA issuer
+    // the fact loader (a few instructions per batch: leaves SMSP 0 to the MMA issuer)
+    if constexpr (kBulk) {
+      if (!p.pf_col) loader_loop<K0P, SH, kProdWarps>(p, fr, s_claim, s_cnt, lane);
+    }
   } else if (is_prod_warp(warp)) {
     const int pw = prod_warp_index(warp);
-    producer_loop<K0P, S, SH, kProdWarps>(p, XRing{smem + P::off_x, P::XS, smem + P::off_meta, full, empty}, wcnt,
-                                          s_shift, s_cnt, reinterpret_cast<int32_t*>(smem + P::off_queue), s_claim,
-                                          pw * 32 + lane, pw, lane);
+    producer_loop<K0P, S, SH, kProdWarps, kBulk>(p, XRing{smem + P::off_x, P::XS, smem + P::off_meta, full, empty},
+                                                 wcnt, s_shift, s_cnt, reinterpret_cast<int32_t*>(smem + P::off_queue),
+                                                 s_claim, fr, pw * 32 + lane, pw, lane);
   } else if (warp == 12) {
     // =============================== MMA ISSUER =============================================
     // NL == 2 issue order per tile t (steady state): L2a(t), L1(t+1), L2b(t). Layer 2 is split
@@ -207,11 +221,10 @@ __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_c
         }
       };
       if constexpr (NL >= 2) {
-        // Layer 2 takes A (= H) from TMEM and B (= W2) from SMEM, N = H in one accumulation.
-        // Pipe order per tile t: L2(t) chunks 0..NC/2-1, L1 piece 0 (t+1), L2(t) chunks NC/2..,
-        // L1 piece 1 (t+1), then L2(t+1) once both warpgroups drained D2(t). Warpgroup 0 converts
-        // piece 0 (t+1) into H chunks 0.. while L2(t) finishes (hfree[c] commits release H chunk by
-        // chunk), helps drain D2(t), then converts piece 1 (t+1).
+        // Layer 2 takes A (= H) from TMEM and B (= W2) from SMEM, in two N-halves (D2a, D2b): warpgroup 1
+        // drains one half while the other computes. Pipe order per tile t: L2a(t), L1 piece 0 (t+1),
+        // L2b(t) K-chunks 0..NC/2-1, L1 piece 1 (t+1), L2b(t) K-chunks NC/2.. (hfree[c] commits
+        // release H chunk by chunk to warpgroup 0, which converts tile t+1 meanwhile).
         const uint64_t whdesc = make_sdesc(smem_u32(smem + P::off_wh), 16, 1024, kLayoutSW128);
         constexpr int NC = H / 64;                 // 64-wide K-chunks of H (32 TMEM columns each)
         const uint64_t bb2desc = make_sdesc(smem_u32(smem + P::off_bb + P::BB), 0, 32, kLayoutNone);
@@ -251,46 +264,55 @@ __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_c
           SEQ(SQ_L1);
           ++pc;
         };
+        auto issue_l2_half = [&](int half, uint32_t tile, auto&& mid) {
+          constexpr uint32_t idesc2 = make_idesc_bf16(128, H / 2);
+          WAITQ(half ? SQ_DEMPTY1 : SQ_DEMPTY0, &dempty[half], (tile & 1) ^ 1, 13);   // drained by warpgroup 1
+          tc_fence_after();
+          const uint32_t dcol = tmem_base + TP::D2C + half * (H / 2);
+          // bias first (needs no H chunk): neurons [half*H/2, +H/2) = bias blocks from half*H/16
+          if (elect_one_sync())
+            mma_bf16_ss(dcol, onesdesc, bb2desc + ((uint32_t)(half * (H / 16) * 32) >> 4), idesc2 | kIdescBMajorMN, 0);
+#pragma unroll
+          for (int c = 0; c < NC; ++c) {
+            if (half == 0) { WAITQ(SQ_HFULL, &hfull[c], tile & 1, 12); tc_fence_after(); }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {   // 4 x K=16 inside one 64-wide K-chunk (8 TMEM columns each)
+              const uint64_t bd = whdesc + ((uint32_t)(c * (H * 128) + half * (H / 16) * 1024 + j * 32) >> 4);
+              if (elect_one_sync()) mma_bf16_ts(dcol, tmem_base + TP::HT + c * 32 + j * 8, bd, idesc2, 1);
+            }
+            SEQ(half ? SQ_L2B : SQ_L2A);
+            if (half == 1 && elect_one_sync()) mma_commit(&hfree[c]);   // last reader of H chunk c for this tile
+            if (half == 1 && (c == NC / 2 - 1 || NC == 1)) mid();
+          }
+          if (elect_one_sync()) mma_commit(&dfull[half]);
+        };
+        auto nomid = [] {};
         FLERN_WAIT(W_MMA_FULL, lane == 0, &full[0], 0, 10);
-        if (*meta_of<K0P, H, NL>(smem, 0).count >= 0) {
+        if (*meta_of<P>(smem, 0).count >= 0) {
           tc_fence_after();
           for (int piece = 0; piece < TP::NH1; ++piece) issue_l1_piece(0, piece);
-          constexpr uint32_t idesc2 = make_idesc_bf16(128, H);
-          const uint32_t dcol = tmem_base + TP::D2C;
           for (uint32_t t = 0;; ++t) {
             cur_tile = t;
             SEQ(SQ_TILE);
-            WAITQ(SQ_DEMPTY0, &dempty[0], (t & 1) ^ 1, 13);   // D2(t-1) drained by both warpgroups
             if (lane == 0) FLERN_TRACE(TR_MMA_D2A_FREE, t);
-            tc_fence_after();
-            if (elect_one_sync()) mma_bf16_ss(dcol, onesdesc, bb2desc, idesc2 | kIdescBMajorMN, 0);   // bias
+            issue_l2_half(0, t, nomid);
+            if (lane == 0) FLERN_TRACE(TR_MMA_L2A_DONE, t);
             const int s1 = (t + 1) % S;
             const uint32_t ph1 = ((t + 1) / S) & 1;
             int next = -1;   // tile t+1: -1 not yet known, 0 none (end of stream), 1 published
             int pieces = 0;
-#pragma unroll
-            for (int c = 0; c < NC; ++c) {
-              WAITQ(SQ_HFULL, &hfull[c], t & 1, 12);
-              tc_fence_after();
-#pragma unroll
-              for (int j = 0; j < 4; ++j) {   // 4 x K=16 inside one 64-wide K-chunk (8 TMEM columns each)
-                const uint64_t bd = whdesc + ((uint32_t)(c * (H * 128) + j * 32) >> 4);
-                if (elect_one_sync()) mma_bf16_ts(dcol, tmem_base + TP::HT + c * 32 + j * 8, bd, idesc2, 1);
-              }
-              if (elect_one_sync()) mma_commit(&hfree[c]);   // last reader of H chunk c for this tile
-              SEQ(SQ_L2A);
-              if (c == NC / 2 - 1 || (NC == 1 && c == 0)) {   // L1 piece 0 of tile t+1, if published
-                if (__shfl_sync(0xffffffffu, (int)mbar_test_wait(&full[s1], ph1), 0)) {
-                  next = *meta_of<K0P, H, NL>(smem, s1).count >= 0 ? 1 : 0;
-                  if (next == 1) issue_l1_piece(s1, pieces++);
-                }
-              }
+            if (__shfl_sync(0xffffffffu, (int)mbar_test_wait(&full[s1], ph1), 0)) {
+              next = *meta_of<P>(smem, s1).count >= 0 ? 1 : 0;
+              if (next == 1) issue_l1_piece(s1, pieces++);
             }
-            if (elect_one_sync()) mma_commit(&dfull[0]);
+            auto mid = [&] {
+              if (next == 1 && pieces < TP::NH1) issue_l1_piece(s1, pieces++);
+            };
+            issue_l2_half(1, t, mid);
             if (lane == 0) FLERN_TRACE(TR_MMA_L2B_ISSUED, t);
             if (next < 0) {
               WAITQ(SQ_FULL, &full[s1], ph1, 10);
-              next = *meta_of<K0P, H, NL>(smem, s1).count >= 0 ? 1 : 0;
+              next = *meta_of<P>(smem, s1).count >= 0 ? 1 : 0;
             }
             if (next == 0) break;
             while (pieces < TP::NH1) issue_l1_piece(s1, pieces++);
@@ -301,7 +323,7 @@ __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_c
         for (uint32_t t = 0;; ++t) {
           const int s = t % S;
           mbar_wait(&full[s], (t / S) & 1, 10);
-          if (*meta_of<K0P, H, NL>(smem, s).count < 0) break;
+          if (*meta_of<P>(smem, s).count < 0) break;
           const int b = t & 1;
           mbar_wait(&dempty[b], ((t >> 1) & 1) ^ 1, 11);
           tc_fence_after();
@@ -374,86 +396,64 @@ __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_c
     if constexpr (NL >= 2) {
       constexpr int NC = H / 64;
       constexpr int CPP = NC / TP::NH1;   // 64-wide chunks per L1 piece
-      float* s_part = reinterpret_cast<float*>(smem + P::off_part);   // [2][128] warpgroup-0 partial logits
       if (wg == 0) {
-        // ---- warpgroup 0: L1 pieces -> ReLU -> bf16 -> H in TMEM; upper half of the D2 drain ----
+        // ---- warpgroup 0: L1 pieces -> ReLU -> bf16 -> H in TMEM (layer-2 A operand), chunk by chunk ----
         uint32_t pcs = 0;   // L1 pieces consumed
-        // one L1 piece of tile tt into H chunks [piece*CPP, +CPP); waits for layer 2 of tile tt-1 to
-        // release each chunk (hfree)
-        auto convert_piece = [&](uint32_t tt, int piece) {
-          FLERN_WAIT(W_WG0_D1FULL, tid == 128, d1full, pcs & 1, 21);
-          ++pcs;
-          tc_fence_after();
-          if (p.dbg_mode & 1) {   // diagnostic: keep the protocol, skip the math
-            release(d1empty)();
+        for (uint32_t t = 0; !p.no_model; ++t) {
+          const int s = t % S;
+          FLERN_WAIT(W_WG0_FULL, tid == 128, &full[s], (t / S) & 1, 20);
+          if (*meta_of<P>(smem, s).count < 0) break;
+          if (tid == 128) FLERN_TRACE(TR_W0_FULL, t);
+#pragma unroll 1
+          for (int piece = 0; piece < TP::NH1; ++piece) {
+            FLERN_WAIT(W_WG0_D1FULL, tid == 128, d1full, pcs & 1, 21);
+            ++pcs;
+            if (tid == 128 && piece == 0) FLERN_TRACE(TR_W0_D1FULL, t);
+            tc_fence_after();
+            if (p.dbg_mode & 1) {   // diagnostic: keep the protocol, skip the math
+              release(d1empty)();
+              for (int cc = 0; cc < CPP; ++cc) {
+                const int c = piece * CPP + cc;
+                mbar_wait(&hfree[c], (t & 1) ^ 1, 22);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&hfull[c]);
+              }
+              continue;
+            }
+#pragma unroll
             for (int cc = 0; cc < CPP; ++cc) {
               const int c = piece * CPP + cc;
-              mbar_wait(&hfree[c], (tt & 1) ^ 1, 22);
+              uint32_t pk[32];
+              {
+                uint32_t va[32], vb[32];   // both halves of the chunk in flight, one wait
+                tmem_ld32_async(tmem_base + lane_off + cc * 64, va);
+                tmem_ld32_async(tmem_base + lane_off + cc * 64 + 32, vb);
+                tmem_ld_wait(va);
+                tmem_ld_wait(vb);
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {   // D1 already holds the bias (kOnesBytes)
+                  pk[i] = relu_bf16x2(__uint_as_float(va[2 * i]), __uint_as_float(va[2 * i + 1]));
+                  pk[16 + i] = relu_bf16x2(__uint_as_float(vb[2 * i]), __uint_as_float(vb[2 * i + 1]));
+                }
+              }
+              if (cc == CPP - 1) release(d1empty)();   // the whole piece is in registers: R1 is free
+              FLERN_WAIT(W_WG0_HFREE, tid == 128, &hfree[c], (t & 1) ^ 1, 22);   // L2b(t-1) done with chunk c
+              if (tid == 128 && c == 0) FLERN_TRACE(TR_W0_HFREE0, t);
+              tc_fence_after();
+              tmem_st32(tmem_base + lane_off + TP::HT + c * 32, pk);   // K = 64c .. 64c+63, packed pairs
+              tc_fence_before();
               __syncwarp();
               if (lane == 0) mbar_arrive(&hfull[c]);
             }
-            return;
           }
-#pragma unroll
-          for (int cc = 0; cc < CPP; ++cc) {
-            const int c = piece * CPP + cc;
-            uint32_t pk[32];
-            {
-              uint32_t va[32], vb[32];   // both halves of the chunk in flight, one wait
-              tmem_ld32_async(tmem_base + lane_off + cc * 64, va);
-              tmem_ld32_async(tmem_base + lane_off + cc * 64 + 32, vb);
-              tmem_ld_wait(va);
-              tmem_ld_wait(vb);
-#pragma unroll
-              for (int i = 0; i < 16; ++i) {   // D1 already holds the bias (kOnesBytes)
-                pk[i] = relu_bf16x2(__uint_as_float(va[2 * i]), __uint_as_float(va[2 * i + 1]));
-                pk[16 + i] = relu_bf16x2(__uint_as_float(vb[2 * i]), __uint_as_float(vb[2 * i + 1]));
-              }
-            }
-            if (cc == CPP - 1) release(d1empty)();   // the whole piece is in registers: R1 is free
-            FLERN_WAIT(W_WG0_HFREE, tid == 128, &hfree[c], (tt & 1) ^ 1, 22);   // L2(tt-1) done with chunk c
-            tc_fence_after();
-            tmem_st32(tmem_base + lane_off + TP::HT + c * 32, pk);   // K = 64c .. 64c+63, packed pairs
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&hfull[c]);
-          }
-        };
-        // does tile tt exist (published and not the end marker)?
-        auto has_tile = [&](uint32_t tt) {
-          const int s = tt % S;
-          FLERN_WAIT(W_WG0_FULL, tid == 128, &full[s], (tt / S) & 1, 20);
-          return *meta_of<K0P, H, NL>(smem, s).count >= 0;
-        };
-        if (!p.no_model && has_tile(0)) {
-          for (int piece = 0; piece < TP::NH1; ++piece) convert_piece(0, piece);
-          for (uint32_t t = 0;; ++t) {
-            if (tid == 128) FLERN_TRACE(TR_W0_FULL, t);
-            const bool more = has_tile(t + 1);
-            if (more) convert_piece(t + 1, 0);
-            if (tid == 128) FLERN_TRACE(TR_W0_D1FULL, t);
-            // upper half of D2(t): relu(D2) . w_out partial -> SMEM for warpgroup 1
-            FLERN_WAIT(W_WG0_D1FULL, tid == 128, &dfull[0], t & 1, 21);
-            tc_fence_after();
-            float2 acc4[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
-                              make_float2(0.f, 0.f)};
-            if (!(p.dbg_mode & 1)) dot_cols(TP::D2C + H / 2, H / 2, H / 2, acc4, release(&dempty[0]));
-            else release(&dempty[0])();
-            s_part[(t & 1) * kTile + r] = dot_sum(acc4);
-            __syncwarp();
-            if (lane == 0) mbar_arrive(pready);
-            if (tid == 128) FLERN_TRACE(TR_W0_HFREE0, t);
-            if (!more) break;
-            for (int piece = 1; piece < TP::NH1; ++piece) convert_piece(t + 1, piece);
-            if (tid == 128) FLERN_TRACE(TR_W0_DONE, t);
-          }
+          if (tid == 128) FLERN_TRACE(TR_W0_DONE, t);
         }
       } else {
-        // ---- warpgroup 1: lower half of the D2 drain, logit = both halves + b_out, predicate, group-by ----
+        // ---- warpgroup 1: logit = relu(D2) . w_out + b_out, predicate, group-by ----
         for (uint32_t t = 0;; ++t) {
           const int s = t % S;
           FLERN_WAIT(W_WG1_FULL, tid == 256, &full[s], (t / S) & 1, 23);
-          const Meta m = meta_of<K0P, H, NL>(smem, s);
+          const Meta m = meta_of<P>(smem, s);
           const int count = *m.count;
           if (count < 0) break;
           if (tid == 256) FLERN_TRACE(TR_W1_FULL, t);
@@ -461,16 +461,16 @@ __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_c
           if (!p.no_model) {
             float2 acc4[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
                               make_float2(0.f, 0.f)};
-            FLERN_WAIT(W_WG1_DFULL, tid == 256, &dfull[0], t & 1, 24);
-            if (tid == 256) FLERN_TRACE(TR_W1_DFULL0, t);
-            tc_fence_after();
-            if (!(p.dbg_mode & 1)) dot_cols(TP::D2C, H / 2, 0, acc4, release(&dempty[0]));
-            else release(&dempty[0])();
-            if (tid == 256) FLERN_TRACE(TR_W1_DOTA, t);
-            const float mine = dot_sum(acc4);
-            FLERN_WAIT(W_WG1_DFULL, tid == 256, pready, t & 1, 26);   // warpgroup 0's half
-            logit = (mine + s_part[(t & 1) * kTile + r]) + p.bout;
-            if (tid == 256) FLERN_TRACE(TR_W1_DOTB, t);
+#pragma unroll 1
+            for (int h = 0; h < 2; ++h) {
+              FLERN_WAIT(W_WG1_DFULL, tid == 256, &dfull[h], t & 1, 24);
+              if (tid == 256) FLERN_TRACE(h ? TR_W1_DFULL1 : TR_W1_DFULL0, t);
+              tc_fence_after();
+              if (!(p.dbg_mode & 1)) dot_cols(TP::D2C + h * (H / 2), H / 2, h * (H / 2), acc4, release(&dempty[h]));
+              else release(&dempty[h])();
+              if (tid == 256) FLERN_TRACE(h ? TR_W1_DOTB : TR_W1_DOTA, t);
+            }
+            logit = dot_sum(acc4) + p.bout;
           }
           finish_tile(m, count, s, logit);
           if (tid == 256) FLERN_TRACE(TR_W1_AGG, t);
@@ -482,7 +482,7 @@ __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_c
       for (uint32_t t = wg;; t += 2) {
         const int s = t % S;
         mbar_wait(&full[s], (t / S) & 1, 25);
-        const Meta m = meta_of<K0P, H, NL>(smem, s);
+        const Meta m = meta_of<P>(smem, s);
         const int count = *m.count;
         if (count < 0) break;
         float logit = 0.f;

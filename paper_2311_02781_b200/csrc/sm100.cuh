@@ -284,6 +284,29 @@ __device__ __forceinline__ T ldg_nc(const T* p) {
   return __ldg(p);
 }
 
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+// 1D bulk copy global -> this CTA's shared memory, completing `bytes` on the mbarrier (16-byte
+// aligned addresses, bytes a multiple of 16)
+__device__ __forceinline__ void bulk_g2s(void* dst_smem, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst_smem)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ int32_t lds32(uint32_t addr) {
+  int32_t v;
+  asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
+  return v;
+}
+__device__ __forceinline__ int2 lds64(uint32_t addr) {
+  int2 v;
+  asm volatile("ld.shared.v2.b32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(addr) : "memory");
+  return v;
+}
+
 // Bulk L2 prefetch (cp.async.bulk.prefetch.L2): a hint, no completion tracking. addr and bytes must be
 // 16-byte aligned / a multiple of 16.
 __device__ __forceinline__ void prefetch_l2_bulk(const void* addr, uint32_t bytes) {

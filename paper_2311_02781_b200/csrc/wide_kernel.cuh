@@ -57,17 +57,6 @@ struct WidePlan {
   static_assert(K0P * 2 <= 128 && K0P % 16 == 0, "layer-1 K");
 };
 
-__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-               : "memory");
-}
-// 1D bulk copy global -> this CTA's shared memory, completing `bytes` on the mbarrier
-__device__ __forceinline__ void bulk_g2s(void* dst_smem, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                   smem_u32(dst_smem)),
-               "l"(src), "r"(bytes), "r"(smem_u32(bar))
-               : "memory");
-}
 __device__ __forceinline__ void fence_proxy_async_global() {
   asm volatile("fence.proxy.async.global;" ::: "memory");
 }
@@ -136,8 +125,8 @@ __global__ void __launch_bounds__(kThreadsWide, 1) flern_query_wide_kernel(const
   const uint8_t* img_wh = p.wimg + P::img_w1;
 
   if (warp < 4) {
-    producer_loop<K0P, S, SH, kProdWarpsWide>(p, XRing{smem + P::off_x, P::XS, smem + P::off_meta, xfull, xempty}, wcnt, s_norm, s_cnt,
-                          reinterpret_cast<int32_t*>(smem + P::off_queue), s_claim, tid, warp, lane);
+    producer_loop<K0P, S, SH, kProdWarpsWide, false>(p, XRing{smem + P::off_x, P::XS, smem + P::off_meta, xfull, xempty}, wcnt, s_norm, s_cnt,
+                          reinterpret_cast<int32_t*>(smem + P::off_queue), s_claim, FactRing{}, tid, warp, lane);
   } else if (warp == 13) {
     // =============================== LOADER (bulk copies into the operand ring) ==============
     if (lane == 0) {
