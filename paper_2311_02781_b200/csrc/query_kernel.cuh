@@ -58,7 +58,7 @@ struct SmemPlan {
   static constexpr uint32_t SEQB = 0;
 #endif
   static constexpr uint32_t off_part = off_misc + kMiscBytes;                 // [2][128] fp32 partial logits
-  static constexpr uint32_t off_fring = off_part + 2 * kTile * 4;             // fact ring (NCS > 0), 128-aligned
+  static constexpr uint32_t off_fring = off_part + 2 * kTile * 4;             // fact ring (NCS > 0)
   static constexpr uint32_t off_fhdr = off_fring + kFactStages * FSB;
   static constexpr uint32_t off_seq = off_fring + FR;
   static constexpr uint32_t total = off_seq + SEQB;
@@ -125,6 +125,8 @@ __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_c
   uint64_t* hfree = bars + 18;      // [4] NL=2: L2b finished reading H chunk c (commit)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + P::off_misc);
   int32_t* wcnt = reinterpret_cast<int32_t*>(smem + P::off_misc + 16);     // [3][8] warp counts
+  // hcnt[c] (NL=2): warpgroup-0 warps that stored H chunk c in TMEM (4 per tile, monotonic) -> MMA issuer
+  uint32_t* hcnt = reinterpret_cast<uint32_t*>(smem + P::off_part);
   unsigned long long* acc = reinterpret_cast<unsigned long long*>(smem + P::off_acc);
   float* s_wout = reinterpret_cast<float*>(smem + P::off_wout);
   float* s_shift = reinterpret_cast<float*>(smem + P::off_norm);
@@ -152,6 +154,7 @@ __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_c
     }
     for (int i = tid; i < kMaxGroups * 4; i += kThreads) acc[i] = 0ull;
     if (tid < kCounters) s_cnt[tid] = 0;
+    if (tid < 8) reinterpret_cast<uint32_t*>(smem + P::off_part)[tid] = 0u;   // hcnt
     if (tid == 0) { s_claim[0] = claim0; s_claim[1] = claim0 + 1; }
     fence_proxy_async_smem();   // weights written by st.shared are read by the tensor core
   }
@@ -274,7 +277,15 @@ __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_c
             mma_bf16_ss(dcol, onesdesc, bb2desc + ((uint32_t)(half * (H / 16) * 32) >> 4), idesc2 | kIdescBMajorMN, 0);
 #pragma unroll
           for (int c = 0; c < NC; ++c) {
-            if (half == 0) { WAITQ(SQ_HFULL, &hfull[c], tile & 1, 12); tc_fence_after(); }
+            // H chunks come in pairs (one L1 piece each); a warp stores chunk c before c+1, so the count
+            // of the pair's second chunk covers both: one wait per pair
+            if (half == 0 && (c % 2 == 0 || NC == 1)) {
+              const int cw = (NC == 1) ? 0 : c + 1;
+              SEQ(SQ_HFULL);
+              sm_count_wait(&hcnt[cw], 4u * (tile + 1), 12);
+              SEQ(SQ_HFULL + 1);
+              tc_fence_after();
+            }
 #pragma unroll
             for (int j = 0; j < 4; ++j) {   // 4 x K=16 inside one 64-wide K-chunk (8 TMEM columns each)
               const uint64_t bd = whdesc + ((uint32_t)(c * (H * 128) + half * (H / 16) * 1024 + j * 32) >> 4);
@@ -416,7 +427,7 @@ __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_c
                 const int c = piece * CPP + cc;
                 mbar_wait(&hfree[c], (t & 1) ^ 1, 22);
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&hfull[c]);
+                if (lane == 0) sm_count_add(&hcnt[c], 1u);
               }
               continue;
             }
@@ -443,7 +454,7 @@ __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_c
               tmem_st32(tmem_base + lane_off + TP::HT + c * 32, pk);   // K = 64c .. 64c+63, packed pairs
               tc_fence_before();
               __syncwarp();
-              if (lane == 0) mbar_arrive(&hfull[c]);
+              if (lane == 0) sm_count_add(&hcnt[c], 1u);
             }
           }
           if (tid == 128) FLERN_TRACE(TR_W0_DONE, t);

@@ -94,6 +94,30 @@ __device__ __forceinline__ void mbar_spin(uint64_t* bar, uint32_t parity, int ta
   }
 }
 
+// Shared-memory counters as a lighter hand-off than an mbarrier for the MMA issue warp: arrivals
+// are red.release adds, the waiter polls with ld.acquire (~30 cycles when already satisfied; an
+// mbarrier try_wait costs the issuing warp several times that under load).
+__device__ __forceinline__ void sm_count_add(uint32_t* ctr, uint32_t v) {
+  asm volatile("red.release.cta.shared::cta.add.u32 [%0], %1;" ::"r"(smem_u32(ctr)), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t sm_count_load(const uint32_t* ctr) {
+  uint32_t v;
+  asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];" : "=r"(v) : "r"(smem_u32(ctr)) : "memory");
+  return v;
+}
+// wait until *ctr >= target (unsigned wrap-safe), with the mbarrier watchdog's 4 s limit
+__device__ __forceinline__ void sm_count_wait(const uint32_t* ctr, uint32_t target, int tag) {
+  if ((int32_t)(sm_count_load(ctr) - target) >= 0) return;
+  const uint64_t t0 = globaltimer_ns();
+  uint32_t n = 0;
+  while ((int32_t)(sm_count_load(ctr) - target) < 0) {
+    if ((++n & 65535u) == 0 && globaltimer_ns() - t0 > 4000000000ull) {
+      printf("flern: counter watchdog (tag %d) block %d thread %d\n", tag, (int)blockIdx.x, (int)threadIdx.x);
+      __trap();
+    }
+  }
+}
+
 // Named barrier among `nthreads` threads (id 1..15; 0 is __syncthreads).
 __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
@@ -244,6 +268,20 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32
       "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
       : "memory");
 }
+
+// The same store without the wait (several stores, then one tmem_st_wait()).
+__device__ __forceinline__ void tmem_st32_nowait(uint32_t taddr, const uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]),
+      "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]),
+      "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
 // Packed fp32x2 arithmetic (sm_100: FADD2 / FFMA2 — two lanes of fp32 per instruction).
 __device__ __forceinline__ float2 add2(float2 a, float2 b) {
