@@ -247,7 +247,7 @@ __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_c
 #endif
         auto WAITQ = [&](uint32_t tag, uint64_t* bar, uint32_t par, int code) {
           SEQ(tag);
-          mbar_wait(bar, par, code);
+          mbar_wait_nohint(bar, par, code);
           SEQ(tag + 1);
         };
         auto issue_l1_piece = [&](int s, int piece) {
@@ -298,7 +298,7 @@ __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_c
           if (elect_one_sync()) mma_commit(&dfull[half]);
         };
         auto nomid = [] {};
-        FLERN_WAIT(W_MMA_FULL, lane == 0, &full[0], 0, 10);
+        mbar_wait_nohint(&full[0], 0, 10);
         if (*meta_of<P>(smem, 0).count >= 0) {
           tc_fence_after();
           for (int piece = 0; piece < TP::NH1; ++piece) issue_l1_piece(0, piece);

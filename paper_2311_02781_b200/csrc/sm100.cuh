@@ -78,6 +78,33 @@ __device__ __noinline__ void mbar_wait_slow(uint64_t* bar, uint32_t parity, int 
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity, int tag) {
   if (!mbar_try_wait(bar, parity)) mbar_wait_slow(bar, parity, tag);
 }
+// For the MMA issue warp: a try_wait with a suspend-time hint costs the tensor pipe ~200 cycles even on
+// a completed phase (scripts/tile_mma_bench.cu), so it polls without the hint. Everyone else sleeps
+// (mbar_wait): spinning waiters would take the issue slots the working warps need.
+__device__ __forceinline__ bool mbar_try_wait_nohint(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __noinline__ void mbar_wait_nohint_slow(uint64_t* bar, uint32_t parity, int tag) {
+  uint64_t t0 = globaltimer_ns();
+  uint32_t n = 0;
+  while (!mbar_try_wait_nohint(bar, parity)) {
+    if ((++n & 4095u) == 0 && globaltimer_ns() - t0 > 4000000000ull) {
+      printf("flern: mbarrier watchdog (tag %d) block %d thread %d parity %u\n", tag, (int)blockIdx.x,
+             (int)threadIdx.x, parity);
+      __trap();
+    }
+  }
+}
+__device__ __forceinline__ void mbar_wait_nohint(uint64_t* bar, uint32_t parity, int tag) {
+  if (!mbar_try_wait_nohint(bar, parity)) mbar_wait_nohint_slow(bar, parity, tag);
+}
 
 // Spin on the non-blocking test_wait (for the MMA issue warp: a try_wait there costs the tensor pipe
 // far more than its own latency; same watchdog as mbar_wait).

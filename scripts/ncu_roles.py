@@ -5,18 +5,49 @@ Each SASS instruction inherits the file:line of the CUDA line it follows; inline
 intrinsics) inherit the role of the nearest preceding instruction with a role-defining line."""
 import csv, sys, collections
 
-ROLE_LINES = {   # (file suffix, lo, hi) -> role
-    ("producer.cuh", 1, 9999): "producer",
-    ("query_kernel.cuh", 101, 142): "setup",
-    ("query_kernel.cuh", 143, 251): "mma",
-    ("query_kernel.cuh", 297, 351): "wg0",
-    ("query_kernel.cuh", 352, 406): "wg1",
-    ("query_kernel.cuh", 407, 9999): "teardown",
-    ("query_kernel.cuh", 252, 296): "epi-common",
-    ("common.cuh", 199, 298): "groupby",
-    ("common.cuh", 324, 9999): "teardown",
-    ("wide_kernel.cuh", 1, 9999): "wide",
-}
+def _c(marker):
+    import os
+    src = os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "paper_2311_02781_b200", "csrc", "common.cuh")
+    for i, l in enumerate(open(src).read().split("\n")):
+        if marker in l:
+            return i + 1
+    return 99999
+
+
+def _ranges():
+    """Role line ranges of query_kernel.cuh, found from the section markers in the source."""
+    import os
+    src = os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "paper_2311_02781_b200", "csrc",
+                       "query_kernel.cuh")
+    lines = open(src).read().split("\n")
+    def find(marker, start=0):
+        for i in range(start, len(lines)):
+            if marker in lines[i]:
+                return i + 1
+        return len(lines)
+    setup = find("one-time setup")
+    mma = find("MMA ISSUER")
+    epi = find("EPILOGUE (warps")
+    wg0 = find("---- warpgroup 0:", epi)
+    wg1 = find("---- warpgroup 1:", epi)
+    nl1 = find("---- NL == 1:", epi)
+    tear = find("---- teardown", epi)
+    return {
+        ("producer.cuh", 1, 99999): "producer",
+        ("query_kernel.cuh", setup, mma - 1): "setup/dispatch",
+        ("query_kernel.cuh", mma, epi - 1): "mma",
+        ("query_kernel.cuh", epi, wg0 - 1): "epi-common",
+        ("query_kernel.cuh", wg0, wg1 - 1): "wg0",
+        ("query_kernel.cuh", wg1, nl1 - 1): "wg1",
+        ("query_kernel.cuh", nl1, tear - 1): "nl1-epilogue",
+        ("query_kernel.cuh", tear, 99999): "teardown",
+        ("common.cuh", _c("Predicate + group-by of one"), _c("Guided work distribution") - 1): "groupby",
+        ("common.cuh", _c("write_partials_and_reduce("), 99999): "teardown",
+        ("wide_kernel.cuh", 1, 99999): "wide",
+    }
+
+
+ROLE_LINES = _ranges()
 
 
 def role_of(f, line):
