@@ -867,12 +867,20 @@ extern "C" FLERN_API flern_status flern_run_query(flern_ctx* ctx, const flern_qu
     cfg.stream = ctx->stream;
     cudaLaunchAttribute attr[1];
     const HashTable& h0 = ctx->hts[q->probes[0].ht_id];
-    if (ctx->persist_max > 0 && ctx->window_max > 0 && !getenv("FLERN_NO_L2_WINDOW")) {   // build side persists in L2
+    // persisting L2 window: the build side of the join (narrow kernel), or the wide kernel's per-CTA
+    // activation scratch, which is written and read back once per layer and must not be evicted to HBM
+    void* wbase = h0.slots;
+    size_t wbytes = h0.bytes;
+    if (ke->scratch_per_cta && !getenv("FLERN_WINDOW_HT")) {
+      wbase = ctx->scratch;
+      wbytes = (size_t)grid * ke->scratch_per_cta;
+    }
+    if (ctx->persist_max > 0 && ctx->window_max > 0 && !getenv("FLERN_NO_L2_WINDOW")) {
       attr[0].id = cudaLaunchAttributeAccessPolicyWindow;
-      attr[0].val.accessPolicyWindow.base_ptr = h0.slots;
-      attr[0].val.accessPolicyWindow.num_bytes = std::min(h0.bytes, ctx->window_max);
+      attr[0].val.accessPolicyWindow.base_ptr = wbase;
+      attr[0].val.accessPolicyWindow.num_bytes = std::min(wbytes, ctx->window_max);
       attr[0].val.accessPolicyWindow.hitRatio =
-          (float)std::min(1.0, (double)ctx->persist_max / (double)std::min(h0.bytes, ctx->window_max));
+          (float)std::min(1.0, (double)ctx->persist_max / (double)std::min(wbytes, ctx->window_max));
       attr[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
       attr[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
       cfg.attrs = attr;

@@ -13,9 +13,9 @@
 //     read back as the next layer's A operand by bulk copies; the scratch (2 x 256 KB per CTA) is
 //     small enough to stay in L2.
 //
-// Warp roles (448 threads = 14 warps): producers 0-3 (producer.cuh), epilogue warpgroups 4-7 (even
-// N-chunks) and 8-11 (odd N-chunks; also predicate + group-by), warp 12 = TMEM allocator + MMA
-// issuer, warp 13 = bulk-copy loader.
+// Warp roles (448 threads = 14 warps): bulk-copy loader 0, producers 1-3 and 13 (producer.cuh),
+// epilogue warpgroups 4-7 (even N-chunks) and 8-11 (odd N-chunks; also predicate + group-by), warp 12 =
+// TMEM allocator + MMA issuer (SMSP 0 holds only the loader, two epilogue warps and the issuer).
 #pragma once
 #include "producer.cuh"
 
@@ -70,7 +70,7 @@ __global__ void __launch_bounds__(kThreadsWide, 1) flern_query_wide_kernel(const
   constexpr int S = P::S, RS = P::RS, NCH = P::NCH, KB = P::KB;
   extern __shared__ __align__(1024) uint8_t smem[];
   const int tid = threadIdx.x;
-  const int warp = tid >> 5, lane = tid & 31;
+  const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0), lane = tid & 31;   // warp-uniform (see query_kernel)
   FLERN_CTA_STAMP(TR_CTA_START);
   // first two row chunks (guided distribution, see chunk_rows); the atomic's latency hides under the setup
   int64_t claim0 = 0;
@@ -83,7 +83,7 @@ __global__ void __launch_bounds__(kThreadsWide, 1) flern_query_wide_kernel(const
   uint64_t* rempty = bars + 12;       // [RS] MMA commit
   uint64_t* dfull = bars + 16;        // [2] MMA commit -> epilogue
   uint64_t* dempty = bars + 18;       // [2] epilogue (4 warps) -> MMA
-  uint64_t* actrdy = bars + 20;       // [2] a hidden layer's activations are in the scratch (NCH*4)
+  uint64_t* actrdy = bars + 20;       // [2][NCH] N-chunk n of a hidden layer's activations is in scratch buffer b (4)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + P::off_misc);
   int32_t* wcnt = reinterpret_cast<int32_t*>(smem + P::off_misc + 16);
   int64_t* s_cnt = reinterpret_cast<int64_t*>(smem + P::off_misc + 112);
@@ -111,23 +111,27 @@ __global__ void __launch_bounds__(kThreadsWide, 1) flern_query_wide_kernel(const
   if (tid == 0) {
     for (int s = 0; s < S; ++s) { mbar_init(&xfull[s], 32 * kProdWarpsWide); mbar_init(&xempty[s], 4); }
     for (int s = 0; s < RS; ++s) { mbar_init(&rfull[s], 1); mbar_init(&rempty[s], 1); }
-    for (int i = 0; i < 2; ++i) { mbar_init(&dfull[i], 1); mbar_init(&dempty[i], 4); mbar_init(&actrdy[i], NCH * 4); }
+    for (int i = 0; i < 2; ++i) { mbar_init(&dfull[i], 1); mbar_init(&dempty[i], 4); }
+    for (int i = 0; i < 2 * NCH; ++i) mbar_init(&actrdy[i], 4);
     fence_mbar_init();
   }
   if (warp == 12) { tmem_alloc(tmem_slot, 512); tmem_relinquish(); }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem_base = *tmem_slot;
+  if (*tmem_slot != 0u) __trap();   // one CTA per SM: the 512-column allocation starts at column 0
+  constexpr uint32_t tmem_base = 0;
   FLERN_CTA_STAMP(TR_CTA_SETUP);
   uint8_t* scratch = p.scratch + (size_t)blockIdx.x * P::scratch_per_cta;   // act[0] | act[1]
   const uint8_t* img_w1 = p.wimg;
   const uint8_t* img_wh = p.wimg + P::img_w1;
 
-  if (warp < 4) {
-    producer_loop<K0P, S, SH, kProdWarpsWide, false>(p, XRing{smem + P::off_x, P::XS, smem + P::off_meta, xfull, xempty}, wcnt, s_norm, s_cnt,
-                          reinterpret_cast<int32_t*>(smem + P::off_queue), s_claim, FactRing{}, tid, warp, lane);
-  } else if (warp == 13) {
+  if (warp == 1 || warp == 2 || warp == 3 || warp == 13) {   // producers, off the MMA issuer's SMSP 0
+    const int pw = warp == 13 ? 3 : warp - 1;
+    producer_loop<K0P, S, SH, kProdWarpsWide, false>(p, XRing{smem + P::off_x, P::XS, smem + P::off_meta, xfull, xempty},
+                                                     wcnt, s_norm, s_cnt, reinterpret_cast<int32_t*>(smem + P::off_queue),
+                                                     s_claim, FactRing{}, pw * 32 + lane, pw, lane);
+  } else if (warp == 0) {
     // =============================== LOADER (bulk copies into the operand ring) ==============
     if (lane == 0) {
       uint32_t slot = 0;
@@ -143,7 +147,6 @@ __global__ void __launch_bounds__(kThreadsWide, 1) flern_query_wide_kernel(const
         mbar_wait(&xfull[s], (t / S) & 1, 41);
         if (*meta_at(smem + P::off_meta, s).count < 0) break;
         for (int l = 1; l <= NL; ++l) {
-          if (l >= 2) mbar_wait(&actrdy[(l - 2) & 1], t & 1, 42);   // layer l-1 is in the scratch
           const uint8_t* act = scratch + (size_t)((l - 2) & 1) * KB * kABlock;
           for (int n = 0; n < NCH; ++n) {
             if (l == 1) {
@@ -152,6 +155,10 @@ __global__ void __launch_bounds__(kThreadsWide, 1) flern_query_wide_kernel(const
             } else {
               const uint8_t* wl = img_wh + (size_t)(l - 2) * NCH * KB * kBBlock + (size_t)n * KB * kBBlock;
               for (int kb = 0; kb < KB; ++kb) {
+                // K-block kb of layer l's input is N-chunk kb / 4 of layer l-1: wait for that chunk only
+                // (per-chunk hand-off: layer l starts while layer l-1's last chunks are still drained)
+                if (n == 0 && kb % (kNChunk / 64) == 0)
+                  mbar_wait(&actrdy[((l - 2) & 1) * NCH + kb / (kNChunk / 64)], t & 1, 42);
                 const uint32_t st = acquire(kABlock + kBBlock);
                 uint8_t* dst = smem + P::off_ring + st * P::RING;
                 bulk_g2s(dst, act + (size_t)kb * kABlock, kABlock, &rfull[st]);
@@ -165,51 +172,52 @@ __global__ void __launch_bounds__(kThreadsWide, 1) flern_query_wide_kernel(const
     __syncwarp();
   } else if (warp == 12) {
     // =============================== MMA ISSUER =============================================
-    if (lane == 0) {
+    // warp-uniform loop, elect.sync per tcgen05 instruction, waits without a suspend hint
+    {
       constexpr uint32_t idesc = make_idesc_bf16(128, kNChunk);
       const uint32_t x0 = smem_u32(smem + P::off_x);
       const uint32_t ring = smem_u32(smem + P::off_ring);
       uint32_t slot = 0, c = 0;
       for (uint32_t t = 0;; ++t) {
         const int s = t % S;
-        mbar_wait(&xfull[s], (t / S) & 1, 43);
+        mbar_wait_nohint(&xfull[s], (t / S) & 1, 43);
         if (*meta_at(smem + P::off_meta, s).count < 0) break;
         for (int l = 1; l <= NL; ++l) {
           for (int n = 0; n < NCH; ++n, ++c) {
             const uint32_t b = c & 1;
-            mbar_wait(&dempty[b], ((c >> 1) & 1) ^ 1, 44);
+            mbar_wait_nohint(&dempty[b], ((c >> 1) & 1) ^ 1, 44);
             tc_fence_after();
             const uint32_t dcol = tmem_base + b * kNChunk;
             if (l == 1) {
               const uint32_t st = slot % RS;
-              mbar_wait(&rfull[st], (slot / RS) & 1, 45);
+              mbar_wait_nohint(&rfull[st], (slot / RS) & 1, 45);
               tc_fence_after();
               const uint32_t bb = ring + st * P::RING + kABlock;
 #pragma unroll
               for (int ks = 0; ks < K0P / 16; ++ks) {
                 const uint64_t ad = make_sdesc(x0 + s * P::XS + ks * 2 * (kTile * 16), kTile * 16, 128, kLayoutNone);
                 const uint64_t bd = make_sdesc(bb + ks * 2 * (kNChunk * 16), kNChunk * 16, 128, kLayoutNone);
-                mma_bf16_ss(dcol, ad, bd, idesc, ks > 0);
+                if (elect_one_sync()) mma_bf16_ss(dcol, ad, bd, idesc, ks > 0);
               }
-              mma_commit(&rempty[st]);
+              if (elect_one_sync()) mma_commit(&rempty[st]);
               ++slot;
             } else {
               for (int kb = 0; kb < KB; ++kb) {
                 const uint32_t st = slot % RS;
-                mbar_wait(&rfull[st], (slot / RS) & 1, 46);
+                mbar_wait_nohint(&rfull[st], (slot / RS) & 1, 46);
                 tc_fence_after();
                 const uint32_t ab = ring + st * P::RING, bb = ab + kABlock;
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
                   const uint64_t ad = make_sdesc(ab + j * 32, 16, 1024, kLayoutSW128);
                   const uint64_t bd = make_sdesc(bb + j * 32, 16, 1024, kLayoutSW128);
-                  mma_bf16_ss(dcol, ad, bd, idesc, (kb | j) != 0);
+                  if (elect_one_sync()) mma_bf16_ss(dcol, ad, bd, idesc, (kb | j) != 0);
                 }
-                mma_commit(&rempty[st]);
+                if (elect_one_sync()) mma_commit(&rempty[st]);
                 ++slot;
               }
             }
-            mma_commit(&dfull[b]);
+            if (elect_one_sync()) mma_commit(&dfull[b]);
           }
         }
       }
@@ -291,7 +299,7 @@ __global__ void __launch_bounds__(kThreadsWide, 1) flern_query_wide_kernel(const
           if (l < NL) {   // this chunk of layer l's activations is in the scratch
             fence_proxy_async_global();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&actrdy[(l - 1) & 1]);
+            if (lane == 0) mbar_arrive(&actrdy[((l - 1) & 1) * NCH + n]);
           }
         }
       }
