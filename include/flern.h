@@ -89,6 +89,14 @@ enum {
  * Errors: FLERN_E_DUPLICATE (name in use), FLERN_E_INVALID_ARG, FLERN_E_OOM, FLERN_E_CUDA. */
 FLERN_API flern_status flern_load_table(flern_ctx* ctx, const char* name, int64_t nrows, int32_t ncols,
                                         const flern_column* cols, uint32_t flags, int32_t* table_id);
+/* Refill a table loaded with FLERN_COPY_HOST / FLERN_COPY_DEVICE in place: the next batch of the
+ * same columns (the step's new input), `nrows` <= the rows it was loaded with, copied into the
+ * context-owned columns it already has (no allocation). `cols` names every column of the table
+ * (any order) with the same dtypes. flags: FLERN_COPY_HOST or FLERN_COPY_DEVICE. Synchronous.
+ * Errors: FLERN_E_NOT_FOUND (no such table / column), FLERN_E_INVALID_ARG (borrowed table, more rows
+ * than its capacity, missing column), FLERN_E_TYPE (dtype differs), FLERN_E_CUDA. */
+FLERN_API flern_status flern_update_table(flern_ctx* ctx, int32_t table_id, int64_t nrows, int32_t ncols,
+                                          const flern_column* cols, uint32_t flags);
 /* Drop a table (frees copied columns; borrowed ones stay the caller's). Hash tables built on it
  * stay valid (they hold their own key slots and payload). */
 FLERN_API flern_status flern_drop_table(flern_ctx* ctx, int32_t table_id);

@@ -31,6 +31,7 @@ struct Column {
 struct Table {
   std::string name;
   int64_t nrows = 0;
+  int64_t capacity = 0;   // rows the owned columns can hold (flern_update_table)
   std::vector<Column> cols;
   bool alive = false;
   const Column* find(const char* n) const {
@@ -308,6 +309,7 @@ extern "C" FLERN_API flern_status flern_load_table(flern_ctx* ctx, const char* n
   Table t;
   t.name = name;
   t.nrows = nrows;
+  t.capacity = nrows;
   t.alive = true;
   const size_t bytes = (size_t)nrows * 4;
   for (int32_t i = 0; i < ncols; ++i) {
@@ -342,6 +344,53 @@ extern "C" FLERN_API flern_status flern_load_table(flern_ctx* ctx, const char* n
   }
   ctx->tables.push_back(std::move(t));
   *table_id = (int32_t)ctx->tables.size() - 1;
+  return FLERN_OK;
+}
+
+extern "C" FLERN_API flern_status flern_update_table(flern_ctx* ctx, int32_t table_id, int64_t nrows, int32_t ncols,
+                                                     const flern_column* cols, uint32_t flags) {
+  if (!ctx) return FLERN_E_INVALID_ARG;
+  if (table_id < 0 || table_id >= (int32_t)ctx->tables.size() || !ctx->tables[table_id].alive)
+    return fail(ctx, FLERN_E_NOT_FOUND, "no table with id %d", table_id);
+  Table& t = ctx->tables[table_id];
+  const uint32_t mode = flags & (FLERN_COPY_HOST | FLERN_COPY_DEVICE | FLERN_BORROW_DEVICE);
+  if (mode != FLERN_COPY_HOST && mode != FLERN_COPY_DEVICE)
+    return fail(ctx, FLERN_E_INVALID_ARG, "flern_update_table '%s': COPY_HOST or COPY_DEVICE", t.name.c_str());
+  if (nrows < 0 || !cols || ncols != (int32_t)t.cols.size())
+    return fail(ctx, FLERN_E_INVALID_ARG, "flern_update_table '%s': %d columns given, the table has %zu",
+                t.name.c_str(), ncols, t.cols.size());
+  if (nrows > t.capacity)
+    return fail(ctx, FLERN_E_INVALID_ARG, "flern_update_table '%s': %lld rows exceed its %lld-row capacity",
+                t.name.c_str(), (long long)nrows, (long long)t.capacity);
+  std::vector<int> slot(ncols, -1);
+  for (int32_t i = 0; i < ncols; ++i) {
+    if (!cols[i].name)
+      return fail(ctx, FLERN_E_INVALID_ARG, "flern_update_table '%s': column %d has no name", t.name.c_str(), i);
+    for (size_t j = 0; j < t.cols.size(); ++j)
+      if (t.cols[j].name == cols[i].name) slot[i] = (int)j;
+    if (slot[i] < 0)
+      return fail(ctx, FLERN_E_NOT_FOUND, "flern_update_table: table '%s' has no column '%s'", t.name.c_str(), cols[i].name);
+    const Column& c = t.cols[slot[i]];
+    if (!c.owned && t.capacity > 0)
+      return fail(ctx, FLERN_E_INVALID_ARG, "flern_update_table '%s': column '%s' is borrowed", t.name.c_str(), cols[i].name);
+    if (c.dtype != cols[i].dtype)
+      return fail(ctx, FLERN_E_TYPE, "flern_update_table '%s': column '%s' changes dtype", t.name.c_str(), cols[i].name);
+    if (nrows > 0 && !cols[i].data)
+      return fail(ctx, FLERN_E_INVALID_ARG, "flern_update_table '%s': column '%s' has no data", t.name.c_str(), cols[i].name);
+    if (reinterpret_cast<uintptr_t>(cols[i].data) % 4 != 0)
+      return fail(ctx, FLERN_E_INVALID_ARG, "flern_update_table '%s': column '%s' is not 4-byte aligned", t.name.c_str(),
+                  cols[i].name);
+    for (int32_t j = 0; j < i; ++j)
+      if (slot[j] == slot[i])
+        return fail(ctx, FLERN_E_DUPLICATE, "flern_update_table '%s': column '%s' appears twice", t.name.c_str(), cols[i].name);
+  }
+  CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+  const size_t bytes = (size_t)nrows * 4;
+  for (int32_t i = 0; i < ncols && bytes > 0; ++i)
+    CUDA_TRY(ctx, cudaMemcpyAsync(t.cols[slot[i]].dptr, cols[i].data, bytes,
+                                  mode == FLERN_COPY_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, ctx->stream));
+  CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));  // host buffers may be reused on return
+  t.nrows = nrows;
   return FLERN_OK;
 }
 

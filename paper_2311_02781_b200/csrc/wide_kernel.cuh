@@ -134,6 +134,9 @@ __global__ void __launch_bounds__(kThreadsWide, 1) flern_query_wide_kernel(const
   } else if (warp == 0) {
     // =============================== LOADER (bulk copies into the operand ring) ==============
     if (lane == 0) {
+      // weights (re-read by every tile) and the activation scratch (re-read by the next layer) stay in
+      // L2 ahead of the streamed fact columns
+      const uint64_t keep = l2_policy_evict_last();
       uint32_t slot = 0;
       auto acquire = [&](uint32_t bytes) -> uint32_t {
         const uint32_t st = slot % RS;
@@ -151,7 +154,7 @@ __global__ void __launch_bounds__(kThreadsWide, 1) flern_query_wide_kernel(const
           for (int n = 0; n < NCH; ++n) {
             if (l == 1) {
               const uint32_t st = acquire(P::W1C);
-              bulk_g2s(smem + P::off_ring + st * P::RING + kABlock, img_w1 + (size_t)n * P::W1C, P::W1C, &rfull[st]);
+              bulk_g2s_hint(smem + P::off_ring + st * P::RING + kABlock, img_w1 + (size_t)n * P::W1C, P::W1C, &rfull[st], keep);
             } else {
               const uint8_t* wl = img_wh + (size_t)(l - 2) * NCH * KB * kBBlock + (size_t)n * KB * kBBlock;
               for (int kb = 0; kb < KB; ++kb) {
@@ -161,8 +164,8 @@ __global__ void __launch_bounds__(kThreadsWide, 1) flern_query_wide_kernel(const
                   mbar_wait(&actrdy[((l - 2) & 1) * NCH + kb / (kNChunk / 64)], t & 1, 42);
                 const uint32_t st = acquire(kABlock + kBBlock);
                 uint8_t* dst = smem + P::off_ring + st * P::RING;
-                bulk_g2s(dst, act + (size_t)kb * kABlock, kABlock, &rfull[st]);
-                bulk_g2s(dst + kABlock, wl + (size_t)kb * kBBlock, kBBlock, &rfull[st]);
+                bulk_g2s_hint(dst, act + (size_t)kb * kABlock, kABlock, &rfull[st], keep);
+                bulk_g2s_hint(dst + kABlock, wl + (size_t)kb * kBBlock, kBBlock, &rfull[st], keep);
               }
             }
           }
@@ -233,6 +236,7 @@ __global__ void __launch_bounds__(kThreadsWide, 1) flern_query_wide_kernel(const
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
     GroupAgg agg;
     agg.init();
+    const uint64_t keep = l2_policy_evict_last();   // activation scratch: keep in L2 for the next layer
     for (uint32_t t = 0;; ++t) {
       const int s = t % S;
       mbar_wait(&xfull[s], (t / S) & 1, 47);
@@ -274,8 +278,8 @@ __global__ void __launch_bounds__(kThreadsWide, 1) flern_query_wide_kernel(const
               uint8_t* rowp = act + (size_t)kb * kABlock + (r >> 3) * 1024 + (r & 7) * 128;
 #pragma unroll
               for (int jj = 0; jj < 4; ++jj)
-                st_global_v4(rowp + (((jj0 + jj) ^ (r & 7)) << 4), pk[4 * jj], pk[4 * jj + 1], pk[4 * jj + 2],
-                             pk[4 * jj + 3]);
+                st_global_v4_hint(rowp + (((jj0 + jj) ^ (r & 7)) << 4), pk[4 * jj], pk[4 * jj + 1], pk[4 * jj + 2],
+                                  pk[4 * jj + 3], keep);
             } else {
               const float4* w4 = reinterpret_cast<const float4*>(s_wout + n * kNChunk + cc * 32);
 #pragma unroll

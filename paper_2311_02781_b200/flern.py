@@ -29,7 +29,7 @@ FLERN_I32, FLERN_F32, FLERN_DATE32, FLERN_DEC32, FLERN_DICT32 = 1, 2, 3, 4, 5
 FLERN_COPY_HOST, FLERN_COPY_DEVICE, FLERN_BORROW_DEVICE = 0x1, 0x2, 0x4
 FLERN_Q_RESULT_DEVICE, FLERN_Q_ASYNC, FLERN_Q_BOTH_CLASSES, FLERN_Q_NO_MODEL = 0x1, 0x2, 0x4, 0x8
 EXPORTED = ["flern_create", "flern_destroy", "flern_last_error", "flern_version", "flern_load_table",
-            "flern_drop_table", "flern_load_model", "flern_build_hashtable", "flern_run_query",
+            "flern_update_table", "flern_drop_table", "flern_load_model", "flern_build_hashtable", "flern_run_query",
             "flern_query_launches"]
 
 
@@ -69,6 +69,8 @@ _lib.flern_version.restype = ctypes.c_char_p
 _lib.flern_load_table.argtypes = [c_p, ctypes.c_char_p, c_i64, c_i32, ctypes.POINTER(FlernColumn), c_u32,
                                   ctypes.POINTER(c_i32)]
 _lib.flern_load_table.restype = c_i32
+_lib.flern_update_table.argtypes = [c_p, c_i32, c_i64, c_i32, ctypes.POINTER(FlernColumn), c_u32]
+_lib.flern_update_table.restype = c_i32
 _lib.flern_drop_table.argtypes = [c_p, c_i32]
 _lib.flern_drop_table.restype = c_i32
 _lib.flern_load_model.argtypes = [c_p, ctypes.c_char_p, c_i32, ctypes.POINTER(c_i32), ctypes.POINTER(c_p),
@@ -135,8 +137,7 @@ def _check(ctx, rc):
         raise FlernError(rc, flern_last_error(ctx))
 
 
-def flern_load_table(ctx, name: str, columns: dict, flags: int = FLERN_COPY_HOST, dtypes: dict | None = None) -> int:
-    """columns: {name: array} (numpy host arrays, or torch tensors on host / device per flags)."""
+def _columns(columns: dict, dtypes: dict | None):
     names = list(columns)
     n = len(columns[names[0]]) if names else 0
     arr = (FlernColumn * len(names))()
@@ -152,8 +153,20 @@ def flern_load_table(ctx, name: str, columns: dict, flags: int = FLERN_COPY_HOST
         b = c.encode()
         keep.append(b)
         arr[i] = FlernColumn(b, dt, 0, _ptr(a))
+    return n, arr, keep
+
+
+def flern_update_table(ctx, table_id: int, columns: dict, flags: int = FLERN_COPY_HOST, dtypes: dict | None = None):
+    """Refill a copied table in place with the next batch of the same columns (no allocation)."""
+    n, arr, keep = _columns(columns, dtypes)
+    _check(ctx, _lib.flern_update_table(ctx, table_id, n, len(arr), arr, flags))
+
+
+def flern_load_table(ctx, name: str, columns: dict, flags: int = FLERN_COPY_HOST, dtypes: dict | None = None) -> int:
+    """columns: {name: array} (numpy host arrays, or torch tensors on host / device per flags)."""
+    n, arr, keep = _columns(columns, dtypes)
     tid = c_i32()
-    _check(ctx, _lib.flern_load_table(ctx, name.encode(), n, len(names), arr, flags, ctypes.byref(tid)))
+    _check(ctx, _lib.flern_load_table(ctx, name.encode(), n, len(arr), arr, flags, ctypes.byref(tid)))
     return tid.value
 
 

@@ -304,3 +304,45 @@ def test_generic_producer_path(name, monkeypatch):
     cfg = D.with_sf(D.CONFIGS[name], sf, match_rate=0.9)
     db = D.make_database(cfg)
     parity.check(cfg, db, D.make_model(cfg, db))
+
+
+def test_update_table_refills_in_place():
+    """flern_update_table: the next batch of a copied fact table, no allocation; the result equals a
+    fresh load of the same rows, fewer rows are fine, more rows / borrowed tables / unknown columns are
+    errors that name the offender."""
+    import torch
+    from paper_2311_02781_b200 import flern as F
+    from paper_2311_02781_b200.session import GpuQuery
+    cfg = D.with_sf(D.CONFIGS["c2"], 0.004, match_rate=0.9)
+    db = D.make_database(cfg)
+    model = D.make_model(cfg, db)
+    G = cfg.ngroups
+    gq = GpuQuery(cfg, db, model)
+    try:
+        base = gq.run(count=np.zeros(G, np.int64), sum=np.zeros(G, np.int64))
+        ref_c, ref_s = np.zeros(G, np.int64), np.zeros(G, np.int64)
+        gq.run(count=ref_c, sum=ref_s)
+        perm = np.random.default_rng(7).permutation(db.fact_n)
+        shuffled = {k: np.ascontiguousarray(v[perm]) for k, v in db.fact.items()}
+        F.flern_update_table(gq.ctx, gq.fact_id, shuffled, F.FLERN_COPY_HOST)   # same rows, new order
+        c, s_ = np.zeros(G, np.int64), np.zeros(G, np.int64)
+        r = gq.run(count=c, sum=s_)
+        assert r.rows_scanned == db.fact_n and r.rows_joined == base.rows_joined
+        assert (c == ref_c).all() and (s_ == ref_s).all()
+        half = {k: np.ascontiguousarray(v[: db.fact_n // 2]) for k, v in db.fact.items()}
+        F.flern_update_table(gq.ctx, gq.fact_id, half, F.FLERN_COPY_HOST)      # fewer rows
+        r = gq.run(count=np.zeros(G, np.int64), sum=np.zeros(G, np.int64))
+        assert r.rows_scanned == db.fact_n // 2
+        bigger = {k: np.concatenate([v, v[:8]]) for k, v in db.fact.items()}
+        with pytest.raises(F.FlernError, match="capacity"):
+            F.flern_update_table(gq.ctx, gq.fact_id, bigger, F.FLERN_COPY_HOST)
+        bad = dict(half)
+        bad["no_such_col"] = bad.pop(next(iter(bad)))
+        with pytest.raises(F.FlernError, match="no_such_col"):
+            F.flern_update_table(gq.ctx, gq.fact_id, bad, F.FLERN_COPY_HOST)
+        dev = {k: torch.from_numpy(v).cuda() for k, v in db.fact.items()}
+        tid = F.flern_load_table(gq.ctx, "borrowed", dev, F.FLERN_BORROW_DEVICE)
+        with pytest.raises(F.FlernError, match="borrowed"):
+            F.flern_update_table(gq.ctx, tid, db.fact, F.FLERN_COPY_HOST)
+    finally:
+        gq.close()
