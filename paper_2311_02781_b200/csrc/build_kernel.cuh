@@ -64,4 +64,27 @@ __global__ void pack_payload_kernel(const __grid_constant__ PayloadCols cols, in
   }
 }
 
+// Fat direct-addressed table (key range <= capacity, so every key owns its entry): entry h =
+// {key, build row, payload words...}, fs words (8 = one 32-byte sector, or 16). A probe reads the
+// entry's first 16 bytes (key check) and the payload words from the same sector(s): one dependent
+// global access per probe instead of slot -> payload row.
+__global__ void fill_fat_kernel(int32_t* e, int64_t cap, int32_t fs) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < cap; i += (int64_t)gridDim.x * blockDim.x) {
+    e[i * fs] = kEmptyKey;
+    e[i * fs + 1] = -1;
+  }
+}
+__global__ void build_fat_kernel(const int32_t* __restrict__ keys, int64_t nrows, int32_t* __restrict__ e, HashFn hf,
+                                 int32_t fs, const __grid_constant__ PayloadCols cols, int32_t npay,
+                                 int32_t* __restrict__ flags) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nrows; i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t key = keys[i];
+    if (key == kEmptyKey) { atomicExch(&flags[1], 1); continue; }
+    int32_t* ent = e + (int64_t)hash_slot(key, hf) * fs;
+    if (atomicCAS(ent, kEmptyKey, key) != kEmptyKey) { atomicExch(&flags[0], 1); continue; }   // duplicate key
+    ent[1] = (int32_t)i;
+    for (int32_t w = 0; w < npay; ++w) ent[2 + w] = cols.col[w][i];
+  }
+}
+
 }  // namespace flern

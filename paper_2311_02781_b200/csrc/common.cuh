@@ -66,7 +66,9 @@ __host__ __device__ __forceinline__ uint32_t hash_slot(int32_t key, const HashFn
 }
 
 struct ProbeDesc {
-  const int2* slots;        // {key, build row}, capacity = mask + 1
+  const int2* slots;        // {key, build row}, capacity = mask + 1; fat tables: entries of fstride words
+  int32_t fstride;          // 0: slots + separate payload; 8 / 16: direct-addressed fat entries
+                            // {key, build row, payload words...} (one sector read per probe, payload included)
   HashFn hf;
   uint32_t mask;
   const int32_t* payload;   // row-major [build rows][pstride]

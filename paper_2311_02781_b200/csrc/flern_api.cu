@@ -62,6 +62,7 @@ struct HashTable {
   int32_t* payload = nullptr;
   size_t bytes = 0;
   int32_t pstride = 0;
+  int32_t fstride = 0;                   // > 0: fat direct-addressed entries (build_fat_kernel)
   std::vector<std::string> pcols;
   std::vector<flern_dtype> ptypes;
   int find(const char* n) const {
@@ -634,6 +635,38 @@ extern "C" FLERN_API flern_status flern_build_hashtable(flern_ctx* ctx, int32_t 
     while (((uint64_t)1 << lg) < range) ++lg;
   h.log2cap = lg;
   const int64_t cap = (int64_t)1 << lg;
+  // Direct addressing with few payload words: fat entries {key, row, payload} of 8 or 16 words, so a
+  // probe is one dependent access that also brings the payload (bounded to 8 GB of entries)
+  const int32_t fs = npayload + 2 <= 8 ? 8 : (npayload + 2 <= 16 ? 16 : 0);
+  if (direct && t.nrows > 0 && fs > 0 && (uint64_t)cap * fs * 4 <= (8ull << 30) && !getenv("FLERN_NO_FAT")) {
+    h.fstride = fs;
+    h.bytes = (size_t)cap * fs * sizeof(int32_t);
+    CUDA_TRY(ctx, cudaMalloc(&h.slots, h.bytes));
+    h.payload = reinterpret_cast<int32_t*>(h.slots);   // word offsets of payload columns are relative to this
+    HashFn hf{};
+    hf.mask = (uint32_t)(cap - 1);
+    hf.shift = 32u - lg;
+    hf.kmin = mm[0];
+    hf.mode = 2u;
+    int32_t* ent = reinterpret_cast<int32_t*>(h.slots);
+    CUDA_TRY(ctx, cudaMemsetAsync(ctx->dflags, 0, 16, ctx->stream));
+    fill_fat_kernel<<<grid_for(cap), 256, 0, ctx->stream>>>(ent, cap, fs);
+    build_fat_kernel<<<grid_for(t.nrows), 256, 0, ctx->stream>>>(static_cast<const int32_t*>(kc->dptr), t.nrows, ent,
+                                                                 hf, fs, pc, npayload, ctx->dflags);
+    CUDA_TRY(ctx, cudaGetLastError());
+    int32_t ff[3] = {0, 0, 0};
+    CUDA_TRY(ctx, cudaMemcpyAsync(ff, ctx->dflags, sizeof(ff), cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    h.hf = hf;
+    if (ff[0] || ff[1]) {
+      cudaFree(h.slots);
+      if (ff[1]) return fail(ctx, FLERN_E_INVALID_ARG, "key column '%s' contains the reserved value INT32_MIN", key_col);
+      return fail(ctx, FLERN_E_DUP_KEY, "key column '%s' of table '%s' is not unique", key_col, t.name.c_str());
+    }
+    ctx->hts.push_back(std::move(h));
+    *ht_id = (int32_t)ctx->hts.size() - 1;
+    return FLERN_OK;
+  }
   // one allocation: slots then payload, so one L2 access-policy window can cover the build side
   h.bytes = cap * sizeof(unsigned long long) + std::max<int64_t>(1, t.nrows) * h.pstride * sizeof(int32_t);
   CUDA_TRY(ctx, cudaMalloc(&h.slots, h.bytes));
@@ -717,6 +750,7 @@ extern "C" FLERN_API flern_status flern_run_query(flern_ctx* ctx, const flern_qu
     d.mask = h.hf.mask;
     d.payload = h.payload;
     d.pstride = h.pstride;
+    d.fstride = h.fstride;
     d.src = pr.src;
     if (pr.src < 0) {
       const Column* c = fact.find(pr.key_col);

@@ -120,10 +120,11 @@ __device__ __forceinline__ void produce_batch(ProdState& st, const QueryParams& 
       //    only a row that meets neither its key nor an empty slot there continues (rare, warp-
       //    uniform slow path); a miss drops the row
       int32_t brow[R][kMaxProbes];
+      const int32_t* pb[R][kMaxProbes];   // payload words of the matched build row (dz when none)
 #pragma unroll
       for (int q = 0; q < kMaxProbes; ++q) {
 #pragma unroll
-        for (int r = 0; r < R; ++r) brow[r][q] = -1;
+        for (int r = 0; r < R; ++r) { brow[r][q] = -1; pb[r][q] = dz; }
         if (q >= p.nprobes) continue;
         const ProbeDesc& pd = p.probe[q];
         int32_t kq[R];
@@ -131,9 +132,21 @@ __device__ __forceinline__ void produce_batch(ProdState& st, const QueryParams& 
         int4 wa[R], wb[R];
 #pragma unroll
         for (int r = 0; r < R; ++r)   // probe 1 is keyed by a payload word of probe 0's build row
-          kq[r] = q == 0 ? key[r]
-                         : ld1(p.probe[0].payload + (int64_t)(valid[r] ? brow[r][0] : 0) * p.probe[0].pstride +
-                                   pd.key_word, valid[r]);
+          kq[r] = q == 0 ? key[r] : ld1(pb[r][0] + pd.key_word, valid[r]);
+        if (pd.fstride) {
+          // fat direct-addressed table: the key's own entry {key, row, payload...}; one 16-byte load
+          // decides the match, the payload words come from the same sector (warp-uniform branch)
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+            const int32_t* e = reinterpret_cast<const int32_t*>(pd.slots) + (int64_t)hash_slot(kq[r], pd.hf) * pd.fstride;
+            const int4 x = ldg_nc(reinterpret_cast<const int4*>(valid[r] && !synth ? e : dz));
+            const bool hit = valid[r] && (x.x == kq[r] || synth);
+            brow[r][q] = hit ? (synth ? 0 : x.y) : -1;
+            pb[r][q] = hit && !synth ? e + 2 : dz;
+            valid[r] = hit;
+          }
+          continue;
+        }
 #pragma unroll
         for (int r = 0; r < R; ++r) {
           h[r] = hash_slot(kq[r], pd.hf);
@@ -178,6 +191,7 @@ __device__ __forceinline__ void produce_batch(ProdState& st, const QueryParams& 
         for (int r = 0; r < R; ++r) {
           brow[r][q] = res[r];
           valid[r] = res[r] >= 0;
+          pb[r][q] = valid[r] && !synth ? pd.payload + (int64_t)res[r] * pd.pstride : dz;
         }
       }
       if (t == 0) FLERN_TRACE(TR_P_PROBED, bidx);
@@ -190,10 +204,8 @@ __device__ __forceinline__ void produce_batch(ProdState& st, const QueryParams& 
       // 3. build-side loads (payload words of the matched rows), all issued before any use
 #pragma unroll
       for (int r = 0; r < R; ++r) {
-        const int64_t b0 = valid[r] ? brow[r][0] : 0;
-        const int64_t b1 = (valid[r] && p.nprobes > 1) ? brow[r][1] : 0;
-        const int32_t* rb0 = p.probe[0].payload + b0 * p.probe[0].pstride;
-        const int32_t* rb1 = p.probe[1].payload + b1 * p.probe[1].pstride;
+        const int32_t* rb0 = pb[r][0];
+        const int32_t* rb1 = pb[r][1];
         if (p.grp.src > 0) gv[r] = ld1((p.grp.src == 1 ? rb0 : rb1) + p.grp.word, valid[r] && !synth);
         if (p.sum.src > 0) sv[r] = ld1((p.sum.src == 1 ? rb0 : rb1) + p.sum.word, valid[r] && !synth);
 #pragma unroll
