@@ -20,8 +20,10 @@ __host__ __device__ constexpr int prod_warp_index(int warp) { return warp < 4 ? 
 __host__ __device__ constexpr bool is_prod_warp(int warp) { return (warp >= 1 && warp <= 3) || warp >= 13; }
 // consecutive fact rows per producer thread per batch (one 16/8/4-byte vector load per column);
 // fewer for wide inputs (register budget: R * K0P/2 packed bf16 pairs stay live)
-__host__ __device__ constexpr int rows_per_thread(int K0P) { return K0P <= 16 ? 2 : 1; }
-__host__ __device__ constexpr int batch_rows(int K0P, int npt) { return npt * rows_per_thread(K0P); }
+// (one hidden layer: the consumer side is light, so each producer thread takes 4 rows -- more
+// probes in flight per warp for the HBM-bound shapes)
+__host__ __device__ constexpr int rows_per_thread(int K0P, int NL) { return K0P <= 16 ? (NL == 1 ? 4 : 2) : 1; }
+__host__ __device__ constexpr int batch_rows(int K0P, int NL, int npt) { return npt * rows_per_thread(K0P, NL); }
 // pre-filter scan chunk: 8 rows per producer thread (two 16-byte loads)
 __host__ __device__ constexpr int scan_rows(int npt) { return 8 * npt; }
 // survivor queue: pending (< one batch) + one scan chunk
@@ -91,7 +93,7 @@ struct QueryParams {
   unsigned long long* work; // chunk-claim counter (guided distribution, see chunk_rows); zero between launches
   int64_t claim_big;        // rows per "big" chunk (multiple of claim_small); chunks [0, claim_nbig) are big
   int64_t claim_nbig;       // 2 x grid, or 0 for small inputs
-  int64_t claim_small;      // rows per later chunk: batch_rows(K0P, npt), or scan_rows(npt) with a pre-filter
+  int64_t claim_small;      // rows per later chunk: batch_rows(K0P, NL, npt), or scan_rows(npt) with a pre-filter
   int32_t nprobes;
   ProbeDesc probe[kMaxProbes];
   const int32_t* pf_col;    // nullptr = no pre-filter

@@ -920,7 +920,7 @@ extern "C" FLERN_API flern_status flern_run_query(flern_ctx* ctx, const flern_qu
   // one persistent CTA per SM; rows are claimed as chunks (guided schedule, chunk_rows in common.cuh):
   // 2*grid contiguous halves of an 85% static share, then small chunks on demand
   const int npt = 32 * (ke->threads == kThreads ? kProdWarps : kProdWarpsWide);   // producer threads
-  const int64_t chunk = p.pf_col ? (int64_t)scan_rows(npt) : (int64_t)batch_rows(m.K0P, npt);
+  const int64_t chunk = p.pf_col ? (int64_t)scan_rows(npt) : (int64_t)batch_rows(m.K0P, m.NL, npt);
   const int grid = (int)std::min<int64_t>(ctx->num_sms, std::max<int64_t>(1, (n + chunk - 1) / chunk));
   p.claim_small = chunk;
   p.claim_big = (int64_t)(0.85 * (double)n / (2.0 * grid)) / chunk * chunk;

@@ -35,7 +35,7 @@ __device__ __forceinline__ void produce_batch(ProdState& st, const QueryParams& 
                                               const float* s_normf, int64_t row0, bool whole, const bool (&in)[R],
                                               int bidx, int64_t row_end, int t, int warp, int lane,
                                               uint32_t sfa = 0, int rel = 0, int nfull = 0, FR&& features_read = nullptr) {
-  constexpr int kBR = batch_rows(K0P, 32 * NPW);
+  constexpr int kBR = 32 * NPW * R;
   constexpr bool kSpec = SH::NF >= 0;   // feature shape known at compile time
   const int nfact = kSpec ? SH::NF : p.nfact;
   const int nfeat = kSpec ? SH::NF + SH::ND0 + SH::ND1 : p.nfeat;
@@ -90,7 +90,13 @@ __device__ __forceinline__ void produce_batch(ProdState& st, const QueryParams& 
       // fact column c of my R rows from the fact stage (BULK)
       auto loadF = [&](int c, int32_t (&v)[R]) {
         const uint32_t a = sfa + (uint32_t)(c * kBR + rel) * 4u;
-        if (R == 2 && rel + R <= nfull) {
+        if (R == 4 && rel + R <= nfull) {
+          const int4 x = lds128(a);
+          v[0] = x.x;
+          v[1 % R] = x.y;
+          v[2 % R] = x.z;
+          v[3 % R] = x.w;
+        } else if (R == 2 && rel + R <= nfull) {
           const int2 x = lds64(a);
           v[0] = x.x;
           v[R - 1] = x.y;
@@ -292,13 +298,13 @@ __device__ __forceinline__ void produce_batch(ProdState& st, const QueryParams& 
 }
 
 // `tid` is the thread's index in the producer group [0, 32*NPW), `warp` its warp in the group.
-template <int K0P, int S, class SH, int NPW, bool BULK>
+template <int K0P, int NL, int S, class SH, int NPW, bool BULK>
 __device__ __forceinline__ void producer_loop(const QueryParams& p, const XRing& ring, int32_t* wcnt,
                                               const float* s_normf, int64_t* s_cnt, int32_t* queue,
                                               int64_t* s_claim, const FactRing& fr, int tid, int warp, int lane) {
   constexpr int NPT = 32 * NPW;
-  constexpr int R = rows_per_thread(K0P);
-  constexpr int kBatch = batch_rows(K0P, NPT);
+  constexpr int R = rows_per_thread(K0P, NL);
+  constexpr int kBatch = batch_rows(K0P, NL, NPT);
   constexpr int kScanChunk = scan_rows(NPT);
   constexpr int kQueueCap = (int)queue_bytes(NPT) / 4;
   const int t = tid;   // 0..127
@@ -474,10 +480,10 @@ __device__ __forceinline__ void producer_loop(const QueryParams& p, const XRing&
 // The fact loader (one warp, BULK kernels without a pre-filter): claims row chunks (guided
 // distribution, chunk_rows) and streams each batch's fact columns into the fact ring with one 1D
 // bulk copy per column; the copies complete on the stage's full barrier (expect_tx).
-template <int K0P, class SH, int NPW>
+template <int K0P, int NL, class SH, int NPW>
 __device__ __forceinline__ void loader_loop(const QueryParams& p, const FactRing& fr, int64_t* s_claim, int64_t* s_cnt,
                                             int lane) {
-  constexpr int kBR = batch_rows(K0P, 32 * NPW);
+  constexpr int kBR = batch_rows(K0P, NL, 32 * NPW);
   constexpr int NCS = fact_cols(SH::NF);
   const int64_t n = p.nrows;
   RowChunk cur = chunk_rows(p, s_claim[0]), nxt = chunk_rows(p, s_claim[1]);

@@ -27,7 +27,7 @@ namespace flern {
 // NCS > 0: a fact-column ring of kFactStages stages x NCS columns x one batch (FactRing)
 template <int K0P, int H, int NL, int NCS = 0>
 struct SmemPlan {
-  static constexpr uint32_t FSB = (uint32_t)NCS * batch_rows(K0P, 32 * kProdWarps) * 4;   // one fact stage
+  static constexpr uint32_t FSB = (uint32_t)NCS * batch_rows(K0P, NL, 32 * kProdWarps) * 4;   // one fact stage
   static constexpr uint32_t FR = kFactStages * FSB + (NCS > 0 ? 64 : 0);                  // stages + headers
   static constexpr uint32_t WH = (NL >= 2) ? (uint32_t)H * H * 2 : 0;         // hidden->hidden W, SW128
   static constexpr uint32_t HB = 0;   // the hidden activation lives in TMEM (TmemPlan::HT)
@@ -187,11 +187,11 @@ __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_c
   if (warp == 0) {
     // the fact loader (a few instructions per batch: leaves SMSP 0 to the MMA issuer)
     if constexpr (kBulk) {
-      if (!p.pf_col) loader_loop<K0P, SH, kProdWarps>(p, fr, s_claim, s_cnt, lane);
+      if (!p.pf_col) loader_loop<K0P, NL, SH, kProdWarps>(p, fr, s_claim, s_cnt, lane);
     }
   } else if (is_prod_warp(warp)) {
     const int pw = prod_warp_index(warp);
-    producer_loop<K0P, S, SH, kProdWarps, kBulk>(p, XRing{smem + P::off_x, P::XS, smem + P::off_meta, full, empty},
+    producer_loop<K0P, NL, S, SH, kProdWarps, kBulk>(p, XRing{smem + P::off_x, P::XS, smem + P::off_meta, full, empty},
                                                  wcnt, s_shift, s_cnt, reinterpret_cast<int32_t*>(smem + P::off_queue),
                                                  s_claim, fr, pw * 32 + lane, pw, lane);
   } else if (warp == 12) {

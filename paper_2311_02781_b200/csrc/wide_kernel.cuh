@@ -128,7 +128,7 @@ __global__ void __launch_bounds__(kThreadsWide, 1) flern_query_wide_kernel(const
 
   if (warp == 1 || warp == 2 || warp == 3 || warp == 13) {   // producers, off the MMA issuer's SMSP 0
     const int pw = warp == 13 ? 3 : warp - 1;
-    producer_loop<K0P, S, SH, kProdWarpsWide, false>(p, XRing{smem + P::off_x, P::XS, smem + P::off_meta, xfull, xempty},
+    producer_loop<K0P, NL, S, SH, kProdWarpsWide, false>(p, XRing{smem + P::off_x, P::XS, smem + P::off_meta, xfull, xempty},
                                                      wcnt, s_norm, s_cnt, reinterpret_cast<int32_t*>(smem + P::off_queue),
                                                      s_claim, FactRing{}, pw * 32 + lane, pw, lane);
   } else if (warp == 0) {
