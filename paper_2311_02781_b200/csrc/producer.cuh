@@ -371,87 +371,128 @@ __device__ __forceinline__ void producer_loop(const QueryParams& p, const XRing&
     }
   } else {
     int nq = 0;        // survivors queued (uniform across the producer group)
-    // scan rows cb + 4t + 4*NPT*j (j = 0, 1; each warp instruction covers 128 contiguous rows); the
-    // next chunk's loads are issued before this chunk is compacted (software pipeline)
-    auto scan_load = [&](int64_t cb, int64_t row_end, int32_t (&x)[8]) {
+    // one scan chunk: my 8 filter values x (rows cb + 4t + 4*NPT*j + u, j = 0, 1) -> ballot
+    // compaction of the survivors into the SMEM queue; full batches of NPT survivors (all of them
+    // after the last chunk) go through the probe / gather body, one row per thread
+    auto scan_chunk = [&](int64_t cb, int64_t row_end, const int32_t (&x)[8], bool last) {
+      uint32_t bits = 0;
 #pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        const int64_t r0 = cb + 4 * t + 4 * NPT * j;
-        if (r0 + 4 <= row_end) {
-          const int4 v = ldg_nc(reinterpret_cast<const int4*>(p.pf_col + r0));
-          x[4 * j] = v.x; x[4 * j + 1] = v.y; x[4 * j + 2] = v.z; x[4 * j + 3] = v.w;
-        } else {
+      for (int j = 0; j < 2; ++j)
 #pragma unroll
-          for (int u = 0; u < 4; ++u) x[4 * j + u] = r0 + u < row_end ? ldg_nc(p.pf_col + r0 + u) : 0;
+        for (int u = 0; u < 4; ++u) {
+          const int64_t rr = cb + 4 * t + 4 * NPT * j + u;
+          if (rr < row_end && p.pf_lo <= x[4 * j + u] && x[4 * j + u] < p.pf_hi) bits |= 1u << (4 * j + u);
         }
+      const int my = __popc(bits);
+      int incl = my;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      if (lane == 31) wcnt[16 + warp] = incl;
+      named_bar_sync(1, NPT);
+      int woff = 0, total = 0;
+#pragma unroll
+      for (int w = 0; w < NPW; ++w) {
+        const int c = wcnt[16 + w];
+        woff += (w < warp) ? c : 0;
+        total += c;
+      }
+      int pos = nq + woff + incl - my;
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (bits & (1u << (4 * j + u))) queue[pos++] = (int32_t)(cb + 4 * t + 4 * NPT * j + u);
+      nq += total;
+      named_bar_sync(1, NPT);   // queue written (and wcnt[16..] read) by all
+      while (nq >= NPT || (last && nq > 0)) {
+        const bool in1[1] = {t < nq};
+        const int64_t row = in1[0] ? (int64_t)queue[t] : 0;
+        if (t == 0) FLERN_TRACE(TR_P_START, bidx);
+        produce_batch<K0P, S, 1, SH, NPW>(st, p, ring, wcnt, s_normf, row, true, in1, bidx, n, t, warp, lane);
+        ++bidx;
+        const int taken = min(nq, NPT);
+        // shift the rest of the queue to the front
+        int32_t keep[kQueueCap / NPT + 1];
+        int nk = 0;
+        for (int i = taken + t; i < nq; i += NPT) keep[nk++] = queue[i];
+        named_bar_sync(1, NPT);
+        nk = 0;
+        for (int i = taken + t; i < nq; i += NPT) queue[i - taken] = keep[nk++];
+        nq -= taken;
+        named_bar_sync(1, NPT);
       }
     };
-    int32_t xnext[8];
-    if (cur.lo < n) scan_load(cur.lo, cur.hi, xnext);
-    while (cur.lo < n) {
-      int64_t a = 0;
-      if (t == 0) a = claim_chunk(p, 1);
-      if (t == 0) s_cnt[0] += cur.hi - cur.lo;   // rows scanned by this CTA
-      for (int64_t cb = cur.lo; cb < cur.hi; cb += kScanChunk) {
-        const int64_t row_end = cur.hi;
-        const bool last_block = cb + kScanChunk >= cur.hi;
-        int32_t x[8];
+    if (BULK) {
+      // the loader streams the filter column chunk by chunk into the fact ring (column slot 0):
+      // the scan reads shared memory, HBM sees one bulk stream
+      for (uint32_t b = 0;; ++b) {
+        const int f = b % kFactStages;
+        mbar_wait(&fr.full[f], (b / kFactStages) & 1, 8);
+        const int64_t cb = fr.hdr[2 * f];
+        const int nrows = (int)fr.hdr[2 * f + 1];
+        int32_t x[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        if (nrows > 0) {
+          const uint32_t sa = smem_u32(fr.base + f * fr.stage_bytes);
+          const int nfull = nrows & ~3;
 #pragma unroll
-        for (int u = 0; u < 8; ++u) x[u] = xnext[u];
-        if (!last_block) scan_load(cb + kScanChunk, cur.hi, xnext);
-        else if (nxt.lo < n) scan_load(nxt.lo, nxt.hi, xnext);
-        uint32_t bits = 0;
+          for (int j = 0; j < 2; ++j) {
+            const int rel = 4 * t + 4 * NPT * j;
+            if (rel + 4 <= nfull) {
+              const int4 v = lds128(sa + 4u * rel);
+              x[4 * j] = v.x; x[4 * j + 1] = v.y; x[4 * j + 2] = v.z; x[4 * j + 3] = v.w;
+            } else {
 #pragma unroll
-        for (int j = 0; j < 2; ++j)
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const int64_t rr = cb + 4 * t + 4 * NPT * j + u;
-            if (rr < row_end && p.pf_lo <= x[4 * j + u] && x[4 * j + u] < p.pf_hi) bits |= 1u << (4 * j + u);
+              for (int u = 0; u < 4; ++u)
+                x[4 * j + u] = rel + u < nfull ? lds32(sa + 4u * (rel + u))
+                                               : (rel + u < nrows ? ldg_nc(p.pf_col + cb + rel + u) : 0);
+            }
           }
-        const int my = __popc(bits);
-        int incl = my;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const int x = __shfl_up_sync(0xffffffffu, incl, o);
-          if (lane >= o) incl += x;
         }
-        if (lane == 31) wcnt[16 + warp] = incl;
-        named_bar_sync(1, NPT);
-        int woff = 0, total = 0;
-#pragma unroll
-        for (int w = 0; w < NPW; ++w) {
-          const int c = wcnt[16 + w];
-          woff += (w < warp) ? c : 0;
-          total += c;
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&fr.empty[f]);   // the stage is read: the loader may refill it
+        if (nrows < 0) {
+          const int32_t none[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+          scan_chunk(0, 0, none, true);   // drain the queue
+          break;
         }
-        int pos = nq + woff + incl - my;
-#pragma unroll
-        for (int j = 0; j < 2; ++j)
-#pragma unroll
-          for (int u = 0; u < 4; ++u)
-            if (bits & (1u << (4 * j + u))) queue[pos++] = (int32_t)(cb + 4 * t + 4 * NPT * j + u);
-        nq += total;
-        named_bar_sync(1, NPT);   // queue written (and wcnt[16..] read) by all
-        const bool last = last_block && nxt.lo >= n;
-        while (nq >= NPT || (last && nq > 0)) {
-          const bool in1[1] = {t < nq};
-          const int64_t row = in1[0] ? (int64_t)queue[t] : 0;
-          if (t == 0) FLERN_TRACE(TR_P_START, bidx);
-          produce_batch<K0P, S, 1, SH, NPW>(st, p, ring, wcnt, s_normf, row, true, in1, bidx, n, t, warp, lane);
-          ++bidx;
-          const int taken = min(nq, NPT);
-          // shift the rest of the queue to the front
-          int32_t keep[kQueueCap / NPT + 1];
-          int nk = 0;
-          for (int i = taken + t; i < nq; i += NPT) keep[nk++] = queue[i];
-          named_bar_sync(1, NPT);
-          nk = 0;
-          for (int i = taken + t; i < nq; i += NPT) queue[i - taken] = keep[nk++];
-          nq -= taken;
-          named_bar_sync(1, NPT);
-        }
+        scan_chunk(cb, cb + nrows, x, false);
       }
-      advance(a);
+    } else {
+      // scan rows cb + 4t + 4*NPT*j (j = 0, 1; each warp instruction covers 128 contiguous rows); the
+      // next chunk's loads are issued before this chunk is compacted (software pipeline)
+      auto scan_load = [&](int64_t cb, int64_t row_end, int32_t (&x)[8]) {
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const int64_t r0 = cb + 4 * t + 4 * NPT * j;
+          if (r0 + 4 <= row_end) {
+            const int4 v = ldg_nc(reinterpret_cast<const int4*>(p.pf_col + r0));
+            x[4 * j] = v.x; x[4 * j + 1] = v.y; x[4 * j + 2] = v.z; x[4 * j + 3] = v.w;
+          } else {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) x[4 * j + u] = r0 + u < row_end ? ldg_nc(p.pf_col + r0 + u) : 0;
+          }
+        }
+      };
+      int32_t xnext[8];
+      if (cur.lo < n) scan_load(cur.lo, cur.hi, xnext);
+      while (cur.lo < n) {
+        int64_t a = 0;
+        if (t == 0) a = claim_chunk(p, 1);
+        if (t == 0) s_cnt[0] += cur.hi - cur.lo;   // rows scanned by this CTA
+        for (int64_t cb = cur.lo; cb < cur.hi; cb += kScanChunk) {
+          const bool last_block = cb + kScanChunk >= cur.hi;
+          int32_t x[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) x[u] = xnext[u];
+          if (!last_block) scan_load(cb + kScanChunk, cur.hi, xnext);
+          else if (nxt.lo < n) scan_load(nxt.lo, nxt.hi, xnext);
+          scan_chunk(cb, cur.hi, x, last_block && nxt.lo >= n);
+        }
+        advance(a);
+      }
     }
   }
   if (st.fill > 0) {   // flush the partial tile
@@ -486,6 +527,9 @@ __device__ __forceinline__ void loader_loop(const QueryParams& p, const FactRing
   constexpr int kBR = batch_rows(K0P, NL, 32 * NPW);
   constexpr int NCS = fact_cols(SH::NF);
   const int64_t n = p.nrows;
+  // with a pre-filter only the filter column is staged, one scan chunk per stage (column slot 0)
+  const bool pf = p.pf_col != nullptr;
+  const int64_t step = pf ? (int64_t)scan_rows(32 * NPW) : (int64_t)kBR;
   RowChunk cur = chunk_rows(p, s_claim[0]), nxt = chunk_rows(p, s_claim[1]);
   uint32_t b = 0;
   auto publish = [&](int64_t row0, int nrows) {
@@ -495,17 +539,22 @@ __device__ __forceinline__ void loader_loop(const QueryParams& p, const FactRing
       fr.hdr[2 * f] = row0;
       fr.hdr[2 * f + 1] = nrows;
       const int n4 = nrows > 0 ? (nrows & ~3) : 0;   // whole 16-byte granules; the producers read the rest
-      uint32_t bytes = 0;
+      uint8_t* dst = fr.base + f * fr.stage_bytes;
+      if (pf) {
+        mbar_arrive_expect_tx(&fr.full[f], (uint32_t)n4 * 4u);
+        if (n4 > 0) bulk_g2s(dst, p.pf_col + row0, (uint32_t)n4 * 4u, &fr.full[f]);
+      } else {
+        uint32_t bytes = 0;
 #pragma unroll
-      for (int c = 0; c < NCS; ++c)
-        if (fact_col_ptr(p, c)) bytes += (uint32_t)n4 * 4u;
-      mbar_arrive_expect_tx(&fr.full[f], bytes);
-      if (n4 > 0) {
-        uint8_t* dst = fr.base + f * fr.stage_bytes;
+        for (int c = 0; c < NCS; ++c)
+          if (fact_col_ptr(p, c)) bytes += (uint32_t)n4 * 4u;
+        mbar_arrive_expect_tx(&fr.full[f], bytes);
+        if (n4 > 0) {
 #pragma unroll
-        for (int c = 0; c < NCS; ++c) {
-          const int32_t* src = fact_col_ptr(p, c);
-          if (src) bulk_g2s(dst + c * kBR * 4, src + row0, (uint32_t)n4 * 4u, &fr.full[f]);
+          for (int c = 0; c < NCS; ++c) {
+            const int32_t* src = fact_col_ptr(p, c);
+            if (src) bulk_g2s(dst + c * kBR * 4, src + row0, (uint32_t)n4 * 4u, &fr.full[f]);
+          }
         }
       }
     }
@@ -519,7 +568,7 @@ __device__ __forceinline__ void loader_loop(const QueryParams& p, const FactRing
       s_cnt[0] += cur.hi - cur.lo;   // rows scanned by this CTA
     }
     a = __shfl_sync(0xffffffffu, a, 0);
-    for (int64_t base = cur.lo; base < cur.hi; base += kBR) publish(base, (int)min((int64_t)kBR, cur.hi - base));
+    for (int64_t base = cur.lo; base < cur.hi; base += step) publish(base, (int)min(step, cur.hi - base));
     cur = nxt;
     nxt = chunk_rows(p, a);
   }

@@ -70,6 +70,7 @@ struct SmemPlan {
   static_assert(NL == 1 || NL == 2, "hidden layers");
   static_assert(off_ones % 16 == 0 && BB % 16 == 0, "operand alignment");
   static_assert(off_fring % 16 == 0 && FSB % 16 == 0, "fact ring alignment");
+  static_assert(NCS == 0 || FSB >= (uint32_t)scan_rows(32 * kProdWarps) * 4, "a fact stage holds one scan chunk");
 };
 
 // TMEM columns (NL >= 2). Layer 1 runs as NH1 N-pieces into R1; warpgroup 0 turns each piece
@@ -187,7 +188,7 @@ __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_c
   if (warp == 0) {
     // the fact loader (a few instructions per batch: leaves SMSP 0 to the MMA issuer)
     if constexpr (kBulk) {
-      if (!p.pf_col) loader_loop<K0P, NL, SH, kProdWarps>(p, fr, s_claim, s_cnt, lane);
+      loader_loop<K0P, NL, SH, kProdWarps>(p, fr, s_claim, s_cnt, lane);
     }
   } else if (is_prod_warp(warp)) {
     const int pw = prod_warp_index(warp);
