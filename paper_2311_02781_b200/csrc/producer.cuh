@@ -88,9 +88,22 @@ __device__ __forceinline__ void produce_batch(ProdState& st, const QueryParams& 
       for (int r = 0; r < R; ++r) any |= valid[r];
       const bool anyld = any && !synth;
       // fact column c of my R rows from the fact stage (BULK)
+      // a full batch (every batch but a table's last) takes the vector path in every thread: a
+      // warp-uniform test, so the tail path's predicated loads are not issued alongside it
+      const bool full_batch = nfull == kBR;
       auto loadF = [&](int c, int32_t (&v)[R]) {
         const uint32_t a = sfa + (uint32_t)(c * kBR + rel) * 4u;
-        if (R == 4 && rel + R <= nfull) {
+        if (R == 4 && full_batch) {
+          const int4 x = lds128(a);
+          v[0] = x.x;
+          v[1 % R] = x.y;
+          v[2 % R] = x.z;
+          v[3 % R] = x.w;
+        } else if (R == 2 && full_batch) {
+          const int2 x = lds64(a);
+          v[0] = x.x;
+          v[R - 1] = x.y;
+        } else if (R == 4 && rel + R <= nfull) {
           const int4 x = lds128(a);
           v[0] = x.x;
           v[1 % R] = x.y;
