@@ -114,7 +114,6 @@ struct QueryParams {
   float thr_logit;          // select logit > thr_logit  (score > t  <=>  logit > ln(t/(1-t)))
   int32_t no_model;         // diagnostic: skip the MLP, select every joined row (scan/probe/gather only)
   int32_t dbg_mode;         // diagnostic (env FLERN_DBG_MODE): bit 0 = epilogues skip their math, bit 1 = producer issues no global loads
-  int32_t sched;            // MMA issue order variant (env FLERN_SCHED; tuning)
   const uint8_t* wimg;      // weight image: [Wh (SW128) | W1 (interleave)] bf16, exact SMEM layout
   const float* bias;        // [NL][H]
   const float* wout;        // [H]

@@ -830,13 +830,12 @@ extern "C" FLERN_API flern_status flern_run_query(flern_ctx* ctx, const flern_qu
     if (!is_int_type(c->dtype)) return fail(ctx, FLERN_E_TYPE, "pre-filter column '%s' must be integer-typed", q->prefilter_col);
     p.pf_col = static_cast<const int32_t*>(c->dptr);
     p.pf_lo = q->pf_lo;
-    p.pf_hi = q->pf_hi;
+    p.pf_hi = getenv("FLERN_DBG_PF_EMPTY") ? q->pf_lo : q->pf_hi;   // diagnostic: scan cost alone
   }
   p.ngroups = q->ngroups;
   p.both_classes = both ? 1 : 0;
   p.no_model = (q->flags & FLERN_Q_NO_MODEL) ? 1 : 0;
   p.dbg_mode = getenv("FLERN_DBG_MODE") ? atoi(getenv("FLERN_DBG_MODE")) : 0;   // diagnostics only
-  p.sched = getenv("FLERN_SCHED") ? atoi(getenv("FLERN_SCHED")) : 1;              // tuning knob
   const double t = (double)q->threshold;
   p.thr_logit = t <= 0.0 ? -INFINITY : (t >= 1.0 ? INFINITY : (float)std::log(t / (1.0 - t)));
   uint8_t* img = m.dbuf;

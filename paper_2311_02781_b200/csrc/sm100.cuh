@@ -106,21 +106,6 @@ __device__ __forceinline__ void mbar_wait_nohint(uint64_t* bar, uint32_t parity,
   if (!mbar_try_wait_nohint(bar, parity)) mbar_wait_nohint_slow(bar, parity, tag);
 }
 
-// Spin on the non-blocking test_wait (for the MMA issue warp: a try_wait there costs the tensor pipe
-// far more than its own latency; same watchdog as mbar_wait).
-__device__ __forceinline__ void mbar_spin(uint64_t* bar, uint32_t parity, int tag) {
-  if (mbar_test_wait(bar, parity)) return;
-  uint64_t t0 = globaltimer_ns();
-  uint32_t n = 0;
-  while (!mbar_test_wait(bar, parity)) {
-    if ((++n & 65535u) == 0 && globaltimer_ns() - t0 > 4000000000ull) {
-      printf("flern: mbarrier watchdog (spin, tag %d) block %d thread %d parity %u\n", tag, (int)blockIdx.x,
-             (int)threadIdx.x, parity);
-      __trap();
-    }
-  }
-}
-
 // Shared-memory counters as a lighter hand-off than an mbarrier for the MMA issue warp: arrivals
 // are red.release adds, the waiter polls with ld.acquire (~30 cycles when already satisfied; an
 // mbarrier try_wait costs the issuing warp several times that under load).
@@ -165,12 +150,6 @@ __device__ __forceinline__ bool elect_one_sync() {
   asm volatile("{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.u32 %0, 1, 0, P;\n\t}" : "=r"(pred));
   return pred != 0;
 }
-
-// Per-warpgroup register re-allocation (all 128 threads of a warpgroup execute it).
-template <uint32_t N>
-__device__ __forceinline__ void setmaxnreg_inc() { asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(N)); }
-template <uint32_t N>
-__device__ __forceinline__ void setmaxnreg_dec() { asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(N)); }
 
 // ------------------------------------------------------------------------------- TMEM
 __device__ __forceinline__ void tmem_alloc(uint32_t* dst_smem, uint32_t ncols) {  // whole warp
@@ -296,20 +275,6 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32
       : "memory");
 }
 
-// The same store without the wait (several stores, then one tmem_st_wait()).
-__device__ __forceinline__ void tmem_st32_nowait(uint32_t taddr, const uint32_t (&r)[32]) {
-  asm volatile(
-      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
-      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
-      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
-      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
-      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]),
-      "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]),
-      "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
-      : "memory");
-}
-__device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
-
 // Packed fp32x2 arithmetic (sm_100: FADD2 / FFMA2 — two lanes of fp32 per instruction).
 __device__ __forceinline__ float2 add2(float2 a, float2 b) {
   float2 d;
@@ -383,11 +348,6 @@ __device__ __forceinline__ uint64_t l2_policy_evict_last() {
   asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
   return pol;
 }
-__device__ __forceinline__ uint64_t l2_policy_evict_first() {
-  uint64_t pol;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-  return pol;
-}
 __device__ __forceinline__ void st_global_v4_hint(void* ptr, uint32_t a, uint32_t b, uint32_t c, uint32_t d, uint64_t pol) {
   asm volatile("st.global.L2::cache_hint.v4.b32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(ptr), "r"(a), "r"(b), "r"(c), "r"(d),
                "l"(pol)
@@ -399,34 +359,6 @@ __device__ __forceinline__ void bulk_g2s_hint(void* dst_smem, const void* src, u
           smem_u32(dst_smem)),
       "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
       : "memory");
-}
-
-// Bulk L2 prefetch (cp.async.bulk.prefetch.L2): a hint, no completion tracking. addr and bytes must be
-// 16-byte aligned / a multiple of 16.
-__device__ __forceinline__ void prefetch_l2_bulk(const void* addr, uint32_t bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(addr), "r"(bytes) : "memory");
-}
-
-__device__ __forceinline__ void prefetch_l2(const void* addr) {
-  asm volatile("prefetch.global.L2 [%0];" ::"l"(addr));
-}
-
-// Predicated read-only global loads: no branch, so a run of them issues back to back (the
-// destination keeps its previous value when the predicate is false).
-__device__ __forceinline__ void ldp(int32_t& x, const int32_t* ptr, bool pred) {
-  asm("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q ld.global.nc.b32 %0, [%1];\n\t}"
-      : "+r"(x)
-      : "l"(ptr), "r"((int)pred));
-}
-__device__ __forceinline__ void ldp2(int32_t& x, int32_t& y, const int32_t* ptr, bool pred) {
-  asm("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %3, 0;\n\t@q ld.global.nc.v2.b32 {%0, %1}, [%2];\n\t}"
-      : "+r"(x), "+r"(y)
-      : "l"(ptr), "r"((int)pred));
-}
-__device__ __forceinline__ void ldp4(int32_t& x, int32_t& y, int32_t& z, int32_t& w, const int32_t* ptr, bool pred) {
-  asm("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %5, 0;\n\t@q ld.global.nc.v4.b32 {%0, %1, %2, %3}, [%4];\n\t}"
-      : "+r"(x), "+r"(y), "+r"(z), "+r"(w)
-      : "l"(ptr), "r"((int)pred));
 }
 
 }  // namespace flern

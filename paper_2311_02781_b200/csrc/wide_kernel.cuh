@@ -60,9 +60,6 @@ struct WidePlan {
 __device__ __forceinline__ void fence_proxy_async_global() {
   asm volatile("fence.proxy.async.global;" ::: "memory");
 }
-__device__ __forceinline__ void st_global_v4(void* ptr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
-  asm volatile("st.global.v4.b32 [%0], {%1,%2,%3,%4};" ::"l"(ptr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
-}
 
 template <int K0P, int H, int NL, class SH>
 __global__ void __launch_bounds__(kThreadsWide, 1) flern_query_wide_kernel(const __grid_constant__ QueryParams p) {
