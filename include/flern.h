@@ -185,6 +185,18 @@ typedef struct {
  * and counted in counters[3]. */
 FLERN_API flern_status flern_run_query(flern_ctx* ctx, const flern_query* q, flern_result* res);
 
+/* Run `q` over `nrows` fact rows streamed from host memory (pinned for full PCIe speed), the
+ * host-resident-fact optimisation of the paper's GPU data movement (§3.2): the rows are
+ * copied into the fact table's own device columns (as flern_update_table) in chunks of `chunk_rows`
+ * (rounded up to a multiple of 4) on a second stream, and each chunk's query launch waits only for
+ * its own copy, so copies and queries overlap. `host_cols` names columns of q->fact_table (a COPY
+ * table with capacity >= nrows); aggregates are summed over the chunks (int64, exact). Host results
+ * only (no FLERN_Q_ASYNC / FLERN_Q_RESULT_DEVICE, no debug exports); synchronous.
+ * Errors: as flern_update_table and flern_run_query. */
+FLERN_API flern_status flern_run_query_streamed(flern_ctx* ctx, const flern_query* q, int64_t nrows, int32_t ncols,
+                                                const flern_column* host_cols, int64_t chunk_rows, flern_result* res);
+
+
 #define FLERN_TRACE_EVENTS 26
 
 /* Number of CUDA kernels flern_run_query launches per call (for launch accounting): 1. */

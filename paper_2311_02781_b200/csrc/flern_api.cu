@@ -96,6 +96,13 @@ struct flern_ctx {
   uint8_t* scratch = nullptr;     // wide kernel activation scratch (grown on demand)
   size_t scratch_bytes = 0;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  // flern_run_query_streamed: row window of the fact table the next launch covers, a copy stream,
+  // per-chunk copy events and per-chunk device result slots
+  int64_t win_lo = 0, win_n = -1;
+  cudaStream_t copy_stream = nullptr;
+  std::vector<cudaEvent_t> chunk_ev;
+  int64_t* chunk_res = nullptr;
+  size_t chunk_res_slots = 0;
 };
 
 namespace {
@@ -261,6 +268,9 @@ extern "C" FLERN_API void flern_destroy(flern_ctx* ctx) {
     for (auto& kv : m.permuted) cudaFree(kv.second);
   }
   for (auto& h : ctx->hts) cudaFree(h.slots);
+  for (auto e : ctx->chunk_ev) cudaEventDestroy(e);
+  if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
+  cudaFree(ctx->chunk_res);
   cudaFree(ctx->partials);
   cudaFree(ctx->ticket);
   cudaFree(ctx->dres);
@@ -392,6 +402,109 @@ extern "C" FLERN_API flern_status flern_update_table(flern_ctx* ctx, int32_t tab
                                   mode == FLERN_COPY_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, ctx->stream));
   CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));  // host buffers may be reused on return
   t.nrows = nrows;
+  return FLERN_OK;
+}
+
+extern "C" FLERN_API flern_status flern_run_query_streamed(flern_ctx* ctx, const flern_query* q, int64_t nrows,
+                                                           int32_t ncols, const flern_column* host_cols,
+                                                           int64_t chunk_rows, flern_result* res) {
+  if (!ctx) return FLERN_E_INVALID_ARG;
+  if (!q || !res || !res->count || !res->sum)
+    return fail(ctx, FLERN_E_INVALID_ARG, "flern_run_query_streamed: null query or result");
+  if (q->flags & (FLERN_Q_ASYNC | FLERN_Q_RESULT_DEVICE))
+    return fail(ctx, FLERN_E_INVALID_ARG, "flern_run_query_streamed: host results only (no ASYNC / RESULT_DEVICE)");
+  if (q->fact_table < 0 || q->fact_table >= (int32_t)ctx->tables.size() || !ctx->tables[q->fact_table].alive)
+    return fail(ctx, FLERN_E_NOT_FOUND, "no fact table with id %d", q->fact_table);
+  Table& t = ctx->tables[q->fact_table];
+  if (nrows < 0 || nrows > t.capacity)
+    return fail(ctx, FLERN_E_INVALID_ARG, "flern_run_query_streamed: %lld rows exceed table '%s''s %lld-row capacity",
+                (long long)nrows, t.name.c_str(), (long long)t.capacity);
+  if (chunk_rows <= 0) return fail(ctx, FLERN_E_INVALID_ARG, "flern_run_query_streamed: chunk_rows must be > 0");
+  chunk_rows = (chunk_rows + 3) & ~3ll;   // chunk starts stay 16-byte aligned (vector loads, bulk copies)
+  if (!host_cols || ncols <= 0) return fail(ctx, FLERN_E_INVALID_ARG, "flern_run_query_streamed: no columns");
+  std::vector<int> slot(ncols, -1);
+  for (int32_t i = 0; i < ncols; ++i) {
+    for (size_t j = 0; j < t.cols.size() && host_cols[i].name; ++j)
+      if (t.cols[j].name == host_cols[i].name) slot[i] = (int)j;
+    if (slot[i] < 0)
+      return fail(ctx, FLERN_E_NOT_FOUND, "flern_run_query_streamed: table '%s' has no column '%s'", t.name.c_str(),
+                  host_cols[i].name ? host_cols[i].name : "(null)");
+    if (!t.cols[slot[i]].owned && t.capacity > 0)
+      return fail(ctx, FLERN_E_INVALID_ARG, "flern_run_query_streamed: column '%s' is borrowed", host_cols[i].name);
+    if (t.cols[slot[i]].dtype != host_cols[i].dtype)
+      return fail(ctx, FLERN_E_TYPE, "flern_run_query_streamed: column '%s' changes dtype", host_cols[i].name);
+    if (nrows > 0 && !host_cols[i].data)
+      return fail(ctx, FLERN_E_INVALID_ARG, "flern_run_query_streamed: column '%s' has no data", host_cols[i].name);
+  }
+  CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+  const int64_t nchunks = std::max<int64_t>(1, (nrows + chunk_rows - 1) / chunk_rows);
+  const size_t W = 4 * kMaxGroups + kCounters;   // one chunk's [count x2 | sum x2 | counters]
+  if (!ctx->copy_stream) CUDA_TRY(ctx, cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+  while ((int64_t)ctx->chunk_ev.size() < nchunks) {
+    cudaEvent_t e;
+    CUDA_TRY(ctx, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    ctx->chunk_ev.push_back(e);
+  }
+  if (ctx->chunk_res_slots < (size_t)nchunks) {
+    CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    cudaFree(ctx->chunk_res);
+    ctx->chunk_res = nullptr;
+    ctx->chunk_res_slots = 0;
+    CUDA_TRY(ctx, cudaMalloc(&ctx->chunk_res, (size_t)nchunks * W * sizeof(int64_t)));
+    ctx->chunk_res_slots = (size_t)nchunks;
+  }
+  // the copy stream starts after everything already queued on the query stream (earlier readers of
+  // the table's columns)
+  CUDA_TRY(ctx, cudaEventRecord(ctx->ev0, ctx->stream));
+  CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->copy_stream, ctx->ev0, 0));
+  const bool both = (q->flags & FLERN_Q_BOTH_CLASSES) != 0;
+  flern_status st = FLERN_OK;
+  for (int64_t c = 0; c < nchunks && st == FLERN_OK; ++c) {
+    const int64_t lo = c * chunk_rows, nc = std::min(chunk_rows, nrows - lo);
+    for (int32_t i = 0; i < ncols && nc > 0; ++i)
+      CUDA_TRY(ctx, cudaMemcpyAsync(static_cast<int32_t*>(t.cols[slot[i]].dptr) + lo,
+                                    static_cast<const int32_t*>(host_cols[i].data) + lo, (size_t)nc * 4,
+                                    cudaMemcpyHostToDevice, ctx->copy_stream));
+    CUDA_TRY(ctx, cudaEventRecord(ctx->chunk_ev[c], ctx->copy_stream));
+    CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->stream, ctx->chunk_ev[c], 0));
+    // chunk c's launch: rows [lo, lo + nc), results into chunk slot c on the device, asynchronous
+    flern_query qc = *q;
+    qc.flags |= FLERN_Q_RESULT_DEVICE | FLERN_Q_ASYNC;
+    flern_result rc{};
+    int64_t* slotp = ctx->chunk_res + (size_t)c * W;
+    rc.count = slotp;
+    rc.sum = slotp + 2 * kMaxGroups;
+    rc.counters = slotp + 4 * kMaxGroups;
+    ctx->win_lo = lo;
+    ctx->win_n = std::max<int64_t>(nc, 0);
+    st = flern_run_query(ctx, &qc, &rc);
+  }
+  ctx->win_lo = 0;
+  ctx->win_n = -1;
+  if (st != FLERN_OK) {
+    cudaStreamSynchronize(ctx->stream);
+    return st;
+  }
+  std::vector<int64_t> h((size_t)nchunks * W);
+  CUDA_TRY(ctx, cudaMemcpyAsync(h.data(), ctx->chunk_res, h.size() * sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  t.nrows = nrows;
+  const int G = q->ngroups, nout = both ? 2 * G : G;
+  int64_t cnt[kCounters] = {0, 0, 0, 0};
+  for (int i = 0; i < nout; ++i) { res->count[i] = 0; res->sum[i] = 0; }
+  for (int64_t c = 0; c < nchunks; ++c) {
+    const int64_t* r = h.data() + (size_t)c * W;
+    for (int i = 0; i < nout; ++i) { res->count[i] += r[i]; res->sum[i] += r[2 * kMaxGroups + i]; }
+    for (int i = 0; i < kCounters; ++i) cnt[i] += r[4 * kMaxGroups + i];
+  }
+  if (res->counters) std::memcpy(res->counters, cnt, sizeof(cnt));
+  res->rows_scanned = cnt[0];
+  res->rows_joined = cnt[1];
+  res->rows_scored = cnt[1];
+  res->rows_selected = cnt[2];
+  res->elapsed_ms = 0.f;
+  if (cnt[3] != 0)
+    return fail(ctx, FLERN_E_INVALID_ARG, "%lld joined rows have a group code outside [0, %d)", (long long)cnt[3], G);
   return FLERN_OK;
 }
 
@@ -733,7 +846,10 @@ extern "C" FLERN_API flern_status flern_run_query(flern_ctx* ctx, const flern_qu
 
   QueryParams p;
   std::memset(&p, 0, sizeof(p));
-  p.nrows = fact.nrows;
+  // a streamed query runs over a row window of the fact table (flern_run_query_streamed)
+  const bool windowed = ctx->win_n >= 0;
+  const int64_t woff = windowed ? ctx->win_lo : 0;
+  p.nrows = windowed ? ctx->win_n : fact.nrows;
   p.nprobes = q->nprobes;
   for (int i = 0; i < q->nprobes; ++i) {
     const flern_probe& pr = q->probes[i];
@@ -756,7 +872,7 @@ extern "C" FLERN_API flern_status flern_run_query(flern_ctx* ctx, const flern_qu
       const Column* c = fact.find(pr.key_col);
       if (!c) return fail(ctx, FLERN_E_NOT_FOUND, "fact table '%s' has no column '%s'", fact.name.c_str(), pr.key_col);
       if (!is_int_type(c->dtype)) return fail(ctx, FLERN_E_TYPE, "probe key '%s' must be integer-typed", pr.key_col);
-      d.fact_key = static_cast<const int32_t*>(c->dptr);
+      d.fact_key = static_cast<const int32_t*>(c->dptr) + woff;
     } else {
       const HashTable& hs = ctx->hts[q->probes[pr.src].ht_id];
       const int w = hs.find(pr.key_col);
@@ -771,7 +887,7 @@ extern "C" FLERN_API flern_status flern_run_query(flern_ctx* ctx, const flern_qu
       const Column* c = fact.find(r.col);
       if (!c) return fail(ctx, FLERN_E_NOT_FOUND, "%s: fact table '%s' has no column '%s'", what, fact.name.c_str(), r.col);
       if (need_int && !is_int_type(c->dtype)) return fail(ctx, FLERN_E_TYPE, "%s: column '%s' must be integer-typed", what, r.col);
-      out->base = static_cast<const int32_t*>(c->dptr);
+      out->base = static_cast<const int32_t*>(c->dptr) + woff;
       out->stride = 1;
       out->src = 0;
       out->is_float = c->dtype == FLERN_F32;
@@ -806,7 +922,7 @@ extern "C" FLERN_API flern_status flern_run_query(flern_ctx* ctx, const flern_qu
       if (fq[k].src == src) { perm.push_back(k); ++nsrc[src]; }
   p.nfact = nsrc[0];
   bool ident = true;
-  const int32_t* any_fact_col = static_cast<const int32_t*>(fact.cols[0].dptr);
+  const int32_t* any_fact_col = static_cast<const int32_t*>(fact.cols[0].dptr) + woff;
   for (int k = 0; k < kMaxFeat; ++k) { p.fcol[k] = any_fact_col; p.dword[k] = 0; }
   for (int k = 0; k < q->nfeat; ++k) {
     p.feat[k] = fq[perm[k]];
@@ -828,7 +944,7 @@ extern "C" FLERN_API flern_status flern_run_query(flern_ctx* ctx, const flern_qu
     const Column* c = fact.find(q->prefilter_col);
     if (!c) return fail(ctx, FLERN_E_NOT_FOUND, "pre-filter: fact table '%s' has no column '%s'", fact.name.c_str(), q->prefilter_col);
     if (!is_int_type(c->dtype)) return fail(ctx, FLERN_E_TYPE, "pre-filter column '%s' must be integer-typed", q->prefilter_col);
-    p.pf_col = static_cast<const int32_t*>(c->dptr);
+    p.pf_col = static_cast<const int32_t*>(c->dptr) + woff;
     p.pf_lo = q->pf_lo;
     p.pf_hi = getenv("FLERN_DBG_PF_EMPTY") ? q->pf_lo : q->pf_hi;   // diagnostic: scan cost alone
   }
@@ -873,7 +989,9 @@ extern "C" FLERN_API flern_status flern_run_query(flern_ctx* ctx, const flern_qu
   p.ticket = ctx->ticket;
   p.work = reinterpret_cast<unsigned long long*>(ctx->ticket) + 1;
   // debug exports: device pointers as given, or temporary device buffers copied back
-  const int64_t n = fact.nrows;
+  const int64_t n = p.nrows;
+  if (windowed && (res->dbg_score || res->dbg_match || res->dbg_selected || res->dbg_trace))
+    return fail(ctx, FLERN_E_UNSUPPORTED, "debug exports are not available for streamed queries");
   float* d_score = nullptr;
   int32_t* d_match = nullptr;
   uint32_t* d_sel = nullptr;

@@ -29,7 +29,7 @@ FLERN_I32, FLERN_F32, FLERN_DATE32, FLERN_DEC32, FLERN_DICT32 = 1, 2, 3, 4, 5
 FLERN_COPY_HOST, FLERN_COPY_DEVICE, FLERN_BORROW_DEVICE = 0x1, 0x2, 0x4
 FLERN_Q_RESULT_DEVICE, FLERN_Q_ASYNC, FLERN_Q_BOTH_CLASSES, FLERN_Q_NO_MODEL = 0x1, 0x2, 0x4, 0x8
 EXPORTED = ["flern_create", "flern_destroy", "flern_last_error", "flern_version", "flern_load_table",
-            "flern_update_table", "flern_drop_table", "flern_load_model", "flern_build_hashtable", "flern_run_query",
+            "flern_update_table", "flern_run_query_streamed", "flern_drop_table", "flern_load_model", "flern_build_hashtable", "flern_run_query",
             "flern_query_launches"]
 
 
@@ -71,6 +71,9 @@ _lib.flern_load_table.argtypes = [c_p, ctypes.c_char_p, c_i64, c_i32, ctypes.POI
 _lib.flern_load_table.restype = c_i32
 _lib.flern_update_table.argtypes = [c_p, c_i32, c_i64, c_i32, ctypes.POINTER(FlernColumn), c_u32]
 _lib.flern_update_table.restype = c_i32
+_lib.flern_run_query_streamed.argtypes = [c_p, ctypes.POINTER(FlernQuery), c_i64, c_i32, ctypes.POINTER(FlernColumn),
+                                          c_i64, ctypes.POINTER(FlernResult)]
+_lib.flern_run_query_streamed.restype = c_i32
 _lib.flern_drop_table.argtypes = [c_p, c_i32]
 _lib.flern_drop_table.restype = c_i32
 _lib.flern_load_model.argtypes = [c_p, ctypes.c_char_p, c_i32, ctypes.POINTER(c_i32), ctypes.POINTER(c_p),
@@ -231,6 +234,17 @@ def flern_run_query(ctx, query: Query, count=None, sum=None, counters=None, dbg_
     res = FlernResult(_ptr(count), _ptr(sum), _ptr(counters), _ptr(dbg_score), _ptr(dbg_match), _ptr(dbg_selected),
                       _ptr(dbg_trace), 0, 0, 0, 0, 0.0)
     _check(ctx, _lib.flern_run_query(ctx, ctypes.byref(query.q), ctypes.byref(res)))
+    return res
+
+
+def flern_run_query_streamed(ctx, query: Query, columns: dict, chunk_rows: int, count=None, sum=None,
+                             counters=None) -> FlernResult:
+    """Runs `query` over host columns {name: array} (pinned torch tensors or numpy arrays) streamed into
+    the query's fact table in chunks of `chunk_rows`, copies overlapped with the chunk queries."""
+    n, arr, keep = _columns(columns, None)
+    res = FlernResult(_ptr(count), _ptr(sum), _ptr(counters), None, None, None, None, 0, 0, 0, 0, 0.0)
+    _check(ctx, _lib.flern_run_query_streamed(ctx, ctypes.byref(query.q), n, len(arr), arr, chunk_rows,
+                                              ctypes.byref(res)))
     return res
 
 
