@@ -151,7 +151,8 @@ typedef struct {
   float threshold;                /* select rows with score > threshold. <= 0: all; >= 1: none;
                                      NaN: FLERN_E_INVALID_ARG */
   flern_colref group_col;         /* integer codes in [0, ngroups) */
-  int32_t ngroups;                /* 1..64 */
+  int32_t ngroups;                /* 1..2^22: up to 64 groups are aggregated per CTA in registers / SMEM;
+                                     larger domains with per-row int64 atomics into the result (NEXT-1) */
   flern_colref sum_col;           /* integer column, summed exactly in int64 */
   uint32_t flags;                 /* FLERN_Q_* below */
 } flern_query;

@@ -6,7 +6,8 @@
 namespace flern {
 
 constexpr int kMaxFeat = 48;
-constexpr int kMaxGroups = 64;
+constexpr int kMaxGroups = 64;          // group domains aggregated per CTA (registers / SMEM partials)
+constexpr int kMaxGroupsLarge = 1 << 22; // larger domains: per-row int64 atomics into the global result
 constexpr int kMaxProbes = 2;
 constexpr int kTile = 128;
 // Narrow kernel: 16 warps. SMSP k runs warps k, k+4, k+8, k+12. The MMA issuer (warp 12) shares
@@ -186,7 +187,7 @@ struct Meta {  // view of one stage's metadata block
   int32_t* count;
   int32_t* rowid;
   int32_t* val;
-  uint8_t* grp;
+  int32_t* grp;   // group code, -1 = outside [0, ngroups)
 };
 
 // Query feature shape the producer is compiled for: NF fact-column features, ND0 / ND1 payload
@@ -204,7 +205,7 @@ struct FixedShape {
 
 // The ring of X stages the producer fills: S stages of [128 rows x K0P] bf16 (interleaved K-major)
 // plus a metadata block per stage (count, fact row id, sum value, group code).
-constexpr uint32_t kMetaBytes = 16 + 4 * kTile + 4 * kTile + kTile;
+constexpr uint32_t kMetaBytes = 16 + 4 * kTile + 4 * kTile + 4 * kTile;
 struct XRing {
   uint8_t* x;
   uint32_t xs;       // bytes per X stage
@@ -215,7 +216,7 @@ struct XRing {
 __device__ __forceinline__ Meta meta_at(uint8_t* meta, int s) {
   uint8_t* m = meta + s * kMetaBytes;
   return Meta{reinterpret_cast<int32_t*>(m), reinterpret_cast<int32_t*>(m + 16),
-              reinterpret_cast<int32_t*>(m + 16 + 4 * kTile), m + 16 + 8 * kTile};
+              reinterpret_cast<int32_t*>(m + 16 + 4 * kTile), reinterpret_cast<int32_t*>(m + 16 + 8 * kTile)};
 }
 
 // Fact-column ring (narrow kernel, producer shapes fixed at compile time): the loader warp copies
@@ -248,9 +249,11 @@ __device__ __forceinline__ const int32_t* fact_col_ptr(const QueryParams& p, int
 constexpr int kFastGroups = 8;
 struct GroupAgg {
   unsigned long long ac[2][2], as[2][2];      // ballot path
+  uint32_t nsel;                              // large-domain path: selected rows of this thread
   uint32_t fc[2][kFastGroups];                // fast path: [class][group] row counts (this thread)
   long long fs[2][kFastGroups];               // fast path: sums
   __device__ __forceinline__ void init() {
+    nsel = 0u;
 #pragma unroll
     for (int u = 0; u < 2; ++u)
 #pragma unroll
@@ -265,15 +268,24 @@ struct GroupAgg {
                                        int64_t* s_cnt, uint64_t* empty_bar) {
     const bool valid = r < count;
     const bool sel = valid && (p.no_model || logit > p.thr_logit);
-    const int g = valid ? (int)m.grp[r] : 255;
+    const int g = valid ? m.grp[r] : -1;
     const int32_t val = valid ? m.val[r] : 0;
-    if (valid && g == 255) atomicAdd(reinterpret_cast<unsigned long long*>(&s_cnt[3]), 1ull);
+    if (valid && g < 0) atomicAdd(reinterpret_cast<unsigned long long*>(&s_cnt[3]), 1ull);
     if (p.dbg_score && valid) p.dbg_score[m.rowid[r]] = 1.f / (1.f + __expf(-logit));
     if (p.dbg_selected && sel) atomicOr(p.dbg_selected + (m.rowid[r] >> 5), 1u << (m.rowid[r] & 31));
     __syncwarp();
     if (lane == 0) mbar_arrive(empty_bar);
     const int cls = sel ? 0 : 1;
-    const bool agg = valid && g != 255 && (sel || p.both_classes);
+    const bool agg = valid && g >= 0 && (sel || p.both_classes);
+    if (p.ngroups > kMaxGroups) {   // large domain: straight into the global result (zeroed by the host)
+      if (agg) {
+        const int64_t o = (int64_t)cls * p.ngroups + g;
+        atomicAdd(reinterpret_cast<unsigned long long*>(p.out_count + o), 1ull);
+        atomicAdd(reinterpret_cast<unsigned long long*>(p.out_sum + o), (unsigned long long)(long long)val);
+      }
+      nsel += (valid && g >= 0 && sel) ? 1u : 0u;
+      return;
+    }
     if (p.ngroups <= kFastGroups) {
 #pragma unroll
       for (int gg = 0; gg < kFastGroups; ++gg) {
@@ -306,7 +318,14 @@ struct GroupAgg {
       pending &= ~mm;
     }
   }
-  __device__ __forceinline__ void flush(unsigned long long* acc, int lane, int ngroups) {
+  __device__ __forceinline__ void flush(unsigned long long* acc, int lane, int ngroups, int64_t* s_cnt) {
+    if (ngroups > kMaxGroups) {   // the aggregates are already global; only the selected-row counter
+      unsigned long long n = nsel;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) n += __shfl_xor_sync(0xffffffffu, n, o);
+      if (lane == 0 && n) atomicAdd(reinterpret_cast<unsigned long long*>(&s_cnt[2]), n);
+      return;
+    }
     if (ngroups <= kFastGroups) {
 #pragma unroll
       for (int c = 0; c < 2; ++c)
@@ -370,12 +389,13 @@ __device__ __forceinline__ int64_t claim_chunk(const QueryParams& p, int64_t k) 
 __device__ __forceinline__ void write_partials_and_reduce(const QueryParams& p, unsigned long long* acc,
                                                           int64_t* s_cnt, unsigned int* s_is_last, int tid,
                                                           int nthreads) {
-  const int G = p.ngroups;
+  const bool large = p.ngroups > kMaxGroups;   // large domains aggregate straight into the result
+  const int G = large ? 0 : p.ngroups;
   const int W = G * 4 + kCounters;
   for (int i = tid; i < G * 4; i += nthreads)
     if (acc[i]) atomicAdd(&p.partials[i], acc[i]);
   if (tid == 0) {
-    unsigned long long sel = 0;
+    unsigned long long sel = large ? (unsigned long long)s_cnt[2] : 0ull;
     for (int g = 0; g < G; ++g) sel += acc[g * 4 + 0];
     const unsigned long long c[kCounters] = {(unsigned long long)s_cnt[0], (unsigned long long)s_cnt[1], sel,
                                              (unsigned long long)s_cnt[3]};

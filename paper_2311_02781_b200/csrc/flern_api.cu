@@ -103,6 +103,9 @@ struct flern_ctx {
   std::vector<cudaEvent_t> chunk_ev;
   int64_t* chunk_res = nullptr;
   size_t chunk_res_slots = 0;
+  // host-side results of large group domains (> kMaxGroups): [count | sum] device buffer
+  int64_t* big_res = nullptr;
+  size_t big_slots = 0;
 };
 
 namespace {
@@ -167,7 +170,7 @@ constexpr bool plan_fits() {
   constexpr uint32_t HB = 0;   // H lives in TMEM
   constexpr uint32_t W1 = (uint32_t)H * K0P * 2;
   constexpr uint32_t XS = (uint32_t)kTile * K0P * 2;
-  constexpr uint32_t META = 16 + 9 * kTile;
+  constexpr uint32_t META = kMetaBytes;
   constexpr uint32_t FIXED = WH + HB + W1 + NL * H * 4 + H * 4 + kMaxGroups * 4 * 8 + queue_bytes(32 * kProdWarps) + kMaxFeat * 8 +
                              64 * 8 + 128;
   return FIXED + 3 * (XS + META) <= 232448;
@@ -271,6 +274,7 @@ extern "C" FLERN_API void flern_destroy(flern_ctx* ctx) {
   for (auto e : ctx->chunk_ev) cudaEventDestroy(e);
   if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
   cudaFree(ctx->chunk_res);
+  cudaFree(ctx->big_res);
   cudaFree(ctx->partials);
   cudaFree(ctx->ticket);
   cudaFree(ctx->dres);
@@ -840,8 +844,10 @@ extern "C" FLERN_API flern_status flern_run_query(flern_ctx* ctx, const flern_qu
   if (q->nfeat > 0 && !q->feats) return fail(ctx, FLERN_E_INVALID_ARG, "null feature list");
   if (q->nprobes < 1 || q->nprobes > kMaxProbes || !q->probes)
     return fail(ctx, FLERN_E_UNSUPPORTED, "queries need 1..%d probes (got %d)", kMaxProbes, q->nprobes);
-  if (q->ngroups < 1 || q->ngroups > kMaxGroups)
-    return fail(ctx, FLERN_E_UNSUPPORTED, "ngroups %d outside 1..%d", q->ngroups, kMaxGroups);
+  if (q->ngroups < 1 || q->ngroups > kMaxGroupsLarge)
+    return fail(ctx, FLERN_E_UNSUPPORTED, "ngroups %d outside 1..%d", q->ngroups, kMaxGroupsLarge);
+  if (q->ngroups > kMaxGroups && ctx->win_n >= 0)
+    return fail(ctx, FLERN_E_UNSUPPORTED, "streamed queries aggregate at most %d groups", kMaxGroups);
   if (std::isnan(q->threshold)) return fail(ctx, FLERN_E_INVALID_ARG, "threshold is NaN");
 
   QueryParams p;
@@ -979,8 +985,25 @@ extern "C" FLERN_API flern_status flern_run_query(flern_ctx* ctx, const flern_qu
   CUDA_TRY(ctx, cudaSetDevice(ctx->device));
   const int G = q->ngroups;
   const int nout = both ? 2 * G : G;
+  const bool large = G > kMaxGroups;   // per-row atomics straight into a zeroed result (GroupAgg)
   int64_t* d_count = dev_out ? res->count : ctx->dres;
   int64_t* d_sum = dev_out ? res->sum : ctx->dres + 2 * kMaxGroups;
+  if (large) {
+    if (!dev_out) {
+      if (ctx->big_slots < (size_t)nout) {
+        CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+        cudaFree(ctx->big_res);
+        ctx->big_res = nullptr;
+        ctx->big_slots = 0;
+        CUDA_TRY(ctx, cudaMalloc(&ctx->big_res, (size_t)2 * nout * sizeof(int64_t)));
+        ctx->big_slots = (size_t)nout;
+      }
+      d_count = ctx->big_res;
+      d_sum = ctx->big_res + nout;
+    }
+    CUDA_TRY(ctx, cudaMemsetAsync(d_count, 0, (size_t)nout * sizeof(int64_t), ctx->stream));
+    CUDA_TRY(ctx, cudaMemsetAsync(d_sum, 0, (size_t)nout * sizeof(int64_t), ctx->stream));
+  }
   int64_t* d_counters = (dev_out && res->counters) ? res->counters : ctx->dres + 4 * kMaxGroups;
   p.out_count = d_count;
   p.out_sum = d_sum;
@@ -1107,8 +1130,13 @@ extern "C" FLERN_API flern_status flern_run_query(flern_ctx* ctx, const flern_qu
   for (void* v : temps) cudaFree(v);
   const int64_t* cnt = dev_out ? hcnt : hres + 4 * kMaxGroups;
   if (!dev_out) {
-    std::memcpy(res->count, hres, nout * sizeof(int64_t));
-    std::memcpy(res->sum, hres + 2 * kMaxGroups, nout * sizeof(int64_t));
+    if (large) {
+      CUDA_TRY(ctx, cudaMemcpy(res->count, d_count, (size_t)nout * sizeof(int64_t), cudaMemcpyDeviceToHost));
+      CUDA_TRY(ctx, cudaMemcpy(res->sum, d_sum, (size_t)nout * sizeof(int64_t), cudaMemcpyDeviceToHost));
+    } else {
+      std::memcpy(res->count, hres, nout * sizeof(int64_t));
+      std::memcpy(res->sum, hres + 2 * kMaxGroups, nout * sizeof(int64_t));
+    }
     if (res->counters) std::memcpy(res->counters, cnt, kCounters * sizeof(int64_t));
   }
   res->rows_scanned = cnt[0];

@@ -292,7 +292,7 @@ __device__ __forceinline__ void produce_batch(ProdState& st, const QueryParams& 
             st_shared_v4(smem_u32(xs + c8 * (kTile * 16) + (tp >> 3) * 128 + (tp & 7) * 16), pk[r][4 * c8],
                          pk[r][4 * c8 + 1], pk[r][4 * c8 + 2], pk[r][4 * c8 + 3]);
           m.rowid[tp] = (int32_t)(row0 + r);
-          m.grp[tp] = (gv[r] >= 0 && gv[r] < p.ngroups) ? (uint8_t)gv[r] : (uint8_t)255;
+          m.grp[tp] = (gv[r] >= 0 && gv[r] < p.ngroups) ? gv[r] : -1;
           m.val[tp] = sv[r];
         }
         if ((seg + 1) * kTile <= end) {   // stage complete: publish

@@ -33,7 +33,7 @@ struct SmemPlan {
   static constexpr uint32_t HB = 0;   // the hidden activation lives in TMEM (TmemPlan::HT)
   static constexpr uint32_t W1 = (uint32_t)H * K0P * 2;                       // layer-1 W, interleave
   static constexpr uint32_t XS = (uint32_t)kTile * K0P * 2;                   // one X stage, interleave
-  static constexpr uint32_t META = 16 + 4 * kTile + 4 * kTile + kTile;        // count, rowid, val, grp
+  static constexpr uint32_t META = kMetaBytes;                                 // count, rowid, val, grp
   static constexpr uint32_t BB = bias_operand_bytes(H);                       // one layer's bias B operand
   static constexpr uint32_t FIXED = WH + HB + W1 + kOnesBytes + NL * BB + H * 4 + kMaxGroups * 4 * 8 +
                                     queue_bytes(32 * kProdWarps) + kMaxFeat * 8 + 64 * 8 + kMiscBytes +
@@ -93,7 +93,7 @@ template <class P>
 __device__ __forceinline__ Meta meta_of(uint8_t* base, int s) {
   uint8_t* m = base + P::off_meta + s * P::META;
   return Meta{reinterpret_cast<int32_t*>(m), reinterpret_cast<int32_t*>(m + 16),
-              reinterpret_cast<int32_t*>(m + 16 + 4 * kTile), m + 16 + 8 * kTile};
+              reinterpret_cast<int32_t*>(m + 16 + 4 * kTile), reinterpret_cast<int32_t*>(m + 16 + 8 * kTile)};
 }
 
 template <int K0P, int H, int NL, class SH>
@@ -359,7 +359,7 @@ __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_c
     auto finish_tile = [&](const Meta& m, int count, int s, float logit) {
       agg.tile(p, m, count, r, lane, logit, s_cnt, &empty[s]);
     };
-    auto flush_acc = [&]() { agg.flush(acc, lane, p.ngroups); };
+    auto flush_acc = [&]() { agg.flush(acc, lane, p.ngroups, s_cnt); };
     // relu(D) . w_out over `ncols` TMEM columns at `col` (D already holds the bias, see
     // kOnesBytes), with relu(x) * w = x * (w/2) + |x| * (w/2): two packed FMAs per column pair,
     // the |x| an operand modifier, so the dot needs no max instruction (s_wout holds w_out / 2,

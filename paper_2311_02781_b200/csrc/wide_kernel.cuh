@@ -316,7 +316,7 @@ __global__ void __launch_bounds__(kThreadsWide, 1) flern_query_wide_kernel(const
         agg.tile(p, m, count, r, lane, logit, s_cnt, &xempty[s]);
       }
     }
-    if (wg == 1) agg.flush(acc, lane, p.ngroups);
+    if (wg == 1) agg.flush(acc, lane, p.ngroups, s_cnt);
   }
 
   tc_fence_before();

@@ -374,3 +374,17 @@ def test_streamed_query_equals_resident(chunk):
         assert (c2 == rc).all() and (s2 == rs).all()
     finally:
         gq.close()
+
+
+@pytest.mark.parametrize("sf,both", [(0.0005, False), (0.004, False), (0.004, True)])
+def test_large_group_domain(sf, both):
+    """NEXT-1: GROUP BY a fact column with more than 64 groups (l_partkey: ~100 and ~800 dense codes),
+    aggregated with per-row int64 atomics straight into the result; exact against the oracle, with the
+    two-class conservation check."""
+    import dataclasses
+    base = D.with_sf(D.CONFIGS["c2"], sf, match_rate=0.9)
+    db = D.make_database(base)
+    G = int(db.fact["l_partkey"].max()) + 1
+    assert G > 64
+    cfg = dataclasses.replace(base, group=("fact", "l_partkey"), ngroups=G)
+    parity.check(cfg, db, D.make_model(cfg, db), both=both)
