@@ -388,3 +388,24 @@ def test_large_group_domain(sf, both):
     assert G > 64
     cfg = dataclasses.replace(base, group=("fact", "l_partkey"), ngroups=G)
     parity.check(cfg, db, D.make_model(cfg, db), both=both)
+
+
+@pytest.mark.parametrize("name,sf", [("c4p", 0.05), ("c3", 0.01)])
+def test_streamed_query_prefilter_and_two_probes(name, sf):
+    """flern_run_query_streamed over the pre-filter path (filter column windowed per chunk) and the
+    two-probe wide-MLP chain: the streamed aggregates equal the resident query's."""
+    from paper_2311_02781_b200 import flern as F
+    from paper_2311_02781_b200.session import GpuQuery
+    cfg = D.with_sf(D.CONFIGS[name], sf, match_rate=0.9)
+    db = D.make_database(cfg)
+    gq = GpuQuery(cfg, db, D.make_model(cfg, db))
+    G = cfg.ngroups
+    try:
+        rc, rs = np.zeros(G, np.int64), np.zeros(G, np.int64)
+        ref = gq.run(count=rc, sum=rs)
+        c, s_ = np.zeros(G, np.int64), np.zeros(G, np.int64)
+        r = F.flern_run_query_streamed(gq.ctx, gq.query, db.fact, 10000, count=c, sum=s_)
+        assert (c == rc).all() and (s_ == rs).all()
+        assert (r.rows_scanned, r.rows_joined) == (ref.rows_scanned, ref.rows_joined)
+    finally:
+        gq.close()
