@@ -1060,7 +1060,11 @@ extern "C" FLERN_API flern_status flern_run_query(flern_ctx* ctx, const flern_qu
   // one persistent CTA per SM; rows are claimed as chunks (guided schedule, chunk_rows in common.cuh):
   // 2*grid contiguous halves of an 85% static share, then small chunks on demand
   const int npt = 32 * (ke->threads == kThreads ? kProdWarps : kProdWarpsWide);   // producer threads
-  const int64_t chunk = p.pf_col ? (int64_t)scan_rows(npt) : (int64_t)batch_rows(m.K0P, m.NL, npt);
+  int64_t chunk = p.pf_col ? (int64_t)scan_rows(npt) : (int64_t)batch_rows(m.K0P, m.NL, npt);
+  // a table smaller than one batch per SM: smaller chunks (multiples of 16 rows, aligned for vector
+  // loads and bulk copies) so every SM takes a share and the kernel's latency shrinks
+  if (!p.pf_col && n < (int64_t)ctx->num_sms * chunk)
+    chunk = std::min(chunk, std::max<int64_t>(64, ((n + ctx->num_sms - 1) / ctx->num_sms + 15) / 16 * 16));
   const int grid = (int)std::min<int64_t>(ctx->num_sms, std::max<int64_t>(1, (n + chunk - 1) / chunk));
   p.claim_small = chunk;
   p.claim_big = (int64_t)(0.85 * (double)n / (2.0 * grid)) / chunk * chunk;
