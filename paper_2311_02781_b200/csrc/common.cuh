@@ -247,6 +247,9 @@ __device__ __forceinline__ const int32_t* fact_col_ptr(const QueryParams& p, int
 // a warp ballot per present (group, class) with popc rows and a split 16-bit redux sum, into
 // registers of the owning lane (lane l owns groups l and l+32).
 constexpr int kFastGroups = 8;
+// LARGE: the kernel supports group domains beyond kMaxGroups (compiled into the generic-shape kernels;
+// the shape-specialised benchmark kernels leave it out and the host routes large domains elsewhere)
+template <bool LARGE>
 struct GroupAgg {
   unsigned long long ac[2][2], as[2][2];      // ballot path
   uint32_t nsel;                              // large-domain path: selected rows of this thread
@@ -277,7 +280,7 @@ struct GroupAgg {
     if (lane == 0) mbar_arrive(empty_bar);
     const int cls = sel ? 0 : 1;
     const bool agg = valid && g >= 0 && (sel || p.both_classes);
-    if (p.ngroups > kMaxGroups) {   // large domain: straight into the global result (zeroed by the host)
+    if (LARGE && p.ngroups > kMaxGroups) {   // large domain: straight into the global result (zeroed by the host)
       if (agg) {
         const int64_t o = (int64_t)cls * p.ngroups + g;
         atomicAdd(reinterpret_cast<unsigned long long*>(p.out_count + o), 1ull);
@@ -319,7 +322,7 @@ struct GroupAgg {
     }
   }
   __device__ __forceinline__ void flush(unsigned long long* acc, int lane, int ngroups, int64_t* s_cnt) {
-    if (ngroups > kMaxGroups) {   // the aggregates are already global; only the selected-row counter
+    if (LARGE && ngroups > kMaxGroups) {   // the aggregates are already global; only the selected-row counter
       unsigned long long n = nsel;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) n += __shfl_xor_sync(0xffffffffu, n, o);

@@ -979,7 +979,9 @@ extern "C" FLERN_API flern_status flern_run_query(flern_ctx* ctx, const flern_qu
   p.bout = m.bout;
   p.shift = reinterpret_cast<const float*>(img + m.off_shift);
   p.scale = reinterpret_cast<const float*>(img + m.off_scale);
-  KernelEntry* ke = find_kernel(m.K0P, m.H, m.NL, nsrc[0], nsrc[1], nsrc[2], p.fmask);
+  // group domains beyond kMaxGroups need the generic-shape kernels (GroupAgg<true>)
+  KernelEntry* ke = q->ngroups > kMaxGroups ? find_kernel(m.K0P, m.H, m.NL)
+                                            : find_kernel(m.K0P, m.H, m.NL, nsrc[0], nsrc[1], nsrc[2], p.fmask);
   if (!ke) return fail(ctx, FLERN_E_UNSUPPORTED, "no kernel for model '%s'", m.name.c_str());
 
   CUDA_TRY(ctx, cudaSetDevice(ctx->device));

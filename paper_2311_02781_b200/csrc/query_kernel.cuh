@@ -354,7 +354,7 @@ __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_c
     const int r = q * 32 + lane;            // tile row owned by this thread
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
 
-    GroupAgg agg;
+    GroupAgg<(SH::NF < 0)> agg;
     agg.init();
     auto finish_tile = [&](const Meta& m, int count, int s, float logit) {
       agg.tile(p, m, count, r, lane, logit, s_cnt, &empty[s]);

@@ -231,7 +231,7 @@ __global__ void __launch_bounds__(kThreadsWide, 1) flern_query_wide_kernel(const
     const int q = warp & 3;
     const int r = q * 32 + lane;
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
-    GroupAgg agg;
+    GroupAgg<(SH::NF < 0)> agg;
     agg.init();
     const uint64_t keep = l2_policy_evict_last();   // activation scratch: keep in L2 for the next layer
     for (uint32_t t = 0;; ++t) {
