@@ -409,3 +409,30 @@ def test_streamed_query_prefilter_and_two_probes(name, sf):
         assert (r.rows_scanned, r.rows_joined) == (ref.rows_scanned, ref.rows_joined)
     finally:
         gq.close()
+
+
+@pytest.mark.parametrize("name", ["c3", "c4"])
+def test_wide_full_size_sampled(name):
+    """Configs 3 and 4 at their full size (SF10, 60M fact rows, two probes, 32-1024-1024-1024-1) in the
+    launch configuration bench.py times: join ids, scores and selection on sampled row ranges against
+    the oracle; aggregates at -INF exact against the brute-force join (over the pre-filter survivors
+    for C4)."""
+    from paper_2311_02781_b200.session import GpuQuery
+    cfg = D.CONFIGS[name]
+    db = D.make_database(cfg)
+    model = D.make_model(cfg, db)
+    gq = GpuQuery(cfg, db, model)
+    try:
+        n = db.fact_n
+        rng = np.random.default_rng(11)
+        starts = sorted(rng.integers(0, n - 1000, size=5).tolist()) + [n - 700]
+        _, worst = parity.sample_check(cfg, db, model, gq, [(s, min(n, s + 700)) for s in starts])
+        g = parity.run_gpu(cfg, db, model, threshold=-math.inf, gq=gq, debug=False)
+        keep = np.ones(n, bool)
+        if cfg.prefilter:
+            col, lo, hi = cfg.prefilter
+            keep = (db.fact[col] >= lo) & (db.fact[col] < hi)
+        cnt, sm = H.brute_aggregate(cfg, db, keep)
+        assert g["count"].tolist() == cnt.tolist() and g["sum"].tolist() == sm.tolist()
+    finally:
+        gq.close()
