@@ -212,6 +212,7 @@ struct XRing {
   uint8_t* meta;     // S blocks of kMetaBytes
   uint64_t* full;    // [S] producers (128 arrivals) -> consumers
   uint64_t* empty;   // [S] consumers (4 warps) -> producers
+  uint32_t* ticket = nullptr;   // per-warp tiles (see produce_batch PW): next stage ticket (SMEM counter)
 };
 __device__ __forceinline__ Meta meta_at(uint8_t* meta, int s) {
   uint8_t* m = meta + s * kMetaBytes;

@@ -30,7 +30,10 @@ struct ProdState {
 // the batch, column stride kBR rows; see FactRing); my rows are [rel, rel + R) of the batch. The
 // few tail rows past nfull (table end, not a whole 16-byte granule) are read from global memory.
 // features_read() runs once every fact-stage read of this batch has completed.
-template <int K0P, int S, int R, class SH, int NPW, bool BULK = false, class FR = void (*)()>
+// PW (per-warp tiles, 32 * R == kTile): each warp compacts its own 128 rows into a stage of its own
+// (a ticket from an SMEM counter fixes the stage order the consumers follow), so producer warps never
+// wait for each other; the stage may hold fewer than 128 rows (count in its metadata).
+template <int K0P, int S, int R, class SH, int NPW, bool BULK = false, bool PW = false, class FR = void (*)()>
 __device__ __forceinline__ void produce_batch(ProdState& st, const QueryParams& p, const XRing& ring, int32_t* wcnt,
                                               const float* s_normf, int64_t row0, bool whole, const bool (&in)[R],
                                               int bidx, int64_t row_end, int t, int warp, int lane,
@@ -254,6 +257,37 @@ __device__ __forceinline__ void produce_batch(ProdState& st, const QueryParams& 
         const int x = __shfl_up_sync(0xffffffffu, incl, o);
         if (lane >= o) incl += x;
       }
+      if constexpr (PW) {
+        static_assert(32 * R == kTile, "per-warp tiles: one warp batch is one tile");
+        const int total = __shfl_sync(0xffffffffu, incl, 31);
+        st.n_joined += my_cnt;
+        if (total == 0) return;
+        uint32_t tk = 0;
+        if (lane == 0) tk = atomicAdd(ring.ticket, 1u);
+        tk = __shfl_sync(0xffffffffu, tk, 0);
+        const int ts = (int)(tk % (uint32_t)S);
+        FLERN_WAIT(W_PROD_EMPTY, t == 0, &ring.empty[ts], ((tk / S) & 1) ^ 1, 2);
+        uint8_t* xs = ring.x + ts * ring.xs;
+        const Meta m = meta_at(ring.meta, ts);
+        int tp = incl - my_cnt;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          if (!valid[r]) continue;
+#pragma unroll
+          for (int c8 = 0; c8 < K0P / 8; ++c8)
+            st_shared_v4(smem_u32(xs + c8 * (kTile * 16) + (tp >> 3) * 128 + (tp & 7) * 16), pk[r][4 * c8],
+                         pk[r][4 * c8 + 1], pk[r][4 * c8 + 2], pk[r][4 * c8 + 3]);
+          m.rowid[tp] = (int32_t)(row0 + r);
+          m.grp[tp] = (gv[r] >= 0 && gv[r] < p.ngroups) ? gv[r] : -1;
+          m.val[tp] = sv[r];
+          ++tp;
+        }
+        if (lane == 0) *m.count = total;
+        fence_proxy_async_smem();
+        mbar_arrive(&ring.full[ts]);   // 32 arrivals: this warp
+        if (t == 0) FLERN_TRACE(TR_P_DONE, bidx);
+        return;
+      }
       if (lane == 31) wcnt[st.buf * 8 + warp] = incl;
       named_bar_sync(1, 32 * NPW);
       int woff = 0, total = 0;
@@ -311,7 +345,7 @@ __device__ __forceinline__ void produce_batch(ProdState& st, const QueryParams& 
 }
 
 // `tid` is the thread's index in the producer group [0, 32*NPW), `warp` its warp in the group.
-template <int K0P, int NL, int S, class SH, int NPW, bool BULK>
+template <int K0P, int NL, int S, class SH, int NPW, bool BULK, bool PW = false>
 __device__ __forceinline__ void producer_loop(const QueryParams& p, const XRing& ring, int32_t* wcnt,
                                               const float* s_normf, int64_t* s_cnt, int32_t* queue,
                                               int64_t* s_claim, const FactRing& fr, int tid, int warp, int lane) {
@@ -362,7 +396,7 @@ __device__ __forceinline__ void producer_loop(const QueryParams& p, const XRing&
         __syncwarp();
         if (lane == 0) mbar_arrive(&fr.empty[f]);
       };
-      produce_batch<K0P, S, R, SH, NPW, true>(st, p, ring, wcnt, s_normf, srow0 + rel, rel + R <= nrows, in, bidx,
+      produce_batch<K0P, S, R, SH, NPW, true, PW>(st, p, ring, wcnt, s_normf, srow0 + rel, rel + R <= nrows, in, bidx,
                                               srow0 + nrows, t, warp, lane,
                                               smem_u32(fr.base + f * fr.stage_bytes), rel, nrows & ~3, release);
     }
@@ -508,6 +542,22 @@ __device__ __forceinline__ void producer_loop(const QueryParams& p, const XRing&
       }
     }
   }
+  if (PW && BULK && !p.pf_col) {
+    // per-warp tiles: every warp has published its last stage once all pass the barrier; one warp
+    // then takes two more tickets for the end-of-stream markers (see below)
+    named_bar_sync(1, NPT);
+    if (warp == 0) {
+      for (int e = 0; e < 2; ++e) {
+        uint32_t tk = 0;
+        if (lane == 0) tk = atomicAdd(ring.ticket, 1u);
+        tk = __shfl_sync(0xffffffffu, tk, 0);
+        const int ts = (int)(tk % (uint32_t)S);
+        mbar_wait(&ring.empty[ts], ((tk / S) & 1) ^ 1, 5);
+        if (lane == 0) *meta_at(ring.meta, ts).count = -1;
+        mbar_arrive(&ring.full[ts]);
+      }
+    }
+  } else {
   if (st.fill > 0) {   // flush the partial tile
       fence_proxy_async_smem();
       if (t == 0) *meta_at(ring.meta, st.stage).count = st.fill;
@@ -525,6 +575,7 @@ __device__ __forceinline__ void producer_loop(const QueryParams& p, const XRing&
     ++st.acq;
     if (t == 0) *meta_at(ring.meta, st.stage).count = -1;
     mbar_arrive(&ring.full[st.stage]);
+  }
     int64_t nj = st.n_joined;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) nj += __shfl_down_sync(0xffffffffu, nj, o);

@@ -38,7 +38,10 @@ struct SmemPlan {
   static constexpr uint32_t FIXED = WH + HB + W1 + kOnesBytes + NL * BB + H * 4 + kMaxGroups * 4 * 8 +
                                     queue_bytes(32 * kProdWarps) + kMaxFeat * 8 + 64 * 8 + kMiscBytes +
                                     2 * kTile * 4 + FR;
-  static constexpr int S = (FIXED + 4 * (XS + META) <= 232448) ? 4 : 3;
+  // per-warp tiles (PW, NL == 1 with 4 rows per producer thread): every producer warp may hold a stage
+  static constexpr bool PW = NCS > 0 && NL == 1 && 32 * rows_per_thread(K0P, NL) == kTile;
+  static constexpr int S = (PW && FIXED + 8 * (XS + META) <= 232448) ? 8
+                           : ((FIXED + 4 * (XS + META) <= 232448) ? 4 : 3);
   static constexpr uint32_t off_wh = 0;                                       // [Wh | W1] = weight image
   static constexpr uint32_t off_w1 = off_wh + WH;
   static constexpr uint32_t off_hb = off_w1 + W1;
@@ -113,15 +116,15 @@ __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_c
   if (tid == 0) claim0 = claim_chunk(p, 2);
 
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + P::off_bar);
-  uint64_t* full = bars;            // [S]   producers -> MMA/epilogue (128 arrivals)
-  uint64_t* empty = bars + S;       // [S]   epilogue WG0 -> producers (4 arrivals)
+  uint64_t* full = bars + 32;       // [S <= 8] producers -> MMA/epilogue (all producer threads; PW: one warp)
+  uint64_t* empty = bars + 40;      // [S <= 8] epilogue warpgroup -> producers (4 arrivals)
   uint64_t* d1full = bars + 8;      // NL=2: L1 piece commit -> warpgroup 0
   uint64_t* d1empty = bars + 9;     // NL=2: warpgroup 0 (4 warps) read the L1 piece out of R1 -> MMA
   uint64_t* dfull = bars + 10;      // [2] NL=2: layer-2 N-halves D2a/D2b (commit); NL=1: ping-pong D buffers
   uint64_t* dempty = bars + 12;     // [2] warpgroup 1 (4 warps) drained it -> MMA
   uint64_t* pready = bars + 24;     // NL=2: warpgroup 0's partial logits of the tile are in SMEM (4 warps)
-  uint64_t* ffull = bars + 26;      // [kFactStages] fact ring: loader -> producers
-  uint64_t* fempty = bars + 28;     // [kFactStages] fact ring: producer warps -> loader
+  uint64_t* ffull = bars + 48;      // [kFactStages <= 4] fact ring: loader -> producers
+  uint64_t* fempty = bars + 52;     // [kFactStages <= 4] fact ring: producer warps -> loader
   uint64_t* hfull = bars + 14;      // [4] NL=2: warpgroup 0 stored H chunk c in TMEM (4 warps)
   uint64_t* hfree = bars + 18;      // [4] NL=2: L2b finished reading H chunk c (commit)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + P::off_misc);
@@ -159,9 +162,13 @@ __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_c
     if (tid == 0) { s_claim[0] = claim0; s_claim[1] = claim0 + 1; }
     fence_proxy_async_smem();   // weights written by st.shared are read by the tensor core
   }
-  static_assert(S <= 4, "stage ring");
+  static_assert(S <= 8 && kFactStages <= 4, "stage rings");
+  uint32_t* s_ticket = reinterpret_cast<uint32_t*>(smem + P::off_misc + 176);   // PW stage tickets
+  // per-warp tiles run on the bulk path without a pre-filter (the pre-filter path compacts across warps)
+  const bool pw = P::PW && p.pf_col == nullptr;
   if (tid == 0) {
-    for (int s = 0; s < S; ++s) { mbar_init(&full[s], 32 * kProdWarps); mbar_init(&empty[s], 4); }
+    *s_ticket = 0u;
+    for (int s = 0; s < S; ++s) { mbar_init(&full[s], pw ? 32 : 32 * kProdWarps); mbar_init(&empty[s], 4); }
     mbar_init(d1full, 1);
     mbar_init(d1empty, 4);
     for (int i = 0; i < 2; ++i) { mbar_init(&dfull[i], 1); mbar_init(&dempty[i], 4); }
@@ -192,7 +199,7 @@ __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_c
     }
   } else if (is_prod_warp(warp)) {
     const int pw = prod_warp_index(warp);
-    producer_loop<K0P, NL, S, SH, kProdWarps, kBulk>(p, XRing{smem + P::off_x, P::XS, smem + P::off_meta, full, empty},
+    producer_loop<K0P, NL, S, SH, kProdWarps, kBulk, P::PW>(p, XRing{smem + P::off_x, P::XS, smem + P::off_meta, full, empty, s_ticket},
                                                  wcnt, s_shift, s_cnt, reinterpret_cast<int32_t*>(smem + P::off_queue),
                                                  s_claim, fr, pw * 32 + lane, pw, lane);
   } else if (warp == 12) {
