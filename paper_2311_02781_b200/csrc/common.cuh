@@ -231,9 +231,10 @@ __host__ __device__ constexpr int fact_cols(int nf) { return 3 + nf; }
 struct FactRing {
   uint8_t* base = nullptr;
   uint32_t stage_bytes = 0;
-  int64_t* hdr = nullptr;      // [kFactStages][2]
+  int64_t* hdr = nullptr;      // [stages][2]
   uint64_t* full = nullptr;    // [kFactStages] loader (1 arrival + tx bytes) -> producers
   uint64_t* empty = nullptr;   // [kFactStages] producer warps -> loader
+  int stages = kFactStages;    // 2 or 4 (SmemPlan::FST)
 };
 __device__ __forceinline__ const int32_t* fact_col_ptr(const QueryParams& p, int c) {
   return c == 0 ? p.probe[0].fact_key

@@ -143,6 +143,11 @@ __device__ __forceinline__ void produce_batch(ProdState& st, const QueryParams& 
       //    uniform slow path); a miss drops the row
       int32_t brow[R][kMaxProbes];
       const int32_t* pb[R][kMaxProbes];   // payload words of the matched build row (dz when none)
+      // a fat last probe is resolved late: its payload words are loaded from the key's entry before
+      // the match is known (same sector, always a valid address), so the probe and the payload loads
+      // overlap instead of taking two dependent round trips; the match then masks the row
+      int32_t dkey[R], dseen[R], drow[R];
+      int dq = -1;
 #pragma unroll
       for (int q = 0; q < kMaxProbes; ++q) {
 #pragma unroll
@@ -158,6 +163,19 @@ __device__ __forceinline__ void produce_batch(ProdState& st, const QueryParams& 
         if (pd.fstride) {
           // fat direct-addressed table: the key's own entry {key, row, payload...}; one 16-byte load
           // decides the match, the payload words come from the same sector (warp-uniform branch)
+          if (q == p.nprobes - 1) {
+            dq = q;
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+              const int32_t* e = reinterpret_cast<const int32_t*>(pd.slots) + (int64_t)hash_slot(kq[r], pd.hf) * pd.fstride;
+              const int2 x = ldg_nc(reinterpret_cast<const int2*>(valid[r] && !synth ? e : dz));
+              dkey[r] = kq[r];
+              dseen[r] = x.x;
+              drow[r] = x.y;
+              pb[r][q] = valid[r] && !synth ? e + 2 : dz;
+            }
+            continue;
+          }
 #pragma unroll
           for (int r = 0; r < R; ++r) {
             const int32_t* e = reinterpret_cast<const int32_t*>(pd.slots) + (int64_t)hash_slot(kq[r], pd.hf) * pd.fstride;
@@ -217,12 +235,6 @@ __device__ __forceinline__ void produce_batch(ProdState& st, const QueryParams& 
         }
       }
       if (t == 0) FLERN_TRACE(TR_P_PROBED, bidx);
-      if (p.dbg_match) {
-#pragma unroll
-        for (int r = 0; r < R; ++r)
-          if (in[r])
-            for (int q = 0; q < p.nprobes; ++q) p.dbg_match[(row0 + r) * p.nprobes + q] = brow[r][q];
-      }
       // 3. build-side loads (payload words of the matched rows), all issued before any use
 #pragma unroll
       for (int r = 0; r < R; ++r) {
@@ -233,6 +245,20 @@ __device__ __forceinline__ void produce_batch(ProdState& st, const QueryParams& 
 #pragma unroll
         for (int k = 0; k < K0P; ++k)
           if (k >= nfact && k < nfeat) v[k][r] = ld1((((dprobe1 >> k) & 1) ? rb1 : rb0) + p.dword[k], valid[r] && !synth);
+      }
+      if (dq >= 0) {   // resolve the late fat probe
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const bool hit = valid[r] && (dseen[r] == dkey[r] || synth);
+          brow[r][dq] = hit ? (synth ? 0 : drow[r]) : -1;
+          valid[r] = hit;
+        }
+      }
+      if (p.dbg_match) {
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+          if (in[r])
+            for (int q = 0; q < p.nprobes; ++q) p.dbg_match[(row0 + r) * p.nprobes + q] = brow[r][q];
       }
       if constexpr (BULK) {
 #pragma unroll
@@ -382,8 +408,8 @@ __device__ __forceinline__ void producer_loop(const QueryParams& p, const XRing&
   if (BULK && !p.pf_col) {
     // batches come from the loader warp's fact ring (loader_loop), which also claims the row chunks
     for (uint32_t b = 0;; ++b, ++bidx) {
-      const int f = b % kFactStages;
-      mbar_wait(&fr.full[f], (b / kFactStages) & 1, 6);
+      const int f = b % fr.stages;
+      mbar_wait(&fr.full[f], (b / fr.stages) & 1, 6);
       const int64_t srow0 = fr.hdr[2 * f];
       const int nrows = (int)fr.hdr[2 * f + 1];
       if (nrows < 0) break;
@@ -476,8 +502,8 @@ __device__ __forceinline__ void producer_loop(const QueryParams& p, const XRing&
       // the loader streams the filter column chunk by chunk into the fact ring (column slot 0):
       // the scan reads shared memory, HBM sees one bulk stream
       for (uint32_t b = 0;; ++b) {
-        const int f = b % kFactStages;
-        mbar_wait(&fr.full[f], (b / kFactStages) & 1, 8);
+        const int f = b % fr.stages;
+        mbar_wait(&fr.full[f], (b / fr.stages) & 1, 8);
         const int64_t cb = fr.hdr[2 * f];
         const int nrows = (int)fr.hdr[2 * f + 1];
         int32_t x[8] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -597,8 +623,8 @@ __device__ __forceinline__ void loader_loop(const QueryParams& p, const FactRing
   RowChunk cur = chunk_rows(p, s_claim[0]), nxt = chunk_rows(p, s_claim[1]);
   uint32_t b = 0;
   auto publish = [&](int64_t row0, int nrows) {
-    const int f = b % kFactStages;
-    mbar_wait(&fr.empty[f], ((b / kFactStages) & 1) ^ 1, 7);
+    const int f = b % fr.stages;
+    mbar_wait(&fr.empty[f], ((b / fr.stages) & 1) ^ 1, 7);
     if (lane == 0) {
       fr.hdr[2 * f] = row0;
       fr.hdr[2 * f + 1] = nrows;

@@ -28,7 +28,10 @@ namespace flern {
 template <int K0P, int H, int NL, int NCS = 0>
 struct SmemPlan {
   static constexpr uint32_t FSB = (uint32_t)NCS * batch_rows(K0P, NL, 32 * kProdWarps) * 4;   // one fact stage
-  static constexpr uint32_t FR = kFactStages * FSB + (NCS > 0 ? 64 : 0);                  // stages + headers
+  // per-warp tiles (PW, NL == 1 with 4 rows per producer thread): every producer warp may hold a stage
+  static constexpr bool PW = NCS > 0 && NL == 1 && 32 * rows_per_thread(K0P, NL) == kTile;
+  static constexpr int FST = (PW && FSB * 4 <= 120 * 1024) ? 4 : kFactStages;   // fact stages (slack between warps)
+  static constexpr uint32_t FR = FST * FSB + (NCS > 0 ? 64 : 0);                  // stages + headers
   static constexpr uint32_t WH = (NL >= 2) ? (uint32_t)H * H * 2 : 0;         // hidden->hidden W, SW128
   static constexpr uint32_t HB = 0;   // the hidden activation lives in TMEM (TmemPlan::HT)
   static constexpr uint32_t W1 = (uint32_t)H * K0P * 2;                       // layer-1 W, interleave
@@ -38,8 +41,6 @@ struct SmemPlan {
   static constexpr uint32_t FIXED = WH + HB + W1 + kOnesBytes + NL * BB + H * 4 + kMaxGroups * 4 * 8 +
                                     queue_bytes(32 * kProdWarps) + kMaxFeat * 8 + 64 * 8 + kMiscBytes +
                                     2 * kTile * 4 + FR;
-  // per-warp tiles (PW, NL == 1 with 4 rows per producer thread): every producer warp may hold a stage
-  static constexpr bool PW = NCS > 0 && NL == 1 && 32 * rows_per_thread(K0P, NL) == kTile;
   static constexpr int S = (PW && FIXED + 8 * (XS + META) <= 232448) ? 8
                            : ((FIXED + 4 * (XS + META) <= 232448) ? 4 : 3);
   static constexpr uint32_t off_wh = 0;                                       // [Wh | W1] = weight image
@@ -62,7 +63,7 @@ struct SmemPlan {
 #endif
   static constexpr uint32_t off_part = off_misc + kMiscBytes;                 // [2][128] fp32 partial logits
   static constexpr uint32_t off_fring = off_part + 2 * kTile * 4;             // fact ring (NCS > 0)
-  static constexpr uint32_t off_fhdr = off_fring + kFactStages * FSB;
+  static constexpr uint32_t off_fhdr = off_fring + FST * FSB;
   static constexpr uint32_t off_seq = off_fring + FR;
   static constexpr uint32_t total = off_seq + SEQB;
   static constexpr uint32_t wimg_bytes = WH + W1;                              // contiguous [Wh | W1]
@@ -162,7 +163,7 @@ __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_c
     if (tid == 0) { s_claim[0] = claim0; s_claim[1] = claim0 + 1; }
     fence_proxy_async_smem();   // weights written by st.shared are read by the tensor core
   }
-  static_assert(S <= 8 && kFactStages <= 4, "stage rings");
+  static_assert(S <= 8 && P::FST <= 4, "stage rings");
   uint32_t* s_ticket = reinterpret_cast<uint32_t*>(smem + P::off_misc + 176);   // PW stage tickets
   // per-warp tiles run on the bulk path without a pre-filter (the pre-filter path compacts across warps)
   const bool pw = P::PW && p.pf_col == nullptr;
@@ -173,7 +174,7 @@ __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_c
     mbar_init(d1empty, 4);
     for (int i = 0; i < 2; ++i) { mbar_init(&dfull[i], 1); mbar_init(&dempty[i], 4); }
     mbar_init(pready, 4);
-    for (int f = 0; f < kFactStages; ++f) { mbar_init(&ffull[f], 1); mbar_init(&fempty[f], kProdWarps); }
+    for (int f = 0; f < P::FST; ++f) { mbar_init(&ffull[f], 1); mbar_init(&fempty[f], kProdWarps); }
     for (int c = 0; c < 4; ++c) { mbar_init(&hfull[c], 4); mbar_init(&hfree[c], 1); }
     fence_mbar_init();
   }
@@ -191,7 +192,7 @@ __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_c
   FLERN_CTA_STAMP(TR_CTA_SETUP);
 
 
-  const FactRing fr{smem + P::off_fring, P::FSB, reinterpret_cast<int64_t*>(smem + P::off_fhdr), ffull, fempty};
+  const FactRing fr{smem + P::off_fring, P::FSB, reinterpret_cast<int64_t*>(smem + P::off_fhdr), ffull, fempty, P::FST};
   if (warp == 0) {
     // the fact loader (a few instructions per batch: leaves SMSP 0 to the MMA issuer)
     if constexpr (kBulk) {
