@@ -292,6 +292,15 @@ struct GroupAgg {
       return;
     }
     if (p.ngroups <= kFastGroups) {
+      if (!p.both_classes) {   // only selected rows aggregate: class 0 alone (half the predicated adds)
+#pragma unroll
+        for (int gg = 0; gg < kFastGroups; ++gg) {
+          const bool h0 = agg && g == gg;
+          fc[0][gg] += h0 ? 1u : 0u;
+          fs[0][gg] += h0 ? (long long)val : 0ll;
+        }
+        return;
+      }
 #pragma unroll
       for (int gg = 0; gg < kFastGroups; ++gg) {
         const bool h0 = agg && g == gg && cls == 0, h1 = agg && g == gg && cls == 1;

@@ -270,7 +270,8 @@ __device__ __forceinline__ void produce_batch(ProdState& st, const QueryParams& 
 #pragma unroll
       for (int r = 0; r < R; ++r)
 #pragma unroll
-        for (int k = 0; k < K0P; k += 2) pk[r][k / 2] = cvt_pair(k, v[k][r], v[k + 1][r]);
+        for (int k = 0; k < K0P; k += 2)   // padding pairs past a compile-time feature count are zero
+          pk[r][k / 2] = (kSpec && k >= SH::NF + SH::ND0 + SH::ND1) ? 0u : cvt_pair(k, v[k][r], v[k + 1][r]);
       if constexpr (BULK) features_read();
       if (t == 0) FLERN_TRACE(TR_P_GATHERED, bidx);
       // compaction: position of each surviving row in the batch (warp scan + per-warp counts)
