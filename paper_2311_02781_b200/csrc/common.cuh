@@ -268,6 +268,15 @@ struct GroupAgg {
 #pragma unroll
       for (int g = 0; g < kFastGroups; ++g) { fc[c][g] = 0u; fs[c][g] = 0ll; }
   }
+  template <int NG>
+  __device__ __forceinline__ void add_sel(bool agg, int g, int32_t val) {
+#pragma unroll
+    for (int gg = 0; gg < NG; ++gg) {
+      const bool h0 = agg && g == gg;
+      fc[0][gg] += h0 ? 1u : 0u;
+      fs[0][gg] += h0 ? (long long)val : 0ll;
+    }
+  }
   // releases the X stage (empty barrier) as soon as the metadata has been read
   __device__ __forceinline__ void tile(const QueryParams& p, const Meta& m, int count, int r, int lane, float logit,
                                        int64_t* s_cnt, uint64_t* empty_bar) {
@@ -293,12 +302,10 @@ struct GroupAgg {
     }
     if (p.ngroups <= kFastGroups) {
       if (!p.both_classes) {   // only selected rows aggregate: class 0 alone (half the predicated adds)
-#pragma unroll
-        for (int gg = 0; gg < kFastGroups; ++gg) {
-          const bool h0 = agg && g == gg;
-          fc[0][gg] += h0 ? 1u : 0u;
-          fs[0][gg] += h0 ? (long long)val : 0ll;
-        }
+        // predicated adds over the groups present only (warp-uniform choice of the unrolled width)
+        if (p.ngroups <= 4) add_sel<4>(agg, g, val);
+        else if (p.ngroups <= 6) add_sel<6>(agg, g, val);
+        else add_sel<kFastGroups>(agg, g, val);
         return;
       }
 #pragma unroll

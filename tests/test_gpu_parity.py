@@ -390,6 +390,19 @@ def test_large_group_domain(sf, both):
     parity.check(cfg, db, D.make_model(cfg, db), both=both)
 
 
+@pytest.mark.parametrize("col,G,both", [("l_returnflag", 3, False), ("l_shipmode", 7, False), ("l_linenumber", 8, False),
+                                         ("l_shipmode", 7, True), ("l_linenumber", 40, False)])
+@pytest.mark.parametrize("name", ["c1", "c2"])
+def test_small_group_domains(name, col, G, both):
+    """Every width of the per-thread group-by registers (<= 4, <= 6, <= 8 groups, one and two classes)
+    and the ballot path (9..64 groups): GROUP BY a small-domain fact column, exact against the oracle."""
+    import dataclasses
+    cfg = dataclasses.replace(D.with_sf(D.CONFIGS[name], 0.003, match_rate=0.9), group=("fact", col), ngroups=G)
+    db = D.make_database(cfg)
+    assert col in db.fact
+    parity.check(cfg, db, D.make_model(cfg, db), both=both)
+
+
 @pytest.mark.parametrize("name,sf", [("c4p", 0.05), ("c3", 0.01)])
 def test_streamed_query_prefilter_and_two_probes(name, sf):
     """flern_run_query_streamed over the pre-filter path (filter column windowed per chunk) and the
