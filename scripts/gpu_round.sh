@@ -21,3 +21,6 @@ tail -2 gpurun_out/ncu_c2_$TAG.log
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:flern_query_wide -s 4 -c 1 -o gpurun_out/prof_c3_$TAG -f \
   python bench.py --workload c3 --steps 3 --warmup 3 --no-cpu-baseline --e2e-steps 1 > gpurun_out/ncu_c3_$TAG.log 2>&1
 tail -2 gpurun_out/ncu_c3_$TAG.log
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:flern_query -s 4 -c 1 -o gpurun_out/prof_c1x_$TAG -f \
+  python bench.py --workload c1x --steps 3 --warmup 3 --no-cpu-baseline --e2e-steps 1 > gpurun_out/ncu_c1x_$TAG.log 2>&1
+tail -2 gpurun_out/ncu_c1x_$TAG.log

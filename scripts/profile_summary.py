@@ -44,8 +44,18 @@ ll = "\n".join(f"| {len(v)} | {sum(v) / len(v):,.0f} | {100 * sum(v) / tot:.1f}%
 b = json.loads(open(os.path.join(P, f"{tag}_bench_c2.json")).read())
 dr = float(re.search(r"DRAM read .*?\| ([0-9.]+) Mbyte", c2).group(1))
 dw = float(re.search(r"DRAM write .*?\| ([0-9.]+) Mbyte", c2).group(1))
-json.dump({"c2": (dr + dw) * 1e6, "_source": f"ncu --set full, profiles/{tag}_ncu_summary.md "
-           "(dram__bytes_read.sum + dram__bytes_write.sum, one launch)"}, open(os.path.join(P, "traffic.json"), "w"), indent=1)
+c1x = ""
+traffic = {"c2": (dr + dw) * 1e6}
+if os.path.exists(os.path.join(G, f"prof_c1x_{run}.ncu-rep")):
+    c1x = sh(f"python scripts/ncu_summary.py gpurun_out/prof_c1x_{run}.ncu-rep")
+    m1 = re.search(r"DRAM read .*?\| ([0-9.]+) ([MG])byte", c1x)
+    m2 = re.search(r"DRAM write .*?\| ([0-9.]+) ([MG])byte", c1x)
+    if m1 and m2:
+        sc = lambda m: float(m.group(1)) * (1e9 if m.group(2) == "G" else 1e6)
+        traffic["c1x"] = sc(m1) + sc(m2)
+traffic["_source"] = (f"ncu --set full, profiles/{tag}_ncu_summary.md "
+                      "(dram__bytes_read.sum + dram__bytes_write.sum, one launch)")
+json.dump(traffic, open(os.path.join(P, "traffic.json"), "w"), indent=1)
 x3 = d3.get("l1tex__m_xbar2l1tex_read_bytes.sum", ("", "?"))
 x3s = d3.get("l1tex__m_xbar2l1tex_read_bytes.sum.per_second", ("", "?"))
 md = f"""# {tag} — ncu evidence for the bench lines (`profiles/{tag}_bench_*.json`)
@@ -91,6 +101,12 @@ leg, `flern_run_query_streamed`). Bench: {b['roofline']['avg_launch_ms'] * 1e3:.
 - L2 → SM traffic {x3[1]} {x3[0]} per launch ({x3s[1]} {x3s[0]}): each 128-row tile re-streams 4 MB of
   weights and reads its activations four times; with the power cap (≈1.7 GHz) this bounds the kernel near
   70% of the sustained bf16 peak (DESIGN.md §12).
+
+## C1x query kernel (`--set full`, the HBM-bound supplementary row: C1 shape at SF10)
+
+{c1x if c1x else "(not captured in this run)"}
+- Compulsory DRAM bytes: 1,680 MB of fact columns plus the build entries the sorted probe stream touches
+  (15 M orders × 32 B) ≈ 2.16 GB per launch.
 
 ## SASS evidence (tcgen05 / TMEM / TMA)
 
