@@ -24,3 +24,12 @@ tail -2 gpurun_out/ncu_c3_$TAG.log
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:flern_query -s 4 -c 1 -o gpurun_out/prof_c1x_$TAG -f \
   python bench.py --workload c1x --steps 3 --warmup 3 --no-cpu-baseline --e2e-steps 1 > gpurun_out/ncu_c1x_$TAG.log 2>&1
 tail -2 gpurun_out/ncu_c1x_$TAG.log
+# the reports (~27 MB each) exceed gpurun's 64 MiB copy-back together: extract what profile_summary.py
+# reads into text on the box, keep the C2 report only
+for w in c2 c3 c1x; do
+  [ -f gpurun_out/prof_${w}_$TAG.ncu-rep ] && python scripts/ncu_summary.py gpurun_out/prof_${w}_$TAG.ncu-rep > gpurun_out/ncusum_${w}_$TAG.md
+done
+ncu -i gpurun_out/prof_c3_$TAG.ncu-rep --page raw --csv > gpurun_out/raw_c3_$TAG.csv 2>/dev/null
+ncu -i gpurun_out/prof_c2_$TAG.ncu-rep --page source --csv --print-source cuda,sass > /tmp/_src.csv 2>/dev/null
+python scripts/ncu_roles.py /tmp/_src.csv 3 > gpurun_out/roles_c2_$TAG.txt
+rm -f gpurun_out/prof_c3_$TAG.ncu-rep gpurun_out/prof_c1x_$TAG.ncu-rep

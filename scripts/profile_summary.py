@@ -17,11 +17,17 @@ def sh(cmd):
     return subprocess.run(cmd, shell=True, capture_output=True, text=True, cwd=ROOT).stdout
 
 
-c2 = sh(f"python scripts/ncu_summary.py gpurun_out/prof_c2_{run}.ncu-rep")
-c3 = sh(f"python scripts/ncu_summary.py gpurun_out/prof_c3_{run}.ncu-rep")
-sh(f"ncu -i gpurun_out/prof_c2_{run}.ncu-rep --page source --csv --print-source cuda,sass > /tmp/_src.csv")
-roles = sh("python scripts/ncu_roles.py /tmp/_src.csv 3")
-raw3 = list(csv.reader(sh(f"ncu -i gpurun_out/prof_c3_{run}.ncu-rep --page raw --csv").splitlines()))
+def extract(name, cmd):
+    """Text extracted on the box by gpu_round.sh (reports too large to copy back), else from the report."""
+    f = os.path.join(G, name)
+    return open(f).read() if os.path.exists(f) else sh(cmd)
+
+
+c2 = extract(f"ncusum_c2_{run}.md", f"python scripts/ncu_summary.py gpurun_out/prof_c2_{run}.ncu-rep")
+c3 = extract(f"ncusum_c3_{run}.md", f"python scripts/ncu_summary.py gpurun_out/prof_c3_{run}.ncu-rep")
+roles = extract(f"roles_c2_{run}.txt", f"ncu -i gpurun_out/prof_c2_{run}.ncu-rep --page source --csv "
+                f"--print-source cuda,sass > /tmp/_src.csv; python scripts/ncu_roles.py /tmp/_src.csv 3")
+raw3 = list(csv.reader(extract(f"raw_c3_{run}.csv", f"ncu -i gpurun_out/prof_c3_{run}.ncu-rep --page raw --csv").splitlines()))
 d3 = {k: (u, v) for k, u, v in zip(raw3[0], raw3[1], raw3[2])} if len(raw3) > 2 else {}
 rows = list(csv.reader(open(os.path.join(P, f"{tag}_launches_c2.csv"))))
 hdr, agg = None, collections.defaultdict(list)
@@ -46,8 +52,8 @@ dr = float(re.search(r"DRAM read .*?\| ([0-9.]+) Mbyte", c2).group(1))
 dw = float(re.search(r"DRAM write .*?\| ([0-9.]+) Mbyte", c2).group(1))
 c1x = ""
 traffic = {"c2": (dr + dw) * 1e6}
-if os.path.exists(os.path.join(G, f"prof_c1x_{run}.ncu-rep")):
-    c1x = sh(f"python scripts/ncu_summary.py gpurun_out/prof_c1x_{run}.ncu-rep")
+if os.path.exists(os.path.join(G, f"ncusum_c1x_{run}.md")) or os.path.exists(os.path.join(G, f"prof_c1x_{run}.ncu-rep")):
+    c1x = extract(f"ncusum_c1x_{run}.md", f"python scripts/ncu_summary.py gpurun_out/prof_c1x_{run}.ncu-rep")
     m1 = re.search(r"DRAM read .*?\| ([0-9.]+) ([MG])byte", c1x)
     m2 = re.search(r"DRAM write .*?\| ([0-9.]+) ([MG])byte", c1x)
     if m1 and m2:
