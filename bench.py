@@ -351,7 +351,7 @@ def main():
     if rank == 0:
         tf_peak, hbm_peak, peak_src = peaks()
         peak_kind = "burst"
-        fpr = flops_per_row(cfg.dims)
+        fpr = 0 if args.no_model else flops_per_row(cfg.dims)   # --no-model runs no MLP
         avg_kernel_ms = sum(kernel_ms) / len(kernel_ms)
         if avg_kernel_ms > 50.0:   # a launch this long runs under the power cap: the sustained figure
             tf_peak, peak_src = sustained_peak()
