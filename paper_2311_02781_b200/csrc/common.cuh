@@ -28,7 +28,13 @@ __host__ __device__ constexpr int batch_rows(int K0P, int NL, int npt) { return 
 // pre-filter scan chunk: 8 rows per producer thread (two 16-byte loads)
 __host__ __device__ constexpr int scan_rows(int npt) { return 8 * npt; }
 // survivor queue: pending (< one batch) + one scan chunk
-__host__ __device__ constexpr uint32_t queue_bytes(int npt) { return (uint32_t)(scan_rows(npt) + npt) * 4u; }
+// survivor queue: one scan chunk's survivors on top of a partial gather batch (up to 2 rows per thread)
+__host__ __device__ constexpr uint32_t queue_bytes(int npt) { return (uint32_t)(scan_rows(npt) + 2 * npt) * 4u; }
+// fact row ids of a gather batch (pre-filter survivors: arbitrary rows)
+template <int R>
+struct RowIds {
+  int64_t v[R];
+};
 // misc block: tmem slot @0, warp counts [3][8] @16, counters [4] @112, last-CTA flag @144, claims [2] @152
 constexpr uint32_t kMiscBytes = 192;
 constexpr int32_t kEmptyKey = (int32_t)0x80000000;         // INT32_MIN marks an empty slot

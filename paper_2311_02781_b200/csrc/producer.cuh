@@ -33,11 +33,19 @@ struct ProdState {
 // PW (per-warp tiles, 32 * R == kTile): each warp compacts its own 128 rows into a stage of its own
 // (a ticket from an SMEM counter fixes the stage order the consumers follow), so producer warps never
 // wait for each other; the stage may hold fewer than 128 rows (count in its metadata).
-template <int K0P, int S, int R, class SH, int NPW, bool BULK = false, bool PW = false, class FR = void (*)()>
+// GATHER: the R rows of this thread are arbitrary fact rows (*rid; pre-filter survivors), read with
+// scalar loads.
+template <int K0P, int S, int R, class SH, int NPW, bool BULK = false, bool PW = false, bool GATHER = false,
+          class FR = void (*)()>
 __device__ __forceinline__ void produce_batch(ProdState& st, const QueryParams& p, const XRing& ring, int32_t* wcnt,
                                               const float* s_normf, int64_t row0, bool whole, const bool (&in)[R],
                                               int bidx, int64_t row_end, int t, int warp, int lane,
-                                              uint32_t sfa = 0, int rel = 0, int nfull = 0, FR&& features_read = nullptr) {
+                                              uint32_t sfa = 0, int rel = 0, int nfull = 0, FR&& features_read = nullptr,
+                                              const RowIds<R>* rid = nullptr) {
+  auto rowv = [&](int r) -> int64_t {
+    if constexpr (GATHER) return rid->v[r];
+    else return row0 + r;
+  };
   constexpr int kBR = 32 * NPW * R;
   constexpr bool kSpec = SH::NF >= 0;   // feature shape known at compile time
   const int nfact = kSpec ? SH::NF : p.nfact;
@@ -57,7 +65,10 @@ __device__ __forceinline__ void produce_batch(ProdState& st, const QueryParams& 
     auto ld1 = [&](const int32_t* ptr, bool need) -> int32_t { return ldg_nc(need ? ptr : dz); };
     // R rows of a column starting at row0 (vector path; the scalar tail handles a partial group)
     auto loadR = [&](const int32_t* col, int64_t row0, bool whole, bool need, int32_t (&v)[R]) {
-      if (R == 1 || whole) {
+      if constexpr (GATHER) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) v[r] = ld1(col + rid->v[r], need && in[r]);
+      } else if (R == 1 || whole) {
         if constexpr (R == 4) {
           const int4 x = ld4(col, row0, need);
           v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
@@ -258,7 +269,7 @@ __device__ __forceinline__ void produce_batch(ProdState& st, const QueryParams& 
 #pragma unroll
         for (int r = 0; r < R; ++r)
           if (in[r])
-            for (int q = 0; q < p.nprobes; ++q) p.dbg_match[(row0 + r) * p.nprobes + q] = brow[r][q];
+            for (int q = 0; q < p.nprobes; ++q) p.dbg_match[rowv(r) * p.nprobes + q] = brow[r][q];
       }
       if constexpr (BULK) {
 #pragma unroll
@@ -304,7 +315,7 @@ __device__ __forceinline__ void produce_batch(ProdState& st, const QueryParams& 
           for (int c8 = 0; c8 < K0P / 8; ++c8)
             st_shared_v4(smem_u32(xs + c8 * (kTile * 16) + (tp >> 3) * 128 + (tp & 7) * 16), pk[r][4 * c8],
                          pk[r][4 * c8 + 1], pk[r][4 * c8 + 2], pk[r][4 * c8 + 3]);
-          m.rowid[tp] = (int32_t)(row0 + r);
+          m.rowid[tp] = (int32_t)rowv(r);
           m.grp[tp] = (gv[r] >= 0 && gv[r] < p.ngroups) ? gv[r] : -1;
           m.val[tp] = sv[r];
           ++tp;
@@ -352,7 +363,7 @@ __device__ __forceinline__ void produce_batch(ProdState& st, const QueryParams& 
           for (int c8 = 0; c8 < K0P / 8; ++c8)
             st_shared_v4(smem_u32(xs + c8 * (kTile * 16) + (tp >> 3) * 128 + (tp & 7) * 16), pk[r][4 * c8],
                          pk[r][4 * c8 + 1], pk[r][4 * c8 + 2], pk[r][4 * c8 + 3]);
-          m.rowid[tp] = (int32_t)(row0 + r);
+          m.rowid[tp] = (int32_t)rowv(r);
           m.grp[tp] = (gv[r] >= 0 && gv[r] < p.ngroups) ? gv[r] : -1;
           m.val[tp] = sv[r];
         }
@@ -481,13 +492,22 @@ __device__ __forceinline__ void producer_loop(const QueryParams& p, const XRing&
           if (bits & (1u << (4 * j + u))) queue[pos++] = (int32_t)(cb + 4 * t + 4 * NPT * j + u);
       nq += total;
       named_bar_sync(1, NPT);   // queue written (and wcnt[16..] read) by all
-      while (nq >= NPT || (last && nq > 0)) {
-        const bool in1[1] = {t < nq};
-        const int64_t row = in1[0] ? (int64_t)queue[t] : 0;
+      // gather batches of RG survivors per thread (more rows in flight per batch: the survivors' loads
+      // are random-row round trips)
+      constexpr int RG = R >= 2 ? 2 : 1;
+      while (nq >= RG * NPT || (last && nq > 0)) {
+        bool inq[RG];
+        RowIds<RG> rid;
+#pragma unroll
+        for (int r = 0; r < RG; ++r) {
+          inq[r] = t + r * NPT < nq;
+          rid.v[r] = inq[r] ? (int64_t)queue[t + r * NPT] : 0;
+        }
         if (t == 0) FLERN_TRACE(TR_P_START, bidx);
-        produce_batch<K0P, S, 1, SH, NPW>(st, p, ring, wcnt, s_normf, row, true, in1, bidx, n, t, warp, lane);
+        produce_batch<K0P, S, RG, SH, NPW, false, false, true>(st, p, ring, wcnt, s_normf, 0, true, inq, bidx, n, t, warp,
+                                                               lane, 0u, 0, 0, nullptr, &rid);
         ++bidx;
-        const int taken = min(nq, NPT);
+        const int taken = min(nq, RG * NPT);
         // shift the rest of the queue to the front
         int32_t keep[kQueueCap / NPT + 1];
         int nk = 0;
