@@ -186,12 +186,14 @@ def test_bad_group_code_is_reported():
 
 # ---------------------------------------------------------------------------------- full size
 @pytest.mark.slow
-def test_c2_full_size_sampled():
-    """Config 2 at its full size (SF1, 6.0M rows) in the launch configuration bench.py times:
-    join ids, scores and selection on sampled row ranges against the oracle; aggregates at
-    -INF and with the linear-threshold model exact at full size."""
+@pytest.mark.parametrize("name,sf", [("c2", 1.0), ("c1", 10.0)])
+def test_c2_full_size_sampled(name, sf):
+    """Config 2 at its full size (SF1, 6.0M rows), and the C1 shape at SF10 (bench's c1x row, 60M
+    rows, per-warp tiles), in the launch configuration bench.py times: join ids, scores and selection on
+    sampled row ranges against the oracle; aggregates at -INF and with the linear-threshold model exact
+    at full size."""
     from paper_2311_02781_b200.session import GpuQuery
-    cfg = D.CONFIGS["c2"]
+    cfg = D.with_sf(D.CONFIGS[name], sf)
     db = D.make_database(cfg)
     model = D.make_model(cfg, db)
     gq = GpuQuery(cfg, db, model)
