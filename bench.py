@@ -47,6 +47,20 @@ def flops_per_row(dims):
     return 2 * sum(dims[i] * dims[i + 1] for i in range(len(dims) - 1))
 
 
+def binding_roofline(flops_per_row, rows, alg_bytes, launch_ms, tf_peak, hbm_peak, tf_src="", hbm_src=""):
+    """Both rooflines of one launch; the binding one (longer algorithmic time at peak) comes first."""
+    s = launch_ms / 1e3
+    tf = flops_per_row * rows / s / 1e12
+    gb = alg_bytes / s / 1e9
+    tensor_rf = {"bound": "tensor", "achieved": tf, "peak": tf_peak, "unit": "TFLOP/s", "frac": tf / tf_peak,
+                 "flops_per_row": flops_per_row, "peak_source": tf_src}
+    hbm_rf = {"bound": "hbm", "achieved": gb, "peak": hbm_peak, "unit": "GB/s", "frac": gb / hbm_peak,
+              "alg_bytes_per_launch": alg_bytes, "peak_source": hbm_src}
+    t_tensor = flops_per_row * rows / (tf_peak * 1e12)
+    t_hbm = alg_bytes / (hbm_peak * 1e9)
+    return (tensor_rf, hbm_rf) if t_tensor >= t_hbm else (hbm_rf, tensor_rf)
+
+
 def workload_cfg(name, world):
     if name == "c2":
         base, sf1 = D.CONFIGS["c2"], 1.0
@@ -356,7 +370,6 @@ def main():
         if avg_kernel_ms > 50.0:   # a launch this long runs under the power cap: the sustained figure
             tf_peak, peak_src = sustained_peak()
             peak_kind = "sustained"
-        achieved = fpr * rows_scored_rank / (avg_kernel_ms / 1e3) / 1e12
         # algorithmic HBM bytes per launch: every staged fact column once; with a
         # pre-filter, the filter column for every row plus the other columns of the scored rows only
         # (build side and weights not counted: a lower bound, so `achieved` is conservative)
@@ -366,17 +379,8 @@ def main():
             alg_bytes = 4 * db.fact_n + other * rows_scored_rank
         else:
             alg_bytes = h2d
-        hbm_achieved = alg_bytes / (avg_kernel_ms / 1e3) / 1e9
-        tensor_rf = {"bound": "tensor", "achieved": achieved, "peak": tf_peak, "unit": "TFLOP/s",
-                     "frac": achieved / tf_peak, "flops_per_row": fpr,
-                     "peak_source": f"{peak_src} ({peak_kind})"}
-        hbm_rf = {"bound": "hbm", "achieved": hbm_achieved, "peak": hbm_peak, "unit": "GB/s",
-                  "frac": hbm_achieved / hbm_peak, "alg_bytes_per_launch": alg_bytes,
-                  "peak_source": f"{peak_src} (copy bandwidth)"}
-        # the binding roofline is the one whose algorithmic time at peak is longer
-        t_tensor = fpr * rows_scored_rank / (tf_peak * 1e12)
-        t_hbm = alg_bytes / (hbm_peak * 1e9)
-        primary, secondary = (tensor_rf, hbm_rf) if t_tensor >= t_hbm else (hbm_rf, tensor_rf)
+        primary, secondary = binding_roofline(fpr, rows_scored_rank, alg_bytes, avg_kernel_ms, tf_peak, hbm_peak,
+                                              f"{peak_src} ({peak_kind})", f"{peak_src} (copy bandwidth)")
         traffic = None
         tp = os.path.join(ROOT, "profiles", "traffic.json")
         if os.path.exists(tp):
