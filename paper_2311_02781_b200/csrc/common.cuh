@@ -310,6 +310,7 @@ struct GroupAgg {
       if (!p.both_classes) {   // only selected rows aggregate: class 0 alone (half the predicated adds)
         // predicated adds over the groups present only (warp-uniform choice of the unrolled width)
         if (p.ngroups <= 4) add_sel<4>(agg, g, val);
+        else if (p.ngroups == 5) add_sel<5>(agg, g, val);   // the 5 order priorities
         else if (p.ngroups <= 6) add_sel<6>(agg, g, val);
         else add_sel<kFastGroups>(agg, g, val);
         return;
