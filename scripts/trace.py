@@ -62,6 +62,9 @@ if n:
           f"{(su - st).max() / 1e3:.1f} us; loop end min/median/max "
           f"{(le.min() - z) / 1e3:.1f}/{np.median(le - z) / 1e3:.1f}/{(le.max() - z) / 1e3:.1f} us; "
           f"last exit {(ex.max() - z) / 1e3:.1f} us; kernel (events) {r.elapsed_ms * 1e3:.1f} us")
+    te = (ex - le) / 1e3
+    print(f"  teardown (exit - loop end) us: min {te.min():.1f} median {np.median(te):.1f} max {te.max():.1f}; "
+          f"last CTA to exit: {int(np.argmax(ex))} (loop end {(le[np.argmax(ex)] - z) / 1e3:.1f} us)")
     order = np.argsort(le - st)
     print("  slowest CTAs (loop us):", [(int(i), round(float(le[i] - st[i]) / 1e3, 1)) for i in order[-6:]])
     print("  fastest CTAs (loop us):", [(int(i), round(float(le[i] - st[i]) / 1e3, 1)) for i in order[:6]])
