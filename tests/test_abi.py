@@ -62,3 +62,14 @@ def test_no_gpu_means_error_not_fallback():
     from paper_2311_02781_b200 import flern as F
     with pytest.raises(F.FlernError):
         F.flern_create(0)
+
+
+def test_missing_library_fails_loudly():
+    """Without the built library the binding refuses to import: there is no fallback path."""
+    import subprocess
+    import sys
+    env = dict(os.environ, FLERN_LIB="libflern_does_not_exist.so")
+    r = subprocess.run([sys.executable, "-c", "import paper_2311_02781_b200.flern"], cwd=ROOT, env=env,
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode != 0
+    assert "ImportError" in r.stderr and "libflern_does_not_exist.so is missing" in r.stderr

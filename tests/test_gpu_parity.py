@@ -106,6 +106,18 @@ def test_ragged_sizes(nfact):
     assert r["gpu"]["rows_scanned"] == nfact
 
 
+@pytest.mark.parametrize("name", ["c2", "c3", "c4p"])
+@pytest.mark.parametrize("nfact", [0, 1, 129, 255, 4_097])
+def test_ragged_sizes_other_kernels(name, nfact):
+    """Ragged fact sizes (empty, one row, a partial tile, a partial last batch) on the two-hidden-layer
+    narrow kernel (C2, the bench's), the wide kernel (C3) and the pre-filter path (C4p)."""
+    cfg = D.with_sf(D.CONFIGS[name], 0.002)
+    db = _custom_db(cfg, nfact, seed=nfact + 11)
+    model = D.make_model(cfg, D.make_database(cfg))
+    r = parity.check(cfg, db, model)
+    assert r["gpu"]["rows_scanned"] == nfact
+
+
 @pytest.mark.parametrize("name,miss", [("c2", 1.0), ("c1", 1.0), ("c1", 0.97)])
 def test_all_probes_miss(name, miss):
     """Every (or nearly every) probe misses: empty tiles never reach the MLP; with per-warp tiles (C1)
