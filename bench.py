@@ -171,8 +171,11 @@ class ClockSampler:
                 "reasons": sorted(self.reasons), "samples": len(self.samples), "source": "nvml"}
 
 
-def cpu_baseline(cfg, db, model, seconds=15.0):
-    """The oracle, as it stands, on the host's cores: a bounded prefix of this workload."""
+def cpu_baseline(cfg, db, model, seconds=25.0):
+    """The oracle, as it stands, on the host's cores: a bounded prefix of this workload.
+
+    The sample is sized from a short first pass, which runs slower per row than the long one (thread
+    start-up, cold caches), so a 25 s target lands at ~10-15 s of oracle work."""
     import oracle as O
     threads = os.cpu_count() or 1
     probe = min(db.fact_n, 2000 * threads)
