@@ -93,7 +93,7 @@ leg, `flern_run_query_streamed`). Bench: {b['roofline']['avg_launch_ms'] * 1e3:.
 - DRAM traffic {dr + dw:.0f} MB per launch: the 312 MB of fact columns plus the touched build entries
   (1.5 M × 32 B): no re-reads; ≈7% of HBM bandwidth — the kernel is not memory-bound.
 - Roofline (bench line): 139,776 flop/row × 6,002,157 rows ÷ {b['roofline']['avg_launch_ms']:.4f} ms =
-  **{b['roofline']['achieved']:.0f} TFLOP/s = {100 * b['roofline']['frac']:.1f}% of 1,677** (measured bf16 burst peak).
+  **{b['roofline']['achieved']:.0f} TFLOP/s = {100 * b['roofline']['frac']:.1f}% of {b['roofline']['peak']:,}** (bf16 burst peak, {b['roofline'].get('peak_source', '')}).
 
 ### Warp-stall samples by role (`scripts/ncu_roles.py`)
 
