@@ -511,10 +511,9 @@ __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_c
           tc_fence_after();
           float2 acc4[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
                             make_float2(0.f, 0.f)};
-          dot_cols(wg * H, H, 0, acc4, [] {});
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&dempty[wg]);
+          // D[wg] is released as soon as its last columns are in registers (before the last
+          // chunk's math), so the MMA of tile t + 2 can start earlier
+          dot_cols(wg * H, H, 0, acc4, release(&dempty[wg]));
           logit = dot_sum(acc4) + p.bout;
         }
         finish_tile(m, count, s, logit);
