@@ -26,6 +26,12 @@ $(PKG)/lib/libflern.so: $(KERNEL_SRCS) $(KERNEL_HDRS)
 	$(NVCC) $(NVFLAGS) -shared -o $@ $(KERNEL_SRCS) 2> build/ptxas.log || (cat build/ptxas.log; exit 1)
 	@grep -E "error|spill|Used" build/ptxas.log | grep -v " 0 bytes spill" | head -40 || true
 
+# diagnostic variant: reads the FLERN_DBG_* / FLERN_NO_* / FLERN_WAIT_HINT A/B knobs from the environment
+# (scripts/ab_env.sh runs with FLERN_LIB=libflern_diag.so); the release library never reads the environment
+$(PKG)/lib/libflern_diag.so: $(KERNEL_SRCS) $(KERNEL_HDRS)
+	@mkdir -p $(PKG)/lib build
+	$(NVCC) $(NVFLAGS) -DFLERN_DIAG -shared -o $@ $(KERNEL_SRCS) 2> build/ptxas_diag.log || (cat build/ptxas_diag.log; exit 1)
+
 # diagnostic variant: per-role mbarrier wait accounting (scripts/trace.py)
 $(PKG)/lib/libflern_tw.so: $(KERNEL_SRCS) $(KERNEL_HDRS)
 	@mkdir -p $(PKG)/lib build

@@ -205,7 +205,7 @@ def run_reference(args):
     import oracle as O
     cfg, sf1 = workload_cfg(args.workload, world)
     db = D.make_database(cfg, rank=0, world=world)
-    model = D.make_model(cfg, db)
+    model = D.make_model(cfg, D.make_database(cfg, max_slots=D.MODEL_SLOTS))
     threads = os.cpu_count() or 1
     # bounded sample per step: ~ (budget / (W+K)) seconds of oracle work each
     probe = min(db.fact_n, 1000 * threads)
@@ -270,7 +270,8 @@ def main():
 
     cfg, sf1 = workload_cfg(args.workload, world)
     db = D.make_database(cfg, rank=rank, world=world)
-    model = D.make_model(cfg, db)
+    # one model for every rank (replicated weights): normalisation from the first rows of the unsharded table
+    model = D.make_model(cfg, D.make_database(cfg, max_slots=D.MODEL_SLOTS))
     # fact shard resident in HBM (torch tensors borrowed by the library, no copy)
     fact_dev = {k: torch.from_numpy(v).to(f"cuda:{local}") for k, v in db.fact.items()}
     gq = GpuQuery(cfg, db, model, device=local, stream=stream.cuda_stream, load_fact=False)
@@ -334,13 +335,13 @@ def main():
     d2h = 2 * G * 8 + 4 * 8
 
     verbose = bool(os.environ.get("FLERN_E2E_VERBOSE"))
-    # the e2e table is allocated once (flern_load_table); every step streams the shard into it from
-    # pinned host memory (the step's H2D), runs the query and reads the result back (D2H)
-    e2e_tid = F.flern_load_table(gq.ctx, "fact_e2e", pinned, F.FLERN_COPY_HOST)
+    # every step streams the shard from pinned host memory (the step's H2D) through the library's ring of
+    # device chunk buffers, runs the query chunk by chunk and reads the result back (D2H); the e2e fact
+    # table is a schema with no rows (flern_run_query_streamed)
+    e2e_tid = F.flern_load_table(gq.ctx, "fact_e2e", {k: np.zeros(0, v.dtype) for k, v in db.fact.items()})
     e2e_q = gq.make_query(e2e_tid)
 
-    # the fact shard streams from pinned host memory in 8 chunks: each chunk's H2D copy (second
-    # stream) overlaps the previous chunk's query (flern_run_query_streamed, the paper's §3.2)
+    # 8 chunks: each chunk's H2D copy (second stream) overlaps the previous chunk's query (the paper's §3.2)
     chunk = max(4, (db.fact_n + 7) // 8)
 
     def e2e_step():

@@ -281,6 +281,12 @@ def calibration():
     return {}
 
 
+# Order slots of the prefix database a model's normalisation is drawn from: make_model(cfg,
+# make_database(cfg, max_slots=MODEL_SLOTS)) gives every rank of a sharded run the model of the unsharded
+# table (its first 65,536 fact rows and build rows; a slot holds 1-7 lines).
+MODEL_SLOTS = 65536
+
+
 def feature_stats(db: Database, cfg: QueryConfig, nsample: int = 65536):
     shift = np.zeros(len(cfg.feats), np.float32)
     scale = np.ones(len(cfg.feats), np.float32)

@@ -110,9 +110,13 @@ FLERN_API flern_status flern_drop_table(flern_ctx* ctx, int32_t table_id);
  *   in_shift/in_scale: host fp32 [dims[0]] per-feature normalisation applied in fp32 in the
  *   gather, x = (v - shift) * scale, before the bf16 rounding (reading Q4).
  * Everything is copied; the caller may free its arrays on return. Writes *model_id.
- * Supported shapes (this build): dims[0] <= 48; 1 or 2 hidden layers; hidden width a multiple
- * of 16 in [16, 256] (equal widths); others -> FLERN_E_UNSUPPORTED. Errors: FLERN_E_SHAPE,
- * FLERN_E_DUPLICATE, FLERN_E_INVALID_ARG (NULL / non-finite weights). */
+ * Supported shapes (this build; equal hidden widths, dims[0] <= 48):
+ *   on-chip MLP kernel: 1 hidden layer of 64 / 128 / 256; 2 hidden layers of 64 / 128, or of 256
+ *     with dims[0] <= 16;
+ *   streamed-weight kernel: 2 hidden layers of 512 (dims[0] <= 32) or 1024; 3 hidden layers of 1024.
+ * (the list of compiled kernels, FLERN_KERNELS / FLERN_WIDE_KERNELS in flern_api.cu)
+ * Others -> FLERN_E_UNSUPPORTED. Errors: FLERN_E_SHAPE, FLERN_E_DUPLICATE, FLERN_E_INVALID_ARG
+ * (NULL / non-finite weights). */
 FLERN_API flern_status flern_load_model(flern_ctx* ctx, const char* name, int32_t nlayers, const int32_t* dims,
                                         const float* const* W, const float* const* b, const float* in_shift,
                                         const float* in_scale, int32_t* model_id);
@@ -122,7 +126,8 @@ FLERN_API flern_status flern_load_model(flern_ctx* ctx, const char* name, int32_
  * table (power-of-two capacity >= 2*nrows, linear probing) mapping key_col -> build row, plus a
  * row-major payload of `payload_cols` (the build columns the query later uses as features,
  * group key, sum column or the key of a chained probe). key_col must be integer-typed and
- * != INT32_MIN. Errors: FLERN_E_DUP_KEY (key not unique), FLERN_E_NOT_FOUND, FLERN_E_TYPE.
+ * != INT32_MIN (the empty-slot marker: FLERN_E_INVALID_ARG); a probe key equal to INT32_MIN simply
+ * finds no match. Errors: FLERN_E_DUP_KEY (key not unique), FLERN_E_NOT_FOUND, FLERN_E_TYPE.
  * Synchronous. Writes *ht_id. */
 FLERN_API flern_status flern_build_hashtable(flern_ctx* ctx, int32_t table_id, const char* key_col,
                                              int32_t npayload, const char* const* payload_cols, int32_t* ht_id);
@@ -163,8 +168,10 @@ enum {
                                   and elapsed_ms are not filled (read `counters` instead) */
   FLERN_Q_BOTH_CLASSES = 0x4,  /* count/sum hold [2][ngroups]: [0] score > t, [1] joined rows with score <= t
                                   (the CASE WHEN sentiment < 0.5 / >= 0.5 query of P:1346-1354) */
-  FLERN_Q_NO_MODEL = 0x8       /* diagnostic: skip the MLP and select every joined row (measures the
+  FLERN_Q_NO_MODEL = 0x8,      /* diagnostic: skip the MLP and select every joined row (measures the
                                   scan -> probe -> gather -> aggregate part alone) */
+  FLERN_Q_GENERIC_KERNEL = 0x10 /* testing: run the kernel whose producer reads the feature shape at run
+                                  time instead of one specialised for it (same results, slower) */
 };
 
 typedef struct {
@@ -186,14 +193,21 @@ typedef struct {
  * and counted in counters[3]. */
 FLERN_API flern_status flern_run_query(flern_ctx* ctx, const flern_query* q, flern_result* res);
 
-/* Run `q` over `nrows` fact rows streamed from host memory (pinned for full PCIe speed), the
- * host-resident-fact optimisation of the paper's GPU data movement (§3.2): the rows are
- * copied into the fact table's own device columns (as flern_update_table) in chunks of `chunk_rows`
- * (rounded up to a multiple of 4) on a second stream, and each chunk's query launch waits only for
- * its own copy, so copies and queries overlap. `host_cols` names columns of q->fact_table (a COPY
- * table with capacity >= nrows); aggregates are summed over the chunks (int64, exact). Host results
- * only (no FLERN_Q_ASYNC / FLERN_Q_RESULT_DEVICE, no debug exports); synchronous.
- * Errors: as flern_update_table and flern_run_query. */
+/* Run `q` over `nrows` fact rows streamed from host memory (pinned for full PCIe speed): the
+ * host-resident-fact optimisation of the paper's GPU data movement (§3.2; pinned buffers +
+ * cudaMemcpyAsync overlapped with compute). The rows go through a ring of 3 device chunk
+ * buffers of `chunk_rows` rows (rounded up to a multiple of 4) owned by the context: chunk c is copied
+ * into slot c % 3 on a second stream and its query launch waits only for that copy, while the slot's
+ * next copy waits for the launch that read it. So copies and queries overlap and the device footprint
+ * is 3 * chunk_rows * ncols * 4 bytes whatever `nrows` is: fact tables larger than HBM stream through.
+ * q->fact_table supplies the schema only (it may hold 0 rows; its own rows are neither read nor
+ * changed). `host_cols` names columns of that table (same dtypes, each at most once) and must include
+ * every fact column the query reads; host_cols[i].data holds `nrows` values. Aggregates are summed over
+ * the chunks (int64, exact). Host results only (no FLERN_Q_ASYNC / FLERN_Q_RESULT_DEVICE, no debug
+ * exports, <= 64 groups); synchronous. Every check happens before the first copy.
+ * Errors: FLERN_E_NOT_FOUND (unknown table / column, or a column the query reads is not streamed),
+ * FLERN_E_TYPE, FLERN_E_DUPLICATE, FLERN_E_INVALID_ARG, FLERN_E_OOM, FLERN_E_CUDA and those of
+ * flern_run_query. */
 FLERN_API flern_status flern_run_query_streamed(flern_ctx* ctx, const flern_query* q, int64_t nrows, int32_t ncols,
                                                 const flern_column* host_cols, int64_t chunk_rows, flern_result* res);
 

@@ -68,11 +68,13 @@ __global__ void pack_payload_kernel(const __grid_constant__ PayloadCols cols, in
 // {key, build row, payload words...}, fs words (8 = one 32-byte sector, or 16). A probe reads the
 // entry's first 16 bytes (key check) and the payload words from the same sector(s): one dependent
 // global access per probe instead of slot -> payload row.
+// Empty entry: {kEmptyKey, -1, 0...}. The payload words are zeroed too: a probe reads them before it
+// knows whether the key matched (late resolution), so they must be defined.
 __global__ void fill_fat_kernel(int32_t* e, int64_t cap, int32_t fs) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < cap; i += (int64_t)gridDim.x * blockDim.x) {
-    e[i * fs] = kEmptyKey;
-    e[i * fs + 1] = -1;
-  }
+  const int64_t n4 = cap * fs / 4;   // 16-byte stores; fs is 8 or 16
+  int4* e4 = reinterpret_cast<int4*>(e);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x)
+    e4[i] = (i % (fs / 4)) == 0 ? make_int4(kEmptyKey, -1, 0, 0) : make_int4(0, 0, 0, 0);
 }
 __global__ void build_fat_kernel(const int32_t* __restrict__ keys, int64_t nrows, int32_t* __restrict__ e, HashFn hf,
                                  int32_t fs, const __grid_constant__ PayloadCols cols, int32_t npay,

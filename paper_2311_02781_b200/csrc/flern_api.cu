@@ -21,6 +21,8 @@ using namespace flern;
 
 namespace {
 
+constexpr int kRingSlots = 3;   // flern_run_query_streamed: device chunk buffers in the ring
+
 struct Column {
   std::string name;
   flern_dtype dtype;
@@ -72,6 +74,18 @@ struct HashTable {
   }
 };
 
+// Diagnostic knobs (kernel-variant A/B tests in scripts/) are read from the environment only in the
+// diagnostic build (make paper_2311_02781_b200/lib/libflern_diag.so, -DFLERN_DIAG); the release library
+// never looks at the environment, so no stray variable can change its results or code paths.
+const char* diag_env(const char* name) {
+#ifdef FLERN_DIAG
+  return getenv(name);
+#else
+  (void)name;
+  return nullptr;
+#endif
+}
+
 bool is_int_type(flern_dtype t) { return t == FLERN_I32 || t == FLERN_DATE32 || t == FLERN_DEC32 || t == FLERN_DICT32; }
 bool is_valid_type(int t) { return t >= FLERN_I32 && t <= FLERN_DICT32; }
 
@@ -96,11 +110,12 @@ struct flern_ctx {
   uint8_t* scratch = nullptr;     // wide kernel activation scratch (grown on demand)
   size_t scratch_bytes = 0;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-  // flern_run_query_streamed: row window of the fact table the next launch covers, a copy stream,
-  // per-chunk copy events and per-chunk device result slots
-  int64_t win_lo = 0, win_n = -1;
+  // flern_run_query_streamed: a ring of device chunk buffers the host rows stream through, a copy
+  // stream, per-slot events (copy done / query done) and per-chunk device result slots
   cudaStream_t copy_stream = nullptr;
-  std::vector<cudaEvent_t> chunk_ev;
+  uint8_t* ring = nullptr;
+  size_t ring_bytes = 0;
+  std::vector<cudaEvent_t> ring_copied, ring_read;
   int64_t* chunk_res = nullptr;
   size_t chunk_res_slots = 0;
   // host-side results of large group domains (> kMaxGroups): [count | sum] device buffer
@@ -203,7 +218,7 @@ KernelEntry g_kernels[] = {FLERN_KERNELS(FLERN_ENTRY) FLERN_WIDE_KERNELS(FLERN_W
 FLERN_KERNELS(FLERN_FITS)
 
 KernelEntry* find_kernel(int K0P, int H, int NL, int nf = -1, int nd0 = -1, int nd1 = -1, uint64_t fm = 0) {
-  if (nf >= 0 && !getenv("FLERN_GENERIC_ONLY"))
+  if (nf >= 0)
     for (auto& e : g_kernels)   // a producer specialised for exactly this feature shape
       if (e.K0P == K0P && e.H == H && e.NL == NL && e.nf == nf && e.nd0 == nd0 && e.nd1 == nd1 && e.fm == fm) return &e;
   for (auto& e : g_kernels)
@@ -249,7 +264,7 @@ extern "C" FLERN_API flern_status flern_create(int device, void* cuda_stream, fl
   if (cudaMemsetAsync(ctx->ticket, 0, 64, ctx->stream) != cudaSuccess) return FLERN_E_CUDA;
   // let the build side of the join persist in L2 while the fact table streams through
   if (ctx->persist_max > 0) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, ctx->persist_max);
-  if (const char* wh = getenv("FLERN_WAIT_HINT")) {   // tuning knob (see c_wait_hint)
+  if (const char* wh = diag_env("FLERN_WAIT_HINT")) {   // tuning knob (see c_wait_hint)
     const uint32_t v = (uint32_t)strtoul(wh, nullptr, 0);
     if (cudaMemcpyToSymbol(c_wait_hint, &v, sizeof(v)) != cudaSuccess) return FLERN_E_CUDA;
   }
@@ -271,8 +286,10 @@ extern "C" FLERN_API void flern_destroy(flern_ctx* ctx) {
     for (auto& kv : m.permuted) cudaFree(kv.second);
   }
   for (auto& h : ctx->hts) cudaFree(h.slots);
-  for (auto e : ctx->chunk_ev) cudaEventDestroy(e);
+  for (auto e : ctx->ring_copied) cudaEventDestroy(e);
+  for (auto e : ctx->ring_read) cudaEventDestroy(e);
   if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
+  cudaFree(ctx->ring);
   cudaFree(ctx->chunk_res);
   cudaFree(ctx->big_res);
   cudaFree(ctx->partials);
@@ -409,108 +426,6 @@ extern "C" FLERN_API flern_status flern_update_table(flern_ctx* ctx, int32_t tab
   return FLERN_OK;
 }
 
-extern "C" FLERN_API flern_status flern_run_query_streamed(flern_ctx* ctx, const flern_query* q, int64_t nrows,
-                                                           int32_t ncols, const flern_column* host_cols,
-                                                           int64_t chunk_rows, flern_result* res) {
-  if (!ctx) return FLERN_E_INVALID_ARG;
-  if (!q || !res || !res->count || !res->sum)
-    return fail(ctx, FLERN_E_INVALID_ARG, "flern_run_query_streamed: null query or result");
-  if (q->flags & (FLERN_Q_ASYNC | FLERN_Q_RESULT_DEVICE))
-    return fail(ctx, FLERN_E_INVALID_ARG, "flern_run_query_streamed: host results only (no ASYNC / RESULT_DEVICE)");
-  if (q->fact_table < 0 || q->fact_table >= (int32_t)ctx->tables.size() || !ctx->tables[q->fact_table].alive)
-    return fail(ctx, FLERN_E_NOT_FOUND, "no fact table with id %d", q->fact_table);
-  Table& t = ctx->tables[q->fact_table];
-  if (nrows < 0 || nrows > t.capacity)
-    return fail(ctx, FLERN_E_INVALID_ARG, "flern_run_query_streamed: %lld rows exceed table '%s''s %lld-row capacity",
-                (long long)nrows, t.name.c_str(), (long long)t.capacity);
-  if (chunk_rows <= 0) return fail(ctx, FLERN_E_INVALID_ARG, "flern_run_query_streamed: chunk_rows must be > 0");
-  chunk_rows = (chunk_rows + 3) & ~3ll;   // chunk starts stay 16-byte aligned (vector loads, bulk copies)
-  if (!host_cols || ncols <= 0) return fail(ctx, FLERN_E_INVALID_ARG, "flern_run_query_streamed: no columns");
-  std::vector<int> slot(ncols, -1);
-  for (int32_t i = 0; i < ncols; ++i) {
-    for (size_t j = 0; j < t.cols.size() && host_cols[i].name; ++j)
-      if (t.cols[j].name == host_cols[i].name) slot[i] = (int)j;
-    if (slot[i] < 0)
-      return fail(ctx, FLERN_E_NOT_FOUND, "flern_run_query_streamed: table '%s' has no column '%s'", t.name.c_str(),
-                  host_cols[i].name ? host_cols[i].name : "(null)");
-    if (!t.cols[slot[i]].owned && t.capacity > 0)
-      return fail(ctx, FLERN_E_INVALID_ARG, "flern_run_query_streamed: column '%s' is borrowed", host_cols[i].name);
-    if (t.cols[slot[i]].dtype != host_cols[i].dtype)
-      return fail(ctx, FLERN_E_TYPE, "flern_run_query_streamed: column '%s' changes dtype", host_cols[i].name);
-    if (nrows > 0 && !host_cols[i].data)
-      return fail(ctx, FLERN_E_INVALID_ARG, "flern_run_query_streamed: column '%s' has no data", host_cols[i].name);
-  }
-  CUDA_TRY(ctx, cudaSetDevice(ctx->device));
-  const int64_t nchunks = std::max<int64_t>(1, (nrows + chunk_rows - 1) / chunk_rows);
-  const size_t W = 4 * kMaxGroups + kCounters;   // one chunk's [count x2 | sum x2 | counters]
-  if (!ctx->copy_stream) CUDA_TRY(ctx, cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
-  while ((int64_t)ctx->chunk_ev.size() < nchunks) {
-    cudaEvent_t e;
-    CUDA_TRY(ctx, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    ctx->chunk_ev.push_back(e);
-  }
-  if (ctx->chunk_res_slots < (size_t)nchunks) {
-    CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
-    cudaFree(ctx->chunk_res);
-    ctx->chunk_res = nullptr;
-    ctx->chunk_res_slots = 0;
-    CUDA_TRY(ctx, cudaMalloc(&ctx->chunk_res, (size_t)nchunks * W * sizeof(int64_t)));
-    ctx->chunk_res_slots = (size_t)nchunks;
-  }
-  // the copy stream starts after everything already queued on the query stream (earlier readers of
-  // the table's columns)
-  CUDA_TRY(ctx, cudaEventRecord(ctx->ev0, ctx->stream));
-  CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->copy_stream, ctx->ev0, 0));
-  const bool both = (q->flags & FLERN_Q_BOTH_CLASSES) != 0;
-  flern_status st = FLERN_OK;
-  for (int64_t c = 0; c < nchunks && st == FLERN_OK; ++c) {
-    const int64_t lo = c * chunk_rows, nc = std::min(chunk_rows, nrows - lo);
-    for (int32_t i = 0; i < ncols && nc > 0; ++i)
-      CUDA_TRY(ctx, cudaMemcpyAsync(static_cast<int32_t*>(t.cols[slot[i]].dptr) + lo,
-                                    static_cast<const int32_t*>(host_cols[i].data) + lo, (size_t)nc * 4,
-                                    cudaMemcpyHostToDevice, ctx->copy_stream));
-    CUDA_TRY(ctx, cudaEventRecord(ctx->chunk_ev[c], ctx->copy_stream));
-    CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->stream, ctx->chunk_ev[c], 0));
-    // chunk c's launch: rows [lo, lo + nc), results into chunk slot c on the device, asynchronous
-    flern_query qc = *q;
-    qc.flags |= FLERN_Q_RESULT_DEVICE | FLERN_Q_ASYNC;
-    flern_result rc{};
-    int64_t* slotp = ctx->chunk_res + (size_t)c * W;
-    rc.count = slotp;
-    rc.sum = slotp + 2 * kMaxGroups;
-    rc.counters = slotp + 4 * kMaxGroups;
-    ctx->win_lo = lo;
-    ctx->win_n = std::max<int64_t>(nc, 0);
-    st = flern_run_query(ctx, &qc, &rc);
-  }
-  ctx->win_lo = 0;
-  ctx->win_n = -1;
-  if (st != FLERN_OK) {
-    cudaStreamSynchronize(ctx->stream);
-    return st;
-  }
-  std::vector<int64_t> h((size_t)nchunks * W);
-  CUDA_TRY(ctx, cudaMemcpyAsync(h.data(), ctx->chunk_res, h.size() * sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
-  CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
-  t.nrows = nrows;
-  const int G = q->ngroups, nout = both ? 2 * G : G;
-  int64_t cnt[kCounters] = {0, 0, 0, 0};
-  for (int i = 0; i < nout; ++i) { res->count[i] = 0; res->sum[i] = 0; }
-  for (int64_t c = 0; c < nchunks; ++c) {
-    const int64_t* r = h.data() + (size_t)c * W;
-    for (int i = 0; i < nout; ++i) { res->count[i] += r[i]; res->sum[i] += r[2 * kMaxGroups + i]; }
-    for (int i = 0; i < kCounters; ++i) cnt[i] += r[4 * kMaxGroups + i];
-  }
-  if (res->counters) std::memcpy(res->counters, cnt, sizeof(cnt));
-  res->rows_scanned = cnt[0];
-  res->rows_joined = cnt[1];
-  res->rows_scored = cnt[1];
-  res->rows_selected = cnt[2];
-  res->elapsed_ms = 0.f;
-  if (cnt[3] != 0)
-    return fail(ctx, FLERN_E_INVALID_ARG, "%lld joined rows have a group code outside [0, %d)", (long long)cnt[3], G);
-  return FLERN_OK;
-}
 
 extern "C" FLERN_API flern_status flern_drop_table(flern_ctx* ctx, int32_t table_id) {
   if (!ctx) return FLERN_E_INVALID_ARG;
@@ -653,16 +568,13 @@ extern "C" FLERN_API flern_status flern_load_model(flern_ctx* ctx, const char* n
   const int H = nlayers >= 2 ? dims[1] : 0;
   for (int l = 1; l <= NL; ++l)
     if (dims[l] != H) return fail(ctx, FLERN_E_UNSUPPORTED, "model '%s': hidden widths must be equal", name);
-  const bool narrow_ok = NL >= 1 && NL <= 2 && H % 64 == 0 && H >= 64 && H <= 256;
-  const bool wide_ok = NL >= 2 && NL <= 3 && (H == 512 || H == 1024);
-  if (!narrow_ok && !wide_ok)
-    return fail(ctx, FLERN_E_UNSUPPORTED,
-                "model '%s': %d hidden layers of width %d (this build: 1-2 layers of 64/128/192/256, or 2-3 "
-                "layers of 512/1024)", name, NL, H);
   if (K0 > kMaxFeat) return fail(ctx, FLERN_E_UNSUPPORTED, "model '%s': %d inputs > %d", name, K0, kMaxFeat);
   const int K0P = (K0 + 15) / 16 * 16;
-  if (!find_kernel(K0P, H, NL))
-    return fail(ctx, FLERN_E_UNSUPPORTED, "model '%s': shape %d-%d x%d does not fit the on-chip plan", name, K0, H, NL);
+  if (NL < 1 || !find_kernel(K0P, H, NL))   // the compiled kernels define the supported shapes (flern.h)
+    return fail(ctx, FLERN_E_UNSUPPORTED,
+                "model '%s': %d inputs, %d hidden layers of width %d: no kernel in this build (1 hidden layer of "
+                "64/128/256; 2 of 64/128, or 256 with <= 16 inputs; 2 of 512 (<= 32 inputs) or 1024; 3 of 1024)",
+                name, K0, NL, H);
   for (int l = 0; l < nlayers; ++l) {
     if (!W[l] || !b[l]) return fail(ctx, FLERN_E_INVALID_ARG, "model '%s': layer %d has no weights", name, l);
     for (int64_t i = 0; i < (int64_t)dims[l] * dims[l + 1]; ++i)
@@ -755,7 +667,7 @@ extern "C" FLERN_API flern_status flern_build_hashtable(flern_ctx* ctx, int32_t 
   // Direct addressing with few payload words: fat entries {key, row, payload} of 8 or 16 words, so a
   // probe is one dependent access that also brings the payload (bounded to 8 GB of entries)
   const int32_t fs = npayload + 2 <= 8 ? 8 : (npayload + 2 <= 16 ? 16 : 0);
-  if (direct && t.nrows > 0 && fs > 0 && (uint64_t)cap * fs * 4 <= (8ull << 30) && !getenv("FLERN_NO_FAT")) {
+  if (direct && t.nrows > 0 && fs > 0 && (uint64_t)cap * fs * 4 <= (8ull << 30) && !diag_env("FLERN_NO_FAT")) {
     h.fstride = fs;
     h.bytes = (size_t)cap * fs * sizeof(int32_t);
     CUDA_TRY(ctx, cudaMalloc(&h.slots, h.bytes));
@@ -767,7 +679,7 @@ extern "C" FLERN_API flern_status flern_build_hashtable(flern_ctx* ctx, int32_t 
     hf.mode = 2u;
     int32_t* ent = reinterpret_cast<int32_t*>(h.slots);
     CUDA_TRY(ctx, cudaMemsetAsync(ctx->dflags, 0, 16, ctx->stream));
-    fill_fat_kernel<<<grid_for(cap), 256, 0, ctx->stream>>>(ent, cap, fs);
+    fill_fat_kernel<<<grid_for(cap * fs / 4), 256, 0, ctx->stream>>>(ent, cap, fs);
     build_fat_kernel<<<grid_for(t.nrows), 256, 0, ctx->stream>>>(static_cast<const int32_t*>(kc->dptr), t.nrows, ent,
                                                                  hf, fs, pc, npayload, ctx->dflags);
     CUDA_TRY(ctx, cudaGetLastError());
@@ -825,14 +737,25 @@ extern "C" FLERN_API flern_status flern_build_hashtable(flern_ctx* ctx, int32_t 
 }
 
 // ================================================================================ queries
-extern "C" FLERN_API flern_status flern_run_query(flern_ctx* ctx, const flern_query* q, flern_result* res) {
-  if (!ctx) return FLERN_E_INVALID_ARG;
-  if (!q || !res) return fail(ctx, FLERN_E_INVALID_ARG, "flern_run_query: null query or result");
-  const bool dev_out = (q->flags & FLERN_Q_RESULT_DEVICE) != 0;
-  const bool async = (q->flags & FLERN_Q_ASYNC) != 0;
+namespace {
+// A streamed launch reads its fact rows from a ring slot instead of the table's own columns:
+// base[i] = device rows of fact column i for this chunk (nullptr = not streamed), nrows rows.
+struct FactWindow {
+  int64_t nrows = 0;
+  std::vector<const int32_t*> base;
+};
+struct Prepared {
+  QueryParams p;
+  KernelEntry* ke = nullptr;
+  const Model* m = nullptr;
+};
+
+// Every validation of a query and the kernel parameters it resolves to; no device work except
+// caching a model image with permuted inputs. Shared by flern_run_query and flern_run_query_streamed
+// (which validates before its first copy).
+flern_status prepare_query(flern_ctx* ctx, const flern_query* q, const FactWindow* win, Prepared& out) {
+  QueryParams& p = out.p;
   const bool both = (q->flags & FLERN_Q_BOTH_CLASSES) != 0;
-  if (async && !dev_out) return fail(ctx, FLERN_E_INVALID_ARG, "FLERN_Q_ASYNC requires FLERN_Q_RESULT_DEVICE");
-  if (!res->count || !res->sum) return fail(ctx, FLERN_E_INVALID_ARG, "result count/sum pointers are required");
   if (q->fact_table < 0 || q->fact_table >= (int32_t)ctx->tables.size() || !ctx->tables[q->fact_table].alive)
     return fail(ctx, FLERN_E_NOT_FOUND, "no fact table with id %d", q->fact_table);
   const Table& fact = ctx->tables[q->fact_table];
@@ -846,16 +769,22 @@ extern "C" FLERN_API flern_status flern_run_query(flern_ctx* ctx, const flern_qu
     return fail(ctx, FLERN_E_UNSUPPORTED, "queries need 1..%d probes (got %d)", kMaxProbes, q->nprobes);
   if (q->ngroups < 1 || q->ngroups > kMaxGroupsLarge)
     return fail(ctx, FLERN_E_UNSUPPORTED, "ngroups %d outside 1..%d", q->ngroups, kMaxGroupsLarge);
-  if (q->ngroups > kMaxGroups && ctx->win_n >= 0)
+  if (q->ngroups > kMaxGroups && win)
     return fail(ctx, FLERN_E_UNSUPPORTED, "streamed queries aggregate at most %d groups", kMaxGroups);
   if (std::isnan(q->threshold)) return fail(ctx, FLERN_E_INVALID_ARG, "threshold is NaN");
 
-  QueryParams p;
   std::memset(&p, 0, sizeof(p));
-  // a streamed query runs over a row window of the fact table (flern_run_query_streamed)
-  const bool windowed = ctx->win_n >= 0;
-  const int64_t woff = windowed ? ctx->win_lo : 0;
-  p.nrows = windowed ? ctx->win_n : fact.nrows;
+  // a streamed query reads its fact rows from a ring slot (flern_run_query_streamed)
+  p.nrows = win ? win->nrows : fact.nrows;
+  const int32_t* missing = reinterpret_cast<const int32_t*>(1);
+  auto fact_base = [&](const Column* c) -> const int32_t* {
+    if (!win) return static_cast<const int32_t*>(c->dptr);
+    const int32_t* b = win->base[(size_t)(c - fact.cols.data())];
+    return b ? b : missing;
+  };
+  auto not_streamed = [&](const char* col) {
+    return fail(ctx, FLERN_E_NOT_FOUND, "streamed query reads fact column '%s', which host_cols does not supply", col);
+  };
   p.nprobes = q->nprobes;
   for (int i = 0; i < q->nprobes; ++i) {
     const flern_probe& pr = q->probes[i];
@@ -878,7 +807,8 @@ extern "C" FLERN_API flern_status flern_run_query(flern_ctx* ctx, const flern_qu
       const Column* c = fact.find(pr.key_col);
       if (!c) return fail(ctx, FLERN_E_NOT_FOUND, "fact table '%s' has no column '%s'", fact.name.c_str(), pr.key_col);
       if (!is_int_type(c->dtype)) return fail(ctx, FLERN_E_TYPE, "probe key '%s' must be integer-typed", pr.key_col);
-      d.fact_key = static_cast<const int32_t*>(c->dptr) + woff;
+      d.fact_key = fact_base(c);
+      if (d.fact_key == missing) return not_streamed(pr.key_col);
     } else {
       const HashTable& hs = ctx->hts[q->probes[pr.src].ht_id];
       const int w = hs.find(pr.key_col);
@@ -893,7 +823,8 @@ extern "C" FLERN_API flern_status flern_run_query(flern_ctx* ctx, const flern_qu
       const Column* c = fact.find(r.col);
       if (!c) return fail(ctx, FLERN_E_NOT_FOUND, "%s: fact table '%s' has no column '%s'", what, fact.name.c_str(), r.col);
       if (need_int && !is_int_type(c->dtype)) return fail(ctx, FLERN_E_TYPE, "%s: column '%s' must be integer-typed", what, r.col);
-      out->base = static_cast<const int32_t*>(c->dptr) + woff;
+      out->base = fact_base(c);
+      if (out->base == missing) return not_streamed(r.col);
       out->stride = 1;
       out->src = 0;
       out->is_float = c->dtype == FLERN_F32;
@@ -928,8 +859,7 @@ extern "C" FLERN_API flern_status flern_run_query(flern_ctx* ctx, const flern_qu
       if (fq[k].src == src) { perm.push_back(k); ++nsrc[src]; }
   p.nfact = nsrc[0];
   bool ident = true;
-  const int32_t* any_fact_col = static_cast<const int32_t*>(fact.cols[0].dptr) + woff;
-  for (int k = 0; k < kMaxFeat; ++k) { p.fcol[k] = any_fact_col; p.dword[k] = 0; }
+  for (int k = 0; k < kMaxFeat; ++k) { p.fcol[k] = ctx->dummy; p.dword[k] = 0; }   // unused entries: never read
   for (int k = 0; k < q->nfeat; ++k) {
     p.feat[k] = fq[perm[k]];
     ident = ident && perm[k] == k;
@@ -950,14 +880,15 @@ extern "C" FLERN_API flern_status flern_run_query(flern_ctx* ctx, const flern_qu
     const Column* c = fact.find(q->prefilter_col);
     if (!c) return fail(ctx, FLERN_E_NOT_FOUND, "pre-filter: fact table '%s' has no column '%s'", fact.name.c_str(), q->prefilter_col);
     if (!is_int_type(c->dtype)) return fail(ctx, FLERN_E_TYPE, "pre-filter column '%s' must be integer-typed", q->prefilter_col);
-    p.pf_col = static_cast<const int32_t*>(c->dptr) + woff;
+    p.pf_col = fact_base(c);
+    if (p.pf_col == missing) return not_streamed(q->prefilter_col);
     p.pf_lo = q->pf_lo;
-    p.pf_hi = getenv("FLERN_DBG_PF_EMPTY") ? q->pf_lo : q->pf_hi;   // diagnostic: scan cost alone
+    p.pf_hi = diag_env("FLERN_DBG_PF_EMPTY") ? q->pf_lo : q->pf_hi;   // diagnostic: scan cost alone
   }
   p.ngroups = q->ngroups;
   p.both_classes = both ? 1 : 0;
   p.no_model = (q->flags & FLERN_Q_NO_MODEL) ? 1 : 0;
-  p.dbg_mode = getenv("FLERN_DBG_MODE") ? atoi(getenv("FLERN_DBG_MODE")) : 0;   // diagnostics only
+  p.dbg_mode = diag_env("FLERN_DBG_MODE") ? atoi(diag_env("FLERN_DBG_MODE")) : 0;   // diagnostic build only
   const double t = (double)q->threshold;
   p.thr_logit = t <= 0.0 ? -INFINITY : (t >= 1.0 ? INFINITY : (float)std::log(t / (1.0 - t)));
   uint8_t* img = m.dbuf;
@@ -980,9 +911,25 @@ extern "C" FLERN_API flern_status flern_run_query(flern_ctx* ctx, const flern_qu
   p.shift = reinterpret_cast<const float*>(img + m.off_shift);
   p.scale = reinterpret_cast<const float*>(img + m.off_scale);
   // group domains beyond kMaxGroups need the generic-shape kernels (GroupAgg<true>)
-  KernelEntry* ke = q->ngroups > kMaxGroups ? find_kernel(m.K0P, m.H, m.NL)
-                                            : find_kernel(m.K0P, m.H, m.NL, nsrc[0], nsrc[1], nsrc[2], p.fmask);
+  // (FLERN_Q_GENERIC_KERNEL: the run-time-shape producer, for tests that compare the two)
+  KernelEntry* ke = (q->ngroups > kMaxGroups || (q->flags & FLERN_Q_GENERIC_KERNEL))
+                        ? find_kernel(m.K0P, m.H, m.NL)
+                        : find_kernel(m.K0P, m.H, m.NL, nsrc[0], nsrc[1], nsrc[2], p.fmask);
   if (!ke) return fail(ctx, FLERN_E_UNSUPPORTED, "no kernel for model '%s'", m.name.c_str());
+  out.ke = ke;
+  out.m = &m;
+  return FLERN_OK;
+}
+
+// One launch of a prepared query (synchronous unless FLERN_Q_ASYNC).
+flern_status launch_query(flern_ctx* ctx, const flern_query* q, Prepared& pq, flern_result* res, bool windowed) {
+  QueryParams& p = pq.p;
+  KernelEntry* ke = pq.ke;
+  const Model& m = *pq.m;
+  const bool dev_out = (q->flags & FLERN_Q_RESULT_DEVICE) != 0;
+  const bool async = (q->flags & FLERN_Q_ASYNC) != 0;
+  const bool both = (q->flags & FLERN_Q_BOTH_CLASSES) != 0;
+  flern_status st;
 
   CUDA_TRY(ctx, cudaSetDevice(ctx->device));
   const int G = q->ngroups;
@@ -1100,11 +1047,11 @@ extern "C" FLERN_API flern_status flern_run_query(flern_ctx* ctx, const flern_qu
     // activation scratch, which is written and read back once per layer and must not be evicted to HBM
     void* wbase = h0.slots;
     size_t wbytes = h0.bytes;
-    if (ke->scratch_per_cta && !getenv("FLERN_WINDOW_HT")) {
+    if (ke->scratch_per_cta && !diag_env("FLERN_WINDOW_HT")) {
       wbase = ctx->scratch;
       wbytes = (size_t)grid * ke->scratch_per_cta;
     }
-    if (ctx->persist_max > 0 && ctx->window_max > 0 && !getenv("FLERN_NO_L2_WINDOW")) {
+    if (ctx->persist_max > 0 && ctx->window_max > 0 && !diag_env("FLERN_NO_L2_WINDOW")) {
       attr[0].id = cudaLaunchAttributeAccessPolicyWindow;
       attr[0].val.accessPolicyWindow.base_ptr = wbase;
       attr[0].val.accessPolicyWindow.num_bytes = std::min(wbytes, ctx->window_max);
@@ -1152,6 +1099,166 @@ extern "C" FLERN_API flern_status flern_run_query(flern_ctx* ctx, const flern_qu
   float ms = 0.f;
   cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
   res->elapsed_ms = ms;
+  if (cnt[3] != 0)
+    return fail(ctx, FLERN_E_INVALID_ARG, "%lld joined rows have a group code outside [0, %d)", (long long)cnt[3], G);
+  return FLERN_OK;
+}
+}  // namespace
+
+extern "C" FLERN_API flern_status flern_run_query(flern_ctx* ctx, const flern_query* q, flern_result* res) {
+  if (!ctx) return FLERN_E_INVALID_ARG;
+  if (!q || !res) return fail(ctx, FLERN_E_INVALID_ARG, "flern_run_query: null query or result");
+  const bool dev_out = (q->flags & FLERN_Q_RESULT_DEVICE) != 0;
+  const bool async = (q->flags & FLERN_Q_ASYNC) != 0;
+  if (async && !dev_out) return fail(ctx, FLERN_E_INVALID_ARG, "FLERN_Q_ASYNC requires FLERN_Q_RESULT_DEVICE");
+  if (!res->count || !res->sum) return fail(ctx, FLERN_E_INVALID_ARG, "result count/sum pointers are required");
+  Prepared pq;
+  flern_status st = prepare_query(ctx, q, nullptr, pq);
+  if (st != FLERN_OK) return st;
+  return launch_query(ctx, q, pq, res, false);
+}
+
+// The query over host-resident fact rows (§3.2): chunk c of the rows is copied into ring
+// slot c % K on the copy stream, and its launch reads that slot; slot reuse waits for the launch that
+// last read it. The fact table supplies the schema only, so its capacity does not bound nrows.
+extern "C" FLERN_API flern_status flern_run_query_streamed(flern_ctx* ctx, const flern_query* q, int64_t nrows,
+                                                           int32_t ncols, const flern_column* host_cols,
+                                                           int64_t chunk_rows, flern_result* res) {
+  if (!ctx) return FLERN_E_INVALID_ARG;
+  if (!q || !res || !res->count || !res->sum)
+    return fail(ctx, FLERN_E_INVALID_ARG, "flern_run_query_streamed: null query or result");
+  if (q->flags & (FLERN_Q_ASYNC | FLERN_Q_RESULT_DEVICE))
+    return fail(ctx, FLERN_E_INVALID_ARG, "flern_run_query_streamed: host results only (no ASYNC / RESULT_DEVICE)");
+  if (res->dbg_score || res->dbg_match || res->dbg_selected || res->dbg_trace)
+    return fail(ctx, FLERN_E_UNSUPPORTED, "debug exports are not available for streamed queries");
+  if (q->fact_table < 0 || q->fact_table >= (int32_t)ctx->tables.size() || !ctx->tables[q->fact_table].alive)
+    return fail(ctx, FLERN_E_NOT_FOUND, "no fact table with id %d", q->fact_table);
+  const Table& t = ctx->tables[q->fact_table];
+  if (nrows < 0 || nrows >= ((int64_t)1 << 40))
+    return fail(ctx, FLERN_E_INVALID_ARG, "flern_run_query_streamed: bad row count %lld", (long long)nrows);
+  if (chunk_rows <= 0 || chunk_rows >= ((int64_t)1 << 31))
+    return fail(ctx, FLERN_E_INVALID_ARG, "flern_run_query_streamed: chunk_rows must be in [1, 2^31)");
+  chunk_rows = (chunk_rows + 3) & ~3ll;   // ring columns stay 16-byte aligned (vector loads, bulk copies)
+  if (!host_cols || ncols <= 0 || ncols > (int32_t)t.cols.size())
+    return fail(ctx, FLERN_E_INVALID_ARG, "flern_run_query_streamed: %d columns given, table '%s' has %zu", ncols,
+                t.name.c_str(), t.cols.size());
+  // host column i -> fact column slot[i]; every check before any copy or launch
+  std::vector<int> slot(ncols, -1);
+  for (int32_t i = 0; i < ncols; ++i) {
+    if (!host_cols[i].name) return fail(ctx, FLERN_E_INVALID_ARG, "flern_run_query_streamed: column %d has no name", i);
+    for (size_t j = 0; j < t.cols.size(); ++j)
+      if (t.cols[j].name == host_cols[i].name) slot[i] = (int)j;
+    if (slot[i] < 0)
+      return fail(ctx, FLERN_E_NOT_FOUND, "flern_run_query_streamed: table '%s' has no column '%s'", t.name.c_str(),
+                  host_cols[i].name);
+    if (t.cols[slot[i]].dtype != host_cols[i].dtype)
+      return fail(ctx, FLERN_E_TYPE, "flern_run_query_streamed: column '%s' changes dtype", host_cols[i].name);
+    if (nrows > 0 && !host_cols[i].data)
+      return fail(ctx, FLERN_E_INVALID_ARG, "flern_run_query_streamed: column '%s' has no data", host_cols[i].name);
+    if (reinterpret_cast<uintptr_t>(host_cols[i].data) % 4 != 0)
+      return fail(ctx, FLERN_E_INVALID_ARG, "flern_run_query_streamed: column '%s' is not 4-byte aligned",
+                  host_cols[i].name);
+    for (int32_t j = 0; j < i; ++j)
+      if (slot[j] == slot[i])
+        return fail(ctx, FLERN_E_DUPLICATE, "flern_run_query_streamed: column '%s' appears twice", host_cols[i].name);
+  }
+  const int64_t nchunks = std::max<int64_t>(1, (nrows + chunk_rows - 1) / chunk_rows);
+  const int K = (int)std::min<int64_t>(kRingSlots, nchunks);   // ring slots
+  const size_t col_bytes = (size_t)chunk_rows * 4, slot_bytes = col_bytes * (size_t)ncols;
+  // the ring slot layout the launches read; validate the query against it before anything moves
+  std::vector<FactWindow> win(K);
+  auto place = [&](uint8_t* ring) {
+    for (int k = 0; k < K; ++k) {
+      win[k].base.assign(t.cols.size(), nullptr);
+      for (int32_t i = 0; i < ncols; ++i)
+        win[k].base[slot[i]] = reinterpret_cast<const int32_t*>(ring + (size_t)k * slot_bytes + (size_t)i * col_bytes);
+    }
+  };
+  place(reinterpret_cast<uint8_t*>(ctx->dummy));   // addresses only (checked, not dereferenced)
+  win[0].nrows = std::min(chunk_rows, nrows);
+  Prepared pq;
+  flern_status st = prepare_query(ctx, q, &win[0], pq);
+  if (st != FLERN_OK) return st;
+
+  CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+  const size_t W = 4 * kMaxGroups + kCounters;   // one chunk's [count x2 | sum x2 | counters]
+  if (!ctx->copy_stream) CUDA_TRY(ctx, cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+  while ((int)ctx->ring_copied.size() < kRingSlots) {
+    cudaEvent_t a, b;
+    CUDA_TRY(ctx, cudaEventCreateWithFlags(&a, cudaEventDisableTiming));
+    CUDA_TRY(ctx, cudaEventCreateWithFlags(&b, cudaEventDisableTiming));
+    ctx->ring_copied.push_back(a);
+    ctx->ring_read.push_back(b);
+  }
+  if (ctx->ring_bytes < (size_t)K * slot_bytes || ctx->chunk_res_slots < (size_t)nchunks) {
+    CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    CUDA_TRY(ctx, cudaStreamSynchronize(ctx->copy_stream));
+  }
+  if (ctx->ring_bytes < (size_t)K * slot_bytes) {
+    cudaFree(ctx->ring);
+    ctx->ring = nullptr;
+    ctx->ring_bytes = 0;
+    CUDA_TRY(ctx, cudaMalloc(&ctx->ring, (size_t)K * slot_bytes));
+    ctx->ring_bytes = (size_t)K * slot_bytes;
+  }
+  if (ctx->chunk_res_slots < (size_t)nchunks) {
+    cudaFree(ctx->chunk_res);
+    ctx->chunk_res = nullptr;
+    ctx->chunk_res_slots = 0;
+    CUDA_TRY(ctx, cudaMalloc(&ctx->chunk_res, (size_t)nchunks * W * sizeof(int64_t)));
+    ctx->chunk_res_slots = (size_t)nchunks;
+  }
+  place(ctx->ring);
+  // the copy stream starts after everything already queued on the query stream (earlier readers of the
+  // ring from a previous call)
+  CUDA_TRY(ctx, cudaEventRecord(ctx->ev0, ctx->stream));
+  CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->copy_stream, ctx->ev0, 0));
+  const bool both = (q->flags & FLERN_Q_BOTH_CLASSES) != 0;
+  flern_query qc = *q;
+  qc.flags |= FLERN_Q_RESULT_DEVICE | FLERN_Q_ASYNC;
+  for (int64_t c = 0; c < nchunks && st == FLERN_OK; ++c) {
+    const int k = (int)(c % K);
+    const int64_t lo = c * chunk_rows, nc = std::max<int64_t>(0, std::min(chunk_rows, nrows - lo));
+    if (c >= K) CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->copy_stream, ctx->ring_read[k], 0));   // slot k is free
+    for (int32_t i = 0; i < ncols && nc > 0; ++i)
+      CUDA_TRY(ctx, cudaMemcpyAsync(const_cast<int32_t*>(win[k].base[slot[i]]),
+                                    static_cast<const int32_t*>(host_cols[i].data) + lo, (size_t)nc * 4,
+                                    cudaMemcpyHostToDevice, ctx->copy_stream));
+    CUDA_TRY(ctx, cudaEventRecord(ctx->ring_copied[k], ctx->copy_stream));
+    CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->stream, ctx->ring_copied[k], 0));
+    win[k].nrows = nc;
+    Prepared pc;
+    if ((st = prepare_query(ctx, &qc, &win[k], pc)) != FLERN_OK) break;
+    flern_result rc{};
+    int64_t* sp = ctx->chunk_res + (size_t)c * W;
+    rc.count = sp;
+    rc.sum = sp + 2 * kMaxGroups;
+    rc.counters = sp + 4 * kMaxGroups;
+    if ((st = launch_query(ctx, &qc, pc, &rc, true)) != FLERN_OK) break;
+    CUDA_TRY(ctx, cudaEventRecord(ctx->ring_read[k], ctx->stream));
+  }
+  if (st != FLERN_OK) {
+    cudaStreamSynchronize(ctx->stream);
+    cudaStreamSynchronize(ctx->copy_stream);
+    return st;
+  }
+  std::vector<int64_t> h((size_t)nchunks * W);
+  CUDA_TRY(ctx, cudaMemcpyAsync(h.data(), ctx->chunk_res, h.size() * sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  const int G = q->ngroups, nout = both ? 2 * G : G;
+  int64_t cnt[kCounters] = {0, 0, 0, 0};
+  for (int i = 0; i < nout; ++i) { res->count[i] = 0; res->sum[i] = 0; }
+  for (int64_t c = 0; c < nchunks; ++c) {
+    const int64_t* r = h.data() + (size_t)c * W;
+    for (int i = 0; i < nout; ++i) { res->count[i] += r[i]; res->sum[i] += r[2 * kMaxGroups + i]; }
+    for (int i = 0; i < kCounters; ++i) cnt[i] += r[4 * kMaxGroups + i];
+  }
+  if (res->counters) std::memcpy(res->counters, cnt, sizeof(cnt));
+  res->rows_scanned = cnt[0];
+  res->rows_joined = cnt[1];
+  res->rows_scored = cnt[1];
+  res->rows_selected = cnt[2];
+  res->elapsed_ms = 0.f;
   if (cnt[3] != 0)
     return fail(ctx, FLERN_E_INVALID_ARG, "%lld joined rows have a group code outside [0, %d)", (long long)cnt[3], G);
   return FLERN_OK;

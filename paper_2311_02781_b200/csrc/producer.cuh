@@ -191,7 +191,9 @@ __device__ __forceinline__ void produce_batch(ProdState& st, const QueryParams& 
           for (int r = 0; r < R; ++r) {
             const int32_t* e = reinterpret_cast<const int32_t*>(pd.slots) + (int64_t)hash_slot(kq[r], pd.hf) * pd.fstride;
             const int4 x = ldg_nc(reinterpret_cast<const int4*>(valid[r] && !synth ? e : dz));
-            const bool hit = valid[r] && (x.x == kq[r] || synth);
+            // an empty entry is {kEmptyKey, -1}: a probe key equal to kEmptyKey must miss, so a hit
+            // also needs a real build row (P:328-331 emits only joinCond matches)
+            const bool hit = valid[r] && ((x.x == kq[r] && x.y >= 0) || synth);
             brow[r][q] = hit ? (synth ? 0 : x.y) : -1;
             pb[r][q] = hit && !synth ? e + 2 : dz;
             valid[r] = hit;
@@ -260,7 +262,7 @@ __device__ __forceinline__ void produce_batch(ProdState& st, const QueryParams& 
       if (dq >= 0) {   // resolve the late fat probe
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-          const bool hit = valid[r] && (dseen[r] == dkey[r] || synth);
+          const bool hit = valid[r] && ((dseen[r] == dkey[r] && drow[r] >= 0) || synth);   // empty: row -1
           brow[r][dq] = hit ? (synth ? 0 : drow[r]) : -1;
           valid[r] = hit;
         }

@@ -7,7 +7,6 @@ ImportError (there is no fallback of any kind).
 from __future__ import annotations
 
 import ctypes
-import math
 import os
 
 import numpy as np
@@ -27,7 +26,7 @@ ERRORS = {-1: "FLERN_E_INVALID_ARG", -2: "FLERN_E_NOT_FOUND", -3: "FLERN_E_DUPLI
           -10: "FLERN_E_UNSUPPORTED"}
 FLERN_I32, FLERN_F32, FLERN_DATE32, FLERN_DEC32, FLERN_DICT32 = 1, 2, 3, 4, 5
 FLERN_COPY_HOST, FLERN_COPY_DEVICE, FLERN_BORROW_DEVICE = 0x1, 0x2, 0x4
-FLERN_Q_RESULT_DEVICE, FLERN_Q_ASYNC, FLERN_Q_BOTH_CLASSES, FLERN_Q_NO_MODEL = 0x1, 0x2, 0x4, 0x8
+FLERN_Q_RESULT_DEVICE, FLERN_Q_ASYNC, FLERN_Q_BOTH_CLASSES, FLERN_Q_NO_MODEL, FLERN_Q_GENERIC_KERNEL = 0x1, 0x2, 0x4, 0x8, 0x10
 EXPORTED = ["flern_create", "flern_destroy", "flern_last_error", "flern_version", "flern_load_table",
             "flern_update_table", "flern_run_query_streamed", "flern_drop_table", "flern_load_model", "flern_build_hashtable", "flern_run_query",
             "flern_query_launches"]
@@ -247,6 +246,3 @@ def flern_run_query_streamed(ctx, query: Query, columns: dict, chunk_rows: int, 
                                               ctypes.byref(res)))
     return res
 
-
-def logit_threshold(t: float) -> float:
-    return -math.inf if t <= 0 else (math.inf if t >= 1 else math.log(t / (1 - t)))

@@ -1,5 +1,7 @@
 #!/bin/bash
 # A/B a tuning environment variable over workloads: scripts/ab_env.sh VAR "v1 v2 ..." "c2 c1x ..." [extra bench args]
+# The knobs are read only by the diagnostic build (make paper_2311_02781_b200/lib/libflern_diag.so).
+export FLERN_LIB=libflern_diag.so
 VAR=$1; VALS=$2; WLS=$3; shift 3
 for v in $VALS; do
   for w in $WLS; do

@@ -27,7 +27,7 @@ def unpack_bits(words, n):
     return b[:n].astype(bool)
 
 
-def run_gpu(cfg, db, model, threshold=None, both=False, debug=True, gq=None):
+def run_gpu(cfg, db, model, threshold=None, both=False, debug=True, gq=None, flags=0):
     own = gq is None
     gq = gq or GpuQuery(cfg, db, model)
     try:
@@ -40,7 +40,7 @@ def run_gpu(cfg, db, model, threshold=None, both=False, debug=True, gq=None):
         score = np.empty(max(1, n), np.float32) if debug else None
         match = np.empty(max(1, n * P), np.int32) if debug else None
         sel = np.zeros(max(1, (n + 31) // 32), np.uint32) if debug else None
-        q = gq.make_query(gq.fact_id, threshold=threshold, flags=F.FLERN_Q_BOTH_CLASSES if both else 0)
+        q = gq.make_query(gq.fact_id, threshold=threshold, flags=(F.FLERN_Q_BOTH_CLASSES if both else 0) | flags)
         res = gq.run(q, count=count, sum=sm, counters=counters, dbg_score=score, dbg_match=match, dbg_selected=sel)
         out = dict(count=count[:G].copy(), sum=sm[:G].copy(), count_rej=count[G:].copy(), sum_rej=sm[G:].copy(),
                    counters=counters, rows_joined=res.rows_joined, rows_selected=res.rows_selected,
@@ -55,9 +55,9 @@ def run_gpu(cfg, db, model, threshold=None, both=False, debug=True, gq=None):
             gq.close()
 
 
-def check(cfg, db, model, threshold=None, both=False, emu_tol=None, gq=None):
+def check(cfg, db, model, threshold=None, both=False, emu_tol=None, gq=None, flags=0):
     t = cfg.threshold if threshold is None else threshold
-    g = run_gpu(cfg, db, model, threshold=t, both=both, gq=gq)
+    g = run_gpu(cfg, db, model, threshold=t, both=both, gq=gq, flags=flags)
     o = O.run(cfg, db, model, threshold=t, band=BAND, per_row=True)
     n = db.fact_n
     # 1. join ids, bit-exact

@@ -32,8 +32,7 @@ def _worker(rank, world, port, q):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         cfg = D.with_sf(D.CONFIGS["c1"], 0.004, match_rate=0.9)
-        full = D.make_database(cfg)
-        model = D.make_model(cfg, full)   # replicated weights (normalisation from the first rows)
+        model = D.make_model(cfg, D.make_database(cfg, max_slots=D.MODEL_SLOTS))   # replicated weights
         shard = D.make_database(cfg, rank=rank, world=world)
         r = O.run(cfg, shard, model, nthreads=2)
         buf = FD.pack_partials(torch.from_numpy(r.count), torch.from_numpy(r.sum))

@@ -92,7 +92,10 @@ def _custom_db(cfg, nfact, seed=0, miss=0.2):
     for c, v in src.items():
         fact[c] = np.ascontiguousarray(v[rows]) if nfact else v[:0].copy()
     fk = keys[take].copy()
-    fk[rng.random(nfact) < miss] = -7   # misses
+    u = rng.random(nfact)
+    fk[u < miss] = -7   # misses
+    # and some probe keys equal to the empty-slot marker INT32_MIN: they must miss too
+    fk[u < miss / 4] = np.iinfo(np.int32).min
     fact["l_orderkey"] = fk.astype(np.int32)
     return D.Database(cfg.sf, nfact, fact, full.builds)
 
@@ -116,6 +119,20 @@ def test_ragged_sizes_other_kernels(name, nfact):
     model = D.make_model(cfg, D.make_database(cfg))
     r = parity.check(cfg, db, model)
     assert r["gpu"]["rows_scanned"] == nfact
+
+
+@pytest.mark.parametrize("name", ["c1", "c2"])
+def test_int32_min_probe_key_misses(name):
+    """A fact key equal to INT32_MIN (the fat table's empty-entry key) hashes onto an empty entry: it
+    must be a miss, not a join with build row -1 (P:328-331 emits joinCond matches only). Every third
+    fact row carries it; join ids, scores, selection and aggregates against the oracle."""
+    cfg = D.with_sf(D.CONFIGS[name], 0.004, match_rate=0.9)
+    db = D.make_database(cfg)
+    fk = db.fact["l_orderkey"].copy()
+    fk[::3] = np.iinfo(np.int32).min
+    db.fact["l_orderkey"] = fk
+    r = parity.check(cfg, db, D.make_model(cfg, db))
+    assert r["oracle"].match[::3].max() == -1 and r["gpu"]["rows_joined"] < 0.7 * db.fact_n
 
 
 @pytest.mark.parametrize("name,miss", [("c2", 1.0), ("c1", 1.0), ("c1", 0.97)])
@@ -269,7 +286,8 @@ def test_hash_build_key_distributions(kind):
     cfg = D.QueryConfig("h", 0.0, [8, 64, 1], [("fact", f"f{k}") for k in range(8)],
                         [("dim", "fact", "k", "dk")], group=(0, "dg"), ngroups=4, sum_col=("fact", "v"))
     nf = 50000
-    fk = rng.choice(np.concatenate([bkeys, rng.integers(-2**31 + 1, 2**31 - 1, 5000).astype(np.int32)]), nf)
+    fk = rng.choice(np.concatenate([bkeys, rng.integers(-2**31 + 1, 2**31 - 1, 5000).astype(np.int32),
+                                    np.full(500, np.iinfo(np.int32).min, np.int32)]), nf)
     fact = {"k": fk.astype(np.int32), "v": rng.integers(0, 1000, nf).astype(np.int32)}
     for k in range(8):
         fact[f"f{k}"] = rng.normal(size=nf).astype(np.float32)
@@ -317,14 +335,15 @@ def test_wide_mlp_configs(name, sf):
 
 
 @pytest.mark.parametrize("name", ["c1", "c2", "c4p"])
-def test_generic_producer_path(name, monkeypatch):
+def test_generic_producer_path(name):
     """The benchmark shapes run a producer specialised for their feature layout; the same queries
-    through the generic (run-time shape) producer must give the same parity results."""
-    monkeypatch.setenv("FLERN_GENERIC_ONLY", "1")
+    through the generic (run-time shape) producer (FLERN_Q_GENERIC_KERNEL) must give the same parity
+    results."""
+    from paper_2311_02781_b200 import flern as F
     sf = 0.1 if name == "c4p" else 0.004
     cfg = D.with_sf(D.CONFIGS[name], sf, match_rate=0.9)
     db = D.make_database(cfg)
-    parity.check(cfg, db, D.make_model(cfg, db))
+    parity.check(cfg, db, D.make_model(cfg, db), flags=F.FLERN_Q_GENERIC_KERNEL)
 
 
 def test_update_table_refills_in_place():
@@ -371,9 +390,10 @@ def test_update_table_refills_in_place():
 
 @pytest.mark.parametrize("chunk", [1000, 4096, 10**9])
 def test_streamed_query_equals_resident(chunk):
-    """flern_run_query_streamed (host fact rows copied chunk by chunk, copies overlapped with the
-    chunk launches) gives exactly the resident query's aggregates and counters, for chunks
-    that do not divide the table, one row chunk per launch and a single chunk."""
+    """flern_run_query_streamed (host fact rows through a ring of device chunk buffers, copies overlapped
+    with the chunk launches) gives exactly the resident query's aggregates and counters, for
+    chunks that do not divide the table, more chunks than ring slots, and a single chunk; the table's
+    own rows are neither read nor changed."""
     from paper_2311_02781_b200 import flern as F
     from paper_2311_02781_b200.session import GpuQuery
     cfg = D.with_sf(D.CONFIGS["c2"], 0.003, match_rate=0.9)
@@ -389,10 +409,69 @@ def test_streamed_query_equals_resident(chunk):
         r = F.flern_run_query_streamed(gq.ctx, gq.query, host, chunk, count=c, sum=s_)
         assert (c == rc).all() and (s_ == rs).all()
         assert (r.rows_scanned, r.rows_joined, r.rows_selected) == (ref.rows_scanned, ref.rows_joined, ref.rows_selected)
-        # the resident query now sees the streamed rows
+        # the resident table is untouched
         c2, s2 = np.zeros(G, np.int64), np.zeros(G, np.int64)
         gq.run(count=c2, sum=s2)
         assert (c2 == rc).all() and (s2 == rs).all()
+    finally:
+        gq.close()
+
+
+@pytest.mark.parametrize("name,chunk", [("c2", 1000), ("c1", 777), ("c4p", 20000)])
+def test_streamed_beyond_ring_vs_oracle(name, chunk):
+    """NEXT-2 beyond device capacity: the fact table on the device is a schema with 0 rows, the rows live
+    in host memory only and stream through the 3-slot ring in many more chunks than slots. Against the
+    oracle: exact with the linear-threshold model (no band), and the export-free bracket with the random
+    model; counters equal the oracle's."""
+    from paper_2311_02781_b200 import flern as F
+    from paper_2311_02781_b200.session import GpuQuery
+    sf = 0.05 if name == "c4p" else 0.004
+    cfg = D.with_sf(D.CONFIGS[name], sf, match_rate=0.9)
+    db = D.make_database(cfg)
+    G = cfg.ngroups
+    for model in (H.linear_threshold_model(cfg), D.make_model(cfg, db)):
+        gq = GpuQuery(cfg, db, model, load_fact=False)
+        try:
+            schema = {k: np.zeros(0, v.dtype) for k, v in db.fact.items()}
+            gq.set_fact(F.flern_load_table(gq.ctx, "fact_schema", schema))
+            c, s_ = np.zeros(G, np.int64), np.zeros(G, np.int64)
+            r = F.flern_run_query_streamed(gq.ctx, gq.query, db.fact, chunk, count=c, sum=s_)
+            assert -(-db.fact_n // chunk) > 3
+            o = O.run(cfg, db, model, band=parity.BAND)
+            assert r.rows_scanned == db.fact_n and r.rows_joined == o.rows_joined
+            assert np.all(o.count_hi <= c) and np.all(c <= o.count_hi + o.count_band)
+            assert np.all(o.sum_hi <= s_) and np.all(s_ <= o.sum_hi + o.sum_band)
+            if o.rows_band == 0:
+                assert c.tolist() == o.count.tolist() and s_.tolist() == o.sum.tolist()
+        finally:
+            gq.close()
+
+
+def test_streamed_query_validates_before_copying():
+    """A streamed query that cannot run (a column it reads is not streamed, a dtype that changes, a
+    duplicate column) fails before any copy or launch and leaves the context usable."""
+    from paper_2311_02781_b200 import flern as F
+    from paper_2311_02781_b200.session import GpuQuery
+    cfg = D.with_sf(D.CONFIGS["c2"], 0.002, match_rate=0.9)
+    db = D.make_database(cfg)
+    gq = GpuQuery(cfg, db, D.make_model(cfg, db))
+    G = cfg.ngroups
+    try:
+        rc, rs = np.zeros(G, np.int64), np.zeros(G, np.int64)
+        gq.run(count=rc, sum=rs)
+        part = dict(db.fact)
+        part.pop("l_shipmode")
+        with pytest.raises(F.FlernError, match="NOT_FOUND.*l_shipmode"):
+            F.flern_run_query_streamed(gq.ctx, gq.query, part, 1000, count=np.zeros(G, np.int64),
+                                       sum=np.zeros(G, np.int64))
+        bad = dict(db.fact)
+        bad["l_quantity"] = bad["l_quantity"].astype(np.float32)
+        with pytest.raises(F.FlernError, match="TYPE"):
+            F.flern_run_query_streamed(gq.ctx, gq.query, bad, 1000, count=np.zeros(G, np.int64),
+                                       sum=np.zeros(G, np.int64))
+        c, s_ = np.zeros(G, np.int64), np.zeros(G, np.int64)
+        gq.run(count=c, sum=s_)
+        assert (c == rc).all() and (s_ == rs).all()
     finally:
         gq.close()
 

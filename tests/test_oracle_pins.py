@@ -89,6 +89,37 @@ def test_tiny_query_golden():
     assert r.count_rej.tolist() == g["count_rej"] and r.sum_rej.tolist() == g["sum_rej"]
 
 
+def test_tiny_query_normalised_golden():
+    """The same hand-worked query with a non-unit dyadic normalisation x = (v - shift) * scale on a
+    fact feature and a dimension feature (reading Q4) and threshold sigmoid(15)
+    (tests/golden/tiny_query_norm.json): catches a divided scale, an added shift, a shift applied
+    after the scale, or the normalisation dropped for build-side features."""
+    g0, cfg, db, m = _tiny()
+    g = H.golden("tiny_query_norm.json")
+    m.shift = np.array(g["shift"], np.float32)
+    m.scale = np.array(g["scale"], np.float32)
+    t = 1.0 / (1.0 + math.exp(-g["threshold_logit"]))
+    r = O.run(cfg, db, m, per_row=True, threshold=t)
+    assert r.match[:, 0].tolist() == g0["match"]
+    assert [None if np.isnan(x) else x for x in r.logit] == g["logit"]
+    assert r.count.tolist() == g["count"] and r.sum.tolist() == g["sum"]
+    assert r.count_rej.tolist() == g["count_rej"] and r.sum_rej.tolist() == g["sum_rej"]
+
+
+def test_emulate_bf16_gather_rounding():
+    """The diagnostic bf16 emulation's gather: x = bf16_rne((v - shift) * scale), pinned on values whose
+    normalised form is exact in fp32 and falls on or between bf16 steps (ulp 2 at 256): 257 is a tie ->
+    256 (even), 259 a tie -> 260, 258 exact. The fp64 path keeps 257 / 259 / 258. Logistic regression
+    (no hidden layer), so logit = x."""
+    cfg = D.QueryConfig("e", 0.0, [1, 1], [("fact", "v")], [("dim", "fact", "k", "dk")], group=("fact", "g"),
+                        ngroups=1, sum_col=("fact", "g"), threshold=-math.inf)
+    fact = {"k": np.array([1, 1, 1], np.int32), "g": np.zeros(3, np.int32), "v": np.array([513, 517, 515], np.int32)}
+    db = D.Database(0, 3, fact, [("dim", 1, {"dk": np.array([1], np.int32)})])
+    m = H.SimpleModel([1, 1], [[[1.0]]], [[0.0]], shift=[-1.0], scale=[0.5])
+    assert O.run(cfg, db, m, per_row=True).logit.tolist() == [257.0, 259.0, 258.0]
+    assert O.run(cfg, db, m, per_row=True, emulate_bf16=True).logit.tolist() == [256.0, 260.0, 258.0]
+
+
 def test_spec_join_examples():
     """R={(1,a),(2,b)} ⋈ S={(2,x),(3,y)} -> (2,b,x); empty build side -> no rows."""
     _, cfg, _, _ = _tiny()
