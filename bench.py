@@ -39,7 +39,11 @@ WORKLOADS = {
     "c3": "TPC-H-shaped lineitem⋈orders⋈customer (two probes, SF10 per GPU), 32 features -> MLP "
           "32-1024-1024-1024-1, score>0.5, GROUP BY o_orderpriority COUNT/SUM(l_extendedprice)",
     "c4": "config 3 + l_shipdate pre-filter (~2%) before inference (SF10 per GPU), MLP 32-1024-1024-1024-1",
+    "c5": "TPC-H-shaped SF100 lineitem sharded by orderkey range across the GPUs (strong scaling), lineitem⋈orders "
+          "(orders + weights replicated), 16 features -> MLP 16-256-256-1, score>0.5, GROUP BY o_orderpriority "
+          "COUNT/SUM(l_extendedprice), NCCL reduce of the group partials",
 }
+STRONG = {"c5"}          # total work fixed as N grows; the others hold a fixed shard per GPU
 METRIC = "joined rows scored/sec (query+MLP, whole box)"
 
 
@@ -74,6 +78,8 @@ def workload_cfg(name, world):
         base, sf1 = D.CONFIGS["c3"], 10.0
     elif name == "c4":
         base, sf1 = D.CONFIGS["c4"], 10.0
+    elif name == "c5":   # strong scaling: SF100 in total, SF100/N per GPU
+        return D.CONFIGS["c5"], D.CONFIGS["c5"].sf / world
     else:
         raise SystemExit(f"unknown workload {name}")
     return D.with_sf(base, sf1 * world), sf1
@@ -204,7 +210,10 @@ def run_reference(args):
         return
     import oracle as O
     cfg, sf1 = workload_cfg(args.workload, world)
-    db = D.make_database(cfg, rank=0, world=world)
+    strong = args.workload in STRONG
+    # C5 (SF100): a prefix of rank 0's shard (its orders rows restricted to the same slots give the same
+    # join), so the host holds a bounded sample; the oracle's map build is over those orders only
+    db = D.make_database(cfg, rank=0, world=world, max_slots=2_000_000 if strong else None)
     model = D.make_model(cfg, D.make_database(cfg, max_slots=D.MODEL_SLOTS))
     threads = os.cpu_count() or 1
     # bounded sample per step: ~ (budget / (W+K)) seconds of oracle work each
@@ -228,7 +237,8 @@ def run_reference(args):
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": value, "unit": "rows/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t_total / max(1, args.steps),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "higher_is_better": True, "scaling": "strong" if strong else "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
         "config": {"workload": WORKLOADS[args.workload], "sf_per_gpu": sf1, "rows_per_gpu": db.fact_n,
                    "parallelism": f"oracle on rank 0 host cores (N={world})"},
         "cpu_baseline": {"value": value, "unit": "rows/s", "cores": threads, "kind": "oracle", "sample": sample},
@@ -269,18 +279,33 @@ def main():
     torch.cuda.set_stream(stream)
 
     cfg, sf1 = workload_cfg(args.workload, world)
-    db = D.make_database(cfg, rank=rank, world=world)
+    device = f"cuda:{local}"
+    strong = args.workload in STRONG
+    t_gen = time.perf_counter()
+    if strong:
+        # SF100: the shard is generated chunk by chunk straight into HBM; the orders table is drawn in
+        # slot shares and assembled on every GPU by an NCCL all_gather (replicated build side)
+        from datagen import device as DD
+        slo, shi = D.shard_slots(cfg.sf, rank, world)
+        n_fact, fact_dev = DD.fact_to_device(cfg, slo, shi, device)
+        db = D.Database(cfg.sf, n_fact, fact_dev, DD.builds_to_device(cfg, device, rank, world))
+        # host rows for the e2e leg and the cpu_baseline sample: a prefix of the shard (bounded host memory)
+        host = D.make_database(cfg, rank=rank, world=world, max_slots=min(shi - slo, 10_000_000))
+    else:
+        db = host = D.make_database(cfg, rank=rank, world=world)
+        # fact shard resident in HBM (torch tensors borrowed by the library, no copy)
+        fact_dev = {k: torch.from_numpy(v).to(device) for k, v in db.fact.items()}
+    gen_s = time.perf_counter() - t_gen
     # one model for every rank (replicated weights): normalisation from the first rows of the unsharded table
     model = D.make_model(cfg, D.make_database(cfg, max_slots=D.MODEL_SLOTS))
-    # fact shard resident in HBM (torch tensors borrowed by the library, no copy)
-    fact_dev = {k: torch.from_numpy(v).to(f"cuda:{local}") for k, v in db.fact.items()}
     gq = GpuQuery(cfg, db, model, device=local, stream=stream.cuda_stream, load_fact=False)
     gq.set_fact(F.flern_load_table(gq.ctx, "fact", fact_dev, F.FLERN_BORROW_DEVICE))
+    fact_bytes = sum(v.numel() * 4 for v in fact_dev.values())
     G = cfg.ngroups
-    out_count = torch.zeros(G, dtype=torch.int64, device=f"cuda:{local}")
-    out_sum = torch.zeros(G, dtype=torch.int64, device=f"cuda:{local}")
-    counters = torch.zeros(4, dtype=torch.int64, device=f"cuda:{local}")
-    partial = torch.zeros(2 * G, dtype=torch.int64, device=f"cuda:{local}")
+    out_count = torch.zeros(G, dtype=torch.int64, device=device)
+    out_sum = torch.zeros(G, dtype=torch.int64, device=device)
+    counters = torch.zeros(4, dtype=torch.int64, device=device)
+    partial = torch.zeros(2 * G, dtype=torch.int64, device=device)
     q_async = gq.make_query(gq.fact_id, flags=F.FLERN_Q_RESULT_DEVICE | F.FLERN_Q_ASYNC |
                             (F.FLERN_Q_NO_MODEL if args.no_model else 0))
 
@@ -315,7 +340,7 @@ def main():
             dist.barrier()
     ms_total = t_start.elapsed_time(t_end)
     kernel_ms = [a.elapsed_time(b) for a, b in evs]
-    t = torch.tensor([ms_total, float(rows_scored_rank)], dtype=torch.float64, device=f"cuda:{local}")
+    t = torch.tensor([ms_total, float(rows_scored_rank)], dtype=torch.float64, device=device)
     if world > 1:
         tmax = t[:1].clone()
         dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
@@ -327,9 +352,10 @@ def main():
     ms_per_step = ms_total / args.steps
     value = rows_total / (ms_per_step / 1e3)
 
-    # ---- end to end through the public API with host buffers (pinned), every step:
-    #      H2D of the fact shard + query + D2H of the result
-    pinned = {k: torch.from_numpy(v).pin_memory() for k, v in db.fact.items()}
+    # ---- end to end through the public API with host buffers (pinned), every step: H2D of the step's
+    #      fact rows + query + D2H of the result. Rows: this rank's shard (C5: a prefix of it, so the host
+    #      holds a bounded sample; the metric is a rate)
+    pinned = {k: torch.from_numpy(v).pin_memory() for k, v in host.fact.items()}
     h2d = sum(v.numel() * 4 for v in pinned.values())
     host_count, host_sum = np.zeros(G, np.int64), np.zeros(G, np.int64)
     d2h = 2 * G * 8 + 4 * 8
@@ -338,11 +364,11 @@ def main():
     # every step streams the shard from pinned host memory (the step's H2D) through the library's ring of
     # device chunk buffers, runs the query chunk by chunk and reads the result back (D2H); the e2e fact
     # table is a schema with no rows (flern_run_query_streamed)
-    e2e_tid = F.flern_load_table(gq.ctx, "fact_e2e", {k: np.zeros(0, v.dtype) for k, v in db.fact.items()})
+    e2e_tid = F.flern_load_table(gq.ctx, "fact_e2e", {k: np.zeros(0, v.dtype) for k, v in host.fact.items()})
     e2e_q = gq.make_query(e2e_tid)
 
     # 8 chunks: each chunk's H2D copy (second stream) overlaps the previous chunk's query (the paper's §3.2)
-    chunk = max(4, (db.fact_n + 7) // 8)
+    chunk = max(4, (host.fact_n + 7) // 8)
 
     def e2e_step():
         t0 = time.perf_counter()
@@ -352,7 +378,7 @@ def main():
         return r
 
     for _ in range(2):
-        e2e_step()
+        e2e_rows = int(e2e_step().rows_scored)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -361,10 +387,12 @@ def main():
         e2e_step()
     torch.cuda.synchronize()
     e2e_s = (time.perf_counter() - t0) / args.e2e_steps
-    et = torch.tensor([e2e_s], dtype=torch.float64, device=f"cuda:{local}")
+    et = torch.tensor([e2e_s], dtype=torch.float64, device=device)
+    er = torch.tensor([float(e2e_rows)], dtype=torch.float64, device=device)
     if world > 1:
         dist.all_reduce(et, op=dist.ReduceOp.MAX)
-    e2e_value = rows_total / float(et.item())
+        dist.all_reduce(er, op=dist.ReduceOp.SUM)
+    e2e_value = float(er.item()) / float(et.item())
 
     if rank == 0:
         tf_peak, hbm_peak, peak_src = peaks()
@@ -382,7 +410,7 @@ def main():
             other = sum(4 for k in db.fact if k != pf_name)
             alg_bytes = 4 * db.fact_n + other * rows_scored_rank
         else:
-            alg_bytes = h2d
+            alg_bytes = fact_bytes
         primary, secondary = binding_roofline(fpr, rows_scored_rank, alg_bytes, avg_kernel_ms, tf_peak, hbm_peak,
                                               f"{peak_src} ({peak_kind})", f"{peak_src} (copy bandwidth)")
         traffic = None
@@ -392,13 +420,16 @@ def main():
                 traffic = json.load(f).get(args.workload)
         line = {
             "metric": METRIC, "value": value, "unit": "rows/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "strong" if strong else "weak",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": {"workload": WORKLOADS[args.workload], "sf_per_gpu": sf1, "rows_per_gpu": db.fact_n,
                        "rows_scored_per_gpu": rows_scored_rank,
-                       "l2": "no flush: inputs larger than L2 (fact columns %.0f MB/GPU > 126 MB)" % (h2d / 1e6),
+                       "l2": "no flush: inputs larger than L2 (fact columns %.0f MB/GPU > 126 MB)" % (fact_bytes / 1e6),
                        "parallelism": f"dp{world}: fact sharded by orderkey range, orders + weights replicated, "
-                                      "NCCL reduce of int64 group partials"},
+                                      "NCCL reduce of int64 group partials",
+                       "build_ms": gq.build_ms, "datagen_s": round(gen_s, 1),
+                       "e2e_sample": f"{host.fact_n} of {db.fact_n} fact rows per GPU streamed per step"},
             "roofline": {**primary, "traffic": traffic,
                          "kernel": "flern_query_wide_kernel" if max(cfg.dims[1:-1]) > 256 else "flern_query_kernel",
                          "avg_launch_ms": avg_kernel_ms, "other": secondary},
@@ -407,7 +438,7 @@ def main():
             "clocks": clk.summary(),
         }
         if not args.no_cpu_baseline and world == 1:
-            line["cpu_baseline"] = cpu_baseline(cfg, db, model)
+            line["cpu_baseline"] = cpu_baseline(cfg, host, model)
         print(json.dumps(line), flush=True)
     gq.close()
     if world > 1:

@@ -665,9 +665,14 @@ extern "C" FLERN_API flern_status flern_build_hashtable(flern_ctx* ctx, int32_t 
   h.log2cap = lg;
   const int64_t cap = (int64_t)1 << lg;
   // Direct addressing with few payload words: fat entries {key, row, payload} of 8 or 16 words, so a
-  // probe is one dependent access that also brings the payload (bounded to 8 GB of entries)
+  // probe is one dependent access that also brings the payload. Bounded to 8 GB of entries, or a third
+  // of the free HBM (SF100's orders: 2^30 entries x 32 B = 34 GB, next to 31 GB of fact columns)
   const int32_t fs = npayload + 2 <= 8 ? 8 : (npayload + 2 <= 16 ? 16 : 0);
-  if (direct && t.nrows > 0 && fs > 0 && (uint64_t)cap * fs * 4 <= (8ull << 30) && !diag_env("FLERN_NO_FAT")) {
+  size_t free_b = 0, total_b = 0;
+  if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) free_b = 0;
+  const uint64_t fat_bytes = (uint64_t)cap * (uint64_t)(fs > 0 ? fs : 1) * 4;
+  const bool fat_fits = fat_bytes <= (8ull << 30) || fat_bytes <= free_b / 3;
+  if (direct && t.nrows > 0 && fs > 0 && fat_fits && !diag_env("FLERN_NO_FAT")) {
     h.fstride = fs;
     h.bytes = (size_t)cap * fs * sizeof(int32_t);
     CUDA_TRY(ctx, cudaMalloc(&h.slots, h.bytes));

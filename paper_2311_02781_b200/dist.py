@@ -27,10 +27,15 @@ def combine_partials(buf: torch.Tensor, dst: int | None = 0, group=None) -> torc
     single-rank run over the whole fact table."""
     if not dist.is_available() or not dist.is_initialized() or dist.get_world_size(group) == 1:
         return buf
+    # gloo (CPU process groups: tests, or several ranks sharing one GPU) reduces host tensors
+    staged = buf.is_cuda and dist.get_backend(group) == "gloo"
+    t = buf.cpu() if staged else buf
     if dst is None:
-        dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=group)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
     else:
-        dist.reduce(buf, dst=dst, op=dist.ReduceOp.SUM, group=group)
+        dist.reduce(t, dst=dst, op=dist.ReduceOp.SUM, group=group)
+    if staged:
+        buf.copy_(t)
     return buf
 
 

@@ -8,6 +8,8 @@ sum_col, threshold, prefilter, build_cols(p)); `db` has .fact (dict of columns),
 """
 from __future__ import annotations
 
+import time
+
 from . import flern as F
 
 
@@ -24,12 +26,17 @@ class GpuQuery:
         if load_fact:
             self.fact_id = F.flern_load_table(self.ctx, "fact", db.fact, fact_flags)
         self.build_ids, self.ht_ids = [], []
+        self.build_ms = 0.0   # flern_build_hashtable wall time (synchronous), all probes
         for p, (bt, src, key, bkey) in enumerate(cfg.probes):
             name, nrows, cols = db.builds[p]
-            tid = F.flern_load_table(self.ctx, f"{name}#{p}", cols, F.FLERN_COPY_HOST)
+            first = next(iter(cols.values()))
+            on_dev = getattr(first, "is_cuda", False)   # device tensors (datagen.device) are borrowed in place
+            tid = F.flern_load_table(self.ctx, f"{name}#{p}", cols, F.FLERN_BORROW_DEVICE if on_dev else F.FLERN_COPY_HOST)
             payload = [c for c in cfg.build_cols(p) if c != bkey]
             self.build_ids.append(tid)
+            t0 = time.perf_counter()
             self.ht_ids.append(F.flern_build_hashtable(self.ctx, tid, bkey, payload))
+            self.build_ms += 1e3 * (time.perf_counter() - t0)
         self.model_id = F.flern_load_model(self.ctx, "udf", model.dims, model.W, model.b, model.shift, model.scale)
         self.query = self.make_query(self.fact_id)
 

@@ -3,8 +3,8 @@
 Calls only oracle/ (and the input generator). For each config it builds the model with a raw
 output layer (w = u ~ U(±1), b = 0), runs the ORACLE on the first 65,536 joined rows of the
 config's database (a prefix of 65,536 order slots: the first rows are identical to the full
-database's), and stores mu = mean(logit_raw), s = 2 / std(logit_raw). datagen.make_model then
-uses w = bf16(s*u), b = bf16(-s*mu): std(logit) ~ 1 and selectivity ~ 50%, which keeps the
+database's), and stores mu = mean(logit_raw), s = TARGET_STD / std(logit_raw) (TARGET_STD = 1).
+datagen.make_model then uses w = bf16(s*u), b = bf16(-s*mu): std(logit) ~ 1 and selectivity ~ 50%, which keeps the
 parity band |B| (scores within 1e-2 of 0.5) near 3.2% of rows (hard part H6).
 """
 import json
