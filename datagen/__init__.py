@@ -166,6 +166,7 @@ class QueryConfig:
     threshold: float = 0.5
     model_seed: int = SEED
     match_rate: float = 1.0
+    multi: tuple = ()               # probes whose build keys may repeat (every match is emitted)
 
     def fact_cols(self):
         cols = []

@@ -30,7 +30,7 @@ class OrTable(ctypes.Structure):
 
 class OrProbe(ctypes.Structure):
     _fields_ = [("build_table", c_i32), ("src", c_i32), ("key_col", ctypes.c_char_p),
-                ("build_key_col", ctypes.c_char_p)]
+                ("build_key_col", ctypes.c_char_p), ("multi", c_i32)]
 
 
 class OrColref(ctypes.Structure):
@@ -147,7 +147,8 @@ def run(cfg, db, model, threshold=None, band=1e-2, per_row=False, emulate_bf16=F
         btables[i] = _table(cols, m, keep)
     probes = (OrProbe * max(1, len(cfg.probes)))()
     for p, (bt, src, key, bkey) in enumerate(cfg.probes):
-        probes[p] = OrProbe(p, _src(src), keep(key.encode()), keep(bkey.encode()))
+        probes[p] = OrProbe(p, _src(src), keep(key.encode()), keep(bkey.encode()),
+                            1 if p in getattr(cfg, "multi", ()) else 0)
     feats = (OrColref * max(1, len(cfg.feats)))()
     for k, (src, c) in enumerate(cfg.feats):
         feats[k] = OrColref(_src(src), keep(c.encode()))

@@ -139,9 +139,17 @@ extern "C" int or_run(const or_table* fact, int32_t nbuild, const or_table* buil
     return true;
   };
 
-  // ---- Build: map.update(leftHash(tuple), tuple) over each build side. ----
+  // ---- Build: map.update(leftHash(tuple), tuple) over each build side. A unique-key
+  // build maps key -> row; a multi build maps key -> every row with that key, in row order. ----
   std::vector<std::unordered_map<int64_t, int64_t>> maps(P);
+  std::vector<std::unordered_map<int64_t, std::vector<int64_t>>> mmaps(P);
   std::vector<Col> probe_key(P);
+  bool any_multi = false;
+  for (int32_t p = 0; p < P; ++p) any_multi = any_multi || q->probes[p].multi != 0;
+  if (any_multi && (res->score || res->logit || res->match || res->selected)) {
+    set_err(res, "per-row exports need unique build keys (a multi probe emits several tuples per row)");
+    return 1;
+  }
   for (int32_t p = 0; p < P; ++p) {
     const or_probe& pr = q->probes[p];
     if (pr.src >= p) { set_err(res, "probe source must be the fact table or an earlier probe"); return 1; }
@@ -151,6 +159,11 @@ extern "C" int or_run(const or_table* fact, int32_t nbuild, const or_table* buil
     if (!resolve(pr.src, pr.key_col, &probe_key[p])) return 1;
     if (bk.is_float || probe_key[p].is_float) { set_err(res, std::string("join key must be integer: ") + pr.key_col); return 1; }
     const or_table& bt = builds[pr.build_table];
+    if (pr.multi) {
+      mmaps[p].reserve((size_t)bt.nrows * 2);
+      for (int64_t r = 0; r < bt.nrows; ++r) mmaps[p][bk.get_int(r)].push_back(r);   // row order
+      continue;
+    }
     maps[p].reserve((size_t)bt.nrows * 2);
     for (int64_t r = 0; r < bt.nrows; ++r) {
       if (!maps[p].emplace(bk.get_int(r), r).second) {   // reading Q2: build keys must be unique
@@ -187,28 +200,8 @@ extern "C" int or_run(const or_table* fact, int32_t nbuild, const or_table* buil
     Acc& acc = accs[t];
     std::vector<double> x(K), h, hn;
     std::vector<int64_t> rows(P + 1);   // rows[0] = fact row, rows[p+1] = build row of probe p
-    for (int64_t i = a; i < b; ++i) {   // the record loop (P:757)
-      acc.scanned++;
-      const int64_t oi = i - lo;        // output index
-      if (res->score) res->score[oi] = NAN;
-      if (res->logit) res->logit[oi] = NAN;
-      if (res->match) for (int32_t p = 0; p < P; ++p) res->match[oi * P + p] = -1;
-      if (res->selected) res->selected[oi] = 0;
-      if (has_pf) {                     // pre-filter on a fact column (north_star config 4)
-        const int64_t v = pfcol.get_int(i);
-        if (!(q->pf_lo <= v && v < q->pf_hi)) continue;
-      }
-      acc.prefiltered++;
-      rows[0] = i;
-      bool hit = true;
-      for (int32_t p = 0; p < P && hit; ++p) {   // probe: inner join, a miss drops the row
-        const int64_t key = probe_key[p].get_int(rows[q->probes[p].src + 1]);
-        auto it = maps[p].find(key);
-        if (it == maps[p].end()) { hit = false; break; }
-        rows[p + 1] = it->second;
-        if (res->match) res->match[oi * P + p] = it->second;
-      }
-      if (!hit) continue;
+    // one joined tuple (fact row oi's output index): features -> model -> predicate -> group-by
+    auto tuple = [&](int64_t oi) -> bool {
       acc.joined++;
       // features: `float *tensor = data[i]->xs; // conversion` + normalisation (reading Q4)
       for (int32_t k = 0; k < K; ++k) {
@@ -216,7 +209,8 @@ extern "C" int or_run(const or_table* fact, int32_t nbuild, const or_table* buil
         if (!emu) {
           x[k] = (fcol[k].get(r) - (double)model->shift[k]) * (double)model->scale[k];
         } else {
-          // diagnostic: the GPU's documented gather, fp32 sub then fp32 mul, then bf16 RNE
+          // diagnostic: approximates the GPU's gather (fp32 sub then fp32 mul, then bf16 RNE; the GPU
+          // contracts it into one FFMA with -shift*scale, ~1 fp32 ulp apart, far inside the bf16 step)
           const float v = fcol[k].get_f32(r);
           const float d = v - model->shift[k];
           const float s = d * model->scale[k];
@@ -230,7 +224,7 @@ extern "C" int or_run(const or_table* fact, int32_t nbuild, const or_table* buil
       const int64_t g = gcol.get_int(rows[q->group.src + 1]);
       if (g < 0 || g >= G) {
         acc.err = "group code " + std::to_string(g) + " outside [0, ngroups)";
-        return;
+        return false;
       }
       const int64_t s = scol.get_int(rows[q->sum.src + 1]);
       const bool sel = score > q->threshold;   // `if (*y2 > 0.5)`, strict (reading Q8)
@@ -246,6 +240,67 @@ extern "C" int or_run(const or_table* fact, int32_t nbuild, const or_table* buil
         acc.sum_rej[g] += s;
       }
       if (in_band) { acc.band++; acc.cnt_band[g] += 1; acc.sum_band[g] += s; }
+      return true;
+    };
+    static const std::vector<int64_t> kNone;
+    std::vector<std::vector<int64_t>> single(P);   // a unique probe's match as a one-element list
+    std::vector<size_t> pos(P, 0);
+    std::vector<const std::vector<int64_t>*> lst(P, nullptr);
+    for (int64_t i = a; i < b; ++i) {   // the record loop (P:757)
+      acc.scanned++;
+      const int64_t oi = i - lo;        // output index
+      if (res->score) res->score[oi] = NAN;
+      if (res->logit) res->logit[oi] = NAN;
+      if (res->match) for (int32_t p = 0; p < P; ++p) res->match[oi * P + p] = -1;
+      if (res->selected) res->selected[oi] = 0;
+      if (has_pf) {                     // pre-filter on a fact column (north_star config 4)
+        const int64_t v = pfcol.get_int(i);
+        if (!(q->pf_lo <= v && v < q->pf_hi)) continue;
+      }
+      acc.prefiltered++;
+      rows[0] = i;
+      if (!any_multi) {
+        bool hit = true;
+        for (int32_t p = 0; p < P && hit; ++p) {   // probe: inner join, a miss drops the row
+          const int64_t key = probe_key[p].get_int(rows[q->probes[p].src + 1]);
+          auto it = maps[p].find(key);
+          if (it == maps[p].end()) { hit = false; break; }
+          rows[p + 1] = it->second;
+          if (res->match) res->match[oi * P + p] = it->second;
+        }
+        if (hit && !tuple(oi)) return;
+        continue;
+      }
+      // a multi probe emits every match: the joined tuples in nested-loop order, probes in
+      // order, a multi probe's matches in build-row order; a miss anywhere ends that branch
+      int32_t p = 0;
+      while (p >= 0) {
+        if (p == P) {
+          if (!tuple(oi)) return;
+          --p;
+          continue;
+        }
+        if (lst[p] == nullptr) {   // entering probe p: look its key up
+          const int64_t key = probe_key[p].get_int(rows[q->probes[p].src + 1]);
+          if (q->probes[p].multi) {
+            auto it = mmaps[p].find(key);
+            lst[p] = it == mmaps[p].end() ? &kNone : &it->second;
+          } else {
+            auto it = maps[p].find(key);
+            single[p].clear();
+            if (it != maps[p].end()) single[p].push_back(it->second);
+            lst[p] = &single[p];
+          }
+          pos[p] = 0;
+        }
+        if (pos[p] < lst[p]->size()) {
+          rows[p + 1] = (*lst[p])[pos[p]++];
+          ++p;
+        } else {   // probe p exhausted: back to p - 1
+          lst[p] = nullptr;
+          --p;
+        }
+      }
     }
   };
   if (nthreads == 1) {

@@ -30,7 +30,10 @@ typedef struct {
   int32_t build_table;       /* index into builds[] */
   int32_t src;               /* -1 = fact row, else index of an earlier probe */
   const char* key_col;       /* probe-side key column (on src) */
-  const char* build_key_col; /* build-side key column (unique) */
+  const char* build_key_col; /* build-side key column (unique unless multi) */
+  int32_t multi;             /* 1: duplicate build keys allowed; the probe emits every match, in build-row
+                                order (P:328-331 `for (lTuple <- map(rightHash(rTuple)) ...)`
+                                multimap semantics, S:216 insertion order within a key) */
 } or_probe;
 typedef struct { int32_t src; const char* col; } or_colref;   /* src: -1 fact, p = probe p's build row */
 
@@ -64,11 +67,13 @@ typedef struct {
   int64_t* count_rej; int64_t* sum_rej;    /* [ngroups] joined rows with score <= threshold (optional) */
   int64_t* count_hi; int64_t* sum_hi;      /* [ngroups] selected AND outside the band (optional) */
   int64_t* count_band; int64_t* sum_band;  /* [ngroups] inside the band, |score - t| <= band (optional) */
+  /* per-row exports (one joined tuple per fact row): only for queries whose probes are all unique-key
+     (a multi probe can emit several tuples per fact row: or_run returns an error if any is requested) */
   double* score;                           /* [rows] optional: fp64 score, NaN if the row never reached the model */
   double* logit;                           /* [rows] optional: fp64 logit, NaN likewise */
   int64_t* match;                          /* [rows * nprobes] optional: build row id, -1 = miss / not reached */
   uint8_t* selected;                       /* [rows] optional: 1 if selected */
-  int64_t rows_scanned, rows_prefiltered, rows_joined, rows_selected, rows_band;
+  int64_t rows_scanned, rows_prefiltered, rows_joined, rows_selected, rows_band;   /* joined: joined tuples */
   char error[256];
 } or_result;
 

@@ -296,3 +296,54 @@ def test_multithreaded_equals_single_thread():
     b = O.run(cfg, db, model, nthreads=5, per_row=True)
     assert a.count.tolist() == b.count.tolist() and a.sum.tolist() == b.sum.tolist()
     assert np.array_equal(a.score, b.score, equal_nan=True)
+
+
+# ------------------------------------------------------------------- NEXT-4: chains, duplicate keys
+def test_spec_multimap_example():
+    """duplicate left keys {(2,b),(2,c)} ⋈ {(2,x)} -> (2,b,x), (2,c,x): the probe emits every
+    match (P:328-331 iterates map(rightHash(rTuple))). Group by the build row, sum the fact value."""
+    cfg = D.QueryConfig("m", 0.0, [1, 1], [("fact", "v")], [("dim", "fact", "k", "dk")], group=(0, "dg"),
+                        ngroups=3, sum_col=("fact", "v"), threshold=-math.inf, multi=(0,))
+    fact = {"k": np.array([2, 5], np.int32), "v": np.array([7, 11], np.int32)}
+    dim = {"dk": np.array([2, 2, 9], np.int32), "dg": np.array([0, 1, 2], np.int32)}   # b, c, (no match)
+    r = O.run(cfg, D.Database(0, 2, fact, [("dim", 3, dim)]), H.zero_model([1, 1]))
+    assert r.rows_joined == 2 and r.count.tolist() == [1, 1, 0] and r.sum.tolist() == [7, 7, 0]
+    with pytest.raises(O.OracleError, match="per-row exports need unique build keys"):
+        O.run(cfg, D.Database(0, 2, fact, [("dim", 3, dim)]), H.zero_model([1, 1]), per_row=True)
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+@pytest.mark.parametrize("dup", [True, False])
+def test_chain_and_duplicate_keys_match_sorted_expansion(seed, dup):
+    """Three probes (fact->A with repeating keys when `dup`, A->B, fact->C), threshold -INF: joined tuple
+    count and per-group aggregates equal the vectorised sorted-search expansion (tests/helpers.expand_join);
+    with a model selecting on a build-side feature (relu(b_q - 24.5) - relu(24.5 - b_q) > 0, i.e. b_q >= 25)
+    the selected aggregates equal the expansion filtered on B's column: each tuple's features come from its
+    own build rows."""
+    cfg, db = H.star_chain_db(seed, dup=dup)
+    fr, br = H.expand_join(cfg, db)
+    assert len(fr) > 100 and (not dup or len(fr) > len(np.unique(fr)))
+    r = O.run(cfg, db, H.zero_model(cfg.dims), threshold=-math.inf)
+    cnt, sm = H.tuple_aggregate(cfg, db, fr, br, np.ones(len(fr), bool))
+    assert r.rows_joined == len(fr) and r.count.tolist() == cnt.tolist() and r.sum.tolist() == sm.tolist()
+    k = cfg.feats.index((1, "b_q"))
+    W1 = np.zeros((64, 8), np.float32)
+    W1[0, k], W1[1, k] = 1.0, -1.0
+    w2 = np.zeros((1, 64), np.float32)
+    w2[0, 0], w2[0, 1] = 1.0, -1.0
+    shift = np.zeros(8, np.float32)
+    shift[k] = 24.5
+    m = H.SimpleModel(cfg.dims, [W1, w2], [np.zeros(64), np.zeros(1)], shift=shift)
+    r = O.run(cfg, db, m)
+    q = H.tuple_column(cfg, db, (1, "b_q"), fr, br)
+    cnt, sm = H.tuple_aggregate(cfg, db, fr, br, q >= 25)
+    assert r.rows_band == 0 and r.count.tolist() == cnt.tolist() and r.sum.tolist() == sm.tolist()
+
+
+def test_three_probe_chain_join_ids_match_sorted_search():
+    """Unique keys on every probe: per-row join ids of the 3-probe chain equal a sorted-array search per
+    probe (helpers.chain_matches)."""
+    cfg, db = H.star_chain_db(3, dup=False)
+    r = O.run(cfg, db, H.zero_model(cfg.dims), per_row=True, threshold=-math.inf)
+    match, alive = H.chain_matches(cfg, db)
+    assert np.array_equal(r.match, match) and r.rows_joined == int(alive.sum()) > 100
