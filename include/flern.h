@@ -132,6 +132,16 @@ FLERN_API flern_status flern_load_model(flern_ctx* ctx, const char* name, int32_
 FLERN_API flern_status flern_build_hashtable(flern_ctx* ctx, int32_t table_id, const char* key_col,
                                              int32_t npayload, const char* const* payload_cols, int32_t* ht_id);
 
+enum {
+  FLERN_HT_MULTI = 0x1   /* the build key may repeat (a multimap, NEXT-4): a probe emits one joined tuple per
+                            matching build row, in build-row order (P:328-331 iterates map(rightHash(rTuple));
+                            SPEC S:212-216). Without it a repeated key is FLERN_E_DUP_KEY. */
+};
+/* flern_build_hashtable with flags (FLERN_HT_MULTI). flags = 0 is flern_build_hashtable. */
+FLERN_API flern_status flern_build_hashtable_ex(flern_ctx* ctx, int32_t table_id, const char* key_col,
+                                                int32_t npayload, const char* const* payload_cols, uint32_t flags,
+                                                int32_t* ht_id);
+
 /* ------------------------------------------------------------------------------------------ */
 typedef struct {
   int32_t ht_id;       /* hash table to probe */
@@ -148,7 +158,11 @@ typedef struct {
   int32_t fact_table;
   const char* prefilter_col;      /* integer fact column; keep rows with pf_lo <= v < pf_hi; NULL = none */
   int64_t pf_lo, pf_hi;
-  int32_t nprobes;                /* 1 or 2 inner joins, applied in order; a miss drops the row */
+  int32_t nprobes;                /* 1..8 inner joins, applied in order; a miss drops the row. The fused
+                                     kernel probes fact -> A (-> B keyed by a payload column of A) itself;
+                                     any other chain (more probes, a star of fact keys, a multimap build
+                                     side) first expands into joined tuples (2 more launches + 1 host sync;
+                                     per-row debug exports unavailable) */
   const flern_probe* probes;
   int32_t model_id;
   int32_t nfeat;                  /* UDF arguments; must equal the model's dims[0] (FLERN_E_ARITY) */
@@ -214,7 +228,8 @@ FLERN_API flern_status flern_run_query_streamed(flern_ctx* ctx, const flern_quer
 
 #define FLERN_TRACE_EVENTS 26
 
-/* Number of CUDA kernels flern_run_query launches per call (for launch accounting): 1. */
+/* Number of CUDA kernels flern_run_query launches per call (for launch accounting): 1 (an expanded
+ * join adds its two expansion kernels). */
 FLERN_API int32_t flern_query_launches(void);
 
 #ifdef __cplusplus

@@ -8,7 +8,8 @@ namespace flern {
 constexpr int kMaxFeat = 48;
 constexpr int kMaxGroups = 64;          // group domains aggregated per CTA (registers / SMEM partials)
 constexpr int kMaxGroupsLarge = 1 << 22; // larger domains: per-row int64 atomics into the global result
-constexpr int kMaxProbes = 2;
+constexpr int kMaxProbes = 2;            // probes resolved inside the fused kernel (fact -> A, A -> B)
+constexpr int kMaxChain = 8;             // probes of an expanded join (join_kernel.cuh): any chain, multimap
 constexpr int kTile = 128;
 // Narrow kernel: 16 warps. SMSP k runs warps k, k+4, k+8, k+12. The MMA issuer (warp 12) shares
 // SMSP 0 only with the two quadrant-0 epilogue warps: the six producer warps (1, 2, 3, 13, 14, 15)
@@ -136,6 +137,14 @@ struct QueryParams {
   int32_t* dbg_match;       // optional [nrows * nprobes]
   uint32_t* dbg_selected;   // optional bitmap
   unsigned long long* dbg_trace;  // optional [kTraceEvents][kTraceTiles] clock64 stamps of CTA 0
+  // Expanded joins (join_kernel.cuh materialised every joined tuple: chains beyond kMaxProbes, multimap
+  // probes). The kernel then reads rows [0, nrows) of `tuples` = {fact row, idx_0 .. idx_{P-1}} (tstride
+  // words each) instead of probing: payload word w of probe q's match is tbase[q][idx_q * tpstr[q] + w].
+  const int32_t* tuples;           // nullptr: the kernel probes itself
+  int32_t tstride;
+  const int32_t* tbase[kMaxChain];
+  int32_t tpstr[kMaxChain];
+  int64_t scanned;                 // tuple mode: fact rows the expansion scanned (counters[0])
 };
 
 // Pipeline trace (diagnostic): clock64() at each hand-off, CTA 0, first kTraceTiles tiles/batches.
@@ -444,8 +453,8 @@ __device__ __forceinline__ void write_partials_and_reduce(const QueryParams& p, 
           int64_t* out = kind == 0 ? p.out_count : p.out_sum;
           out[cls * G + g] = t;
         }
-      } else {
-        p.out_counters[i - G * 4] = t;
+      } else {   // counters; an expanded join reports the fact rows its expansion scanned
+        p.out_counters[i - G * 4] = (i == G * 4 && p.tuples) ? p.scanned : t;
       }
     }
     if (tid == 0) { *p.ticket = 0u; *p.work = 0ull; }

@@ -14,6 +14,7 @@
 
 #include "flern.h"
 #include "build_kernel.cuh"
+#include "join_kernel.cuh"
 #include "query_kernel.cuh"
 #include "wide_kernel.cuh"
 
@@ -65,6 +66,8 @@ struct HashTable {
   size_t bytes = 0;
   int32_t pstride = 0;
   int32_t fstride = 0;                   // > 0: fat direct-addressed entries (build_fat_kernel)
+  bool multi = false;                    // duplicate keys: {key, start, count, fill} slots + perm (join_kernel.cuh)
+  int32_t* perm = nullptr;               // multi: build rows grouped by key
   std::vector<std::string> pcols;
   std::vector<flern_dtype> ptypes;
   int find(const char* n) const {
@@ -118,6 +121,9 @@ struct flern_ctx {
   std::vector<cudaEvent_t> ring_copied, ring_read;
   int64_t* chunk_res = nullptr;
   size_t chunk_res_slots = 0;
+  // expanded joins (join_kernel.cuh): the tuple buffer (grown on demand) and the pass counter
+  int32_t* tuples = nullptr;
+  size_t tuple_words = 0;
   // host-side results of large group domains (> kMaxGroups): [count | sum] device buffer
   int64_t* big_res = nullptr;
   size_t big_slots = 0;
@@ -291,6 +297,7 @@ extern "C" FLERN_API void flern_destroy(flern_ctx* ctx) {
   if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
   cudaFree(ctx->ring);
   cudaFree(ctx->chunk_res);
+  cudaFree(ctx->tuples);
   cudaFree(ctx->big_res);
   cudaFree(ctx->partials);
   cudaFree(ctx->ticket);
@@ -610,10 +617,22 @@ extern "C" FLERN_API flern_status flern_load_model(flern_ctx* ctx, const char* n
 }
 
 // ================================================================================ hash tables
+namespace {
+flern_status build_multimap(flern_ctx* ctx, HashTable& h, const Table& t, const Column* kc, const PayloadCols& pc,
+                            int32_t npayload, int32_t* ht_id);
+}
+
 extern "C" FLERN_API flern_status flern_build_hashtable(flern_ctx* ctx, int32_t table_id, const char* key_col,
                                                         int32_t npayload, const char* const* payload_cols,
                                                         int32_t* ht_id) {
+  return flern_build_hashtable_ex(ctx, table_id, key_col, npayload, payload_cols, 0u, ht_id);
+}
+
+extern "C" FLERN_API flern_status flern_build_hashtable_ex(flern_ctx* ctx, int32_t table_id, const char* key_col,
+                                                           int32_t npayload, const char* const* payload_cols,
+                                                           uint32_t flags, int32_t* ht_id) {
   if (!ctx) return FLERN_E_INVALID_ARG;
+  if (flags & ~(uint32_t)FLERN_HT_MULTI) return fail(ctx, FLERN_E_INVALID_ARG, "flern_build_hashtable_ex: unknown flags");
   if (!key_col || !ht_id || npayload < 0 || (npayload > 0 && !payload_cols))
     return fail(ctx, FLERN_E_INVALID_ARG, "flern_build_hashtable: bad arguments");
   if (npayload > kMaxFeat + 4) return fail(ctx, FLERN_E_UNSUPPORTED, "at most %d payload columns", kMaxFeat + 4);
@@ -639,6 +658,7 @@ extern "C" FLERN_API flern_status flern_build_hashtable(flern_ctx* ctx, int32_t 
   }
   h.pstride = npayload <= 0 ? 1 : npayload;   // payload rows hold exactly the needed words
   CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+  if (flags & FLERN_HT_MULTI) return build_multimap(ctx, h, t, kc, pc, npayload, ht_id);
   // key range first: it picks the hash function and the capacity
   int32_t mm[2] = {0x7FFFFFFF, (int32_t)0x80000000};
   if (t.nrows > 0) {
@@ -705,7 +725,7 @@ extern "C" FLERN_API flern_status flern_build_hashtable(flern_ctx* ctx, int32_t 
   h.bytes = cap * sizeof(unsigned long long) + std::max<int64_t>(1, t.nrows) * h.pstride * sizeof(int32_t);
   CUDA_TRY(ctx, cudaMalloc(&h.slots, h.bytes));
   h.payload = reinterpret_cast<int32_t*>(h.slots + cap);
-  int32_t flags[3] = {0, 0, 0};
+  int32_t bflags[3] = {0, 0, 0};
   for (int attempt = 0; attempt < 2; ++attempt) {
     HashFn hf{};
     hf.mask = (uint32_t)(cap - 1);
@@ -721,25 +741,91 @@ extern "C" FLERN_API flern_status flern_build_hashtable(flern_ctx* ctx, int32_t 
       build_insert_kernel<<<grid_for(t.nrows), 256, 0, ctx->stream>>>(static_cast<const int32_t*>(kc->dptr), t.nrows,
                                                                       h.slots, hf, ctx->dflags);
     CUDA_TRY(ctx, cudaGetLastError());
-    CUDA_TRY(ctx, cudaMemcpyAsync(flags, ctx->dflags, sizeof(flags), cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_TRY(ctx, cudaMemcpyAsync(bflags, ctx->dflags, sizeof(bflags), cudaMemcpyDeviceToHost, ctx->stream));
     CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
     h.hf = hf;
-    if (!(hf.mode == 1 && flags[2] > 64 && !flags[0] && !flags[1])) break;   // long chains: retry
+    if (!(hf.mode == 1 && bflags[2] > 64 && !bflags[0] && !bflags[1])) break;   // long chains: retry
   }
   if (t.nrows > 0 && npayload > 0)
     pack_payload_kernel<<<grid_for(t.nrows * h.pstride), 256, 0, ctx->stream>>>(pc, npayload, h.pstride, t.nrows,
                                                                                 h.payload);
   CUDA_TRY(ctx, cudaGetLastError());
   CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
-  if (flags[0] || flags[1]) {
+  if (bflags[0] || bflags[1]) {
     cudaFree(h.slots);
-    if (flags[1]) return fail(ctx, FLERN_E_INVALID_ARG, "key column '%s' contains the reserved value INT32_MIN", key_col);
+    if (bflags[1]) return fail(ctx, FLERN_E_INVALID_ARG, "key column '%s' contains the reserved value INT32_MIN", key_col);
     return fail(ctx, FLERN_E_DUP_KEY, "key column '%s' of table '%s' is not unique", key_col, t.name.c_str());
   }
   ctx->hts.push_back(std::move(h));
   *ht_id = (int32_t)ctx->hts.size() - 1;
   return FLERN_OK;
 }
+
+namespace {
+// Multimap build side (FLERN_HT_MULTI, join_kernel.cuh): {key, start, count, fill} slots over the distinct
+// keys (power-of-two capacity >= 2 x rows), perm = the rows of each key in ascending order, payload by row.
+flern_status build_multimap(flern_ctx* ctx, HashTable& h, const Table& t, const Column* kc, const PayloadCols& pc,
+                            int32_t npayload, int32_t* ht_id) {
+  const int64_t n = t.nrows;
+  const int32_t* keys = static_cast<const int32_t*>(kc->dptr);
+  int32_t mm[2] = {0x7FFFFFFF, (int32_t)0x80000000};
+  if (n > 0) {
+    CUDA_TRY(ctx, cudaMemcpyAsync(ctx->dflags + 4, mm, sizeof(mm), cudaMemcpyHostToDevice, ctx->stream));
+    key_minmax_kernel<<<std::min(grid_for(n), 1024), 256, 0, ctx->stream>>>(keys, n, ctx->dflags + 4);
+    CUDA_TRY(ctx, cudaMemcpyAsync(mm, ctx->dflags + 4, sizeof(mm), cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  }
+  const uint64_t range = n > 0 ? (uint64_t)((int64_t)mm[1] - (int64_t)mm[0]) + 1 : 1;
+  uint32_t lg = 6;
+  while (((int64_t)1 << lg) < 2 * n) ++lg;
+  const bool direct = n > 0 && range <= 8ull * (uint64_t)n && range <= (1ull << 30);
+  if (direct)
+    while (((uint64_t)1 << lg) < range) ++lg;
+  const int64_t cap = (int64_t)1 << lg;
+  HashFn hf{};
+  hf.mask = (uint32_t)(cap - 1);
+  hf.shift = 32u - lg;
+  hf.kmin = mm[0];
+  hf.mode = direct ? 2u : ((n > 0 && range <= 16ull * (uint64_t)cap && range < (1ull << 32)) ? 1u : 0u);
+  hf.mulc = hf.mode == 1 ? (uint32_t)std::min<uint64_t>(0xFFFFFFFFull, ((uint64_t)cap << 32) / range) : 0u;
+  const int64_t nb = (cap + kScanBlock - 1) / kScanBlock;
+  const size_t slot_b = (size_t)cap * 16, perm_b = (size_t)std::max<int64_t>(1, n) * 4,
+               pay_b = (size_t)std::max<int64_t>(1, n) * h.pstride * 4, sums_b = (size_t)nb * 4;
+  h.bytes = slot_b + perm_b + pay_b + sums_b;
+  CUDA_TRY(ctx, cudaMalloc(&h.slots, h.bytes));
+  uint8_t* base = reinterpret_cast<uint8_t*>(h.slots);
+  int32_t* w = reinterpret_cast<int32_t*>(base);
+  h.perm = reinterpret_cast<int32_t*>(base + slot_b);
+  h.payload = reinterpret_cast<int32_t*>(base + slot_b + perm_b);
+  int32_t* sums = reinterpret_cast<int32_t*>(base + slot_b + perm_b + pay_b);
+  h.multi = true;
+  h.hf = hf;
+  h.log2cap = lg;
+  CUDA_TRY(ctx, cudaMemsetAsync(ctx->dflags, 0, 16, ctx->stream));
+  mm_fill_kernel<<<grid_for(cap), 256, 0, ctx->stream>>>(reinterpret_cast<int4*>(w), cap);
+  if (n > 0) mm_count_kernel<<<grid_for(n), 256, 0, ctx->stream>>>(keys, n, w, hf, ctx->dflags);
+  mm_block_sums_kernel<<<(unsigned)nb, kScanBlock, 0, ctx->stream>>>(w, cap, sums);
+  mm_scan_sums_kernel<<<1, kScanBlock, 0, ctx->stream>>>(sums, nb);
+  mm_block_scan_kernel<<<(unsigned)nb, kScanBlock, 0, ctx->stream>>>(w, cap, sums);
+  if (n > 0) {
+    mm_place_kernel<<<grid_for(n), 256, 0, ctx->stream>>>(keys, n, w, hf, h.perm);
+    mm_sort_kernel<<<grid_for(cap), 256, 0, ctx->stream>>>(w, cap, h.perm);
+    if (npayload > 0)
+      pack_payload_kernel<<<grid_for(n * h.pstride), 256, 0, ctx->stream>>>(pc, npayload, h.pstride, n, h.payload);
+  }
+  CUDA_TRY(ctx, cudaGetLastError());
+  int32_t flags[3] = {0, 0, 0};
+  CUDA_TRY(ctx, cudaMemcpyAsync(flags, ctx->dflags, sizeof(flags), cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  if (flags[1]) {
+    cudaFree(h.slots);
+    return fail(ctx, FLERN_E_INVALID_ARG, "key column '%s' contains the reserved value INT32_MIN", h.key_col.c_str());
+  }
+  ctx->hts.push_back(std::move(h));
+  *ht_id = (int32_t)ctx->hts.size() - 1;
+  return FLERN_OK;
+}
+}  // namespace
 
 // ================================================================================ queries
 namespace {
@@ -753,6 +839,8 @@ struct Prepared {
   QueryParams p;
   KernelEntry* ke = nullptr;
   const Model* m = nullptr;
+  bool expand = false;   // chains beyond the kernel's own probes / multimap: join_kernel.cuh expansion first
+  ExpandParams ep;
 };
 
 // Every validation of a query and the kernel parameters it resolves to; no device work except
@@ -770,8 +858,8 @@ flern_status prepare_query(flern_ctx* ctx, const flern_query* q, const FactWindo
   if (q->nfeat != m.K0)
     return fail(ctx, FLERN_E_ARITY, "UDF '%s' takes %d arguments, query passes %d", m.name.c_str(), m.K0, q->nfeat);
   if (q->nfeat > 0 && !q->feats) return fail(ctx, FLERN_E_INVALID_ARG, "null feature list");
-  if (q->nprobes < 1 || q->nprobes > kMaxProbes || !q->probes)
-    return fail(ctx, FLERN_E_UNSUPPORTED, "queries need 1..%d probes (got %d)", kMaxProbes, q->nprobes);
+  if (q->nprobes < 1 || q->nprobes > kMaxChain || !q->probes)
+    return fail(ctx, FLERN_E_UNSUPPORTED, "queries need 1..%d probes (got %d)", kMaxChain, q->nprobes);
   if (q->ngroups < 1 || q->ngroups > kMaxGroupsLarge)
     return fail(ctx, FLERN_E_UNSUPPORTED, "ngroups %d outside 1..%d", q->ngroups, kMaxGroupsLarge);
   if (q->ngroups > kMaxGroups && win)
@@ -791,15 +879,52 @@ flern_status prepare_query(flern_ctx* ctx, const flern_query* q, const FactWindo
     return fail(ctx, FLERN_E_NOT_FOUND, "streamed query reads fact column '%s', which host_cols does not supply", col);
   };
   p.nprobes = q->nprobes;
+  // The fused kernel probes a chain fact -> A (-> B keyed by A) of unique-key tables itself; any other
+  // chain, or a multimap build side, is expanded into joined tuples first (join_kernel.cuh)
+  bool expand = q->nprobes > kMaxProbes;
   for (int i = 0; i < q->nprobes; ++i) {
     const flern_probe& pr = q->probes[i];
     if (pr.ht_id < 0 || pr.ht_id >= (int32_t)ctx->hts.size())
       return fail(ctx, FLERN_E_NOT_FOUND, "probe %d: no hash table with id %d", i, pr.ht_id);
+    if (pr.src < -1 || pr.src >= i) return fail(ctx, FLERN_E_INVALID_ARG, "probe %d: source must be -1 or an earlier probe", i);
+    expand = expand || ctx->hts[pr.ht_id].multi || (i == 0) != (pr.src == -1);
+  }
+  out.expand = expand;
+  ExpandParams& ep = out.ep;
+  std::memset(&ep, 0, sizeof(ep));
+  ep.nprobes = q->nprobes;
+  for (int i = 0; i < q->nprobes; ++i) {
+    const flern_probe& pr = q->probes[i];
     const HashTable& h = ctx->hts[pr.ht_id];
     if (!pr.key_col) return fail(ctx, FLERN_E_INVALID_ARG, "probe %d: null key column", i);
-    if (pr.src < -1 || pr.src >= i) return fail(ctx, FLERN_E_INVALID_ARG, "probe %d: source must be -1 or an earlier probe", i);
-    if ((i == 0) != (pr.src == -1))
-      return fail(ctx, FLERN_E_UNSUPPORTED, "probe %d: the first probe is keyed by a fact column, the second by probe 0", i);
+    // expansion view of this probe, and where a tuple's payload words live (QueryParams::tbase/tpstr)
+    ChainProbe& cp = ep.probe[i];
+    cp.kind = h.multi ? CK_MULTI : (h.fstride ? CK_FAT : CK_SLOTS);
+    cp.table = reinterpret_cast<const int32_t*>(h.slots);
+    cp.hf = h.hf;
+    cp.fstride = h.fstride;
+    cp.perm = h.perm;
+    cp.pbase = h.fstride ? reinterpret_cast<const int32_t*>(h.slots) + 2 : h.payload;
+    cp.pstr = h.fstride ? h.fstride : h.pstride;
+    cp.src = pr.src;
+    p.tbase[i] = cp.pbase;
+    p.tpstr[i] = cp.pstr;
+    if (i >= kMaxProbes) {   // expanded only: no in-kernel probe descriptor
+      if (pr.src < 0) {
+        const Column* c = fact.find(pr.key_col);
+        if (!c) return fail(ctx, FLERN_E_NOT_FOUND, "fact table '%s' has no column '%s'", fact.name.c_str(), pr.key_col);
+        if (!is_int_type(c->dtype)) return fail(ctx, FLERN_E_TYPE, "probe key '%s' must be integer-typed", pr.key_col);
+        cp.fact_key = fact_base(c);
+        if (cp.fact_key == missing) return not_streamed(pr.key_col);
+      } else {
+        const HashTable& hs = ctx->hts[q->probes[pr.src].ht_id];
+        const int w = hs.find(pr.key_col);
+        if (w < 0) return fail(ctx, FLERN_E_NOT_FOUND, "probe %d: '%s' is not a payload column of probe %d", i, pr.key_col, pr.src);
+        if (!is_int_type(hs.ptypes[w])) return fail(ctx, FLERN_E_TYPE, "probe key '%s' must be integer-typed", pr.key_col);
+        cp.key_word = w;
+      }
+      continue;
+    }
     ProbeDesc& d = p.probe[i];
     d.slots = reinterpret_cast<const int2*>(h.slots);
     d.hf = h.hf;
@@ -814,12 +939,14 @@ flern_status prepare_query(flern_ctx* ctx, const flern_query* q, const FactWindo
       if (!is_int_type(c->dtype)) return fail(ctx, FLERN_E_TYPE, "probe key '%s' must be integer-typed", pr.key_col);
       d.fact_key = fact_base(c);
       if (d.fact_key == missing) return not_streamed(pr.key_col);
+      cp.fact_key = d.fact_key;
     } else {
       const HashTable& hs = ctx->hts[q->probes[pr.src].ht_id];
       const int w = hs.find(pr.key_col);
       if (w < 0) return fail(ctx, FLERN_E_NOT_FOUND, "probe %d: '%s' is not a payload column of probe %d", i, pr.key_col, pr.src);
       if (!is_int_type(hs.ptypes[w])) return fail(ctx, FLERN_E_TYPE, "probe key '%s' must be integer-typed", pr.key_col);
       d.key_word = w;
+      cp.key_word = w;
     }
   }
   auto resolve = [&](const flern_colref& r, ColDesc* out, bool need_int, const char* what) -> flern_status {
@@ -858,8 +985,8 @@ flern_status prepare_query(flern_ctx* ctx, const flern_query* q, const FactWindo
   // kernel order: fact-column features first (one vector load per column before the probe),
   // then build-payload features; the model image's W1 columns follow the same permutation
   std::vector<int> perm;
-  int nsrc[3] = {0, 0, 0};
-  for (int src = 0; src < 3; ++src)
+  int nsrc[kMaxChain + 1] = {0};
+  for (int src = 0; src <= q->nprobes; ++src)
     for (int k = 0; k < q->nfeat; ++k)
       if (fq[k].src == src) { perm.push_back(k); ++nsrc[src]; }
   p.nfact = nsrc[0];
@@ -915,9 +1042,17 @@ flern_status prepare_query(flern_ctx* ctx, const flern_query* q, const FactWindo
   p.bout = m.bout;
   p.shift = reinterpret_cast<const float*>(img + m.off_shift);
   p.scale = reinterpret_cast<const float*>(img + m.off_scale);
-  // group domains beyond kMaxGroups need the generic-shape kernels (GroupAgg<true>)
-  // (FLERN_Q_GENERIC_KERNEL: the run-time-shape producer, for tests that compare the two)
-  KernelEntry* ke = (q->ngroups > kMaxGroups || (q->flags & FLERN_Q_GENERIC_KERNEL))
+  if (expand) {   // the expansion applies the pre-filter and scans the fact rows
+    ep.nrows = p.nrows;
+    ep.pf_col = p.pf_col;
+    ep.pf_lo = p.pf_lo;
+    ep.pf_hi = p.pf_hi;
+    ep.tstride = 1 + q->nprobes;
+    if (q->nprobes < 2) p.probe[1] = p.probe[0];
+  }
+  // group domains beyond kMaxGroups need the generic-shape kernels (GroupAgg<true>), and so do expanded
+  // joins (tuple input); FLERN_Q_GENERIC_KERNEL: the run-time-shape producer, for tests that compare the two
+  KernelEntry* ke = (expand || q->ngroups > kMaxGroups || (q->flags & FLERN_Q_GENERIC_KERNEL))
                         ? find_kernel(m.K0P, m.H, m.NL)
                         : find_kernel(m.K0P, m.H, m.NL, nsrc[0], nsrc[1], nsrc[2], p.fmask);
   if (!ke) return fail(ctx, FLERN_E_UNSUPPORTED, "no kernel for model '%s'", m.name.c_str());
@@ -965,6 +1100,45 @@ flern_status launch_query(flern_ctx* ctx, const flern_query* q, Prepared& pq, fl
   p.partials = reinterpret_cast<unsigned long long*>(ctx->partials);
   p.ticket = ctx->ticket;
   p.work = reinterpret_cast<unsigned long long*>(ctx->ticket) + 1;
+  if (pq.expand) {
+    // expanded join (join_kernel.cuh): count the joined tuples, size the tuple buffer, write them, then
+    // the fused kernel reads the tuples in place of its probes (one host sync, for the count)
+    if (res->dbg_score || res->dbg_match || res->dbg_selected || res->dbg_trace)
+      return fail(ctx, FLERN_E_UNSUPPORTED, "debug exports are per fact row: not available for expanded joins");
+    ExpandParams& ep = pq.ep;
+    unsigned long long* ctr = reinterpret_cast<unsigned long long*>(ctx->ticket) + 2;
+    ep.counter = ctr;
+    const int eg = std::max(1, std::min(grid_for(ep.nrows), 8 * ctx->num_sms));
+    unsigned long long total = 0;
+    CUDA_TRY(ctx, cudaMemsetAsync(ctr, 0, 8, ctx->stream));
+    if (ep.nrows > 0) expand_count_kernel<<<eg, 256, 0, ctx->stream>>>(ep);
+    CUDA_TRY(ctx, cudaGetLastError());
+    CUDA_TRY(ctx, cudaMemcpyAsync(&total, ctr, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    if (total >= ((unsigned long long)1 << 31))
+      return fail(ctx, FLERN_E_UNSUPPORTED, "the join expands to %llu tuples (at most 2^31 - 1 per call)", total);
+    const size_t words = std::max<size_t>(1, (size_t)total * (size_t)ep.tstride);
+    if (ctx->tuple_words < words) {
+      cudaFree(ctx->tuples);
+      ctx->tuples = nullptr;
+      ctx->tuple_words = 0;
+      if (cudaMalloc(&ctx->tuples, words * 4) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(ctx, FLERN_E_OOM, "cannot allocate %zu bytes for %llu joined tuples", words * 4, total);
+      }
+      ctx->tuple_words = words;
+    }
+    ep.tuples = ctx->tuples;
+    ep.capacity = (int64_t)total;
+    CUDA_TRY(ctx, cudaMemsetAsync(ctr, 0, 8, ctx->stream));
+    if (ep.nrows > 0) expand_write_kernel<<<eg, 256, 0, ctx->stream>>>(ep);
+    CUDA_TRY(ctx, cudaGetLastError());
+    p.tuples = ctx->tuples;
+    p.tstride = ep.tstride;
+    p.scanned = ep.nrows;
+    p.nrows = (int64_t)total;
+    p.pf_col = nullptr;   // applied by the expansion
+  }
   // debug exports: device pointers as given, or temporary device buffers copied back
   const int64_t n = p.nrows;
   if (windowed && (res->dbg_score || res->dbg_match || res->dbg_selected || res->dbg_trace))

@@ -35,8 +35,11 @@ struct ProdState {
 // wait for each other; the stage may hold fewer than 128 rows (count in its metadata).
 // GATHER: the R rows of this thread are arbitrary fact rows (*rid; pre-filter survivors), read with
 // scalar loads.
+// TUPLE (with GATHER): an expanded join (join_kernel.cuh): the rows are joined tuples, row0 + r is my
+// r-th tuple's index and *rid its fact row; the probes are already resolved, so the build-side words
+// come straight from the tuples' payload indices.
 template <int K0P, int S, int R, class SH, int NPW, bool BULK = false, bool PW = false, bool GATHER = false,
-          class FR = void (*)()>
+          bool TUPLE = false, class FR = void (*)()>
 __device__ __forceinline__ void produce_batch(ProdState& st, const QueryParams& p, const XRing& ring, int32_t* wcnt,
                                               const float* s_normf, int64_t row0, bool whole, const bool (&in)[R],
                                               int bidx, int64_t row_end, int t, int warp, int lane,
@@ -159,8 +162,14 @@ __device__ __forceinline__ void produce_batch(ProdState& st, const QueryParams& 
       // overlap instead of taking two dependent round trips; the match then masks the row
       int32_t dkey[R], dseen[R], drow[R];
       int dq = -1;
+      if constexpr (TUPLE) {
 #pragma unroll
-      for (int q = 0; q < kMaxProbes; ++q) {
+        for (int r = 0; r < R; ++r)
+#pragma unroll
+          for (int q = 0; q < kMaxProbes; ++q) { brow[r][q] = -1; pb[r][q] = dz; }
+      }
+#pragma unroll
+      for (int q = 0; q < (TUPLE ? 0 : kMaxProbes); ++q) {
 #pragma unroll
         for (int r = 0; r < R; ++r) { brow[r][q] = -1; pb[r][q] = dz; }
         if (q >= p.nprobes) continue;
@@ -249,8 +258,24 @@ __device__ __forceinline__ void produce_batch(ProdState& st, const QueryParams& 
       }
       if (t == 0) FLERN_TRACE(TR_P_PROBED, bidx);
       // 3. build-side loads (payload words of the matched rows), all issued before any use
+      if constexpr (TUPLE) {
 #pragma unroll
-      for (int r = 0; r < R; ++r) {
+        for (int r = 0; r < R; ++r) {
+          const int32_t* tp = p.tuples + (row0 + r) * (int64_t)p.tstride;
+          auto word = [&](int src1, int w) -> const int32_t* {   // payload word w of probe src1 - 1's match
+            const int q = src1 - 1;
+            const int32_t ix = ld1(tp + 1 + q, valid[r]);
+            return p.tbase[q] + (int64_t)ix * p.tpstr[q] + w;
+          };
+          if (p.grp.src > 0) gv[r] = ld1(word(p.grp.src, p.grp.word), valid[r]);
+          if (p.sum.src > 0) sv[r] = ld1(word(p.sum.src, p.sum.word), valid[r]);
+#pragma unroll
+          for (int k = 0; k < K0P; ++k)
+            if (k >= nfact && k < nfeat) v[k][r] = ld1(word(p.feat[k].src, p.dword[k]), valid[r]);
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < (TUPLE ? 0 : R); ++r) {
         const int32_t* rb0 = pb[r][0];
         const int32_t* rb1 = pb[r][1];
         if (p.grp.src > 0) gv[r] = ld1((p.grp.src == 1 ? rb0 : rb1) + p.grp.word, valid[r] && !synth);
@@ -419,7 +444,33 @@ __device__ __forceinline__ void producer_loop(const QueryParams& p, const XRing&
                   : (c == 1 ? (p.sum.src == 0 ? p.sum.base : nullptr)
                             : (c == 2 ? (p.grp.src == 0 ? p.grp.base : nullptr) : p.fcol[c - 3]));
   };
-  if (BULK && !p.pf_col) {
+  bool expanded = false;
+  if constexpr (SH::NF < 0) {
+    if (p.tuples) {
+      // expanded join (join_kernel.cuh): the rows are joined tuples {fact row, payload index per probe};
+      // no probing here (the fact rows scanned are counted by the expansion)
+      expanded = true;
+      while (cur.lo < n) {
+        int64_t a = 0;
+        if (t == 0) a = claim_chunk(p, 1);
+        for (int64_t base = cur.lo; base < cur.hi; base += kBatch, ++bidx) {
+          const int64_t row0 = base + (int64_t)R * t;
+          bool in[R];
+          RowIds<R> rid;
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+            in[r] = row0 + r < cur.hi;
+            rid.v[r] = in[r] ? (int64_t)ldg_nc(p.tuples + (row0 + r) * (int64_t)p.tstride) : 0;
+          }
+          produce_batch<K0P, S, R, SH, NPW, false, false, true, true>(st, p, ring, wcnt, s_normf, row0, true, in, bidx,
+                                                                     cur.hi, t, warp, lane, 0u, 0, 0, nullptr, &rid);
+        }
+        advance(a);
+      }
+    }
+  }
+  if (expanded) {
+  } else if (BULK && !p.pf_col) {
     // batches come from the loader warp's fact ring (loader_loop), which also claims the row chunks
     for (uint32_t b = 0;; ++b, ++bidx) {
       const int f = b % fr.stages;

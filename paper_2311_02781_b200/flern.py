@@ -26,9 +26,10 @@ ERRORS = {-1: "FLERN_E_INVALID_ARG", -2: "FLERN_E_NOT_FOUND", -3: "FLERN_E_DUPLI
           -10: "FLERN_E_UNSUPPORTED"}
 FLERN_I32, FLERN_F32, FLERN_DATE32, FLERN_DEC32, FLERN_DICT32 = 1, 2, 3, 4, 5
 FLERN_COPY_HOST, FLERN_COPY_DEVICE, FLERN_BORROW_DEVICE = 0x1, 0x2, 0x4
+FLERN_HT_MULTI = 0x1
 FLERN_Q_RESULT_DEVICE, FLERN_Q_ASYNC, FLERN_Q_BOTH_CLASSES, FLERN_Q_NO_MODEL, FLERN_Q_GENERIC_KERNEL = 0x1, 0x2, 0x4, 0x8, 0x10
 EXPORTED = ["flern_create", "flern_destroy", "flern_last_error", "flern_version", "flern_load_table",
-            "flern_update_table", "flern_run_query_streamed", "flern_drop_table", "flern_load_model", "flern_build_hashtable", "flern_run_query",
+            "flern_update_table", "flern_run_query_streamed", "flern_drop_table", "flern_load_model", "flern_build_hashtable", "flern_build_hashtable_ex", "flern_run_query",
             "flern_query_launches"]
 
 
@@ -81,6 +82,9 @@ _lib.flern_load_model.restype = c_i32
 _lib.flern_build_hashtable.argtypes = [c_p, c_i32, ctypes.c_char_p, c_i32, ctypes.POINTER(ctypes.c_char_p),
                                        ctypes.POINTER(c_i32)]
 _lib.flern_build_hashtable.restype = c_i32
+_lib.flern_build_hashtable_ex.argtypes = [c_p, c_i32, ctypes.c_char_p, c_i32, ctypes.POINTER(ctypes.c_char_p), c_u32,
+                                          ctypes.POINTER(c_i32)]
+_lib.flern_build_hashtable_ex.restype = c_i32
 _lib.flern_run_query.argtypes = [c_p, ctypes.POINTER(FlernQuery), ctypes.POINTER(FlernResult)]
 _lib.flern_run_query.restype = c_i32
 _lib.flern_query_launches.argtypes = []
@@ -195,6 +199,15 @@ def flern_build_hashtable(ctx, table_id: int, key_col: str, payload_cols) -> int
     arr = (ctypes.c_char_p * max(1, len(pcs)))(*pcs)
     hid = c_i32()
     _check(ctx, _lib.flern_build_hashtable(ctx, table_id, key_col.encode(), len(pcs), arr, ctypes.byref(hid)))
+    return hid.value
+
+
+def flern_build_hashtable_ex(ctx, table_id: int, key_col: str, payload_cols, flags: int = 0) -> int:
+    """flern_build_hashtable with flags (FLERN_HT_MULTI: the build key may repeat)."""
+    pcs = [c.encode() for c in payload_cols]
+    arr = (ctypes.c_char_p * max(1, len(pcs)))(*pcs)
+    hid = c_i32()
+    _check(ctx, _lib.flern_build_hashtable_ex(ctx, table_id, key_col.encode(), len(pcs), arr, flags, ctypes.byref(hid)))
     return hid.value
 
 

@@ -35,7 +35,8 @@ class GpuQuery:
             payload = [c for c in cfg.build_cols(p) if c != bkey]
             self.build_ids.append(tid)
             t0 = time.perf_counter()
-            self.ht_ids.append(F.flern_build_hashtable(self.ctx, tid, bkey, payload))
+            flags = F.FLERN_HT_MULTI if p in getattr(cfg, "multi", ()) else 0
+            self.ht_ids.append(F.flern_build_hashtable_ex(self.ctx, tid, bkey, payload, flags))
             self.build_ms += 1e3 * (time.perf_counter() - t0)
         self.model_id = F.flern_load_model(self.ctx, "udf", model.dims, model.W, model.b, model.shift, model.scale)
         self.query = self.make_query(self.fact_id)
