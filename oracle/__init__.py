@@ -53,7 +53,8 @@ class OrQuery(ctypes.Structure):
 
 class OrResult(ctypes.Structure):
     _fields_ = [(n, c_p) for n in ("count", "sum", "count_rej", "sum_rej", "count_hi", "sum_hi",
-                                   "count_band", "sum_band", "score", "logit", "match", "selected")] + \
+                                   "count_band", "sum_band", "score", "logit", "match", "selected",
+                                   "tuple_x", "tuple_t")] + [("tuple_cap", c_i64)] + \
                [(n, c_i64) for n in ("rows_scanned", "rows_prefiltered", "rows_joined", "rows_selected",
                                      "rows_band")] + [("error", ctypes.c_char * 256)]
 
@@ -69,6 +70,9 @@ def lib():
         L.or_run.restype = ctypes.c_int
         L.or_mlp_forward.argtypes = [ctypes.POINTER(OrModel), c_i64, c_p, c_p, c_p, c_i32]
         L.or_mlp_forward.restype = ctypes.c_int
+        L.or_mlp_train_step.argtypes = [ctypes.POINTER(OrModel), c_i64, c_p, c_p, c_dbl, ctypes.POINTER(c_p),
+                                         ctypes.POINTER(c_p), ctypes.POINTER(c_p), ctypes.POINTER(c_p), c_p]
+        L.or_mlp_train_step.restype = ctypes.c_int
         L.or_bf16_rne.argtypes = [ctypes.c_float]
         L.or_bf16_rne.restype = ctypes.c_float
         _lib = L
@@ -138,7 +142,7 @@ class OracleResult:
 
 
 def run(cfg, db, model, threshold=None, band=1e-2, per_row=False, emulate_bf16=False, nthreads=0,
-        row_lo=0, row_hi=-1) -> OracleResult:
+        row_lo=0, row_hi=-1, tuples=None) -> OracleResult:
     """Run the oracle on a datagen.Database with a datagen.Model-like object."""
     keep = _Keep()
     fact = _table(db.fact, db.fact_n, keep)
@@ -174,6 +178,9 @@ def run(cfg, db, model, threshold=None, band=1e-2, per_row=False, emulate_bf16=F
         extra["selected"] = np.empty(nrows, np.uint8)
         for k, a in extra.items():
             setattr(res, k, a.ctypes.data)
+    if tuples is not None:   # (X [cap][nfeat], T [cap]) float64 arrays: per-tuple model inputs and targets
+        X, T = tuples
+        res.tuple_x, res.tuple_t, res.tuple_cap = X.ctypes.data, T.ctypes.data, len(T)
     m = _model(model, keep)
     rc = lib().or_run(ctypes.byref(fact), len(db.builds), btables, ctypes.byref(m), ctypes.byref(q),
                       ctypes.byref(res))
@@ -202,3 +209,42 @@ def mlp_forward(model, x: np.ndarray, emulate_bf16=False):
 
 def bf16_rne(v: float) -> float:
     return lib().or_bf16_rne(v)
+
+
+def batch(cfg, db, model, row_lo=0, row_hi=-1, cap=None):
+    """The joined tuples of fact rows [row_lo, row_hi) as a training batch: (X [B][nfeat] normalised model
+    inputs, T [B] targets = the query's sum column), fp64, in the oracle's enumeration order."""
+    hi = db.fact_n if row_hi < 0 else row_hi
+    cap = cap if cap is not None else max(1, 8 * (hi - row_lo))
+    X = np.zeros((cap, len(cfg.feats)), np.float64)
+    T = np.zeros(cap, np.float64)
+    r = run(cfg, db, model, threshold=-np.inf, nthreads=1, row_lo=row_lo, row_hi=hi, tuples=(X, T))
+    assert r.rows_joined <= cap, "tuple capacity"
+    return X[:r.rows_joined], T[:r.rows_joined]
+
+
+def mlp_train_step(model, X, T, lr):
+    """One SGD step on rows X with targets T (or_mlp_train_step): returns dict(loss, dW, db, W, b) in fp64."""
+    keep = _Keep()
+    X = np.ascontiguousarray(X, dtype=np.float64)
+    T = np.ascontiguousarray(T, dtype=np.float64)
+    dims = list(model.dims)
+    L = len(dims) - 1
+    outs = {k: [np.zeros((dims[l + 1], dims[l]) if k in ("dW", "W") else dims[l + 1], np.float64) for l in range(L)]
+            for k in ("dW", "db", "W", "b")}
+    ptrs = {k: keep((c_p * L)(*[a.ctypes.data for a in v])) for k, v in outs.items()}
+    loss = ctypes.c_double(0.0)
+    m = _model(model, keep)
+    rc = lib().or_mlp_train_step(ctypes.byref(m), len(T), X.ctypes.data, T.ctypes.data, float(lr), ptrs["dW"],
+                                 ptrs["db"], ptrs["W"], ptrs["b"], ctypes.addressof(loss))
+    if rc != 0:
+        raise OracleError("or_mlp_train_step: bad model")
+    return dict(loss=loss.value, **outs)
+
+
+def train_step(cfg, db, model, lr, row_lo=0, row_hi=-1):
+    """NEXT-3: one SGD step on the batch the query yields for fact rows [row_lo, row_hi)."""
+    X, T = batch(cfg, db, model, row_lo, row_hi)
+    r = mlp_train_step(model, X, T, lr)
+    r["batch"] = len(T)
+    return r

@@ -182,7 +182,7 @@ extern "C" int or_run(const or_table* fact, int32_t nbuild, const or_table* buil
   Col gcol, scol, pfcol;
   if (!resolve(q->group.src, q->group.col, &gcol)) return 1;
   if (!resolve(q->sum.src, q->sum.col, &scol)) return 1;
-  if (gcol.is_float || scol.is_float) { set_err(res, "group and sum columns must be integer"); return 1; }
+  if (gcol.is_float || (scol.is_float && !res->tuple_t)) { set_err(res, "group and sum columns must be integer"); return 1; }
   const bool has_pf = q->prefilter_col != nullptr;
   if (has_pf && !resolve(-1, q->prefilter_col, &pfcol)) return 1;
 
@@ -194,6 +194,8 @@ extern "C" int or_run(const or_table* fact, int32_t nbuild, const or_table* buil
   if (n < 1024) nthreads = 1;
   const bool emu = q->emulate_bf16 != 0;
   const int32_t K = q->nfeat;
+  if (res->tuple_x && nthreads != 1) { set_err(res, "tuple exports need a single-threaded run"); return 1; }
+  auto scol_val = [&](int64_t r) { return scol.get(r); };   // the sum column as a number (training target)
 
   std::vector<Acc> accs(nthreads, Acc(G));
   auto work = [&](int t, int64_t a, int64_t b) {
@@ -217,6 +219,10 @@ extern "C" int or_run(const or_table* fact, int32_t nbuild, const or_table* buil
           x[k] = (double)or_bf16_rne(s);
         }
       }
+      if (res->tuple_x && acc.joined <= res->tuple_cap) {   // export (single-threaded runs)
+        for (int32_t k = 0; k < K; ++k) res->tuple_x[(acc.joined - 1) * K + k] = x[k];
+        if (res->tuple_t) res->tuple_t[acc.joined - 1] = scol_val(rows[q->sum.src + 1]);
+      }
       const double logit = mlp_logit(*model, x.data(), h, hn, emu);
       const double score = sigmoid(logit);
       if (res->score) res->score[oi] = score;
@@ -226,7 +232,7 @@ extern "C" int or_run(const or_table* fact, int32_t nbuild, const or_table* buil
         acc.err = "group code " + std::to_string(g) + " outside [0, ngroups)";
         return false;
       }
-      const int64_t s = scol.get_int(rows[q->sum.src + 1]);
+      const int64_t s = scol.is_float ? 0 : scol.get_int(rows[q->sum.src + 1]);
       const bool sel = score > q->threshold;   // `if (*y2 > 0.5)`, strict (reading Q8)
       const bool in_band = std::fabs(score - q->threshold) <= q->band;
       if (sel) {
@@ -338,5 +344,66 @@ extern "C" int or_run(const or_table* fact, int32_t nbuild, const or_table* buil
   res->rows_joined = tot.joined;
   res->rows_selected = tot.selected;
   res->rows_band = tot.band;
+  return 0;
+}
+
+// One SGD step (oracle.h): plain forward / backward / update, row by row, k ascending, fp64.
+extern "C" int or_mlp_train_step(const or_model* m, int64_t n, const double* x, const double* t, double lr,
+                                 double* const* dW, double* const* db, double* const* W_out, double* const* b_out,
+                                 double* loss) {
+  const int32_t L = m->nlayers;
+  if (L < 1 || m->dims[L] != 1) return 1;
+  std::vector<std::vector<double>> gW(L), gb(L);
+  for (int32_t l = 0; l < L; ++l) {
+    gW[l].assign((size_t)m->dims[l + 1] * m->dims[l], 0.0);
+    gb[l].assign((size_t)m->dims[l + 1], 0.0);
+  }
+  double sse = 0.0;
+  std::vector<std::vector<double>> z(L + 1), h(L + 1);   // h[0] = x; z[l+1], h[l+1] = layer l's output
+  std::vector<double> delta, prev;
+  for (int64_t i = 0; i < n; ++i) {
+    h[0].assign(x + i * m->dims[0], x + (i + 1) * m->dims[0]);
+    for (int32_t l = 0; l < L; ++l) {   // forward
+      const int32_t in = m->dims[l], out = m->dims[l + 1];
+      z[l + 1].assign(out, 0.0);
+      h[l + 1].assign(out, 0.0);
+      for (int32_t j = 0; j < out; ++j) {
+        double a = (double)m->b[l][j];
+        for (int32_t k = 0; k < in; ++k) a += (double)m->W[l][(int64_t)j * in + k] * h[l][k];
+        z[l + 1][j] = a;
+        h[l + 1][j] = (l + 1 < L) ? (a > 0.0 ? a : 0.0) : a;   // ReLU on hidden layers, linear output
+      }
+    }
+    const double err = h[L][0] - t[i];
+    sse += err * err;
+    delta.assign(1, 2.0 * err / (double)n);   // d loss / d y
+    for (int32_t l = L - 1; l >= 0; --l) {   // backward
+      const int32_t in = m->dims[l], out = m->dims[l + 1];
+      for (int32_t j = 0; j < out; ++j) {
+        gb[l][j] += delta[j];
+        for (int32_t k = 0; k < in; ++k) gW[l][(int64_t)j * in + k] += delta[j] * h[l][k];
+      }
+      if (l == 0) break;
+      prev.assign(in, 0.0);
+      for (int32_t k = 0; k < in; ++k) {
+        double a = 0.0;
+        for (int32_t j = 0; j < out; ++j) a += (double)m->W[l][(int64_t)j * in + k] * delta[j];
+        prev[k] = z[l][k] > 0.0 ? a : 0.0;   // ReLU derivative of the layer below
+      }
+      delta.swap(prev);
+    }
+  }
+  if (loss) *loss = n > 0 ? sse / (double)n : 0.0;
+  for (int32_t l = 0; l < L; ++l) {
+    const int64_t nw = (int64_t)m->dims[l + 1] * m->dims[l];
+    for (int64_t e = 0; e < nw; ++e) {
+      if (dW && dW[l]) dW[l][e] = gW[l][e];
+      if (W_out && W_out[l]) W_out[l][e] = (double)m->W[l][e] - lr * gW[l][e];
+    }
+    for (int32_t j = 0; j < m->dims[l + 1]; ++j) {
+      if (db && db[l]) db[l][j] = gb[l][j];
+      if (b_out && b_out[l]) b_out[l][j] = (double)m->b[l][j] - lr * gb[l][j];
+    }
+  }
   return 0;
 }

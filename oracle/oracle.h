@@ -73,6 +73,12 @@ typedef struct {
   double* logit;                           /* [rows] optional: fp64 logit, NaN likewise */
   int64_t* match;                          /* [rows * nprobes] optional: build row id, -1 = miss / not reached */
   uint8_t* selected;                       /* [rows] optional: 1 if selected */
+  /* per joined tuple, in enumeration order (fact rows ascending, probes nested; single-threaded runs
+     only): the model input x (normalised, fp64) and the sum column's value (the training target of
+     NEXT-3), for at most tuple_cap tuples */
+  double* tuple_x;                         /* [tuple_cap][nfeat] optional */
+  double* tuple_t;                         /* [tuple_cap] optional */
+  int64_t tuple_cap;
   int64_t rows_scanned, rows_prefiltered, rows_joined, rows_selected, rows_band;   /* joined: joined tuples */
   char error[256];
 } or_result;
@@ -85,6 +91,20 @@ int or_run(const or_table* fact, int32_t nbuild, const or_table* builds, const o
  * logits[i] (and scores[i] = 1/(1+exp(-logit)) when scores != NULL). */
 int or_mlp_forward(const or_model* model, int64_t n, const double* x, double* logits, double* scores,
                    int32_t emulate_bf16);
+
+/* One SGD step of the ML-in-charge use case on given rows (NEXT-3; PAPER.md Fig. figure:e2e_training
+ * P:515-518 `for batch, target in sql(...): model.train(batch, target)`, and §4.5: a network
+ * with ReLU after the hidden layers, the Mean Squared Error loss, its gradients, Stochastic Gradient
+ * Descent). Rows x[n][dims[0]] (already normalised) with targets t[n]; the output layer is linear
+ * (regression: y = the last layer's output). fp64 throughout:
+ *   loss = (1/n) sum_i (y_i - t_i)^2
+ *   backward: delta_L = 2 (y - t) / n; dW_l += delta_l (x) h_{l-1}; db_l += delta_l;
+ *             delta_{l-1} = W_l^T delta_l * [z_{l-1} > 0]
+ *   SGD: W_l' = W_l - lr * dW_l, b_l' = b_l - lr * db_l
+ * dW[l] / db[l] ([dims[l+1]][dims[l]] / [dims[l+1]]) receive the gradients, W_out / b_out the updated
+ * parameters (each optional), *loss the loss before the step. n = 0: zero gradients, loss 0. */
+int or_mlp_train_step(const or_model* model, int64_t n, const double* x, const double* t, double lr,
+                      double* const* dW, double* const* db, double* const* W_out, double* const* b_out, double* loss);
 
 /* bf16 round-to-nearest-even of an fp32 value (diagnostic emulation helper). */
 float or_bf16_rne(float v);
