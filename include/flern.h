@@ -226,6 +226,33 @@ FLERN_API flern_status flern_run_query_streamed(flern_ctx* ctx, const flern_quer
                                                 const flern_column* host_cols, int64_t chunk_rows, flern_result* res);
 
 
+/* ------------------------------------------------------------------------------------------ */
+/* ML in charge (NEXT-3): one Stochastic Gradient Descent step of a registered model on the batch a query
+ * yields, `for batch, target in sql("select ... from t1 join t2 ..."): model.train(batch, target)`
+ * (PAPER.md Fig. figure:e2e_training; §4.5: ReLU after the hidden layers, Mean
+ * Squared Error loss, gradients, SGD).
+ *   batch   : the joined tuples of fact rows [row_lo, row_hi) of q->fact_table (row_hi < 0: all rows;
+ *             row_lo a multiple of 4) under q's pre-filter and probes; features q->feats (normalised with
+ *             the model's shift / scale, as in queries); target q->sum_col (any numeric column, int32 exact
+ *             or float32). q->threshold, q->group_col / ngroups and q->flags are ignored.
+ *   model   : q->model_id, dims [K0, 128, 128, 1] with K0 < 48; the output layer is linear (the regression
+ *             output y; queries keep reading sigmoid(y) as the score).
+ *   step    : loss = (1/B) sum (y - t)^2 over the B tuples; W <- W - lr * dL/dW for every weight and bias,
+ *             on fp32 master weights held on the device (bf16 tensor-core operands, fp32 accumulate).
+ * One fused launch (gather -> forward -> backward on tcgen05 -> gradients) plus the update; synchronous.
+ * Errors: FLERN_E_UNSUPPORTED (model shape), FLERN_E_INVALID_ARG (rows, lr), and those of flern_run_query. */
+typedef struct {
+  int64_t rows_scanned;  /* fact rows of the batch range */
+  int64_t rows_joined;   /* B: joined tuples trained on */
+  double loss;           /* mean squared error of the batch before the step */
+  float elapsed_ms;      /* device time of the step */
+} flern_train_result;
+FLERN_API flern_status flern_train_step(flern_ctx* ctx, const flern_query* q, int64_t row_lo, int64_t row_hi, float lr,
+                                        flern_train_result* res);
+/* Read a model's current fp32 weights (after training, the updated ones): W[l] [dims[l+1]][dims[l]],
+ * b[l] [dims[l+1]], caller-owned host arrays in the layout of flern_load_model. */
+FLERN_API flern_status flern_get_model(flern_ctx* ctx, int32_t model_id, float* const* W, float* const* b);
+
 #define FLERN_TRACE_EVENTS 26
 
 /* Number of CUDA kernels flern_run_query launches per call (for launch accounting): 1 (an expanded

@@ -16,6 +16,7 @@
 #include "build_kernel.cuh"
 #include "join_kernel.cuh"
 #include "query_kernel.cuh"
+#include "train_kernel.cuh"
 #include "wide_kernel.cuh"
 
 using namespace flern;
@@ -53,6 +54,16 @@ struct Model {
   std::vector<std::vector<float>> W, b;      // host copies (fp32 as given)
   std::vector<float> shift, scale;
   std::map<std::vector<int>, uint8_t*> permuted;   // images with permuted inputs (see run_query)
+  // training state (flern_train_step, train_kernel.cuh), allocated on the first step
+  float* master = nullptr;          // fp32 [W1 | b1 | W2 | b2 | w3 | b3], model input order
+  uint8_t* timg = nullptr;          // bf16 operand image, kernel input order (tperm)
+  float* tgrad = nullptr;           // gradient accumulators (TrainGrad)
+  float* tnorm = nullptr;           // [scale K0P | c K0P] of the training gather (c_K0 = 1: the ones column)
+  int32_t* tperm = nullptr;         // [K0] kernel input -> model input
+  unsigned long long* trows = nullptr;   // [2] rows scanned, tuples joined
+  std::vector<int> tperm_host;      // the permutation the image was built for
+  int tK0P = 0;
+  bool dirty = false;               // the master weights moved on: the inference images are stale
 };
 struct HashTable {
   int32_t table_id = -1;
@@ -290,6 +301,7 @@ extern "C" FLERN_API void flern_destroy(flern_ctx* ctx) {
   for (auto& m : ctx->models) {
     cudaFree(m.dbuf);
     for (auto& kv : m.permuted) cudaFree(kv.second);
+    cudaFree(m.master);   // one allocation holds the training state
   }
   for (auto& h : ctx->hts) cudaFree(h.slots);
   for (auto e : ctx->ring_copied) cudaEventDestroy(e);
@@ -841,12 +853,15 @@ struct Prepared {
   const Model* m = nullptr;
   bool expand = false;   // chains beyond the kernel's own probes / multimap: join_kernel.cuh expansion first
   ExpandParams ep;
+  std::vector<int> perm;  // kernel input kk = model input perm[kk] (fact-column features first)
 };
+flern_status refresh_model(flern_ctx* ctx, Model& m);
 
 // Every validation of a query and the kernel parameters it resolves to; no device work except
 // caching a model image with permuted inputs. Shared by flern_run_query and flern_run_query_streamed
 // (which validates before its first copy).
-flern_status prepare_query(flern_ctx* ctx, const flern_query* q, const FactWindow* win, Prepared& out) {
+flern_status prepare_query(flern_ctx* ctx, const flern_query* q, const FactWindow* win, Prepared& out,
+                           bool training = false) {
   QueryParams& p = out.p;
   const bool both = (q->flags & FLERN_Q_BOTH_CLASSES) != 0;
   if (q->fact_table < 0 || q->fact_table >= (int32_t)ctx->tables.size() || !ctx->tables[q->fact_table].alive)
@@ -855,6 +870,10 @@ flern_status prepare_query(flern_ctx* ctx, const flern_query* q, const FactWindo
   if (q->model_id < 0 || q->model_id >= (int32_t)ctx->models.size())
     return fail(ctx, FLERN_E_NOT_FOUND, "no model with id %d", q->model_id);
   Model& m = ctx->models[q->model_id];
+  if (m.dirty && !training) {   // trained since its inference images were built
+    const flern_status rs = refresh_model(ctx, m);
+    if (rs != FLERN_OK) return rs;
+  }
   if (q->nfeat != m.K0)
     return fail(ctx, FLERN_E_ARITY, "UDF '%s' takes %d arguments, query passes %d", m.name.c_str(), m.K0, q->nfeat);
   if (q->nfeat > 0 && !q->feats) return fail(ctx, FLERN_E_INVALID_ARG, "null feature list");
@@ -864,7 +883,7 @@ flern_status prepare_query(flern_ctx* ctx, const flern_query* q, const FactWindo
     return fail(ctx, FLERN_E_UNSUPPORTED, "ngroups %d outside 1..%d", q->ngroups, kMaxGroupsLarge);
   if (q->ngroups > kMaxGroups && win)
     return fail(ctx, FLERN_E_UNSUPPORTED, "streamed queries aggregate at most %d groups", kMaxGroups);
-  if (std::isnan(q->threshold)) return fail(ctx, FLERN_E_INVALID_ARG, "threshold is NaN");
+  if (std::isnan(q->threshold) && !training) return fail(ctx, FLERN_E_INVALID_ARG, "threshold is NaN");
 
   std::memset(&p, 0, sizeof(p));
   // a streamed query reads its fact rows from a ring slot (flern_run_query_streamed)
@@ -1006,8 +1025,15 @@ flern_status prepare_query(flern_ctx* ctx, const flern_query* q, const FactWindo
   if (q->nprobes < 2) p.probe[1] = p.probe[0];   // valid pointers for unused address math
   p.dummy = ctx->dummy;
 
-  if ((st = resolve(q->group_col, &p.grp, true, "group column")) != FLERN_OK) return st;
-  if ((st = resolve(q->sum_col, &p.sum, true, "sum column")) != FLERN_OK) return st;
+  if (!training) {
+    if ((st = resolve(q->group_col, &p.grp, true, "group column")) != FLERN_OK) return st;
+  } else {   // training: no group-by (the producer's group code reads a valid dummy)
+    p.grp.base = ctx->dummy;
+    p.grp.stride = 1;
+    p.grp.src = -1;
+  }
+  // the sum column (the training target: any numeric column)
+  if ((st = resolve(q->sum_col, &p.sum, !training, training ? "target column" : "sum column")) != FLERN_OK) return st;
   if (q->prefilter_col) {
     const Column* c = fact.find(q->prefilter_col);
     if (!c) return fail(ctx, FLERN_E_NOT_FOUND, "pre-filter: fact table '%s' has no column '%s'", fact.name.c_str(), q->prefilter_col);
@@ -1058,7 +1084,64 @@ flern_status prepare_query(flern_ctx* ctx, const flern_query* q, const FactWindo
   if (!ke) return fail(ctx, FLERN_E_UNSUPPORTED, "no kernel for model '%s'", m.name.c_str());
   out.ke = ke;
   out.m = &m;
+  out.perm = perm;
   return FLERN_OK;
+}
+
+// Expanded join (join_kernel.cuh): count the joined tuples, size the tuple buffer, write them; the fused
+// kernel then reads the tuples in place of its probes (one host sync, for the count).
+flern_status expand_join(flern_ctx* ctx, Prepared& pq) {
+  QueryParams& p = pq.p;
+  ExpandParams& ep = pq.ep;
+  unsigned long long* ctr = reinterpret_cast<unsigned long long*>(ctx->ticket) + 2;
+  ep.counter = ctr;
+  const int eg = std::max(1, std::min(grid_for(ep.nrows), 8 * ctx->num_sms));
+  unsigned long long total = 0;
+  CUDA_TRY(ctx, cudaMemsetAsync(ctr, 0, 8, ctx->stream));
+  if (ep.nrows > 0) expand_count_kernel<<<eg, 256, 0, ctx->stream>>>(ep);
+  CUDA_TRY(ctx, cudaGetLastError());
+  CUDA_TRY(ctx, cudaMemcpyAsync(&total, ctr, 8, cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  if (total >= ((unsigned long long)1 << 31))
+    return fail(ctx, FLERN_E_UNSUPPORTED, "the join expands to %llu tuples (at most 2^31 - 1 per call)", total);
+  const size_t words = std::max<size_t>(1, (size_t)total * (size_t)ep.tstride);
+  if (ctx->tuple_words < words) {
+    cudaFree(ctx->tuples);
+    ctx->tuples = nullptr;
+    ctx->tuple_words = 0;
+    if (cudaMalloc(&ctx->tuples, words * 4) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(ctx, FLERN_E_OOM, "cannot allocate %zu bytes for %llu joined tuples", words * 4, total);
+    }
+    ctx->tuple_words = words;
+  }
+  ep.tuples = ctx->tuples;
+  ep.capacity = (int64_t)total;
+  CUDA_TRY(ctx, cudaMemsetAsync(ctr, 0, 8, ctx->stream));
+  if (ep.nrows > 0) expand_write_kernel<<<eg, 256, 0, ctx->stream>>>(ep);
+  CUDA_TRY(ctx, cudaGetLastError());
+  p.tuples = ctx->tuples;
+  p.tstride = ep.tstride;
+  p.scanned = ep.nrows;
+  p.nrows = (int64_t)total;
+  p.pf_col = nullptr;   // applied by the expansion
+  return FLERN_OK;
+}
+
+// One persistent CTA per SM; rows are claimed as chunks (guided schedule, chunk_rows in common.cuh):
+// 2*grid contiguous halves of an 85% static share, then small chunks on demand. Returns the grid.
+int plan_claims(flern_ctx* ctx, QueryParams& p, int K0P, int NL, int npt) {
+  const int64_t n = p.nrows;
+  int64_t chunk = p.pf_col ? (int64_t)scan_rows(npt) : (int64_t)batch_rows(K0P, NL, npt);
+  // a table smaller than one batch per SM: smaller chunks (multiples of 16 rows, aligned for vector
+  // loads and bulk copies) so every SM takes a share and the kernel's latency shrinks
+  if (!p.pf_col && n < (int64_t)ctx->num_sms * chunk)
+    chunk = std::min(chunk, std::max<int64_t>(64, ((n + ctx->num_sms - 1) / ctx->num_sms + 15) / 16 * 16));
+  const int grid = (int)std::min<int64_t>(ctx->num_sms, std::max<int64_t>(1, (n + chunk - 1) / chunk));
+  p.claim_small = chunk;
+  p.claim_big = (int64_t)(0.85 * (double)n / (2.0 * grid)) / chunk * chunk;
+  p.claim_nbig = p.claim_big > 0 ? 2 * (int64_t)grid : 0;
+  return grid;
 }
 
 // One launch of a prepared query (synchronous unless FLERN_Q_ASYNC).
@@ -1101,43 +1184,9 @@ flern_status launch_query(flern_ctx* ctx, const flern_query* q, Prepared& pq, fl
   p.ticket = ctx->ticket;
   p.work = reinterpret_cast<unsigned long long*>(ctx->ticket) + 1;
   if (pq.expand) {
-    // expanded join (join_kernel.cuh): count the joined tuples, size the tuple buffer, write them, then
-    // the fused kernel reads the tuples in place of its probes (one host sync, for the count)
     if (res->dbg_score || res->dbg_match || res->dbg_selected || res->dbg_trace)
       return fail(ctx, FLERN_E_UNSUPPORTED, "debug exports are per fact row: not available for expanded joins");
-    ExpandParams& ep = pq.ep;
-    unsigned long long* ctr = reinterpret_cast<unsigned long long*>(ctx->ticket) + 2;
-    ep.counter = ctr;
-    const int eg = std::max(1, std::min(grid_for(ep.nrows), 8 * ctx->num_sms));
-    unsigned long long total = 0;
-    CUDA_TRY(ctx, cudaMemsetAsync(ctr, 0, 8, ctx->stream));
-    if (ep.nrows > 0) expand_count_kernel<<<eg, 256, 0, ctx->stream>>>(ep);
-    CUDA_TRY(ctx, cudaGetLastError());
-    CUDA_TRY(ctx, cudaMemcpyAsync(&total, ctr, 8, cudaMemcpyDeviceToHost, ctx->stream));
-    CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
-    if (total >= ((unsigned long long)1 << 31))
-      return fail(ctx, FLERN_E_UNSUPPORTED, "the join expands to %llu tuples (at most 2^31 - 1 per call)", total);
-    const size_t words = std::max<size_t>(1, (size_t)total * (size_t)ep.tstride);
-    if (ctx->tuple_words < words) {
-      cudaFree(ctx->tuples);
-      ctx->tuples = nullptr;
-      ctx->tuple_words = 0;
-      if (cudaMalloc(&ctx->tuples, words * 4) != cudaSuccess) {
-        cudaGetLastError();
-        return fail(ctx, FLERN_E_OOM, "cannot allocate %zu bytes for %llu joined tuples", words * 4, total);
-      }
-      ctx->tuple_words = words;
-    }
-    ep.tuples = ctx->tuples;
-    ep.capacity = (int64_t)total;
-    CUDA_TRY(ctx, cudaMemsetAsync(ctr, 0, 8, ctx->stream));
-    if (ep.nrows > 0) expand_write_kernel<<<eg, 256, 0, ctx->stream>>>(ep);
-    CUDA_TRY(ctx, cudaGetLastError());
-    p.tuples = ctx->tuples;
-    p.tstride = ep.tstride;
-    p.scanned = ep.nrows;
-    p.nrows = (int64_t)total;
-    p.pf_col = nullptr;   // applied by the expansion
+    if ((st = expand_join(ctx, pq)) != FLERN_OK) return st;
   }
   // debug exports: device pointers as given, or temporary device buffers copied back
   const int64_t n = p.nrows;
@@ -1185,18 +1234,8 @@ flern_status launch_query(flern_ctx* ctx, const flern_query* q, Prepared& pq, fl
   p.dbg_match = d_match;
   p.dbg_selected = d_sel;
 
-  // one persistent CTA per SM; rows are claimed as chunks (guided schedule, chunk_rows in common.cuh):
-  // 2*grid contiguous halves of an 85% static share, then small chunks on demand
   const int npt = 32 * (ke->threads == kThreads ? kProdWarps : kProdWarpsWide);   // producer threads
-  int64_t chunk = p.pf_col ? (int64_t)scan_rows(npt) : (int64_t)batch_rows(m.K0P, m.NL, npt);
-  // a table smaller than one batch per SM: smaller chunks (multiples of 16 rows, aligned for vector
-  // loads and bulk copies) so every SM takes a share and the kernel's latency shrinks
-  if (!p.pf_col && n < (int64_t)ctx->num_sms * chunk)
-    chunk = std::min(chunk, std::max<int64_t>(64, ((n + ctx->num_sms - 1) / ctx->num_sms + 15) / 16 * 16));
-  const int grid = (int)std::min<int64_t>(ctx->num_sms, std::max<int64_t>(1, (n + chunk - 1) / chunk));
-  p.claim_small = chunk;
-  p.claim_big = (int64_t)(0.85 * (double)n / (2.0 * grid)) / chunk * chunk;
-  p.claim_nbig = p.claim_big > 0 ? 2 * (int64_t)grid : 0;
+  const int grid = plan_claims(ctx, p, m.K0P, m.NL, npt);
   if (ke->scratch_per_cta) {   // wide kernel: per-CTA activation scratch
     const size_t need = (size_t)grid * ke->scratch_per_cta;
     if (ctx->scratch_bytes < need) {
@@ -1440,5 +1479,191 @@ extern "C" FLERN_API flern_status flern_run_query_streamed(flern_ctx* ctx, const
   res->elapsed_ms = 0.f;
   if (cnt[3] != 0)
     return fail(ctx, FLERN_E_INVALID_ARG, "%lld joined rows have a group code outside [0, %d)", (long long)cnt[3], G);
+  return FLERN_OK;
+}
+
+// ================================================================================ training (NEXT-3)
+namespace {
+using TrainFn = void (*)(const TrainParams);
+using UpdateFn = void (*)(float*, uint8_t*, const float*, const unsigned long long*, const int32_t*, int32_t, float);
+struct TrainEntry {
+  int K0P;
+  TrainFn fn;
+  UpdateFn upd;
+  uint32_t smem;
+  int gfloats;
+  bool attr_set;
+};
+TrainEntry g_train[] = {
+    {16, flern_train_kernel<16>, train_update_kernel<16>, TrainPlan<16>::total, TrainGrad<16>::floats, false},
+    {32, flern_train_kernel<32>, train_update_kernel<32>, TrainPlan<32>::total, TrainGrad<32>::floats, false},
+    {48, flern_train_kernel<48>, train_update_kernel<48>, TrainPlan<48>::total, TrainGrad<48>::floats, false}};
+
+size_t master_floats(const Model& m) {
+  const size_t H = (size_t)m.H;
+  return H * m.K0 + H + H * H + H + H + 1;
+}
+
+// Pull the trained fp32 master weights back into the host copies and rebuild the inference images.
+flern_status refresh_model(flern_ctx* ctx, Model& m) {
+  if (!m.dirty) return FLERN_OK;
+  CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+  std::vector<float> h(master_floats(m));
+  CUDA_TRY(ctx, cudaMemcpyAsync(h.data(), m.master, h.size() * 4, cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  const size_t H = (size_t)m.H, K0 = (size_t)m.K0;
+  size_t o = 0;
+  std::copy(h.begin() + o, h.begin() + o + H * K0, m.W[0].begin()); o += H * K0;
+  std::copy(h.begin() + o, h.begin() + o + H, m.b[0].begin()); o += H;
+  std::copy(h.begin() + o, h.begin() + o + H * H, m.W[1].begin()); o += H * H;
+  std::copy(h.begin() + o, h.begin() + o + H, m.b[1].begin()); o += H;
+  std::copy(h.begin() + o, h.begin() + o + H, m.W[2].begin()); o += H;
+  m.b[2][0] = h[o];
+  for (auto& kv : m.permuted) cudaFree(kv.second);
+  m.permuted.clear();
+  std::vector<int> ident(m.K0);
+  for (int k = 0; k < m.K0; ++k) ident[k] = k;
+  std::vector<uint8_t> img = model_image(m, ident);
+  CUDA_TRY(ctx, cudaMemcpyAsync(m.dbuf, img.data(), img.size(), cudaMemcpyHostToDevice, ctx->stream));
+  CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  m.dirty = false;
+  return FLERN_OK;
+}
+}  // namespace
+
+extern "C" FLERN_API flern_status flern_train_step(flern_ctx* ctx, const flern_query* q, int64_t row_lo,
+                                                   int64_t row_hi, float lr, flern_train_result* res) {
+  if (!ctx) return FLERN_E_INVALID_ARG;
+  if (!q || !res) return fail(ctx, FLERN_E_INVALID_ARG, "flern_train_step: null query or result");
+  if (!std::isfinite(lr)) return fail(ctx, FLERN_E_INVALID_ARG, "flern_train_step: learning rate is not finite");
+  if (q->model_id < 0 || q->model_id >= (int32_t)ctx->models.size())
+    return fail(ctx, FLERN_E_NOT_FOUND, "no model with id %d", q->model_id);
+  Model& m = ctx->models[q->model_id];
+  if (m.NL != 2 || m.H != kTrainH || m.K0 >= kMaxFeat)
+    return fail(ctx, FLERN_E_UNSUPPORTED,
+                "flern_train_step: model '%s' must be K0-%d-%d-1 with K0 < %d (two hidden layers of %d)", m.name.c_str(),
+                kTrainH, kTrainH, kMaxFeat, kTrainH);
+  if (q->fact_table < 0 || q->fact_table >= (int32_t)ctx->tables.size() || !ctx->tables[q->fact_table].alive)
+    return fail(ctx, FLERN_E_NOT_FOUND, "no fact table with id %d", q->fact_table);
+  const Table& fact = ctx->tables[q->fact_table];
+  if (row_hi < 0) row_hi = fact.nrows;
+  if (row_lo < 0 || row_lo > row_hi || row_hi > fact.nrows)
+    return fail(ctx, FLERN_E_INVALID_ARG, "flern_train_step: rows [%lld, %lld) outside table '%s' (%lld rows)",
+                (long long)row_lo, (long long)row_hi, fact.name.c_str(), (long long)fact.nrows);
+  if (row_lo % 4 != 0) return fail(ctx, FLERN_E_INVALID_ARG, "flern_train_step: row_lo must be a multiple of 4");
+  // the batch: the query's joined tuples of fact rows [row_lo, row_hi)
+  FactWindow win;
+  win.nrows = row_hi - row_lo;
+  for (const auto& c : fact.cols) win.base.push_back(static_cast<const int32_t*>(c.dptr) + row_lo);
+  Prepared pq;
+  flern_status st = prepare_query(ctx, q, &win, pq, true);
+  if (st != FLERN_OK) return st;
+  const int K0 = m.K0, K0P = (K0 + 1 + 15) / 16 * 16;   // + the ones column (db1)
+  TrainEntry* te = nullptr;
+  for (auto& e : g_train)
+    if (e.K0P == K0P) te = &e;
+  if (!te) return fail(ctx, FLERN_E_UNSUPPORTED, "flern_train_step: no training kernel for %d inputs", K0);
+  CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+  const size_t H = (size_t)kTrainH;
+  const size_t img_b = H * K0P * 2 + H * H * 2;
+  if (!m.master) {   // training state: [master | image | grad | norm | perm | rows], one allocation
+    const size_t mf = master_floats(m);
+    const size_t bytes = mf * 4 + 256 + img_b + (size_t)te->gfloats * 4 + 2 * kMaxFeat * 4 + kMaxFeat * 4 + 64;
+    uint8_t* base = nullptr;
+    CUDA_TRY(ctx, cudaMalloc(&base, bytes + 1024));
+    m.master = reinterpret_cast<float*>(base);
+    size_t o = (mf * 4 + 255) / 256 * 256;
+    m.timg = base + o; o += (img_b + 255) / 256 * 256;
+    m.tgrad = reinterpret_cast<float*>(base + o); o += ((size_t)te->gfloats * 4 + 255) / 256 * 256;
+    m.tnorm = reinterpret_cast<float*>(base + o); o += 2 * kMaxFeat * 4;
+    m.tperm = reinterpret_cast<int32_t*>(base + o); o += kMaxFeat * 4;
+    m.trows = reinterpret_cast<unsigned long long*>(base + (o + 15) / 16 * 16);
+    m.tK0P = K0P;
+    std::vector<float> h;
+    h.insert(h.end(), m.W[0].begin(), m.W[0].end());
+    h.insert(h.end(), m.b[0].begin(), m.b[0].end());
+    h.insert(h.end(), m.W[1].begin(), m.W[1].end());
+    h.insert(h.end(), m.b[1].begin(), m.b[1].end());
+    h.insert(h.end(), m.W[2].begin(), m.W[2].end());
+    h.push_back(m.b[2][0]);
+    CUDA_TRY(ctx, cudaMemcpyAsync(m.master, h.data(), h.size() * 4, cudaMemcpyHostToDevice, ctx->stream));
+    m.tperm_host.clear();
+  }
+  // the gather's normalisation in kernel input order, plus the constant-1 column K0 (scale 0, c 1)
+  std::vector<float> nrm(2 * kMaxFeat, 0.f);
+  for (int k = 0; k < K0; ++k) {
+    const int mk = pq.perm[k];
+    nrm[k] = m.scale[mk];
+    nrm[kMaxFeat + k] = (float)(-(double)m.shift[mk] * (double)m.scale[mk]);
+  }
+  nrm[kMaxFeat + K0] = 1.f;
+  CUDA_TRY(ctx, cudaMemcpyAsync(m.tnorm, nrm.data(), nrm.size() * 4, cudaMemcpyHostToDevice, ctx->stream));
+  CUDA_TRY(ctx, cudaMemsetAsync(m.tgrad, 0, (size_t)te->gfloats * 4, ctx->stream));
+  CUDA_TRY(ctx, cudaMemsetAsync(m.trows, 0, 16, ctx->stream));
+  if (m.tperm_host != pq.perm) {   // operand image for this input order (a zero-rows update: no step)
+    CUDA_TRY(ctx, cudaMemcpyAsync(m.tperm, pq.perm.data(), (size_t)K0 * 4, cudaMemcpyHostToDevice, ctx->stream));
+    te->upd<<<grid_for((int64_t)(H * K0P + H * H + H)), 256, 0, ctx->stream>>>(m.master, m.timg, m.tgrad, m.trows,
+                                                                             m.tperm, K0, 0.f);
+    CUDA_TRY(ctx, cudaGetLastError());
+    m.tperm_host = pq.perm;
+  }
+  if (pq.expand && (st = expand_join(ctx, pq)) != FLERN_OK) return st;
+  TrainParams tp;
+  std::memset(&tp, 0, sizeof(tp));
+  tp.q = pq.p;
+  QueryParams& p = tp.q;
+  p.scale = m.tnorm;
+  p.shift = m.tnorm + kMaxFeat;
+  p.partials = reinterpret_cast<unsigned long long*>(ctx->partials);
+  p.ticket = ctx->ticket;
+  p.work = reinterpret_cast<unsigned long long*>(ctx->ticket) + 1;
+  p.ngroups = 1;
+  tp.wimg = m.timg;
+  tp.master = m.master;
+  tp.K0 = K0;
+  tp.grad = m.tgrad;
+  tp.rows = m.trows;
+  const int grid = plan_claims(ctx, p, K0P, 2, 32 * kProdWarpsWide);
+  if (!te->attr_set) {
+    CUDA_TRY(ctx, cudaFuncSetAttribute(te->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)te->smem));
+    te->attr_set = true;
+  }
+  CUDA_TRY(ctx, cudaEventRecord(ctx->ev0, ctx->stream));
+  te->fn<<<grid, kTrainThreads, te->smem, ctx->stream>>>(tp);
+  CUDA_TRY(ctx, cudaGetLastError());
+  // the claim counter is reset by the last CTA of the query kernels; here by the host
+  CUDA_TRY(ctx, cudaMemsetAsync(p.work, 0, 8, ctx->stream));
+  te->upd<<<grid_for((int64_t)(H * K0P + H * H + H)), 256, 0, ctx->stream>>>(m.master, m.timg, m.tgrad, m.trows,
+                                                                           m.tperm, K0, lr);
+  CUDA_TRY(ctx, cudaGetLastError());
+  CUDA_TRY(ctx, cudaEventRecord(ctx->ev1, ctx->stream));
+  unsigned long long rows[2] = {0, 0};
+  double sse = 0.0;
+  CUDA_TRY(ctx, cudaMemcpyAsync(rows, m.trows, 16, cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_TRY(ctx, cudaMemcpyAsync(&sse, m.tgrad + (te->gfloats - 2), 8, cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  m.dirty = true;
+  res->rows_scanned = pq.expand ? pq.ep.nrows : (int64_t)rows[0];
+  res->rows_joined = (int64_t)rows[1];
+  res->loss = rows[1] > 0 ? sse / (double)rows[1] : 0.0;
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
+  res->elapsed_ms = ms;
+  return FLERN_OK;
+}
+
+extern "C" FLERN_API flern_status flern_get_model(flern_ctx* ctx, int32_t model_id, float* const* W, float* const* b) {
+  if (!ctx) return FLERN_E_INVALID_ARG;
+  if (model_id < 0 || model_id >= (int32_t)ctx->models.size())
+    return fail(ctx, FLERN_E_NOT_FOUND, "no model with id %d", model_id);
+  Model& m = ctx->models[model_id];
+  if (!W || !b) return fail(ctx, FLERN_E_INVALID_ARG, "flern_get_model: null output arrays");
+  const flern_status st = refresh_model(ctx, m);
+  if (st != FLERN_OK) return st;
+  for (size_t l = 0; l < m.W.size(); ++l) {
+    if (!W[l] || !b[l]) return fail(ctx, FLERN_E_INVALID_ARG, "flern_get_model: layer %zu has no output array", l);
+    std::memcpy(W[l], m.W[l].data(), m.W[l].size() * 4);
+    std::memcpy(b[l], m.b[l].data(), m.b[l].size() * 4);
+  }
   return FLERN_OK;
 }

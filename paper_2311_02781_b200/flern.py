@@ -29,7 +29,7 @@ FLERN_COPY_HOST, FLERN_COPY_DEVICE, FLERN_BORROW_DEVICE = 0x1, 0x2, 0x4
 FLERN_HT_MULTI = 0x1
 FLERN_Q_RESULT_DEVICE, FLERN_Q_ASYNC, FLERN_Q_BOTH_CLASSES, FLERN_Q_NO_MODEL, FLERN_Q_GENERIC_KERNEL = 0x1, 0x2, 0x4, 0x8, 0x10
 EXPORTED = ["flern_create", "flern_destroy", "flern_last_error", "flern_version", "flern_load_table",
-            "flern_update_table", "flern_run_query_streamed", "flern_drop_table", "flern_load_model", "flern_build_hashtable", "flern_build_hashtable_ex", "flern_run_query",
+            "flern_update_table", "flern_run_query_streamed", "flern_drop_table", "flern_load_model", "flern_build_hashtable", "flern_build_hashtable_ex", "flern_run_query", "flern_train_step", "flern_get_model",
             "flern_query_launches"]
 
 
@@ -87,6 +87,15 @@ _lib.flern_build_hashtable_ex.argtypes = [c_p, c_i32, ctypes.c_char_p, c_i32, ct
 _lib.flern_build_hashtable_ex.restype = c_i32
 _lib.flern_run_query.argtypes = [c_p, ctypes.POINTER(FlernQuery), ctypes.POINTER(FlernResult)]
 _lib.flern_run_query.restype = c_i32
+class FlernTrainResult(ctypes.Structure):
+    _fields_ = [("rows_scanned", c_i64), ("rows_joined", c_i64), ("loss", ctypes.c_double), ("elapsed_ms", ctypes.c_float)]
+
+
+_lib.flern_train_step.argtypes = [c_p, ctypes.POINTER(FlernQuery), c_i64, c_i64, ctypes.c_float,
+                                  ctypes.POINTER(FlernTrainResult)]
+_lib.flern_train_step.restype = c_i32
+_lib.flern_get_model.argtypes = [c_p, c_i32, ctypes.POINTER(c_p), ctypes.POINTER(c_p)]
+_lib.flern_get_model.restype = c_i32
 _lib.flern_query_launches.argtypes = []
 _lib.flern_query_launches.restype = c_i32
 
@@ -259,3 +268,20 @@ def flern_run_query_streamed(ctx, query: Query, columns: dict, chunk_rows: int, 
                                               ctypes.byref(res)))
     return res
 
+
+def flern_train_step(ctx, query: Query, row_lo: int, row_hi: int, lr: float) -> FlernTrainResult:
+    """One SGD step of the query's model on the joined tuples of fact rows [row_lo, row_hi) (target: the
+    query's sum column)."""
+    res = FlernTrainResult(0, 0, 0.0, 0.0)
+    _check(ctx, _lib.flern_train_step(ctx, ctypes.byref(query.q), row_lo, row_hi, lr, ctypes.byref(res)))
+    return res
+
+
+def flern_get_model(ctx, model_id: int, dims):
+    """The model's current fp32 weights: (W list of [out][in], b list of [out])."""
+    L = len(dims) - 1
+    W = [np.zeros((dims[l + 1], dims[l]), np.float32) for l in range(L)]
+    b = [np.zeros(dims[l + 1], np.float32) for l in range(L)]
+    _check(ctx, _lib.flern_get_model(ctx, model_id, (c_p * L)(*[w.ctypes.data for w in W]),
+                                     (c_p * L)(*[x.ctypes.data for x in b])))
+    return W, b
