@@ -43,7 +43,34 @@ WORKLOADS = {
           "(orders + weights replicated), 16 features -> MLP 16-256-256-1, score>0.5, GROUP BY o_orderpriority "
           "COUNT/SUM(l_extendedprice), NCCL reduce of the group partials",
 }
+WORKLOADS["c2s"] = ("C2 with the order keys scattered over 31 bits by a bijection (k -> k * 0x9E3779B1 mod 2^31): "
+                    "the build picks open addressing (Fibonacci hash, 8-byte {key, row} slots + payload rows) and "
+                    "every probe is a random access, instead of the direct-addressed fat entries of C2")
+WORKLOADS["train"] = ("ML in charge (NEXT-3): one SGD step (MSE, 16-128-128-1 regression of l_quantity) per pass over "
+                      "the C2 query's joined rows (SF1 per GPU): gather -> forward -> backward -> update")
 STRONG = {"c5"}          # total work fixed as N grows; the others hold a fixed shard per GPU
+TRAIN_METRIC = "joined rows trained/sec (one SGD step per batch, MSE, 16-128-128-1)"
+TRAIN_DIMS = [16, 128, 128, 1]
+
+
+def scatter_keys(db):
+    """c2s: remap l_orderkey / o_orderkey through the same bijection of [0, 2^31) (odd multiplier), so the
+    join result is unchanged but the keys are sparse and unordered."""
+    f = lambda k: ((k.astype(np.uint64) * np.uint64(0x9E3779B1)) & np.uint64(0x7FFFFFFF)).astype(np.int32)
+    db.fact["l_orderkey"] = f(db.fact["l_orderkey"])
+    name, m, cols = db.builds[0]
+    cols["o_orderkey"] = f(cols["o_orderkey"])
+    return db
+
+
+def make_db(name, cfg, **kw):
+    db = D.make_database(cfg, **kw)
+    return scatter_keys(db) if name == "c2s" else db
+
+
+def train_flops_per_row(dims):
+    """forward + backward (dX and dW): 3x the forward's 2 * sum(in * out) multiply-adds"""
+    return 3 * flops_per_row(dims)
 METRIC = "joined rows scored/sec (query+MLP, whole box)"
 
 
@@ -80,6 +107,10 @@ def workload_cfg(name, world):
         base, sf1 = D.CONFIGS["c4"], 10.0
     elif name == "c5":   # strong scaling: SF100 in total, SF100/N per GPU
         return D.CONFIGS["c5"], D.CONFIGS["c5"].sf / world
+    elif name == "c2s":
+        base, sf1 = D.CONFIGS["c2"], 1.0
+    elif name == "train":
+        base, sf1 = D.with_sf(D.CONFIGS["c2"], 1.0, dims=TRAIN_DIMS, sum_col=("fact", "l_quantity"), name="train"), 1.0
     else:
         raise SystemExit(f"unknown workload {name}")
     return D.with_sf(base, sf1 * world), sf1
@@ -204,6 +235,82 @@ def dist_env():
     return world, rank, local
 
 
+def bench_model(name, cfg):
+    """One model for every rank (replicated weights): normalisation from the first rows of the unsharded
+    table; the training workload's regression output starts small (out_scale 0.05)."""
+    prefix = make_db(name, cfg, max_slots=D.MODEL_SLOTS)
+    return D.make_model(cfg, prefix, out_scale=0.05, out_shift=0.0) if name == "train" else D.make_model(cfg, prefix)
+
+
+def timing_stats(ms):
+    """Per-launch device times: median and the mean without the min and max (the paper averages runs after
+    dropping the lowest and highest)."""
+    s = sorted(ms)
+    core = s[1:-1] if len(s) > 2 else s
+    return {"median_ms": statistics.median(s), "trimmed_mean_ms": sum(core) / len(core), "min_ms": s[0],
+            "max_ms": s[-1]}
+
+
+def run_train(args, cfg, sf1, db, model, gq, fact_bytes, world, rank, local, stream):
+    """--workload train: flern_train_step over the whole shard per step (NEXT-3). One GPU."""
+    import torch
+    from paper_2311_02781_b200 import flern as F
+    if world > 1:
+        raise SystemExit("--workload train runs on one GPU (no cross-rank gradient reduction)")
+    q = gq.make_query(gq.fact_id)
+    lr = 1e-7   # the step is timed, not the learning: a small rate keeps the weights in range
+    for _ in range(args.warmup):
+        F.flern_train_step(gq.ctx, q, 0, -1, lr)
+    torch.cuda.synchronize()
+    step_ms, rows = [], 0
+    t0e, t1e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        t0e.record(stream)
+        for _ in range(args.steps):
+            r = F.flern_train_step(gq.ctx, q, 0, -1, lr)
+            step_ms.append(r.elapsed_ms)
+            rows += r.rows_joined
+        t1e.record(stream)
+        torch.cuda.synchronize()
+    ms_per_step = t0e.elapsed_time(t1e) / args.steps
+    value = rows / args.steps / (ms_per_step / 1e3)
+    # e2e: every step copies the shard from pinned host memory into a table (flern_update_table) and trains
+    pinned = {k: torch.from_numpy(v).pin_memory() for k, v in db.fact.items()}
+    tid = F.flern_load_table(gq.ctx, "fact_e2e", pinned, F.FLERN_COPY_HOST)
+    qe = gq.make_query(tid)
+    t0 = time.perf_counter()
+    for _ in range(max(1, args.e2e_steps)):
+        F.flern_update_table(gq.ctx, tid, pinned, F.FLERN_COPY_HOST)
+        F.flern_train_step(gq.ctx, qe, 0, -1, lr)
+    e2e_s = (time.perf_counter() - t0) / max(1, args.e2e_steps)
+    tf_peak, hbm_peak, peak_src = peaks()
+    avg = sum(step_ms) / len(step_ms)
+    rows_step = rows // args.steps
+    primary, secondary = binding_roofline(train_flops_per_row(cfg.dims), rows_step, fact_bytes, avg, tf_peak, hbm_peak,
+                                          f"{peak_src} (burst)", f"{peak_src} (copy bandwidth)")
+    line = {"metric": TRAIN_METRIC, "value": value, "unit": "rows/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": WORKLOADS["train"], "sf_per_gpu": sf1, "rows_per_gpu": db.fact_n,
+                       "rows_trained_per_step": rows_step, "lr": lr,
+                       "l2": "no flush: inputs larger than L2 (fact columns %.0f MB/GPU > 126 MB)" % (fact_bytes / 1e6)},
+            "roofline": {**primary, "traffic": None, "kernel": "flern_train_kernel + train_update_kernel",
+                         "avg_launch_ms": avg, "timing": timing_stats(step_ms), "other": secondary},
+            "e2e": {"value": rows_step / e2e_s, "unit": "rows/s", "h2d_bytes_per_step": fact_bytes,
+                    "d2h_bytes_per_step": 24},
+            "gpu_launches": args.steps * 2, "clocks": clk.summary()}
+    if not args.no_cpu_baseline:
+        import oracle as O
+        n = min(db.fact_n, 20000)
+        t0 = time.perf_counter()
+        ro = O.train_step(cfg, db, model, lr, 0, n)
+        dt = time.perf_counter() - t0
+        line["cpu_baseline"] = {"value": ro["batch"] / dt, "unit": "rows/s", "cores": 1, "kind": "oracle",
+                                "sample": f"first {n} lineitem rows: batch export + fp64 SGD step, 1 thread, {dt:.1f} s"}
+    print(json.dumps(line), flush=True)
+    gq.close()
+
+
 def run_reference(args):
     world, rank, _ = dist_env()
     if rank != 0:
@@ -213,9 +320,29 @@ def run_reference(args):
     strong = args.workload in STRONG
     # C5 (SF100): a prefix of rank 0's shard (its orders rows restricted to the same slots give the same
     # join), so the host holds a bounded sample; the oracle's map build is over those orders only
-    db = D.make_database(cfg, rank=0, world=world, max_slots=2_000_000 if strong else None)
-    model = D.make_model(cfg, D.make_database(cfg, max_slots=D.MODEL_SLOTS))
+    db = make_db(args.workload, cfg, rank=0, world=world, max_slots=2_000_000 if strong else None)
+    model = bench_model(args.workload, cfg)
     threads = os.cpu_count() or 1
+    if args.workload == "train":   # the oracle's training step (single-threaded fp64) on a bounded batch
+        rows = min(db.fact_n, 20000)
+        t_total, trained = 0.0, 0
+        for i in range(args.warmup + args.steps):
+            t0 = time.perf_counter()
+            r = O.train_step(cfg, db, model, 1e-6, 0, rows)
+            if i >= args.warmup:
+                t_total += time.perf_counter() - t0
+                trained += r["batch"]
+        value = trained / t_total
+        print(json.dumps({
+            "impl": "reference", "metric": TRAIN_METRIC, "value": value, "unit": "rows/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t_total / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": WORKLOADS["train"], "sf_per_gpu": sf1, "rows_per_gpu": db.fact_n},
+            "cpu_baseline": {"value": value, "unit": "rows/s", "cores": 1, "kind": "oracle",
+                             "sample": f"first {rows} lineitem rows per step (batch export + fp64 SGD step, 1 thread)"},
+            "e2e": {"value": value, "unit": "rows/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        }), flush=True)
+        return
     # bounded sample per step: ~ (budget / (W+K)) seconds of oracle work each
     probe = min(db.fact_n, 1000 * threads)
     t0 = time.perf_counter()
@@ -292,15 +419,16 @@ def main():
         # host rows for the e2e leg and the cpu_baseline sample: a prefix of the shard (bounded host memory)
         host = D.make_database(cfg, rank=rank, world=world, max_slots=min(shi - slo, 10_000_000))
     else:
-        db = host = D.make_database(cfg, rank=rank, world=world)
+        db = host = make_db(args.workload, cfg, rank=rank, world=world)
         # fact shard resident in HBM (torch tensors borrowed by the library, no copy)
         fact_dev = {k: torch.from_numpy(v).to(device) for k, v in db.fact.items()}
     gen_s = time.perf_counter() - t_gen
-    # one model for every rank (replicated weights): normalisation from the first rows of the unsharded table
-    model = D.make_model(cfg, D.make_database(cfg, max_slots=D.MODEL_SLOTS))
+    model = bench_model(args.workload, cfg)
     gq = GpuQuery(cfg, db, model, device=local, stream=stream.cuda_stream, load_fact=False)
     gq.set_fact(F.flern_load_table(gq.ctx, "fact", fact_dev, F.FLERN_BORROW_DEVICE))
     fact_bytes = sum(v.numel() * 4 for v in fact_dev.values())
+    if args.workload == "train":
+        return run_train(args, cfg, sf1, db, model, gq, fact_bytes, world, rank, local, stream)
     G = cfg.ngroups
     out_count = torch.zeros(G, dtype=torch.int64, device=device)
     out_sum = torch.zeros(G, dtype=torch.int64, device=device)
@@ -433,7 +561,7 @@ def main():
                        "e2e_sample": f"{host.fact_n} of {db.fact_n} fact rows per GPU streamed per step"},
             "roofline": {**primary, "traffic": traffic,
                          "kernel": "flern_query_wide_kernel" if max(cfg.dims[1:-1]) > 256 else "flern_query_kernel",
-                         "avg_launch_ms": avg_kernel_ms, "other": secondary},
+                         "avg_launch_ms": avg_kernel_ms, "timing": timing_stats(kernel_ms), "other": secondary},
             "e2e": {"value": e2e_value, "unit": "rows/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
             "gpu_launches": args.steps * F.flern_query_launches(),
             "clocks": clk.summary(),

@@ -549,3 +549,24 @@ def test_wide_full_size_sampled(name):
         assert g["count"].tolist() == cnt.tolist() and g["sum"].tolist() == sm.tolist()
     finally:
         gq.close()
+
+
+NARROW_SHAPES = [(k, h, 1) for k in (8, 24, 40) for h in (64, 128, 256)] + \
+                [(k, h, 2) for k in (8, 24, 40) for h in (64, 128)] + [(16, 256, 2)]
+WIDE_SHAPES = [(16, 512, 2), (16, 1024, 2), (16, 1024, 3), (32, 512, 2), (32, 1024, 3), (40, 1024, 2)]
+
+
+@pytest.mark.parametrize("k0,h,nl", NARROW_SHAPES + WIDE_SHAPES)
+def test_every_kernel_shape(k0, h, nl):
+    """Every compiled (K0P, H, hidden layers) kernel with a calibrated random model on config 3's
+    two-probe chain (features: the first k0 of config 3's 32, repeated past 32): scores, selection
+    and aggregates against the oracle."""
+    import dataclasses
+    base = D.CONFIGS["c3"]
+    feats = (base.feats * 2)[:k0]
+    sf = 0.0005 if h >= 512 else 0.002
+    cfg = dataclasses.replace(D.with_sf(base, sf, match_rate=0.9), dims=[k0] + [h] * nl + [1], feats=feats,
+                              name=f"shape{k0}_{h}_{nl}")
+    db = D.make_database(cfg)
+    r = parity.check(cfg, db, _calibrated(cfg, db))
+    assert r["scored"] > 0
