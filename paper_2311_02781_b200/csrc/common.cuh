@@ -145,6 +145,7 @@ struct QueryParams {
   const int32_t* tbase[kMaxChain];
   int32_t tpstr[kMaxChain];
   int64_t scanned;                 // tuple mode: fact rows the expansion scanned (counters[0])
+  int32_t sum_alias;               // >= 0: the sum column is fact feature k's column (staged once, read there)
 };
 
 // Pipeline trace (diagnostic): clock64() at each hand-off, CTA 0, first kTraceTiles tiles/batches.
@@ -253,7 +254,7 @@ struct FactRing {
 };
 __device__ __forceinline__ const int32_t* fact_col_ptr(const QueryParams& p, int c) {
   return c == 0 ? p.probe[0].fact_key
-                : (c == 1 ? (p.sum.src == 0 ? p.sum.base : nullptr)
+                : (c == 1 ? ((p.sum.src == 0 && p.sum_alias < 0) ? p.sum.base : nullptr)
                           : (c == 2 ? (p.grp.src == 0 ? p.grp.base : nullptr) : p.fcol[c - 3]));
 }
 

@@ -281,6 +281,10 @@ extern "C" FLERN_API flern_status flern_create(int device, void* cuda_stream, fl
   if (cudaMemsetAsync(ctx->ticket, 0, 64, ctx->stream) != cudaSuccess) return FLERN_E_CUDA;
   // let the build side of the join persist in L2 while the fact table streams through
   if (ctx->persist_max > 0) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, ctx->persist_max);
+  if (const char* sn = diag_env("FLERN_SPIN_NS")) {   // tuning knob (see c_spin_ns)
+    const uint32_t v = (uint32_t)strtoul(sn, nullptr, 0);
+    if (cudaMemcpyToSymbol(c_spin_ns, &v, sizeof(v)) != cudaSuccess) return FLERN_E_CUDA;
+  }
   if (const char* wh = diag_env("FLERN_WAIT_HINT")) {   // tuning knob (see c_wait_hint)
     const uint32_t v = (uint32_t)strtoul(wh, nullptr, 0);
     if (cudaMemcpyToSymbol(c_wait_hint, &v, sizeof(v)) != cudaSuccess) return FLERN_E_CUDA;
@@ -1034,6 +1038,9 @@ flern_status prepare_query(flern_ctx* ctx, const flern_query* q, const FactWindo
   }
   // the sum column (the training target: any numeric column)
   if ((st = resolve(q->sum_col, &p.sum, !training, training ? "target column" : "sum column")) != FLERN_OK) return st;
+  p.sum_alias = -1;   // the fact loader stages a column once: a sum column that is also a feature reads its slot
+  for (int k = 0; k < p.nfact && p.sum.src == 0; ++k)
+    if (p.fcol[k] == p.sum.base) { p.sum_alias = k; break; }
   if (q->prefilter_col) {
     const Column* c = fact.find(q->prefilter_col);
     if (!c) return fail(ctx, FLERN_E_NOT_FOUND, "pre-filter: fact table '%s' has no column '%s'", fact.name.c_str(), q->prefilter_col);

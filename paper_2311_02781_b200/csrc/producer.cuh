@@ -143,7 +143,7 @@ __device__ __forceinline__ void produce_batch(ProdState& st, const QueryParams& 
       if constexpr (BULK) {
         loadF(0, key);
         if (p.grp.src == 0) loadF(2, gv);
-        if (p.sum.src == 0) loadF(1, sv);
+        if (p.sum.src == 0) loadF(p.sum_alias >= 0 ? 3 + p.sum_alias : 1, sv);   // a feature's stage slot
       } else {
         loadR(p.probe[0].fact_key, row0, whole, anyld, key);
         loadR(p.grp.base, row0, whole, anyld && p.grp.src == 0, gv);
@@ -437,13 +437,6 @@ __device__ __forceinline__ void producer_loop(const QueryParams& p, const XRing&
   mbar_wait(&ring.empty[0], ((st.acq / S) & 1) ^ 1, 1);   // acquire the first stage
   st.acq = 1;
   int bidx = 0;
-  // staged fact column c: 0 = probe key, 1 = sum column, 2 = group column (null when they come from
-  // the build side), 3 + k = fact feature k
-  auto fact_col = [&](int c) -> const int32_t* {
-    return c == 0 ? p.probe[0].fact_key
-                  : (c == 1 ? (p.sum.src == 0 ? p.sum.base : nullptr)
-                            : (c == 2 ? (p.grp.src == 0 ? p.grp.base : nullptr) : p.fcol[c - 3]));
-  };
   bool expanded = false;
   if constexpr (SH::NF < 0) {
     if (p.tuples) {

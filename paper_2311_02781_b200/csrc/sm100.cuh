@@ -62,17 +62,35 @@ __device__ __forceinline__ uint64_t globaltimer_ns() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
-// Wait for the phase with parity `parity` to complete. A watchdog (checked every 4096 failed
-// tries) turns a protocol bug into a trapped kernel the host reports instead of a hung GPU.
+// Watchdog of the wait loops: called every 1024 failed polls (a real branch, out of line, so the poll
+// loop itself stays a few instructions); traps after 4 s, so a protocol bug becomes a kernel error the
+// host reports instead of a hung GPU.
+__device__ __noinline__ void wait_watchdog(uint64_t& t0, int tag, uint32_t parity) {
+  const uint64_t now = globaltimer_ns();
+  if (t0 == 0) {
+    t0 = now;
+  } else if (now - t0 > 4000000000ull) {
+    printf("flern: wait watchdog (tag %d) block %d thread %d parity %u\n", tag, (int)blockIdx.x, (int)threadIdx.x,
+           parity);
+    __trap();
+  }
+}
+// Back-off of the non-MMA waiters between polls (ns; 0 = spin). A try_wait without a suspend hint
+// returns after a short time, so a spinning warp re-issues its poll loop continuously and takes issue
+// slots from the producer and epilogue warps on its SMSP (ncu, r02a: the poll loop was ~45% of C2's
+// executed instructions). __nanosleep parks the warp without issuing.
+#ifndef FLERN_SPIN_NS
+#define FLERN_SPIN_NS 64u
+#endif
+__constant__ uint32_t c_spin_ns = FLERN_SPIN_NS;
+// Wait for the phase with parity `parity` to complete.
 __device__ __noinline__ void mbar_wait_slow(uint64_t* bar, uint32_t parity, int tag) {
-  uint64_t t0 = globaltimer_ns();
+  uint64_t t0 = 0;
   uint32_t n = 0;
+  const uint32_t ns = c_spin_ns;
   while (!mbar_try_wait(bar, parity)) {
-    if ((++n & 4095u) == 0 && globaltimer_ns() - t0 > 4000000000ull) {
-      printf("flern: mbarrier watchdog (tag %d) block %d thread %d parity %u\n", tag, (int)blockIdx.x,
-             (int)threadIdx.x, parity);
-      __trap();
-    }
+    if (ns) __nanosleep(ns);
+    if ((++n & 1023u) == 0) wait_watchdog(t0, tag, parity);
   }
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity, int tag) {
@@ -92,15 +110,10 @@ __device__ __forceinline__ bool mbar_try_wait_nohint(uint64_t* bar, uint32_t par
   return ok != 0;
 }
 __device__ __noinline__ void mbar_wait_nohint_slow(uint64_t* bar, uint32_t parity, int tag) {
-  uint64_t t0 = globaltimer_ns();
+  uint64_t t0 = 0;
   uint32_t n = 0;
-  while (!mbar_try_wait_nohint(bar, parity)) {
-    if ((++n & 4095u) == 0 && globaltimer_ns() - t0 > 4000000000ull) {
-      printf("flern: mbarrier watchdog (tag %d) block %d thread %d parity %u\n", tag, (int)blockIdx.x,
-             (int)threadIdx.x, parity);
-      __trap();
-    }
-  }
+  while (!mbar_try_wait_nohint(bar, parity))
+    if ((++n & 1023u) == 0) wait_watchdog(t0, tag, parity);
 }
 __device__ __forceinline__ void mbar_wait_nohint(uint64_t* bar, uint32_t parity, int tag) {
   if (!mbar_try_wait_nohint(bar, parity)) mbar_wait_nohint_slow(bar, parity, tag);
@@ -120,14 +133,10 @@ __device__ __forceinline__ uint32_t sm_count_load(const uint32_t* ctr) {
 // wait until *ctr >= target (unsigned wrap-safe), with the mbarrier watchdog's 4 s limit
 __device__ __forceinline__ void sm_count_wait(const uint32_t* ctr, uint32_t target, int tag) {
   if ((int32_t)(sm_count_load(ctr) - target) >= 0) return;
-  const uint64_t t0 = globaltimer_ns();
+  uint64_t t0 = 0;
   uint32_t n = 0;
-  while ((int32_t)(sm_count_load(ctr) - target) < 0) {
-    if ((++n & 65535u) == 0 && globaltimer_ns() - t0 > 4000000000ull) {
-      printf("flern: counter watchdog (tag %d) block %d thread %d\n", tag, (int)blockIdx.x, (int)threadIdx.x);
-      __trap();
-    }
-  }
+  while ((int32_t)(sm_count_load(ctr) - target) < 0)
+    if ((++n & 65535u) == 0) wait_watchdog(t0, tag, target);
 }
 
 // Named barrier among `nthreads` threads (id 1..15; 0 is __syncthreads).
