@@ -11,6 +11,7 @@ constexpr int kMaxGroupsLarge = 1 << 22; // larger domains: per-row int64 atomic
 constexpr int kMaxProbes = 2;            // probes resolved inside the fused kernel (fact -> A, A -> B)
 constexpr int kMaxChain = 8;             // probes of an expanded join (join_kernel.cuh): any chain, multimap
 constexpr int kTile = 128;
+constexpr int kWoutConst = 64;           // output-layer weights carried in the kernel parameters
 // Narrow kernel: 16 warps. SMSP k runs warps k, k+4, k+8, k+12. The MMA issuer (warp 12) shares
 // SMSP 0 only with the two quadrant-0 epilogue warps: the six producer warps (1, 2, 3, 13, 14, 15)
 // sit on SMSPs 1-3, so the issuing thread is not starved of issue slots by warps with deep ILP
@@ -146,6 +147,9 @@ struct QueryParams {
   int32_t tpstr[kMaxChain];
   int64_t scanned;                 // tuple mode: fact rows the expansion scanned (counters[0])
   int32_t sum_alias;               // >= 0: the sum column is fact feature k's column (staged once, read there)
+  int32_t pw_fat;                  // 1: per-warp-tile kernels take the pipelined fat-probe producer (producer_pw_fat)
+  float wout_half[kWoutConst];     // w_out / 2 (H <= kWoutConst): the lean epilogue's dot reads it from the
+                                   // constant bank (no shared-memory wavefronts; see nl1_epilogue_lean)
 };
 
 // Pipeline trace (diagnostic): clock64() at each hand-off, CTA 0, first kTraceTiles tiles/batches.

@@ -1054,6 +1054,15 @@ flern_status prepare_query(flern_ctx* ctx, const flern_query* q, const FactWindo
   p.both_classes = both ? 1 : 0;
   p.no_model = (q->flags & FLERN_Q_NO_MODEL) ? 1 : 0;
   p.dbg_mode = diag_env("FLERN_DBG_MODE") ? atoi(diag_env("FLERN_DBG_MODE")) : 0;   // diagnostic build only
+  {   // pipelined fat-probe producer (per-warp-tile kernels): one in-kernel probe into 8-word fat entries
+    const HashTable& h0 = ctx->hts[q->probes[0].ht_id];
+    bool ok = q->nprobes == 1 && !expand && h0.fstride == 8 && !h0.multi && !p.pf_col && p.dbg_mode == 0 &&
+              !diag_env("FLERN_NO_PWFAT");
+    for (int k = p.nfact; k < p.nfeat; ++k) ok = ok && p.dword[k] + 2 < 8;
+    if (p.grp.src == 1) ok = ok && p.grp.word + 2 < 8;
+    if (p.sum.src == 1) ok = ok && p.sum.word + 2 < 8;
+    p.pw_fat = ok ? 1 : 0;
+  }
   const double t = (double)q->threshold;
   p.thr_logit = t <= 0.0 ? -INFINITY : (t >= 1.0 ? INFINITY : (float)std::log(t / (1.0 - t)));
   uint8_t* img = m.dbuf;
@@ -1073,6 +1082,7 @@ flern_status prepare_query(flern_ctx* ctx, const flern_query* q, const FactWindo
   p.bias = reinterpret_cast<const float*>(img + m.off_bias);
   p.wout = reinterpret_cast<const float*>(img + m.off_wout);
   p.bout = m.bout;
+  for (int j = 0; j < kWoutConst; ++j) p.wout_half[j] = j < m.H ? 0.5f * m.W[m.NL][j] : 0.f;
   p.shift = reinterpret_cast<const float*>(img + m.off_shift);
   p.scale = reinterpret_cast<const float*>(img + m.off_scale);
   if (expand) {   // the expansion applies the pre-filter and scans the fact rows

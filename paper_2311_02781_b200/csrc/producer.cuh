@@ -12,6 +12,7 @@
 //     survivors (one row per thread), so rejected rows cost one 4-byte load and a compare.
 #pragma once
 #include "common.cuh"
+#include "pw_producer.cuh"
 
 namespace flern {
 
@@ -349,7 +350,8 @@ __device__ __forceinline__ void produce_batch(ProdState& st, const QueryParams& 
         }
         if (lane == 0) *m.count = total;
         fence_proxy_async_smem();
-        mbar_arrive(&ring.full[ts]);   // 32 arrivals: this warp
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&ring.full[ts]);   // one arrival per warp tile (after the warp's fences)
         if (t == 0) FLERN_TRACE(TR_P_DONE, bidx);
         return;
       }
@@ -462,7 +464,14 @@ __device__ __forceinline__ void producer_loop(const QueryParams& p, const XRing&
       }
     }
   }
-  if (expanded) {
+  bool pwf = false;   // pipelined fat-probe path (one probe into a fat table, per-warp tiles)
+  if constexpr (PW && BULK && SH::NF >= 0 && SH::ND1 == 0) {
+    if (p.pw_fat && !p.pf_col) {
+      pwf = true;
+      st.n_joined = producer_pw_fat<K0P, S, SH, NPW>(p, ring, s_normf, fr, warp, lane);
+    }
+  }
+  if (expanded || pwf) {
   } else if (BULK && !p.pf_col) {
     // batches come from the loader warp's fact ring (loader_loop), which also claims the row chunks
     for (uint32_t b = 0;; ++b, ++bidx) {
@@ -646,8 +655,10 @@ __device__ __forceinline__ void producer_loop(const QueryParams& p, const XRing&
         tk = __shfl_sync(0xffffffffu, tk, 0);
         const int ts = (int)(tk % (uint32_t)S);
         mbar_wait(&ring.empty[ts], ((tk / S) & 1) ^ 1, 5);
-        if (lane == 0) *meta_at(ring.meta, ts).count = -1;
-        mbar_arrive(&ring.full[ts]);
+        if (lane == 0) {
+          *meta_at(ring.meta, ts).count = -1;
+          mbar_arrive(&ring.full[ts]);
+        }
       }
     }
   } else {
@@ -691,7 +702,9 @@ __device__ __forceinline__ void loader_loop(const QueryParams& p, const FactRing
   uint32_t b = 0;
   auto publish = [&](int64_t row0, int nrows) {
     const int f = b % fr.stages;
+    if (lane == 0) FLERN_TRACE(TR_MMA_D2B_FREE, b);
     mbar_wait(&fr.empty[f], ((b / fr.stages) & 1) ^ 1, 7);
+    if (lane == 0) FLERN_TRACE(TR_MMA_L2A_DONE, b);
     if (lane == 0) {
       fr.hdr[2 * f] = row0;
       fr.hdr[2 * f + 1] = nrows;

@@ -20,6 +20,7 @@
 //   warp  12    TMEM allocator + single-thread tcgen05.mma issuer
 // An epilogue warp w may only touch TMEM lanes 32*(w%4) .. +31, hence warpgroup-aligned roles.
 #pragma once
+#include <type_traits>
 #include "producer.cuh"
 
 namespace flern {
@@ -100,6 +101,90 @@ __device__ __forceinline__ Meta meta_of(uint8_t* base, int s) {
               reinterpret_cast<int32_t*>(m + 16 + 4 * kTile), reinterpret_cast<int32_t*>(m + 16 + 8 * kTile)};
 }
 
+// Lean one-hidden-layer epilogue (the HBM-bound C1 shapes): one warpgroup per tile (the two warpgroups
+// alternate, TMEM buffers D[wg]), for plain queries (no debug exports, selected rows only, <= kFastGroups
+// groups: NG = the group count). Per row: both TMEM column blocks in flight with one wait, D released, then
+// relu(D).w_out as x.(w/2) + |x|.(w/2) (one FFMA2 per column, |x| an operand modifier), the predicate
+// (logit > ln(t/(1-t)), Q5) and NG predicated count / sum updates in registers.
+template <int NG, int H, int S, class P>
+__device__ __forceinline__ void nl1_epilogue_lean(const QueryParams& p, uint8_t* smem, uint64_t* full, uint64_t* empty,
+                                                  uint64_t* dfull, uint64_t* dempty, const float* s_wout,
+                                                  unsigned long long* acc, int64_t* s_cnt, int wg, int q, int lane) {
+  static_assert(H == 64 && H <= kWoutConst, "lean epilogue: 64 hidden units (two 32-column TMEM loads)");
+  const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+  const int r = q * 32 + lane;
+  const float thr = p.thr_logit, bout = p.bout;
+  uint32_t cnt[NG];
+  long long sum[NG];
+#pragma unroll
+  for (int g = 0; g < NG; ++g) { cnt[g] = 0u; sum[g] = 0ll; }
+  for (uint32_t t = wg;; t += 2) {
+    const int s = t % S;
+    mbar_wait(&full[s], (t / S) & 1, 25);
+    const Meta m = meta_of<P>(smem, s);
+    const int count = *m.count;
+    if (count < 0) break;
+    mbar_wait(&dfull[wg], (t >> 1) & 1, 26);
+    tc_fence_after();
+    uint32_t va[32], vb[32];
+    tmem_ld32_async(lane_off + wg * H, va);
+    tmem_ld32_async(lane_off + wg * H + 32, vb);
+    const bool valid = r < count;
+    const int g = m.grp[r];   // -1: outside [0, ngroups) (the producer's check)
+    const int32_t val = m.val[r];
+    tmem_ld_wait(va);
+    tmem_ld_wait(vb);
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) {
+      mbar_arrive(&dempty[wg]);   // D[wg] is in registers: the MMA of tile t + 2 may overwrite it
+      mbar_arrive(&empty[s]);     // the X stage (read by that MMA, completed) and its metadata
+    }
+    // w_out / 2 from the kernel parameters (constant bank): compile-time offsets, no shared-memory traffic
+    const float* wc = p.wout_half;
+    float2 a0 = make_float2(0.f, 0.f), a1 = a0, a2 = a0, a3 = a0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const float4 w = make_float4(wc[4 * i], wc[4 * i + 1], wc[4 * i + 2], wc[4 * i + 3]);
+      a0 = fma2(make_float2(__uint_as_float(va[4 * i]), __uint_as_float(va[4 * i + 1])), make_float2(w.x, w.y), a0);
+      a1 = fma2(make_float2(fabsf(__uint_as_float(va[4 * i])), fabsf(__uint_as_float(va[4 * i + 1]))), make_float2(w.x, w.y), a1);
+      a2 = fma2(make_float2(__uint_as_float(va[4 * i + 2]), __uint_as_float(va[4 * i + 3])), make_float2(w.z, w.w), a2);
+      a3 = fma2(make_float2(fabsf(__uint_as_float(va[4 * i + 2])), fabsf(__uint_as_float(va[4 * i + 3]))), make_float2(w.z, w.w), a3);
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const float4 w = make_float4(wc[32 + 4 * i], wc[32 + 4 * i + 1], wc[32 + 4 * i + 2], wc[32 + 4 * i + 3]);
+      a0 = fma2(make_float2(__uint_as_float(vb[4 * i]), __uint_as_float(vb[4 * i + 1])), make_float2(w.x, w.y), a0);
+      a1 = fma2(make_float2(fabsf(__uint_as_float(vb[4 * i])), fabsf(__uint_as_float(vb[4 * i + 1]))), make_float2(w.x, w.y), a1);
+      a2 = fma2(make_float2(__uint_as_float(vb[4 * i + 2]), __uint_as_float(vb[4 * i + 3])), make_float2(w.z, w.w), a2);
+      a3 = fma2(make_float2(fabsf(__uint_as_float(vb[4 * i + 2])), fabsf(__uint_as_float(vb[4 * i + 3]))), make_float2(w.z, w.w), a3);
+    }
+    const float logit = (((a0.x + a1.x) + (a0.y + a1.y)) + ((a2.x + a3.x) + (a2.y + a3.y))) + bout;
+    if (valid && g < 0) atomicAdd(reinterpret_cast<unsigned long long*>(&s_cnt[3]), 1ull);
+    const bool sel = valid && logit > thr;
+#pragma unroll
+    for (int gg = 0; gg < NG; ++gg) {
+      const bool h = sel && g == gg;
+      cnt[gg] += h ? 1u : 0u;
+      sum[gg] += h ? (long long)val : 0ll;
+    }
+  }
+#pragma unroll
+  for (int gg = 0; gg < NG; ++gg) {
+    unsigned long long n = cnt[gg];
+    long long v = sum[gg];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      n += __shfl_xor_sync(0xffffffffu, n, o);
+      v += __shfl_xor_sync(0xffffffffu, v, o);
+    }
+    if (lane == 0 && n) {
+      atomicAdd(&acc[gg * 4 + 0], n);
+      atomicAdd(&acc[gg * 4 + 1], (unsigned long long)v);
+    }
+  }
+}
+
 template <int K0P, int H, int NL, class SH>
 __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_constant__ QueryParams p) {
   // producer shape fixed at compile time -> fact columns staged by the loader warp (FactRing)
@@ -149,6 +234,12 @@ __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_c
     int4* bdst = reinterpret_cast<int4*>(smem + P::off_bb);   // bias B operands (see bias_operand_bytes)
     for (uint32_t i = tid; i < P::bimg_bytes / 16; i += kThreads) bdst[i] = ldg_nc(src + P::wimg_bytes / 16 + i);
     fill_ones_operand(smem + P::off_ones, tid, kThreads);
+    if constexpr (SH::NF >= 0) {   // X-stage K-chunks past a compile-time feature count are never written: zero
+      constexpr int c8z = (SH::NF + SH::ND0 + SH::ND1 + 7) / 8;
+      for (int s = 0; s < S; ++s)
+        for (int i = tid; i < (K0P / 8 - c8z) * kTile; i += kThreads)
+          reinterpret_cast<int4*>(smem + P::off_x + s * P::XS + c8z * (kTile * 16))[i] = make_int4(0, 0, 0, 0);
+    }
     for (int i = tid; i < H; i += kThreads) s_wout[i] = 0.5f * p.wout[i];   // w/2: see dot_cols
     for (int i = tid; i < kMaxFeat / 2; i += kThreads) {   // {scale_k, scale_k+1, c_k, c_k+1} per pair
       const int k = 2 * i;
@@ -169,7 +260,7 @@ __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_c
   const bool pw = P::PW && p.pf_col == nullptr;
   if (tid == 0) {
     *s_ticket = 0u;
-    for (int s = 0; s < S; ++s) { mbar_init(&full[s], pw ? 32 : 32 * kProdWarps); mbar_init(&empty[s], 4); }
+    for (int s = 0; s < S; ++s) { mbar_init(&full[s], pw ? 1 : 32 * kProdWarps); mbar_init(&empty[s], 4); }
     mbar_init(d1full, 1);
     mbar_init(d1empty, 4);
     for (int i = 0; i < 2; ++i) { mbar_init(&dfull[i], 1); mbar_init(&dempty[i], 4); }
@@ -344,11 +435,14 @@ __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_c
           const int s = t % S;
           mbar_wait(&full[s], (t / S) & 1, 10);
           if (*meta_of<P>(smem, s).count < 0) break;
+          if (lane == 0) FLERN_TRACE(TR_MMA_NEXT_READY, t);
           const int b = t & 1;
           mbar_wait(&dempty[b], ((t >> 1) & 1) ^ 1, 11);
+          if (lane == 0) FLERN_TRACE(TR_MMA_D2A_FREE, t);
           tc_fence_after();
           issue_l1(s, b * H);
           if (elect_one_sync()) mma_commit(&dfull[b]);
+          if (lane == 0) FLERN_TRACE(TR_MMA_L1_ISSUED, t);
         }
       }
     }
@@ -499,15 +593,39 @@ __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_c
       }
     } else {
       // ---- NL == 1: the two warpgroups take alternate tiles (TMEM buffer D[wg]) ----
-      for (uint32_t t = wg;; t += 2) {
+      bool lean = false;
+      if constexpr (H == 64 && SH::NF >= 0) {
+        lean = !p.no_model && !p.dbg_score && !p.dbg_selected && !p.both_classes && p.dbg_mode == 0;
+        auto run = [&](auto ng) {
+          nl1_epilogue_lean<decltype(ng)::value, H, S, P>(p, smem, full, empty, dfull, dempty, s_wout, acc, s_cnt, wg, q,
+                                                           lane);
+        };
+        if (lean) {
+          switch (p.ngroups) {
+            case 1: run(std::integral_constant<int, 1>{}); break;
+            case 2: run(std::integral_constant<int, 2>{}); break;
+            case 3: run(std::integral_constant<int, 3>{}); break;
+            case 4: run(std::integral_constant<int, 4>{}); break;
+            case 5: run(std::integral_constant<int, 5>{}); break;
+            case 6: run(std::integral_constant<int, 6>{}); break;
+            case 7: run(std::integral_constant<int, 7>{}); break;
+            case 8: run(std::integral_constant<int, 8>{}); break;
+            default: lean = false;
+          }
+        }
+      }
+      for (uint32_t t = wg; !lean; t += 2) {
         const int s = t % S;
         mbar_wait(&full[s], (t / S) & 1, 25);
         const Meta m = meta_of<P>(smem, s);
         const int count = *m.count;
         if (count < 0) break;
+        const bool tr = (tid & 127) == 0;
+        if (tr) FLERN_TRACE(TR_W1_FULL, t);
         float logit = 0.f;
         if (!p.no_model) {
           mbar_wait(&dfull[wg], (t >> 1) & 1, 26);
+          if (tr) FLERN_TRACE(TR_W1_DFULL0, t);
           tc_fence_after();
           float2 acc4[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
                             make_float2(0.f, 0.f)};
@@ -515,10 +633,12 @@ __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_c
           // chunk's math), so the MMA of tile t + 2 can start earlier
           dot_cols(wg * H, H, 0, acc4, release(&dempty[wg]));
           logit = dot_sum(acc4) + p.bout;
+          if (tr) FLERN_TRACE(TR_W1_DOTA, t);
         }
         finish_tile(m, count, s, logit);
+        if (tr) FLERN_TRACE(TR_W1_AGG, t);
       }
-      flush_acc();
+      if (!lean) flush_acc();
     }
   }
 

@@ -10,7 +10,7 @@
 using namespace flern;
 
 template <int OP>
-__global__ void __launch_bounds__(256, 1) bench(int iters, unsigned long long* out, float seed) {
+__global__ void __launch_bounds__(512, 1) bench(int iters, unsigned long long* out, float seed) {
   __shared__ uint32_t tslot;
   __shared__ __align__(16) uint8_t sbuf[16384 + 1024];
   const int warp = threadIdx.x >> 5;
@@ -87,7 +87,7 @@ __global__ void __launch_bounds__(256, 1) bench(int iters, unsigned long long* o
   uint32_t acc = 0;
 #pragma unroll
   for (int i = 0; i < 16; ++i) acc ^= u[i] ^ __float_as_uint(a[i]);
-  if ((threadIdx.x & 31) == 0) out[blockIdx.x * 8 + warp] = (t1 - t0);
+  if ((threadIdx.x & 31) == 0) out[blockIdx.x * 16 + warp] = (t1 - t0);
   if (acc == 0x12345678u) out[0] = acc;   // keep the work
   if (OP == 4 || OP == 7) {
     tc_fence_before();
@@ -101,16 +101,16 @@ void run(const char* name, int warps, int per_iter) {
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   unsigned long long* d;
-  cudaMalloc(&d, sms * 8 * 8);
+  cudaMalloc(&d, sms * 16 * 8);
   const int iters = 4096;
   bench<OP><<<sms, warps * 32>>>(iters, d, 1.5f);
   bench<OP><<<sms, warps * 32>>>(iters, d, 1.5f);
   cudaDeviceSynchronize();
-  unsigned long long h[148 * 8];
-  cudaMemcpy(h, d, sms * 8 * 8, cudaMemcpyDeviceToHost);
+  unsigned long long h[148 * 16];
+  cudaMemcpy(h, d, sms * 16 * 8, cudaMemcpyDeviceToHost);
   double avg = 0;
   for (int b = 0; b < sms; ++b)
-    for (int w = 0; w < warps; ++w) avg += h[b * 8 + w];
+    for (int w = 0; w < warps; ++w) avg += h[b * 16 + w];
   avg /= sms * warps;
   const double per = avg / iters;
   printf("%-28s warps/SM=%d  cycles/iter %.1f  -> %.2f cycles per warp-instr per warp (%d instr/iter); err=%s\n", name,
@@ -119,7 +119,7 @@ void run(const char* name, int warps, int per_iter) {
 }
 
 int main() {
-  for (int w : {4, 8}) {
+  for (int w : {4, 8, 16}) {
     run<0>("F2FP.RELU.BF16 pack", w, 16);
     run<1>("FMNMX", w, 16);
     run<2>("FFMA2", w, 8);

@@ -33,6 +33,7 @@ def _ranges():
     nl1 = find("---- NL == 1:", epi)
     tear = find("---- teardown", epi)
     return {
+        ("pw_producer.cuh", 1, 99999): "producer",
         ("producer.cuh", 1, 99999): "producer",
         ("query_kernel.cuh", setup, mma - 1): "setup/dispatch",
         ("query_kernel.cuh", mma, epi - 1): "mma",

@@ -45,6 +45,26 @@ for a, b in [("MMA_D2A_FREE", "MMA_L2A_DONE"), ("MMA_L2A_DONE", "MMA_NEXT_READY"
     print(f"  {a:>16s} -> {b:<16s} {d(EV.index(a), EV.index(b)):8.0f}")
 pd = np.diff(tr[EV.index("P_START"), 10:100])
 print("producer batch period:", float(np.median(pd)))
+# fact loader (C1 shapes: stamps of stage b before / after its empty wait) vs the producer warp 0 batches
+lb, la = tr[EV.index("MMA_D2B_FREE")], tr[EV.index("MMA_L2A_DONE")]
+if (la[20:200] > 0).all() and not (tr[EV.index("MMA_L2B_ISSUED"), 20:200] > 0).any():
+    print("  loader: stage period", float(np.median(np.diff(la[20:200]))), " empty-wait", float(np.median((la - lb)[20:200])))
+    ps = tr[EV.index("P_START")]
+    print("  producer w0: issue(b+1) wait", d(EV.index("P_START"), EV.index("P_PROBED")), " gather wait",
+          d(EV.index("P_PROBED"), EV.index("P_GATHERED")), " process", d(EV.index("P_GATHERED"), EV.index("P_DONE")),
+          " done->next", float(np.median((ps[21:200] - tr[EV.index("P_DONE"), 20:199]))))
+    print("  loader publish(b) -> producer w0 start(b-1):", float(np.median(ps[20:200] - la[21:201])))
+    for a, b in [("P_START", "P_PROBED"), ("P_PROBED", "W0_FULL"), ("W0_FULL", "P_GATHERED"), ("P_GATHERED", "W0_D1FULL"),
+                 ("W0_D1FULL", "W0_HFREE0"), ("W0_HFREE0", "W0_DONE"),
+                 ("W0_DONE", "W1_DOTB"), ("W1_DOTB", "P_DONE")]:
+        print(f"    process {a:>10s} -> {b:<10s} {d(EV.index(a), EV.index(b)):8.0f}")
+# NL = 1 pipeline (C1 shapes): MMA issuer and the epilogue warpgroup of each tile
+if (tr[EV.index("MMA_NEXT_READY"), 20:200] > 0).any() and not (tr[EV.index("MMA_L2A_DONE"), 20:200] > 0).any():
+    for a, b in [("MMA_NEXT_READY", "MMA_D2A_FREE"), ("MMA_D2A_FREE", "MMA_L1_ISSUED"), ("MMA_L1_ISSUED", "W1_DFULL0"),
+                 ("W1_FULL", "W1_DFULL0"), ("W1_DFULL0", "W1_DOTA"), ("W1_DOTA", "W1_AGG")]:
+        print(f"  NL1 {a:>16s} -> {b:<16s} {d(EV.index(a), EV.index(b)):8.0f}")
+    print("  NL1 tile period (MMA issue):", float(np.median(np.diff(tr[EV.index("MMA_L1_ISSUED"), 20:200]))))
+    print("  NL1 W1_AGG(t) -> W1_FULL(t+2):", float(np.median(tr[EV.index("W1_FULL"), 22:200] - tr[EV.index("W1_AGG"), 20:198])))
 W = ["MMA<-producer(full)", "MMA<-WG1(dempty0)", "MMA<-WG1(dempty1)", "MMA<-WG0(hfull)", "MMA<-WG0(d1empty)",
      "WG0<-producer(full)", "WG0<-MMA(d1full)", "WG0<-MMA(hfree)", "WG1<-producer(full)", "WG1<-MMA(dfull)",
      "producer<-WG1(empty)", "kernel cycles (CTA0 MMA thread)"]
