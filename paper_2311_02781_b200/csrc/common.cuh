@@ -148,6 +148,7 @@ struct QueryParams {
   int64_t scanned;                 // tuple mode: fact rows the expansion scanned (counters[0])
   int32_t sum_alias;               // >= 0: the sum column is fact feature k's column (staged once, read there)
   int32_t pw_fat;                  // 1: per-warp-tile kernels take the pipelined fat-probe producer (producer_pw_fat)
+  int32_t pw_flags;                // diagnostic A/B bits of producer_pw_fat (FLERN_PW_FLAGS, diagnostic builds; 0 otherwise)
   float wout_half[kWoutConst];     // w_out / 2 (H <= kWoutConst): the lean epilogue's dot reads it from the
                                    // constant bank (no shared-memory wavefronts; see nl1_epilogue_lean)
 };

@@ -204,7 +204,7 @@ constexpr bool plan_fits() {
   constexpr uint32_t XS = (uint32_t)kTile * K0P * 2;
   constexpr uint32_t META = kMetaBytes;
   constexpr uint32_t FIXED = WH + HB + W1 + NL * H * 4 + H * 4 + kMaxGroups * 4 * 8 + queue_bytes(32 * kProdWarps) + kMaxFeat * 8 +
-                             64 * 8 + 128;
+                             96 * 8 + 128;
   return FIXED + 3 * (XS + META) <= 232448;
 }
 
@@ -281,6 +281,7 @@ extern "C" FLERN_API flern_status flern_create(int device, void* cuda_stream, fl
   if (cudaMemsetAsync(ctx->ticket, 0, 64, ctx->stream) != cudaSuccess) return FLERN_E_CUDA;
   // let the build side of the join persist in L2 while the fact table streams through
   if (ctx->persist_max > 0) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, ctx->persist_max);
+#ifdef FLERN_DIAG
   if (const char* sn = diag_env("FLERN_SPIN_NS")) {   // tuning knob (see c_spin_ns)
     const uint32_t v = (uint32_t)strtoul(sn, nullptr, 0);
     if (cudaMemcpyToSymbol(c_spin_ns, &v, sizeof(v)) != cudaSuccess) return FLERN_E_CUDA;
@@ -289,6 +290,7 @@ extern "C" FLERN_API flern_status flern_create(int device, void* cuda_stream, fl
     const uint32_t v = (uint32_t)strtoul(wh, nullptr, 0);
     if (cudaMemcpyToSymbol(c_wait_hint, &v, sizeof(v)) != cudaSuccess) return FLERN_E_CUDA;
   }
+#endif
   if (cudaEventCreate(&ctx->ev0) != cudaSuccess || cudaEventCreate(&ctx->ev1) != cudaSuccess) return FLERN_E_CUDA;
   if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) return FLERN_E_CUDA;
   *out = ctx.release();
@@ -1062,6 +1064,7 @@ flern_status prepare_query(flern_ctx* ctx, const flern_query* q, const FactWindo
     if (p.grp.src == 1) ok = ok && p.grp.word + 2 < 8;
     if (p.sum.src == 1) ok = ok && p.sum.word + 2 < 8;
     p.pw_fat = ok ? 1 : 0;
+    p.pw_flags = diag_env("FLERN_PW_FLAGS") ? atoi(diag_env("FLERN_PW_FLAGS")) : 0;
   }
   const double t = (double)q->threshold;
   p.thr_logit = t <= 0.0 ? -INFINITY : (t >= 1.0 ? INFINITY : (float)std::log(t / (1.0 - t)));

@@ -29,6 +29,14 @@
 
 namespace flern {
 
+// batch-phase stamps of producer warp 0 (scripts/trace.py), compiled into diagnostic builds only: each
+// costs a few issue slots per batch on the SMSPs this path is bound by
+#ifdef FLERN_DIAG
+#define PW_TRACE(ev, idx) do { if (t == 0) FLERN_TRACE(ev, idx); } while (0)
+#else
+#define PW_TRACE(ev, idx) do { } while (0)
+#endif
+
 
 // my 4 rows [rel, rel + 4) of fact-stage column c at byte address a; the tail past the stage's last whole
 // 16-byte granule (nfull) comes from global memory (the table's last rows only)
@@ -138,7 +146,7 @@ __device__ __forceinline__ int64_t producer_pw_fat(const QueryParams& p, const X
   // shared-memory reads, load batch b+1's entries (in flight under batch b's conversion and stores), then
   // convert and store batch b.
   for (uint32_t b = 0; nrows >= 0; ++b) {
-    if (t == 0) FLERN_TRACE(TR_P_START, b);
+    PW_TRACE(TR_P_START, b);
     ecur = enext;
     if (pend >= 0) {
       fence_proxy_async_smem();
@@ -150,7 +158,7 @@ __device__ __forceinline__ int64_t producer_pw_fat(const QueryParams& p, const X
       __syncwarp();
       if (lane == 0) mbar_arrive(&fr.empty[pendf]);
     }
-    if (t == 0) FLERN_TRACE(TR_P_PROBED, b);
+    PW_TRACE(TR_P_PROBED, b);
     int nnext = -1;
     const int f = b % fr.stages;
     const int64_t srow0 = fr.hdr[2 * f];
@@ -230,10 +238,10 @@ __device__ __forceinline__ int64_t producer_pw_fat(const QueryParams& p, const X
         for (int r = 0; r < R; ++r) sv[r] = g1 ? ecur.w[ND0 + 1][r] : ecur.w[ND0][r];
       }
       pendf = f;   // released at the next batch's start (see above)
-      if (t == 0) FLERN_TRACE(TR_W0_FULL, b);
+      PW_TRACE(TR_W0_FULL, b);
       // batch b+1's entry loads: in flight under batch b's conversion and stores
       nnext = pw_issue<kBR>(p, fr, b + 1, rel, ent, kmin, mask, wsrc, nw, enext);
-      if (t == 0) FLERN_TRACE(TR_P_GATHERED, b);
+      PW_TRACE(TR_P_GATHERED, b);
       uint32_t pk[R][K0P / 2];
 #pragma unroll
       for (int r = 0; r < R; ++r)
@@ -249,15 +257,15 @@ __device__ __forceinline__ int64_t producer_pw_fat(const QueryParams& p, const X
           const float2 y = fma2(make_float2(fa, fb), make_float2(nm.x, nm.y), make_float2(nm.z, nm.w));
           pk[r][k / 2] = bf16x2(y.x, y.y);
         }
-      if (t == 0) FLERN_TRACE(TR_W0_D1FULL, b);
+      PW_TRACE(TR_W0_D1FULL, b);
       // 4. the survivors into this warp's own X stage (the ticket fixes the order the consumers follow);
       //    predicated stores, no per-row branches
       if (total > 0) {
         const uint32_t tks = __shfl_sync(0xffffffffu, tk, 0);
-        if (t == 0) FLERN_TRACE(TR_W0_HFREE0, b);
+        PW_TRACE(TR_W0_HFREE0, b);
         const int ts = (int)(tks % (uint32_t)S);
         mbar_wait(&ring.empty[ts], ((tks / S) & 1) ^ 1, 2);
-        if (t == 0) FLERN_TRACE(TR_W0_DONE, b);
+        PW_TRACE(TR_W0_DONE, b);
         const uint32_t xs = smem_u32(ring.x + ts * ring.xs);
         const Meta m = meta_at(ring.meta, ts);
         const uint32_t mrow = smem_u32(m.rowid), mgrp = smem_u32(m.grp), mval = smem_u32(m.val);
@@ -275,13 +283,13 @@ __device__ __forceinline__ int64_t producer_pw_fat(const QueryParams& p, const X
           st_shared_b32_if(valid[r], mval + 4 * tp, (uint32_t)sv[r]);
         }
         if (lane == 0) *m.count = total;
-        if (t == 0) FLERN_TRACE(TR_W1_DOTB, b);
+        PW_TRACE(TR_W1_DOTB, b);
         pend = ts;   // published (proxy fence + arrive) during the next batch, or after the last one
       }
     };
     if (nrows == kBR) batch(std::true_type{});
     else batch(std::false_type{});
-    if (t == 0) FLERN_TRACE(TR_P_DONE, b);
+    PW_TRACE(TR_P_DONE, b);
     nrows = nnext;
   }
   if (pend >= 0) {

@@ -120,11 +120,19 @@ __device__ __forceinline__ void nl1_epilogue_lean(const QueryParams& p, uint8_t*
   for (int g = 0; g < NG; ++g) { cnt[g] = 0u; sum[g] = 0ll; }
   for (uint32_t t = wg;; t += 2) {
     const int s = t % S;
+#ifdef FLERN_DIAG
+    const bool trc = q == 0 && lane == 0;
+#define EPI_TRACE(ev) do { if (trc) FLERN_TRACE(ev, t); } while (0)
+#else
+#define EPI_TRACE(ev) do { } while (0)
+#endif
     mbar_wait(&full[s], (t / S) & 1, 25);
     const Meta m = meta_of<P>(smem, s);
     const int count = *m.count;
     if (count < 0) break;
+    EPI_TRACE(TR_W1_FULL);
     mbar_wait(&dfull[wg], (t >> 1) & 1, 26);
+    EPI_TRACE(TR_W1_DFULL0);
     tc_fence_after();
     uint32_t va[32], vb[32];
     tmem_ld32_async(lane_off + wg * H, va);
@@ -160,6 +168,7 @@ __device__ __forceinline__ void nl1_epilogue_lean(const QueryParams& p, uint8_t*
       a3 = fma2(make_float2(fabsf(__uint_as_float(vb[4 * i + 2])), fabsf(__uint_as_float(vb[4 * i + 3]))), make_float2(w.z, w.w), a3);
     }
     const float logit = (((a0.x + a1.x) + (a0.y + a1.y)) + ((a2.x + a3.x) + (a2.y + a3.y))) + bout;
+    EPI_TRACE(TR_W1_DOTA);
     if (valid && g < 0) atomicAdd(reinterpret_cast<unsigned long long*>(&s_cnt[3]), 1ull);
     const bool sel = valid && logit > thr;
 #pragma unroll
@@ -168,7 +177,9 @@ __device__ __forceinline__ void nl1_epilogue_lean(const QueryParams& p, uint8_t*
       cnt[gg] += h ? 1u : 0u;
       sum[gg] += h ? (long long)val : 0ll;
     }
+    EPI_TRACE(TR_W1_AGG);
   }
+#undef EPI_TRACE
 #pragma unroll
   for (int gg = 0; gg < NG; ++gg) {
     unsigned long long n = cnt[gg];
@@ -431,18 +442,23 @@ __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_c
         }
       } else {
         // NL == 1: layer 1 is the only tensor-core layer; ping-pong TMEM buffers D[t&1]
+#ifdef FLERN_DIAG
+#define NL1_MMA_TRACE(ev, t) do { if (lane == 0) FLERN_TRACE(ev, t); } while (0)
+#else
+#define NL1_MMA_TRACE(ev, t) do { } while (0)
+#endif
         for (uint32_t t = 0;; ++t) {
           const int s = t % S;
           mbar_wait(&full[s], (t / S) & 1, 10);
           if (*meta_of<P>(smem, s).count < 0) break;
-          if (lane == 0) FLERN_TRACE(TR_MMA_NEXT_READY, t);
+          NL1_MMA_TRACE(TR_MMA_NEXT_READY, t);
           const int b = t & 1;
           mbar_wait(&dempty[b], ((t >> 1) & 1) ^ 1, 11);
-          if (lane == 0) FLERN_TRACE(TR_MMA_D2A_FREE, t);
+          NL1_MMA_TRACE(TR_MMA_D2A_FREE, t);
           tc_fence_after();
           issue_l1(s, b * H);
           if (elect_one_sync()) mma_commit(&dfull[b]);
-          if (lane == 0) FLERN_TRACE(TR_MMA_L1_ISSUED, t);
+          NL1_MMA_TRACE(TR_MMA_L1_ISSUED, t);
         }
       }
     }

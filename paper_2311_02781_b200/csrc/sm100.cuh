@@ -26,10 +26,16 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 // Suspend-time hint of mbarrier waits in ns (host-set from FLERN_WAIT_HINT; 0 = the instruction's
 // default, no explicit hint). A waiting thread sleeps in hardware until the phase completes or the
 // hint expires instead of spinning through issue slots the working warps need.
+// Diagnostic builds only: the release build has no constant-memory load on the wait path.
+#ifdef FLERN_DIAG
 __constant__ uint32_t c_wait_hint = 0u;
+#define FLERN_WAIT_HINT_VALUE c_wait_hint
+#else
+#define FLERN_WAIT_HINT_VALUE 0u
+#endif
 __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
   uint32_t ok;
-  const uint32_t hint = c_wait_hint;
+  const uint32_t hint = FLERN_WAIT_HINT_VALUE;
   if (hint) {
     asm volatile(
         "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
@@ -82,12 +88,17 @@ __device__ __noinline__ void wait_watchdog(uint64_t& t0, int tag, uint32_t parit
 #ifndef FLERN_SPIN_NS
 #define FLERN_SPIN_NS 64u
 #endif
+#ifdef FLERN_DIAG
 __constant__ uint32_t c_spin_ns = FLERN_SPIN_NS;
+#define FLERN_SPIN_NS_VALUE c_spin_ns
+#else
+#define FLERN_SPIN_NS_VALUE FLERN_SPIN_NS
+#endif
 // Wait for the phase with parity `parity` to complete.
 __device__ __noinline__ void mbar_wait_slow(uint64_t* bar, uint32_t parity, int tag) {
   uint64_t t0 = 0;
   uint32_t n = 0;
-  const uint32_t ns = c_spin_ns;
+  const uint32_t ns = FLERN_SPIN_NS_VALUE;
   while (!mbar_try_wait(bar, parity)) {
     if (ns) __nanosleep(ns);
     if ((++n & 1023u) == 0) wait_watchdog(t0, tag, parity);

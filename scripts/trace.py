@@ -59,11 +59,11 @@ if (la[20:200] > 0).all() and not (tr[EV.index("MMA_L2B_ISSUED"), 20:200] > 0).a
                  ("W0_DONE", "W1_DOTB"), ("W1_DOTB", "P_DONE")]:
         print(f"    process {a:>10s} -> {b:<10s} {d(EV.index(a), EV.index(b)):8.0f}")
 # NL = 1 pipeline (C1 shapes): MMA issuer and the epilogue warpgroup of each tile
-if (tr[EV.index("MMA_NEXT_READY"), 20:200] > 0).any() and not (tr[EV.index("MMA_L2A_DONE"), 20:200] > 0).any():
+if (tr[EV.index("W1_FULL"), 20:200] > 0).any() and not (tr[EV.index("MMA_L2B_ISSUED"), 20:200] > 0).any():
     for a, b in [("MMA_NEXT_READY", "MMA_D2A_FREE"), ("MMA_D2A_FREE", "MMA_L1_ISSUED"), ("MMA_L1_ISSUED", "W1_DFULL0"),
                  ("W1_FULL", "W1_DFULL0"), ("W1_DFULL0", "W1_DOTA"), ("W1_DOTA", "W1_AGG")]:
         print(f"  NL1 {a:>16s} -> {b:<16s} {d(EV.index(a), EV.index(b)):8.0f}")
-    print("  NL1 tile period (MMA issue):", float(np.median(np.diff(tr[EV.index("MMA_L1_ISSUED"), 20:200]))))
+    print("  NL1 tile period (epilogue):", float(np.median(np.diff(tr[EV.index("W1_AGG"), 20:200]))))
     print("  NL1 W1_AGG(t) -> W1_FULL(t+2):", float(np.median(tr[EV.index("W1_FULL"), 22:200] - tr[EV.index("W1_AGG"), 20:198])))
 W = ["MMA<-producer(full)", "MMA<-WG1(dempty0)", "MMA<-WG1(dempty1)", "MMA<-WG0(hfull)", "MMA<-WG0(d1empty)",
      "WG0<-producer(full)", "WG0<-MMA(d1full)", "WG0<-MMA(hfree)", "WG1<-producer(full)", "WG1<-MMA(dfull)",
