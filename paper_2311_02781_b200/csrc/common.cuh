@@ -197,11 +197,26 @@ enum WaitCat {
     }                                                                                          \
   } while (0)
 #endif
+// Per-tile pipeline stamps (scripts/trace.py): diagnostic builds only (FLERN_DIAG), so the release kernels
+// carry no trace branches or parameter loads in their hot loops.
+#ifdef FLERN_DIAG
 #define FLERN_TRACE(ev, idx)                                                           \
   do {                                                                                 \
     if (p.dbg_trace && blockIdx.x == 0 && (idx) < kTraceTiles)                         \
       p.dbg_trace[(ev) * kTraceTiles + (idx)] = (unsigned long long)clock64();         \
   } while (0)
+#else
+#define FLERN_TRACE(ev, idx) \
+  do {                       \
+  } while (0)
+#endif
+// Diagnostic variants selected by QueryParams::dbg_mode (FLERN_DBG_MODE): 0 in the release build, so the
+// compiler removes those branches
+#ifdef FLERN_DIAG
+#define FLERN_DBG_MODE(p) ((p).dbg_mode)
+#else
+#define FLERN_DBG_MODE(p) 0
+#endif
 
 // Shared-memory plan (byte offsets from a 1024-aligned base), identical on host and device.
 struct Meta {  // view of one stage's metadata block

@@ -97,7 +97,7 @@ __device__ __forceinline__ void produce_batch(ProdState& st, const QueryParams& 
     };
       // diagnostic (FLERN_DBG_MODE bit 1): no global loads at all, every row joins build row 0 -- the
       // consumer side's ceiling with an infinitely fast producer
-      const bool synth = (p.dbg_mode & 2) != 0;
+      const bool synth = (FLERN_DBG_MODE(p) & 2) != 0;
       bool valid[R];
 #pragma unroll
       for (int r = 0; r < R; ++r) valid[r] = in[r];

@@ -540,7 +540,7 @@ __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_c
             ++pcs;
             if (tid == 128 && piece == 0) FLERN_TRACE(TR_W0_D1FULL, t);
             tc_fence_after();
-            if (p.dbg_mode & 33) {   // diagnostic: keep the protocol, skip the math
+            if (FLERN_DBG_MODE(p) & 33) {   // diagnostic: keep the protocol, skip the math
               release(d1empty)();
               for (int cc = 0; cc < CPP; ++cc) {
                 const int c = piece * CPP + cc;
@@ -596,7 +596,7 @@ __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_c
               FLERN_WAIT(W_WG1_DFULL, tid == 256, &dfull[h], t & 1, 24);
               if (tid == 256) FLERN_TRACE(h ? TR_W1_DFULL1 : TR_W1_DFULL0, t);
               tc_fence_after();
-              if (!(p.dbg_mode & 65)) dot_cols(TP::D2C + h * (H / 2), H / 2, h * (H / 2), acc4, release(&dempty[h]));
+              if (!(FLERN_DBG_MODE(p) & 65)) dot_cols(TP::D2C + h * (H / 2), H / 2, h * (H / 2), acc4, release(&dempty[h]));
               else release(&dempty[h])();
               if (tid == 256) FLERN_TRACE(h ? TR_W1_DOTB : TR_W1_DOTA, t);
             }
@@ -611,7 +611,7 @@ __global__ void __launch_bounds__(kThreads, 1) flern_query_kernel(const __grid_c
       // ---- NL == 1: the two warpgroups take alternate tiles (TMEM buffer D[wg]) ----
       bool lean = false;
       if constexpr (H == 64 && SH::NF >= 0) {
-        lean = !p.no_model && !p.dbg_score && !p.dbg_selected && !p.both_classes && p.dbg_mode == 0;
+        lean = !p.no_model && !p.dbg_score && !p.dbg_selected && !p.both_classes && FLERN_DBG_MODE(p) == 0;
         auto run = [&](auto ng) {
           nl1_epilogue_lean<decltype(ng)::value, H, S, P>(p, smem, full, empty, dfull, dempty, s_wout, acc, s_cnt, wg, q,
                                                            lane);
