@@ -579,7 +579,9 @@ __device__ __forceinline__ void producer_loop(const QueryParams& p, const XRing&
       // the scan reads shared memory, HBM sees one bulk stream
       for (uint32_t b = 0;; ++b) {
         const int f = b % fr.stages;
+        if (t == 0) FLERN_TRACE(TR_MMA_NEXT_READY, b);   // (diagnostic builds) pre-filter scan chunk b: wait
         mbar_wait(&fr.full[f], (b / fr.stages) & 1, 8);
+        if (t == 0) FLERN_TRACE(TR_MMA_D2A_FREE, b);
         const int64_t cb = fr.hdr[2 * f];
         const int nrows = (int)fr.hdr[2 * f + 1];
         int32_t x[8] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -608,6 +610,7 @@ __device__ __forceinline__ void producer_loop(const QueryParams& p, const XRing&
           break;
         }
         scan_chunk(cb, cb + nrows, x, false);
+        if (t == 0) FLERN_TRACE(TR_MMA_L1_ISSUED, b);
       }
     } else {
       // scan rows cb + 4t + 4*NPT*j (j = 0, 1; each warp instruction covers 128 contiguous rows); the

@@ -58,6 +58,16 @@ if (la[20:200] > 0).all() and not (tr[EV.index("MMA_L2B_ISSUED"), 20:200] > 0).a
                  ("W0_D1FULL", "W0_HFREE0"), ("W0_HFREE0", "W0_DONE"),
                  ("W0_DONE", "W1_DOTB"), ("W1_DOTB", "P_DONE")]:
         print(f"    process {a:>10s} -> {b:<10s} {d(EV.index(a), EV.index(b)):8.0f}")
+# pre-filter scan (c4p): per scan chunk b of producer thread 0: wait for the chunk, scan + gathers
+if "--pf" in sys.argv:
+    a, w, e = tr[EV.index("MMA_NEXT_READY")], tr[EV.index("MMA_D2A_FREE")], tr[EV.index("MMA_L1_ISSUED")]
+    ok = (a[10:250] > 0) & (e[10:250] > 0)
+    print("  pf chunk period", float(np.median(np.diff(a[10:250][ok]))), " wait", float(np.median((w - a)[10:250][ok])),
+          " scan+gather", float(np.median((e - w)[10:250][ok])), " mean scan+gather", float(np.mean((e - w)[10:250][ok])))
+    gs, gd = tr[EV.index("P_START")], tr[EV.index("P_DONE")]
+    okg = (gs[:200] > 0) & (gd[:200] > 0)
+    if okg.any():
+        print("  gather batches", int(okg.sum()), " median duration", float(np.median((gd - gs)[:200][okg])))
 # NL = 1 pipeline (C1 shapes): MMA issuer and the epilogue warpgroup of each tile
 if (tr[EV.index("W1_FULL"), 20:200] > 0).any() and not (tr[EV.index("MMA_L2B_ISSUED"), 20:200] > 0).any():
     for a, b in [("MMA_NEXT_READY", "MMA_D2A_FREE"), ("MMA_D2A_FREE", "MMA_L1_ISSUED"), ("MMA_L1_ISSUED", "W1_DFULL0"),
