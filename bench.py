@@ -540,6 +540,16 @@ def main():
             alg_bytes = 4 * db.fact_n + other * rows_scored_rank
         else:
             alg_bytes = fact_bytes
+        # + the build side touched once: the key and payload columns the query reads, for
+        # the build rows this rank's shard references (orders: its slot share; other build tables: all rows;
+        # with a pre-filter at most one per scored row)
+        build_bytes = 0
+        for pi, (bt, nb, cols) in enumerate(db.builds):
+            touched = nb // world if pi == 0 else nb
+            if cfg.prefilter:
+                touched = min(touched, rows_scored_rank)
+            build_bytes += 4 * len(cfg.build_cols(pi)) * touched
+        alg_bytes += build_bytes
         primary, secondary = binding_roofline(fpr, rows_scored_rank, alg_bytes, avg_kernel_ms, tf_peak, hbm_peak,
                                               f"{tf_src} ({peak_kind})", f"{peak_src} (copy bandwidth)")
         traffic = None

@@ -249,6 +249,30 @@ def test_c2_full_size_sampled(name, sf):
     assert g["count"].tolist() == cnt.tolist() and g["sum"].tolist() == sm.tolist()
 
 
+@pytest.mark.slow
+@pytest.mark.parametrize("name,sf", [("c2", 1.0), ("c1", 10.0), ("c4p", 10.0)])
+def test_full_size_real_model_aggregates(name, sf):
+    """Bench launch configurations with the real (calibrated) model and no debug exports, so the kernel
+    variant bench.py times runs (C1x: the pipelined one-layer producer and lean epilogue; C2: SF1 in
+    full; C4p: the pre-filter path at SF10): join and selection counts and the aggregates against the
+    oracle over the whole table, through parity rule 4's export-free bracket: rows the oracle scores
+    above the band are selected, rows inside the band may go either way (A_hi <= A_gpu <= A_hi + A_band),
+    and the GPU's selected-row count equals the sum of its group counts."""
+    import oracle as O
+    cfg = D.with_sf(D.CONFIGS[name], sf)
+    db = D.make_database(cfg)
+    model = D.make_model(cfg, db)
+    g = parity.run_gpu(cfg, db, model, debug=False)
+    o = O.run(cfg, db, model, band=parity.BAND)
+    assert g["rows_scanned"] == db.fact_n
+    assert g["rows_joined"] == o.rows_joined
+    assert np.all(o.count_hi <= g["count"]) and np.all(g["count"] <= o.count_hi + o.count_band), (g["count"], o.count_hi)
+    assert np.all(o.sum_hi <= g["sum"]) and np.all(g["sum"] <= o.sum_hi + o.sum_band)
+    assert g["rows_selected"] == int(g["count"].sum())
+    # the band is a small share of the scored rows (calibrated models: std(logit) ~ 1)
+    assert int(o.count_band.sum()) <= 0.10 * max(1, o.rows_joined)
+
+
 def test_no_model_mode_is_join_aggregate():
     """FLERN_Q_NO_MODEL (diagnostic used for the HBM roofline of scan/probe/gather): every joined
     row is selected, so the aggregates equal the brute-force join aggregate."""
