@@ -97,7 +97,16 @@ struct ColDesc {            // a column reference resolved to base pointer + row
   int32_t word;             // payload word (src > 0)
 };
 
+// A CUtensorMap (the 128-byte opaque TMA descriptor cuTensorMapEncodeTiled writes on the host), kept
+// here as raw words so the kernels need no driver header.
+struct alignas(64) TmaDesc {
+  unsigned long long opaque[16];
+};
+
 struct QueryParams {
+  // wide kernel (CTA pairs): 2D uint8 views [rows][128 B] of the weight image (box 32 rows: W1 halves;
+  // box 128 rows: hidden-layer half blocks) and of the activation scratch (box 128 rows)
+  TmaDesc tm_w1, tm_wh, tm_act;
   int64_t nrows;            // fact rows (< 2^31)
   unsigned long long* work; // chunk-claim counter (guided distribution, see chunk_rows); zero between launches
   int64_t claim_big;        // rows per "big" chunk (multiple of claim_small); chunks [0, claim_nbig) are big

@@ -12,6 +12,9 @@
 #include <string>
 #include <vector>
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include "flern.h"
 #include "build_kernel.cuh"
 #include "join_kernel.cuh"
@@ -193,7 +196,8 @@ struct KernelEntry {
   uint32_t smem;
   bool attr_set;
   int threads = kThreads;
-  size_t scratch_per_cta = 0;
+  size_t scratch_per_cta = 0;   // > 0: a wide kernel, launched as CTA pairs (clusters of 2)
+  int max_pairs = 0;            // co-resident clusters (cudaOccupancyMaxActiveClusters), set on first launch
 };
 
 template <int K0P, int H, int NL>
@@ -531,7 +535,8 @@ std::vector<uint8_t> model_image(Model& m, const std::vector<int>& perm) {
 }
 // Wide models (H = 512 / 1024): weights stream through SMEM per (256-neuron N-chunk, 64-wide
 // K-block), so the image is stored block by block in the operand layout the kernel copies verbatim:
-//   W1:  [NCH][256 x K0P] interleaved K-major;  W_l (l >= 2): [NCH][KB][256 x 64] 128B-swizzled.
+//   W1:  [NCH][2 halves][128 x K0P] interleaved K-major;  W_l (l >= 2): [NCH][KB][256 x 64] 128B-swizzled
+//   (a CTA pair splits every block by N: rows [0, 128) for the even CTA, [128, 256) for the odd one).
 std::vector<uint8_t> wide_image(Model& m, const std::vector<int>& perm) {
   const int H = m.H, K0 = m.K0, K0P = m.K0P, NL = m.NL;
   const int NCH = H / 256, KB = H / 64;
@@ -545,11 +550,12 @@ std::vector<uint8_t> wide_image(Model& m, const std::vector<int>& perm) {
   m.total = m.off_scale + (size_t)K0P * 4;
   std::vector<uint8_t> img(m.total, 0);
   for (int n = 0; n < H; ++n) {
-    uint16_t* w1 = reinterpret_cast<uint16_t*>(img.data() + (size_t)(n / 256) * w1c);
-    const int i = n % 256;
+    // N rows [0, 128) and [128, 256) of a chunk are the two CTAs' halves (cta_group::2 splits B by N)
+    const int i = n % 256, h = i / 128, ii = i % 128;
+    uint16_t* w1 = reinterpret_cast<uint16_t*>(img.data() + (size_t)(n / 256) * w1c + (size_t)h * (w1c / 2));
     for (int k = 0; k < K0P; ++k) {
       const float v = k < K0 ? m.W[0][(size_t)n * K0 + perm[k]] : 0.f;
-      const size_t off = (size_t)(k / 8) * (256 * 16) + (i / 8) * 128 + (i % 8) * 16 + (k % 8) * 2;
+      const size_t off = (size_t)(k / 8) * (128 * 16) + (ii / 8) * 128 + (ii % 8) * 16 + (k % 8) * 2;
       w1[off / 2] = bf16_rne_bits(v);
     }
   }
@@ -1150,14 +1156,45 @@ flern_status expand_join(flern_ctx* ctx, Prepared& pq) {
 
 // One persistent CTA per SM; rows are claimed as chunks (guided schedule, chunk_rows in common.cuh):
 // 2*grid contiguous halves of an 85% static share, then small chunks on demand. Returns the grid.
-int plan_claims(flern_ctx* ctx, QueryParams& p, int K0P, int NL, int npt) {
+// A 2D uint8 tensor map [rows][128 B] over `base` with a box of `box_rows` full rows: the TMA view the
+// wide kernel copies pre-laid-out operand blocks through (no swizzle: the bytes are already in the
+// operand layout). cuTensorMapEncodeTiled is a host-only driver call, found through the runtime.
+flern_status encode_rows_map(flern_ctx* ctx, TmaDesc* out, const void* base, size_t rows, uint32_t box_rows) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    cudaDriverEntryPointQueryResult qr;
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &qr) != cudaSuccess ||
+        qr != cudaDriverEntryPointSuccess || !fn)
+      return fail(ctx, FLERN_E_CUDA, "cuTensorMapEncodeTiled is not available from the driver");
+    encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  static_assert(sizeof(TmaDesc) == sizeof(CUtensorMap), "tensor map size");
+  const cuuint64_t dims[2] = {128, (cuuint64_t)std::max<size_t>(rows, box_rows)};
+  const cuuint64_t strides[1] = {128};
+  const cuuint32_t box[2] = {128, box_rows};
+  const cuuint32_t estr[2] = {1, 1};
+  CUtensorMap tm;
+  const CUresult r = encode(&tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box, estr,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(ctx, FLERN_E_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  std::memcpy(out, &tm, sizeof(tm));
+  return FLERN_OK;
+}
+
+// max_ctas: the persistent grid's cap (the SM count; for CTA pairs an even number of co-resident CTAs).
+// pair: the grid is rounded up to whole pairs.
+int plan_claims(flern_ctx* ctx, QueryParams& p, int K0P, int NL, int npt, int max_ctas = 0, bool pair = false) {
   const int64_t n = p.nrows;
+  if (max_ctas <= 0) max_ctas = ctx->num_sms;
   int64_t chunk = p.pf_col ? (int64_t)scan_rows(npt) : (int64_t)batch_rows(K0P, NL, npt);
   // a table smaller than one batch per SM: smaller chunks (multiples of 16 rows, aligned for vector
   // loads and bulk copies) so every SM takes a share and the kernel's latency shrinks
-  if (!p.pf_col && n < (int64_t)ctx->num_sms * chunk)
-    chunk = std::min(chunk, std::max<int64_t>(64, ((n + ctx->num_sms - 1) / ctx->num_sms + 15) / 16 * 16));
-  const int grid = (int)std::min<int64_t>(ctx->num_sms, std::max<int64_t>(1, (n + chunk - 1) / chunk));
+  if (!p.pf_col && n < (int64_t)max_ctas * chunk)
+    chunk = std::min(chunk, std::max<int64_t>(64, ((n + max_ctas - 1) / max_ctas + 15) / 16 * 16));
+  int grid = (int)std::min<int64_t>(max_ctas, std::max<int64_t>(1, (n + chunk - 1) / chunk));
+  if (pair) grid = std::min(max_ctas, (grid + 1) / 2 * 2);
   p.claim_small = chunk;
   p.claim_big = (int64_t)(0.85 * (double)n / (2.0 * grid)) / chunk * chunk;
   p.claim_nbig = p.claim_big > 0 ? 2 * (int64_t)grid : 0;
@@ -1255,7 +1292,29 @@ flern_status launch_query(flern_ctx* ctx, const flern_query* q, Prepared& pq, fl
   p.dbg_selected = d_sel;
 
   const int npt = 32 * (ke->threads == kThreads ? kProdWarps : kProdWarpsWide);   // producer threads
-  const int grid = plan_claims(ctx, p, m.K0P, m.NL, npt);
+  const bool pair = ke->scratch_per_cta != 0;   // wide kernels run as CTA pairs (cta_group::2)
+  if (!ke->attr_set) {
+    CUDA_TRY(ctx, cudaFuncSetAttribute(ke->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ke->smem));
+    ke->attr_set = true;
+  }
+  if (pair && ke->max_pairs == 0) {
+    cudaLaunchConfig_t occ = {};
+    occ.gridDim = dim3(2 * ctx->num_sms);
+    occ.blockDim = dim3(ke->threads);
+    occ.dynamicSmemBytes = ke->smem;
+    cudaLaunchAttribute ca[1];
+    ca[0].id = cudaLaunchAttributeClusterDimension;
+    ca[0].val.clusterDim.x = 2;
+    ca[0].val.clusterDim.y = 1;
+    ca[0].val.clusterDim.z = 1;
+    occ.attrs = ca;
+    occ.numAttrs = 1;
+    int nc = 0;
+    CUDA_TRY(ctx, cudaOccupancyMaxActiveClusters(&nc, ke->fn, &occ));
+    if (nc < 1) return fail(ctx, FLERN_E_CUDA, "no CTA pair of the wide kernel fits on this device");
+    ke->max_pairs = std::min(nc, ctx->num_sms / 2);
+  }
+  const int grid = plan_claims(ctx, p, m.K0P, m.NL, npt, pair ? 2 * ke->max_pairs : 0, pair);
   if (ke->scratch_per_cta) {   // wide kernel: per-CTA activation scratch
     const size_t need = (size_t)grid * ke->scratch_per_cta;
     if (ctx->scratch_bytes < need) {
@@ -1267,10 +1326,11 @@ flern_status launch_query(flern_ctx* ctx, const flern_query* q, Prepared& pq, fl
       ctx->scratch_bytes = need;
     }
     p.scratch = ctx->scratch;
-  }
-  if (!ke->attr_set) {
-    CUDA_TRY(ctx, cudaFuncSetAttribute(ke->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ke->smem));
-    ke->attr_set = true;
+    // TMA views of the weight image and the scratch (host-side encoding, no device work)
+    const size_t img_rows = m.wimg_bytes / 128, act_rows = ctx->scratch_bytes / 128;
+    if ((st = encode_rows_map(ctx, &p.tm_w1, p.wimg, img_rows, 32)) != FLERN_OK) return st;
+    if ((st = encode_rows_map(ctx, &p.tm_wh, p.wimg, img_rows, 128)) != FLERN_OK) return st;
+    if ((st = encode_rows_map(ctx, &p.tm_act, ctx->scratch, act_rows, 128)) != FLERN_OK) return st;
   }
   if (!async) CUDA_TRY(ctx, cudaEventRecord(ctx->ev0, ctx->stream));
   {
@@ -1279,7 +1339,15 @@ flern_status launch_query(flern_ctx* ctx, const flern_query* q, Prepared& pq, fl
     cfg.blockDim = dim3(ke->threads);
     cfg.dynamicSmemBytes = ke->smem;
     cfg.stream = ctx->stream;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
+    if (pair) {
+      attr[cfg.numAttrs].id = cudaLaunchAttributeClusterDimension;
+      attr[cfg.numAttrs].val.clusterDim.x = 2;
+      attr[cfg.numAttrs].val.clusterDim.y = 1;
+      attr[cfg.numAttrs].val.clusterDim.z = 1;
+      ++cfg.numAttrs;
+    }
+    cfg.attrs = attr;
     const HashTable& h0 = ctx->hts[q->probes[0].ht_id];
     // persisting L2 window: the build side of the join (narrow kernel), or the wide kernel's per-CTA
     // activation scratch, which is written and read back once per layer and must not be evicted to HBM
@@ -1290,15 +1358,14 @@ flern_status launch_query(flern_ctx* ctx, const flern_query* q, Prepared& pq, fl
       wbytes = (size_t)grid * ke->scratch_per_cta;
     }
     if (ctx->persist_max > 0 && ctx->window_max > 0 && !diag_env("FLERN_NO_L2_WINDOW")) {
-      attr[0].id = cudaLaunchAttributeAccessPolicyWindow;
-      attr[0].val.accessPolicyWindow.base_ptr = wbase;
-      attr[0].val.accessPolicyWindow.num_bytes = std::min(wbytes, ctx->window_max);
-      attr[0].val.accessPolicyWindow.hitRatio =
+      cudaLaunchAttribute& a = attr[cfg.numAttrs++];
+      a.id = cudaLaunchAttributeAccessPolicyWindow;
+      a.val.accessPolicyWindow.base_ptr = wbase;
+      a.val.accessPolicyWindow.num_bytes = std::min(wbytes, ctx->window_max);
+      a.val.accessPolicyWindow.hitRatio =
           (float)std::min(1.0, (double)ctx->persist_max / (double)std::min(wbytes, ctx->window_max));
-      attr[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-      attr[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-      cfg.attrs = attr;
-      cfg.numAttrs = 1;
+      a.val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+      a.val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
     }
     CUDA_TRY(ctx, cudaLaunchKernelEx(&cfg, ke->fn, p));
   }

@@ -362,6 +362,96 @@ __device__ __forceinline__ int2 lds64(uint32_t addr) {
   return v;
 }
 
+// ------------------------------------------------------------------------------- CTA pairs
+// Two CTAs of a cluster on one TPC cooperate on one tcgen05.mma with cta_group::2 (M = 256: each CTA
+// holds 128 rows of A, half of B's N, and its 128 rows of D in its own TMEM). Only the even CTA issues
+// the MMAs; both CTAs' operand loads complete on the even CTA's mbarrier.
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+// the shared::cluster address of the same shared-memory offset in CTA `rank` of this cluster
+__device__ __forceinline__ uint32_t mapa_rank(uint32_t saddr, uint32_t rank) {
+  uint32_t d;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(d) : "r"(saddr), "r"(rank));
+  return d;
+}
+__device__ __forceinline__ void cluster_sync_all() {   // every thread of every CTA of the cluster
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cl_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cl_addr) : "memory");
+}
+__device__ __forceinline__ void st_cluster_u32(uint32_t cl_addr, uint32_t v) {
+  asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(cl_addr), "r"(v) : "memory");
+}
+// waits whose phase is completed by an arrival from the peer CTA (cluster-scope acquire)
+__device__ __forceinline__ bool mbar_try_wait_cl(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __noinline__ void mbar_wait_cl_slow(uint64_t* bar, uint32_t parity, int tag, bool spin) {
+  uint64_t t0 = 0;
+  uint32_t n = 0;
+  while (!mbar_try_wait_cl(bar, parity)) {
+    if (!spin) __nanosleep(FLERN_SPIN_NS_VALUE);
+    if ((++n & 1023u) == 0) wait_watchdog(t0, tag, parity);
+  }
+}
+__device__ __forceinline__ void mbar_wait_cl(uint64_t* bar, uint32_t parity, int tag) {
+  if (!mbar_try_wait_cl(bar, parity)) mbar_wait_cl_slow(bar, parity, tag, false);
+}
+__device__ __forceinline__ void mbar_wait_cl_nohint(uint64_t* bar, uint32_t parity, int tag) {
+  if (!mbar_try_wait_cl(bar, parity)) mbar_wait_cl_slow(bar, parity, tag, true);
+}
+// TMEM of both CTAs of the pair (one warp in each CTA issues these, as with cta_group::1)
+__device__ __forceinline__ void tmem_alloc_pair(uint32_t* dst_smem, uint32_t ncols) {
+  asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst_smem)),
+               "r"(ncols)
+               : "memory");
+}
+__device__ __forceinline__ void tmem_relinquish_pair() {
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_dealloc_pair(uint32_t taddr, uint32_t ncols) {
+  asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols) : "memory");
+}
+// D[tmem of both CTAs] (+)= A[smem, 128 rows per CTA] * B[smem, N/2 rows per CTA]^T, M = 256, K = 16.
+// Issued by ONE thread of the even CTA; the descriptors address the same offsets in both CTAs.
+__device__ __forceinline__ void mma_bf16_ss_pair(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                                 uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// Arrive once on `bar` (same offset) in every CTA of `mask` when this thread's prior MMAs complete.
+__device__ __forceinline__ void mma_commit_pair(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"(mask)
+      : "memory");
+}
+// 2D tensor-map copy (TMA) into this CTA's shared memory whose bytes complete on an mbarrier of the
+// even CTA of the pair (`mbar_cl`: a shared::cluster address).
+__device__ __forceinline__ void tma_load_2d_pair(void* dst_smem, const void* tmap, int32_t c0, int32_t c1,
+                                                 uint32_t mbar_cl, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(dst_smem)),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(c0), "r"(c1), "r"(mbar_cl), "l"(pol)
+      : "memory");
+}
+
 // L2 eviction-priority policies (createpolicy) and the accesses that carry them.
 __device__ __forceinline__ uint64_t l2_policy_evict_last() {
   uint64_t pol;

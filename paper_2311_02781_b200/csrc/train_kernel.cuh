@@ -5,7 +5,8 @@
 //
 // One persistent kernel per step, the same producer as the query kernels (scan -> probe -> gather ->
 // normalise -> bf16 X tile in SMEM; the query's sum column is the target), then per 128-row tile, on
-// tcgen05 with TMEM accumulators (H = 128 hidden units, 2 hidden layers, linear output):
+// tcgen05 with TMEM accumulators (H = 128 hidden units, 2 hidden layers, linear output; the E phases
+// are split by hidden unit over kTrainCW compute warpgroups, which exchange their parts of y once):
 //   M1  Z1  = X  . W1^T                      (tile rows x H)          -> TMEM [0, 128)
 //   E1  H1  = relu(Z1 + b1) -> bf16 SMEM, mask1 in registers
 //   M2  Z2  = H1 . W2^T                                               -> TMEM [128, 256)
@@ -31,7 +32,9 @@ namespace flern {
 
 constexpr int kTrainH = 128;                // hidden width (M = 128 for the weight-gradient MMAs)
 constexpr int kTrainHA = kTrainH + 16;      // H1 tile width: H + a ones column (db2) + zero padding
-constexpr int kTrainThreads = 288;          // producers 0-3, compute warpgroup 4-7, MMA issuer 8
+constexpr int kTrainCW = 2;                 // compute warpgroups: each takes H / kTrainCW hidden units of every phase
+constexpr int kTrainMmaWarp = 4 + 4 * kTrainCW;
+constexpr int kTrainThreads = 32 * (kTrainMmaWarp + 1);   // producers 0-3, compute warpgroups 4.., MMA issuer last
 constexpr uint32_t kIdescAMajorMN = 1u << 15;
 
 // gradient / statistics buffer (fp32, zeroed before each step): G1 [H][K0P] (column K0 = db1),
@@ -74,7 +77,8 @@ struct TrainPlan {
   static constexpr uint32_t off_meta = off_dy + DYB;
   static constexpr uint32_t off_par = off_meta + S * kMetaBytes;   // b1 | b2 | w3 (fp32)
   static constexpr uint32_t off_queue = off_par + 3 * kTrainH * 4;
-  static constexpr uint32_t off_norm = off_queue + queue_bytes(32 * kProdWarpsWide);
+  static constexpr uint32_t off_xchg = off_queue + queue_bytes(32 * kProdWarpsWide);   // [2][kTrainCW][128] partial y
+  static constexpr uint32_t off_norm = off_xchg + 2 * kTrainCW * kTile * 4;
   static constexpr uint32_t off_bar = off_norm + kMaxFeat * 8;
   static constexpr uint32_t off_misc = off_bar + 32 * 8;
   static constexpr uint32_t total = off_misc + kMiscBytes;
@@ -106,7 +110,7 @@ __global__ void __launch_bounds__(kTrainThreads, 1) flern_train_kernel(const __g
   uint64_t* xfull = bars;          // [S] producers -> MMA / compute
   uint64_t* xempty = bars + 4;     // [S] MMA commit (M6 read the stage) -> producers
   uint64_t* z1full = bars + 8;     // MMA -> compute
-  uint64_t* h1full = bars + 9;     // compute (4 warps) -> MMA
+  uint64_t* h1full = bars + 9;     // compute (4 kTrainCW warps) -> MMA
   uint64_t* z2full = bars + 10;
   uint64_t* dz2full = bars + 11;   // compute (4) -> MMA
   uint64_t* tfree = bars + 12;     // MMA commit after M3-M5: dH1 ready; H1, H2, dZ2, dy tiles free
@@ -156,16 +160,16 @@ __global__ void __launch_bounds__(kTrainThreads, 1) flern_train_kernel(const __g
   if (tid == 0) {
     for (int s = 0; s < S; ++s) { mbar_init(&xfull[s], 32 * kProdWarpsWide); mbar_init(&xempty[s], 1); }
     mbar_init(z1full, 1);
-    mbar_init(h1full, 4);
+    mbar_init(h1full, 4 * kTrainCW);
     mbar_init(z2full, 1);
-    mbar_init(dz2full, 4);
+    mbar_init(dz2full, 4 * kTrainCW);
     mbar_init(tfree, 1);
-    mbar_init(dz1full, 4);
+    mbar_init(dz1full, 4 * kTrainCW);
     mbar_init(dz1free, 1);
     mbar_init(done, 1);
     fence_mbar_init();
   }
-  if (warp == 8) { tmem_alloc(tmem_slot, 512); tmem_relinquish(); }
+  if (warp == kTrainMmaWarp) { tmem_alloc(tmem_slot, 512); tmem_relinquish(); }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -177,7 +181,7 @@ __global__ void __launch_bounds__(kTrainThreads, 1) flern_train_kernel(const __g
     producer_loop<K0P, 2, S, GenericShape, kProdWarpsWide, false>(
         p, XRing{smem + P::off_x, P::XS, smem + P::off_meta, xfull, xempty}, wcnt, s_norm, s_cnt,
         reinterpret_cast<int32_t*>(smem + P::off_queue), s_claim, FactRing{}, warp * 32 + lane, warp, lane);
-  } else if (warp == 8) {
+  } else if (warp == kTrainMmaWarp) {
     // ---------------------------------------------------------------- MMA issuer
     constexpr uint32_t id_fwd1 = make_idesc_bf16(128, H);
     constexpr uint32_t id_fwd2 = make_idesc_bf16(128, H);
@@ -233,15 +237,20 @@ __global__ void __launch_bounds__(kTrainThreads, 1) flern_train_kernel(const __g
     if (lane == 0) *s_ntiles = (int32_t)t;
     if (elect_one_sync()) mma_commit(done);
     __syncwarp();
-  } else if (warp >= 4 && warp < 8) {
-    // ---------------------------------------------------------------- compute warpgroup (row r)
+  } else {
+    // ---------------------------------------------------------------- compute warpgroups (row r)
+    // warpgroup g takes hidden units [g HC, g HC + HC) of every phase; TMEM lane quadrant = warp % 4
+    constexpr int HC = H / kTrainCW, NC = HC / 32;
+    const int g = (warp - 4) >> 2;
     const int q = warp & 3;
     const int r = q * 32 + lane;
+    const int c0 = g * NC;   // first 32-column chunk of this warpgroup
     const uint32_t lo = (uint32_t)(q * 32) << 16;
     uint8_t* h1 = smem + P::off_h1;
     uint8_t* h2 = smem + P::off_h2;
     uint8_t* dz2 = smem + P::off_dz2;
     uint8_t* dyt = smem + P::off_dy;
+    float* xchg = reinterpret_cast<float*>(smem + P::off_xchg);
     double sse = 0.0;
     float sdy = 0.f;
     auto arrive4 = [&](uint64_t* bar) {
@@ -258,11 +267,12 @@ __global__ void __launch_bounds__(kTrainThreads, 1) flern_train_kernel(const __g
       if (count < 0) break;
       const bool valid = r < count;
       // E1: H1 = relu(Z1 + b1), mask1
-      uint32_t mask1[H / 32];
+      uint32_t mask1[NC];
       mbar_wait(z1full, t & 1, 66);
       tc_fence_after();
 #pragma unroll
-      for (int c = 0; c < H / 32; ++c) {
+      for (int cc = 0; cc < NC; ++cc) {
+        const int c = c0 + cc;
         uint32_t v[32];
         tmem_ld32(kTmZ1 + lo + c * 32, v);
         uint32_t bits = 0, pk[16];
@@ -274,21 +284,22 @@ __global__ void __launch_bounds__(kTrainThreads, 1) flern_train_kernel(const __g
           bits |= (z1 > 0.f ? 1u : 0u) << (i + 1);
           pk[i / 2] = relu_bf16x2(z0, z1);
         }
-        mask1[c] = bits;
+        mask1[cc] = bits;
 #pragma unroll
-        for (int g = 0; g < 4; ++g)
-          st_shared_v4(smem_u32(h1 + tile_off(r, c * 32 + g * 8, kTile)), pk[4 * g], pk[4 * g + 1], pk[4 * g + 2],
-                       pk[4 * g + 3]);
+        for (int gg = 0; gg < 4; ++gg)
+          st_shared_v4(smem_u32(h1 + tile_off(r, c * 32 + gg * 8, kTile)), pk[4 * gg], pk[4 * gg + 1], pk[4 * gg + 2],
+                       pk[4 * gg + 3]);
       }
       arrive4(h1full);
       // E2: H2, y, dy, dZ2
       mbar_wait(z2full, t & 1, 67);
       if (t > 0) mbar_wait(dz1free, (t - 1) & 1, 68);   // the H2 / dZ1 tile of t-1 was read by M6
       tc_fence_after();
-      uint32_t mask2[H / 32];
+      uint32_t mask2[NC];
       float y = 0.f;
 #pragma unroll
-      for (int c = 0; c < H / 32; ++c) {
+      for (int cc = 0; cc < NC; ++cc) {
+        const int c = c0 + cc;
         uint32_t v[32];
         tmem_ld32(kTmZ2 + lo + c * 32, v);
         uint32_t bits = 0, pk[16];
@@ -303,61 +314,75 @@ __global__ void __launch_bounds__(kTrainThreads, 1) flern_train_kernel(const __g
           bits |= (z1 > 0.f ? 1u : 0u) << (i + 1);
           pk[i / 2] = bf16x2(a0, a1);
         }
-        mask2[c] = bits;
+        mask2[cc] = bits;
 #pragma unroll
-        for (int g = 0; g < 4; ++g)
-          st_shared_v4(smem_u32(h2 + tile_off(r, c * 32 + g * 8, kTile)), pk[4 * g], pk[4 * g + 1], pk[4 * g + 2],
-                       pk[4 * g + 3]);
+        for (int gg = 0; gg < 4; ++gg)
+          st_shared_v4(smem_u32(h2 + tile_off(r, c * 32 + gg * 8, kTile)), pk[4 * gg], pk[4 * gg + 1], pk[4 * gg + 2],
+                       pk[4 * gg + 3]);
       }
+      // the output unit sums every warpgroup's part (in warpgroup order: the same fp32 sum in each)
+      float* xb = xchg + (t & 1) * kTrainCW * kTile;
+      xb[g * kTile + r] = y;
+      named_bar_sync(2, 32 * 4 * kTrainCW);
+      y = 0.f;
+#pragma unroll
+      for (int gg = 0; gg < kTrainCW; ++gg) y += xb[gg * kTile + r];
       y += b3;
       const int32_t tv = m.val[r];
       const float target = p.sum.is_float ? __int_as_float(tv) : (float)tv;
       const float e = valid ? y - target : 0.f;
       const float dy = 2.f * e;   // d(sum of squared errors)/dy; the update divides by the batch size
-      sse += (double)e * (double)e;
-      sdy += dy;
+      if (g == 0) {
+        sse += (double)e * (double)e;
+        sdy += dy;
+      }
 #pragma unroll
-      for (int c = 0; c < H / 32; ++c) {
+      for (int cc = 0; cc < NC; ++cc) {
+        const int c = c0 + cc;
         uint32_t pk[16];
 #pragma unroll
         for (int i = 0; i < 32; i += 2) {
-          const float g0 = ((mask2[c] >> i) & 1u) ? dy * s_w3[c * 32 + i] : 0.f;
-          const float g1 = ((mask2[c] >> (i + 1)) & 1u) ? dy * s_w3[c * 32 + i + 1] : 0.f;
+          const float g0 = ((mask2[cc] >> i) & 1u) ? dy * s_w3[c * 32 + i] : 0.f;
+          const float g1 = ((mask2[cc] >> (i + 1)) & 1u) ? dy * s_w3[c * 32 + i + 1] : 0.f;
           pk[i / 2] = bf16x2(g0, g1);
         }
 #pragma unroll
-        for (int g = 0; g < 4; ++g)
-          st_shared_v4(smem_u32(dz2 + tile_off(r, c * 32 + g * 8, kTile)), pk[4 * g], pk[4 * g + 1], pk[4 * g + 2],
-                       pk[4 * g + 3]);
+        for (int gg = 0; gg < 4; ++gg)
+          st_shared_v4(smem_u32(dz2 + tile_off(r, c * 32 + gg * 8, kTile)), pk[4 * gg], pk[4 * gg + 1], pk[4 * gg + 2],
+                       pk[4 * gg + 3]);
       }
-      st_shared_v4(smem_u32(dyt + tile_off(r, 0, kTile)), bf16x2(dy, 0.f), 0u, 0u, 0u);
-      st_shared_v4(smem_u32(dyt + tile_off(r, 8, kTile)), 0u, 0u, 0u, 0u);
+      if (g == 0) {
+        st_shared_v4(smem_u32(dyt + tile_off(r, 0, kTile)), bf16x2(dy, 0.f), 0u, 0u, 0u);
+        st_shared_v4(smem_u32(dyt + tile_off(r, 8, kTile)), 0u, 0u, 0u, 0u);
+      }
       arrive4(dz2full);
       // E3: dZ1 = dH1 * mask1 (into the H2 tile: M5 read H2 before tfree)
       mbar_wait(tfree, t & 1, 69);
       tc_fence_after();
 #pragma unroll
-      for (int c = 0; c < H / 32; ++c) {
+      for (int cc = 0; cc < NC; ++cc) {
+        const int c = c0 + cc;
         uint32_t v[32];
         tmem_ld32(kTmZ1 + lo + c * 32, v);
         uint32_t pk[16];
 #pragma unroll
         for (int i = 0; i < 32; i += 2) {
-          const float g0 = (valid && ((mask1[c] >> i) & 1u)) ? __uint_as_float(v[i]) : 0.f;
-          const float g1 = (valid && ((mask1[c] >> (i + 1)) & 1u)) ? __uint_as_float(v[i + 1]) : 0.f;
+          const float g0 = (valid && ((mask1[cc] >> i) & 1u)) ? __uint_as_float(v[i]) : 0.f;
+          const float g1 = (valid && ((mask1[cc] >> (i + 1)) & 1u)) ? __uint_as_float(v[i + 1]) : 0.f;
           pk[i / 2] = bf16x2(g0, g1);
         }
 #pragma unroll
-        for (int g = 0; g < 4; ++g)
-          st_shared_v4(smem_u32(h2 + tile_off(r, c * 32 + g * 8, kTile)), pk[4 * g], pk[4 * g + 1], pk[4 * g + 2],
-                       pk[4 * g + 3]);
+        for (int gg = 0; gg < 4; ++gg)
+          st_shared_v4(smem_u32(h2 + tile_off(r, c * 32 + gg * 8, kTile)), pk[4 * gg], pk[4 * gg + 1], pk[4 * gg + 2],
+                       pk[4 * gg + 3]);
       }
       arrive4(dz1full);
     }
-    // ---- flush: this CTA's weight gradients (TMEM lane j = row j of dW) and statistics
+    // ---- flush: this CTA's weight gradients (TMEM lane j = row j of dW) and statistics; warpgroup g
+    // takes the 32-column chunks c with c % kTrainCW == g
     mbar_wait(done, 0, 70);
     tc_fence_after();
-    float* g = tp.grad;
+    float* gr = tp.grad;
     const int j = r;   // TMEM lane = output neuron of the gradient rows
     if (*s_ntiles > 0) {
       auto red4 = [](float* dst, float a, float b, float c, float d) {
@@ -366,41 +391,43 @@ __global__ void __launch_bounds__(kTrainThreads, 1) flern_train_kernel(const __g
       };
       uint32_t v[32];
 #pragma unroll 1
-      for (int c = 0; c < 5; ++c) {   // dW2 [256, 400) and dW3 [400, 416): columns 256 .. 415
+      for (int c = g; c < 5; c += kTrainCW) {   // dW2 [256, 400) and dW3 [400, 416): columns 256 .. 415
         tmem_ld32(kTmDW2 + lo + c * 32, v);
 #pragma unroll
         for (int i = 0; i < 32; i += 4) {
           const int col = c * 32 + i;   // 0 .. 159: < HA dW2 (incl. db2 at H), HA .. HA+15 dW3 (column 0)
           if (col < HA)
-            red4(g + G::off_g2 + j * HA + col, __uint_as_float(v[i]), __uint_as_float(v[i + 1]),
+            red4(gr + G::off_g2 + j * HA + col, __uint_as_float(v[i]), __uint_as_float(v[i + 1]),
                  __uint_as_float(v[i + 2]), __uint_as_float(v[i + 3]));
           else if (col == HA)
-            atomicAdd(g + G::off_g3 + j, __uint_as_float(v[i]));
+            atomicAdd(gr + G::off_g3 + j, __uint_as_float(v[i]));
         }
       }
 #pragma unroll 1
-      for (int c = 0; c < (K0P + 31) / 32; ++c) {   // dW1 (incl. db1 at column K0)
+      for (int c = g; c < (K0P + 31) / 32; c += kTrainCW) {   // dW1 (incl. db1 at column K0)
         tmem_ld32(kTmDW1 + lo + c * 32, v);
 #pragma unroll
         for (int i = 0; i < 32; i += 4)
           if (c * 32 + i < K0P)
-            red4(g + G::off_g1 + j * K0P + c * 32 + i, __uint_as_float(v[i]), __uint_as_float(v[i + 1]),
+            red4(gr + G::off_g1 + j * K0P + c * 32 + i, __uint_as_float(v[i]), __uint_as_float(v[i + 1]),
                  __uint_as_float(v[i + 2]), __uint_as_float(v[i + 3]));
       }
     }
+    if (g == 0) {
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      sse += __shfl_xor_sync(0xffffffffu, sse, o);
-      sdy += __shfl_xor_sync(0xffffffffu, sdy, o);
-    }
-    if (lane == 0) {
-      atomicAdd(g + G::off_gb3, sdy);
-      atomicAdd(reinterpret_cast<double*>(g + G::off_sse), sse);
+      for (int o = 16; o > 0; o >>= 1) {
+        sse += __shfl_xor_sync(0xffffffffu, sse, o);
+        sdy += __shfl_xor_sync(0xffffffffu, sdy, o);
+      }
+      if (lane == 0) {
+        atomicAdd(gr + G::off_gb3, sdy);
+        atomicAdd(reinterpret_cast<double*>(gr + G::off_sse), sse);
+      }
     }
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 8) { tc_fence_after(); tmem_dealloc(0, 512); }
+  if (warp == kTrainMmaWarp) { tc_fence_after(); tmem_dealloc(0, 512); }
   if (tid == 0) {
     atomicAdd(tp.rows, (unsigned long long)s_cnt[0]);
     atomicAdd(tp.rows + 1, (unsigned long long)s_cnt[1]);

@@ -2,20 +2,21 @@
 // one SM (configs 3 and 4: 32-1024-1024-1024-1, SURVEY.md §8(a) row a5 / hard part H2).
 //
 // Same pipeline as query_kernel.cuh (scan -> probe -> gather -> MLP -> predicate -> group-by, one
-// launch per query), but the MLP runs layer by layer in N-chunks of 256 neurons:
+// launch per query), but the MLP runs layer by layer in N-chunks of 256 neurons, on CTA pairs:
 //   - weights are streamed from global (L2-resident, a few MB) through a ring of SMEM stages with
-//     1D bulk copies (cp.async.bulk) — the image is stored in the exact 128B-swizzled operand layout
-//     per (N-chunk, 64-wide K-block), so no tensor maps are needed;
+//     2D TMA copies (cp.async.bulk.tensor, cta_group::2) — the image is stored in the exact
+//     128B-swizzled operand layout per (N-chunk, 64-wide K-block, N half), so the tensor maps are plain
+//     [rows][128 B] byte views;
 //   - each N-chunk accumulates in one of two TMEM buffers (256 columns each, ping-pong), so one
 //     epilogue warpgroup drains chunk c while the tensor core computes chunk c+1;
 //   - a hidden layer's bf16 activations ([128 rows x H] per tile, 256 KB at H = 1024: more than an SM
 //     holds) go to a per-CTA scratch in global memory in the same swizzled K-block layout and are
-//     read back as the next layer's A operand by bulk copies; the scratch (2 x 256 KB per CTA) is
+//     read back as the next layer's A operand by TMA; the scratch (2 x 256 KB per CTA) is
 //     small enough to stay in L2.
 //
-// Warp roles (448 threads = 14 warps): bulk-copy loader 0, producers 1-3 and 13 (producer.cuh),
+// Warp roles (448 threads = 14 warps per CTA): TMA loader 0, producers 1-3 and 13 (producer.cuh),
 // epilogue warpgroups 4-7 (even N-chunks) and 8-11 (odd N-chunks; also predicate + group-by), warp 12 =
-// TMEM allocator + MMA issuer (SMSP 0 holds only the loader, two epilogue warps and the issuer).
+// TMEM allocator + (even CTA) MMA issuer (SMSP 0 holds only the loader, two epilogue warps and the issuer).
 #pragma once
 #include "producer.cuh"
 
@@ -24,17 +25,20 @@ namespace flern {
 constexpr int kThreadsWide = 448;
 constexpr int kNChunk = 256;          // neurons per N-chunk (one TMEM buffer)
 constexpr uint32_t kABlock = 16384;   // [128 rows x 64 K] bf16, 128B-swizzled
-constexpr uint32_t kBBlock = 32768;   // [256 rows x 64 K] bf16, 128B-swizzled
+constexpr uint32_t kBBlock = 32768;   // [256 rows x 64 K] bf16, 128B-swizzled (global image)
+constexpr uint32_t kBHalf = kBBlock / 2;   // one CTA's half of it: N rows [128 r, 128 r + 128)
+constexpr int kDec = 8;               // pair decisions in flight (ring of tile decisions)
 
 template <int K0P, int H, int NL>
 struct WidePlan {
   static constexpr int NCH = H / kNChunk;      // N-chunks per layer
   static constexpr int KB = H / 64;            // K-blocks of a hidden->hidden layer
-  static constexpr int RS = 3;                 // operand ring stages
+  static constexpr int RS = K0P <= 32 ? 5 : 4;   // operand ring stages (5 x 32 KB: ~2.5K tensor cycles of lookahead)
   static constexpr int S = 4;                  // X stages
-  static constexpr uint32_t RING = kABlock + kBBlock;
+  static constexpr uint32_t RING = kABlock + kBHalf;
   static constexpr uint32_t XS = (uint32_t)kTile * K0P * 2;
-  static constexpr uint32_t W1C = (uint32_t)kNChunk * K0P * 2;   // one W1 N-chunk (interleaved)
+  static constexpr uint32_t W1H = (uint32_t)128 * K0P * 2;           // one CTA's half of a W1 N-chunk
+  static constexpr uint32_t W1C = 2 * W1H;                           // one W1 N-chunk (both halves)
   static constexpr uint32_t off_ring = 0;
   static constexpr uint32_t off_x = off_ring + RS * RING;
   static constexpr uint32_t off_meta = off_x + S * XS;
@@ -45,9 +49,10 @@ struct WidePlan {
   static constexpr uint32_t off_queue = off_xchg + 2 * kTile * 4;
   static constexpr uint32_t off_norm = off_queue + queue_bytes(32 * kProdWarpsWide);
   static constexpr uint32_t off_bar = off_norm + kMaxFeat * 8;
-  static constexpr uint32_t off_misc = off_bar + 64 * 8;
+  static constexpr uint32_t off_dec = off_bar + 64 * 8;                // [kDec] decisions + [S] peer status
+  static constexpr uint32_t off_misc = off_dec + 64;
   static constexpr uint32_t total = off_misc + kMiscBytes;
-  // global weight image: [W1: NCH x W1C][W_2..W_NL: (NL-1) x NCH x KB x kBBlock]
+  // global weight image: [W1: NCH x (2 halves x W1H)][W_2..W_NL: (NL-1) x NCH x KB x kBBlock]
   static constexpr size_t img_w1 = (size_t)NCH * W1C;
   static constexpr size_t img_wh = (size_t)(NL - 1) * NCH * KB * kBBlock;
   static constexpr size_t scratch_per_cta = 2ull * KB * kABlock;   // two activation buffers
@@ -55,12 +60,25 @@ struct WidePlan {
   static_assert(H % 512 == 0 && H <= 1024, "wide hidden width (even number of 256-neuron chunks)");
   static_assert(NL >= 2 && NL <= 3, "wide hidden layers");
   static_assert(K0P * 2 <= 128 && K0P % 16 == 0, "layer-1 K");
+  static_assert(W1H % 4096 == 0, "W1 half = whole 32-row (4 KB) TMA boxes");
+  static_assert(img_w1 % 128 == 0, "hidden blocks start on a 128-byte row of the tensor map");
 };
 
 __device__ __forceinline__ void fence_proxy_async_global() {
   asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
+// The fused query kernel for wide MLPs, run by CTA pairs (a cluster of 2 on one TPC). Each CTA keeps
+// its own scan / probe / gather producers, X tiles, activation scratch, epilogue and group-by; the two
+// CTAs' tiles t form one 256-row MMA tile: the even CTA issues every tcgen05.mma with cta_group::2
+// (M = 256), each CTA loads its own 128 activation rows and HALF of each weight block (N rows
+// [128 r, 128 r + 128)) with TMA, so a weight block crosses L2 -> SM once per 256 rows instead of once
+// per 128 (the kernel is bound by L2 -> SM bytes per tensor cycle).
+//
+// Pairing: the CTAs produce different numbers of tiles (their row chunks join at different rates), so
+// the even CTA's loader decides, per tile t, for both: "stop" when both CTAs are out of rows, else each
+// CTA's row count (0 = a dummy tile: an exhausted CTA runs its half of the MMA on stale rows that the
+// group-by ignores). The odd CTA's loader reports its tile status; every role reads the decision.
 template <int K0P, int H, int NL, class SH>
 __global__ void __launch_bounds__(kThreadsWide, 1) flern_query_wide_kernel(const __grid_constant__ QueryParams p) {
   using P = WidePlan<K0P, H, NL>;
@@ -68,19 +86,26 @@ __global__ void __launch_bounds__(kThreadsWide, 1) flern_query_wide_kernel(const
   extern __shared__ __align__(1024) uint8_t smem[];
   const int tid = threadIdx.x;
   const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0), lane = tid & 31;   // warp-uniform (see query_kernel)
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
   FLERN_CTA_STAMP(TR_CTA_START);
   // first two row chunks (guided distribution, see chunk_rows); the atomic's latency hides under the setup
   int64_t claim0 = 0;
   if (tid == 0) claim0 = claim_chunk(p, 2);
 
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + P::off_bar);
-  uint64_t* xfull = bars;             // [S] producers -> consumers (128)
-  uint64_t* xempty = bars + 4;        // [S] warpgroup 1 (4 warps) -> producers
-  uint64_t* rfull = bars + 8;         // [RS] loader expect_tx + bulk-copy bytes
-  uint64_t* rempty = bars + 12;       // [RS] MMA commit
-  uint64_t* dfull = bars + 16;        // [2] MMA commit -> epilogue
-  uint64_t* dempty = bars + 18;       // [2] epilogue (4 warps) -> MMA
-  uint64_t* actrdy = bars + 20;       // [2][NCH] N-chunk n of a hidden layer's activations is in scratch buffer b (4)
+  uint64_t* xfull = bars;             // [S] producers -> this CTA's loader (128)
+  uint64_t* xempty = xfull + S;       // [S] warpgroup 1 (4 warps) -> producers
+  uint64_t* rfull = xempty + S;       // [RS] even CTA: its loader's expect_tx + both CTAs' TMA bytes
+  uint64_t* rempty = rfull + RS;      // [RS] MMA commit (multicast to both CTAs)
+  uint64_t* dfull = rempty + RS;      // [2] MMA commit (multicast) -> epilogue
+  uint64_t* dempty = dfull + 2;       // [2] even CTA: both CTAs' epilogue warps (8) -> MMA
+  uint64_t* actrdy = dempty + 2;      // [2][NCH] N-chunk n of a hidden layer's activations is in scratch buffer b (4)
+  uint64_t* decb = actrdy + 2 * NCH;  // [kDec] the pair decision for tile t is in dec[t % kDec] (1)
+  uint64_t* pstat = decb + kDec;      // [S] even CTA: the odd CTA's status of tile t is in pst[t % S] (1)
+  static_assert(2 * S + 2 * RS + 4 + 2 * NCH + kDec + S <= 64, "barrier block");
+  int32_t* dec = reinterpret_cast<int32_t*>(smem + P::off_dec);        // -1 stop, else this CTA's row count
+  int32_t* pst = dec + kDec;                                           // odd CTA's count (-1: out of rows)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + P::off_misc);
   int32_t* wcnt = reinterpret_cast<int32_t*>(smem + P::off_misc + 16);
   int64_t* s_cnt = reinterpret_cast<int64_t*>(smem + P::off_misc + 112);
@@ -108,20 +133,20 @@ __global__ void __launch_bounds__(kThreadsWide, 1) flern_query_wide_kernel(const
   if (tid == 0) {
     for (int s = 0; s < S; ++s) { mbar_init(&xfull[s], 32 * kProdWarpsWide); mbar_init(&xempty[s], 4); }
     for (int s = 0; s < RS; ++s) { mbar_init(&rfull[s], 1); mbar_init(&rempty[s], 1); }
-    for (int i = 0; i < 2; ++i) { mbar_init(&dfull[i], 1); mbar_init(&dempty[i], 4); }
+    for (int i = 0; i < 2; ++i) { mbar_init(&dfull[i], 1); mbar_init(&dempty[i], 8); }
     for (int i = 0; i < 2 * NCH; ++i) mbar_init(&actrdy[i], 4);
+    for (int i = 0; i < kDec; ++i) mbar_init(&decb[i], 1);
+    for (int s = 0; s < S; ++s) mbar_init(&pstat[s], 1);
     fence_mbar_init();
   }
-  if (warp == 12) { tmem_alloc(tmem_slot, 512); tmem_relinquish(); }
+  if (warp == 12) { tmem_alloc_pair(tmem_slot, 512); tmem_relinquish_pair(); }
   tc_fence_before();
-  __syncthreads();
+  cluster_sync_all();   // barriers of both CTAs initialised, TMEM of both allocated
   tc_fence_after();
   if (*tmem_slot != 0u) __trap();   // one CTA per SM: the 512-column allocation starts at column 0
   constexpr uint32_t tmem_base = 0;
   FLERN_CTA_STAMP(TR_CTA_SETUP);
-  uint8_t* scratch = p.scratch + (size_t)blockIdx.x * P::scratch_per_cta;   // act[0] | act[1]
-  const uint8_t* img_w1 = p.wimg;
-  const uint8_t* img_wh = p.wimg + P::img_w1;
+  const int scratch_row0 = (int)(((size_t)blockIdx.x * P::scratch_per_cta) >> 7);   // act[0] | act[1], 128-B rows
 
   if (warp == 1 || warp == 2 || warp == 3 || warp == 13) {   // producers, off the MMA issuer's SMSP 0
     const int pw = warp == 13 ? 3 : warp - 1;
@@ -129,40 +154,71 @@ __global__ void __launch_bounds__(kThreadsWide, 1) flern_query_wide_kernel(const
                                                      wcnt, s_norm, s_cnt, reinterpret_cast<int32_t*>(smem + P::off_queue),
                                                      s_claim, FactRing{}, pw * 32 + lane, pw, lane);
   } else if (warp == 0) {
-    // =============================== LOADER (bulk copies into the operand ring) ==============
+    // =============================== LOADER (TMA into the operand ring) + pair decisions =======
     if (lane == 0) {
       // weights (re-read by every tile) and the activation scratch (re-read by the next layer) stay in
       // L2 ahead of the streamed fact columns
       const uint64_t keep = l2_policy_evict_last();
+      const uint32_t rfull_cl = mapa_rank(smem_u32(rfull), 0);   // the even CTA's rfull[0]
       uint32_t slot = 0;
-      auto acquire = [&](uint32_t bytes) -> uint32_t {
+      auto acquire = [&](uint32_t pair_bytes) -> uint32_t {
         const uint32_t st = slot % RS;
-        mbar_wait(&rempty[st], ((slot / RS) & 1) ^ 1, 40);
-        mbar_arrive_expect_tx(&rfull[st], bytes);
+        mbar_wait_cl(&rempty[st], ((slot / RS) & 1) ^ 1, 40);
+        if (leader) mbar_arrive_expect_tx(&rfull[st], pair_bytes);
         ++slot;
         return st;
       };
+      bool out = false;   // this CTA's producers have published their last tile
       for (uint32_t t = 0;; ++t) {
         const int s = t % S;
-        mbar_wait(&xfull[s], (t / S) & 1, 41);
-        if (*meta_at(smem + P::off_meta, s).count < 0) break;
+        int32_t cnt = -1;
+        if (!out) {
+          mbar_wait(&xfull[s], (t / S) & 1, 41);
+          cnt = *meta_at(smem + P::off_meta, s).count;
+          out = cnt < 0;
+        }
+        int32_t mine;
+        if (leader) {
+          mbar_wait_cl(&pstat[s], (t / S) & 1, 49);
+          const int32_t peer = *(volatile int32_t*)&pst[s];
+          const bool stop = cnt < 0 && peer < 0;
+          mine = stop ? -1 : max(cnt, 0);
+          const int32_t theirs = stop ? -1 : max(peer, 0);
+          const int d = t % kDec;
+          dec[d] = mine;
+          mbar_arrive(&decb[d]);
+          st_cluster_u32(mapa_rank(smem_u32(&dec[d]), 1), (uint32_t)theirs);
+          mbar_arrive_cluster(mapa_rank(smem_u32(&decb[d]), 1));
+        } else {
+          st_cluster_u32(mapa_rank(smem_u32(&pst[s]), 0), (uint32_t)cnt);
+          mbar_arrive_cluster(mapa_rank(smem_u32(&pstat[s]), 0));
+          const int d = t % kDec;
+          mbar_wait_cl(&decb[d], (t / kDec) & 1, 50);
+          mine = *(volatile int32_t*)&dec[d];
+        }
+        if (mine < 0) break;
         for (int l = 1; l <= NL; ++l) {
-          const uint8_t* act = scratch + (size_t)((l - 2) & 1) * KB * kABlock;
+          const int act_row = scratch_row0 + (int)((((l - 2) & 1) * KB * kABlock) >> 7);
           for (int n = 0; n < NCH; ++n) {
             if (l == 1) {
               const uint32_t st = acquire(P::W1C);
-              bulk_g2s_hint(smem + P::off_ring + st * P::RING + kABlock, img_w1 + (size_t)n * P::W1C, P::W1C, &rfull[st], keep);
+              uint8_t* dst = smem + P::off_ring + st * P::RING + kABlock;
+              const int row = (int)(((size_t)n * P::W1C + rank * P::W1H) >> 7);
+#pragma unroll
+              for (uint32_t b = 0; b < P::W1H / 4096; ++b)
+                tma_load_2d_pair(dst + b * 4096, &p.tm_w1, 0, row + 32 * b, rfull_cl + st * 8, keep);
             } else {
-              const uint8_t* wl = img_wh + (size_t)(l - 2) * NCH * KB * kBBlock + (size_t)n * KB * kBBlock;
+              const size_t wl = P::img_w1 + (size_t)(l - 2) * NCH * KB * kBBlock + (size_t)n * KB * kBBlock;
               for (int kb = 0; kb < KB; ++kb) {
                 // K-block kb of layer l's input is N-chunk kb / 4 of layer l-1: wait for that chunk only
                 // (per-chunk hand-off: layer l starts while layer l-1's last chunks are still drained)
                 if (n == 0 && kb % (kNChunk / 64) == 0)
                   mbar_wait(&actrdy[((l - 2) & 1) * NCH + kb / (kNChunk / 64)], t & 1, 42);
-                const uint32_t st = acquire(kABlock + kBBlock);
+                const uint32_t st = acquire(2 * (kABlock + kBHalf));
                 uint8_t* dst = smem + P::off_ring + st * P::RING;
-                bulk_g2s_hint(dst, act + (size_t)kb * kABlock, kABlock, &rfull[st], keep);
-                bulk_g2s_hint(dst + kABlock, wl + (size_t)kb * kBBlock, kBBlock, &rfull[st], keep);
+                tma_load_2d_pair(dst, &p.tm_act, 0, act_row + kb * (int)(kABlock >> 7), rfull_cl + st * 8, keep);
+                tma_load_2d_pair(dst + kABlock, &p.tm_wh, 0, (int)((wl + (size_t)kb * kBBlock + rank * kBHalf) >> 7),
+                                 rfull_cl + st * 8, keep);
               }
             }
           }
@@ -171,21 +227,21 @@ __global__ void __launch_bounds__(kThreadsWide, 1) flern_query_wide_kernel(const
     }
     __syncwarp();
   } else if (warp == 12) {
-    // =============================== MMA ISSUER =============================================
+    // =============================== MMA ISSUER (even CTA) ====================================
     // warp-uniform loop, elect.sync per tcgen05 instruction, waits without a suspend hint
-    {
-      constexpr uint32_t idesc = make_idesc_bf16(128, kNChunk);
+    if (leader) {
+      constexpr uint32_t idesc = make_idesc_bf16(256, kNChunk);
       const uint32_t x0 = smem_u32(smem + P::off_x);
       const uint32_t ring = smem_u32(smem + P::off_ring);
       uint32_t slot = 0, c = 0;
       for (uint32_t t = 0;; ++t) {
         const int s = t % S;
-        mbar_wait_nohint(&xfull[s], (t / S) & 1, 43);
-        if (*meta_at(smem + P::off_meta, s).count < 0) break;
+        mbar_wait_nohint(&decb[t % kDec], (t / kDec) & 1, 43);
+        if (*(volatile int32_t*)&dec[t % kDec] < 0) break;
         for (int l = 1; l <= NL; ++l) {
           for (int n = 0; n < NCH; ++n, ++c) {
             const uint32_t b = c & 1;
-            mbar_wait_nohint(&dempty[b], ((c >> 1) & 1) ^ 1, 44);
+            mbar_wait_cl_nohint(&dempty[b], ((c >> 1) & 1) ^ 1, 44);
             tc_fence_after();
             const uint32_t dcol = tmem_base + b * kNChunk;
             if (l == 1) {
@@ -196,10 +252,10 @@ __global__ void __launch_bounds__(kThreadsWide, 1) flern_query_wide_kernel(const
 #pragma unroll
               for (int ks = 0; ks < K0P / 16; ++ks) {
                 const uint64_t ad = make_sdesc(x0 + s * P::XS + ks * 2 * (kTile * 16), kTile * 16, 128, kLayoutNone);
-                const uint64_t bd = make_sdesc(bb + ks * 2 * (kNChunk * 16), kNChunk * 16, 128, kLayoutNone);
-                if (elect_one_sync()) mma_bf16_ss(dcol, ad, bd, idesc, ks > 0);
+                const uint64_t bd = make_sdesc(bb + ks * 2 * (128 * 16), 128 * 16, 128, kLayoutNone);
+                if (elect_one_sync()) mma_bf16_ss_pair(dcol, ad, bd, idesc, ks > 0);
               }
-              if (elect_one_sync()) mma_commit(&rempty[st]);
+              if (elect_one_sync()) mma_commit_pair(&rempty[st], 3);
               ++slot;
             } else {
               for (int kb = 0; kb < KB; ++kb) {
@@ -211,13 +267,13 @@ __global__ void __launch_bounds__(kThreadsWide, 1) flern_query_wide_kernel(const
                 for (int j = 0; j < 4; ++j) {
                   const uint64_t ad = make_sdesc(ab + j * 32, 16, 1024, kLayoutSW128);
                   const uint64_t bd = make_sdesc(bb + j * 32, 16, 1024, kLayoutSW128);
-                  if (elect_one_sync()) mma_bf16_ss(dcol, ad, bd, idesc, (kb | j) != 0);
+                  if (elect_one_sync()) mma_bf16_ss_pair(dcol, ad, bd, idesc, (kb | j) != 0);
                 }
-                if (elect_one_sync()) mma_commit(&rempty[st]);
+                if (elect_one_sync()) mma_commit_pair(&rempty[st], 3);
                 ++slot;
               }
             }
-            if (elect_one_sync()) mma_commit(&dfull[b]);
+            if (elect_one_sync()) mma_commit_pair(&dfull[b], 3);
           }
         }
       }
@@ -231,21 +287,23 @@ __global__ void __launch_bounds__(kThreadsWide, 1) flern_query_wide_kernel(const
     const int q = warp & 3;
     const int r = q * 32 + lane;
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+    const uint32_t dempty_cl = mapa_rank(smem_u32(dempty), 0) + wg * 8;   // the even CTA's dempty[wg]
     GroupAgg<(SH::NF < 0)> agg;
     agg.init();
     const uint64_t keep = l2_policy_evict_last();   // activation scratch: keep in L2 for the next layer
+    uint8_t* scratch = p.scratch + (size_t)blockIdx.x * P::scratch_per_cta;   // act[0] | act[1]
     for (uint32_t t = 0;; ++t) {
       const int s = t % S;
-      mbar_wait(&xfull[s], (t / S) & 1, 47);
-      const Meta m = meta_at(smem + P::off_meta, s);
-      const int count = *m.count;
+      mbar_wait_cl(&decb[t % kDec], (t / kDec) & 1, 47);
+      const int count = *(volatile int32_t*)&dec[t % kDec];
       if (count < 0) break;
+      const Meta m = meta_at(smem + P::off_meta, s);
       float2 pa = make_float2(0.f, 0.f), pb = make_float2(0.f, 0.f);
       for (int l = 1; l <= NL; ++l) {
         uint8_t* act = scratch + (size_t)((l - 1) & 1) * KB * kABlock;   // layer l's output buffer
         for (int n = wg; n < NCH; n += 2) {
           const uint32_t c = (t * NL + (l - 1)) * NCH + n;
-          mbar_wait(&dfull[wg], (c >> 1) & 1, 48);
+          mbar_wait_cl(&dfull[wg], (c >> 1) & 1, 48);
           tc_fence_after();
           const float* bias = s_bias + (l - 1) * H + n * kNChunk;
           uint32_t v[2][32];
@@ -296,7 +354,7 @@ __global__ void __launch_bounds__(kThreadsWide, 1) flern_query_wide_kernel(const
           }
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive(&dempty[wg]);
+          if (lane == 0) mbar_arrive_cluster(dempty_cl);
           if (l < NL) {   // this chunk of layer l's activations is in the scratch
             fence_proxy_async_global();
             __syncwarp();
@@ -321,8 +379,9 @@ __global__ void __launch_bounds__(kThreadsWide, 1) flern_query_wide_kernel(const
 
   tc_fence_before();
   __syncthreads();
+  cluster_sync_all();   // no arrival or TMA write of the peer is still aimed at this CTA
   FLERN_CTA_STAMP(TR_CTA_LOOP_END);
-  if (warp == 12) { tc_fence_after(); tmem_dealloc(tmem_base, 512); }
+  if (warp == 12) { tc_fence_after(); tmem_dealloc_pair(tmem_base, 512); }
   write_partials_and_reduce(p, acc, s_cnt, s_is_last, tid, kThreadsWide);
 }
 
