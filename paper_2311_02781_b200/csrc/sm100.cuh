@@ -386,11 +386,15 @@ __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cl_addr) {
 __device__ __forceinline__ void st_cluster_u32(uint32_t cl_addr, uint32_t v) {
   asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(cl_addr), "r"(v) : "memory");
 }
-// waits whose phase is completed by an arrival from the peer CTA (cluster-scope acquire)
+// Waits whose phase is completed by an arrival from the peer CTA. The wait keeps the default CTA-scope
+// acquire: the data the peer publishes is in this CTA's shared memory (st.shared::cluster before its
+// release.cluster arrive), TMEM or the async proxy, none of it cached in L1. An .acquire.cluster wait
+// compiles to an L1 invalidation (CCTL.IVALL) after every completed wait (ncu r02c: 43% of the wide
+// kernel's stall samples).
 __device__ __forceinline__ bool mbar_try_wait_cl(uint64_t* bar, uint32_t parity) {
   uint32_t ok;
   asm volatile(
-      "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+      "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
       "selp.u32 %0, 1, 0, p;\n\t}"
       : "=r"(ok)
       : "r"(smem_u32(bar)), "r"(parity)

@@ -64,6 +64,63 @@ struct WidePlan {
   static_assert(img_w1 % 128 == 0, "hidden blocks start on a 128-byte row of the tensor map");
 };
 
+// Wait accounting of the first pair's roles (diagnostic builds, scripts/trace_wide.py): cycles spent in
+// each wait, summed into dbg_trace[TR_WAITS][32 + 16 * cta + slot]. Release builds: the bare wait.
+#ifdef FLERN_DIAG
+#define WIDE_WAIT(slot, on, stmt)                                                                          \
+  do {                                                                                                   \
+    const bool on_ = p.dbg_trace && blockIdx.x < 2 && (on);                                              \
+    long long t0_ = 0;                                                                                   \
+    if (on_) t0_ = clock64();                                                                            \
+    stmt;                                                                                                \
+    if (on_)                                                                                             \
+      atomicAdd(&p.dbg_trace[TR_WAITS * kTraceTiles + 32 + 16 * blockIdx.x + (slot)],                    \
+                (unsigned long long)(clock64() - t0_));                                                  \
+  } while (0)
+// the same for the warp-uniform MMA loop: reconverge before the next elect.sync
+#define WIDE_WAIT_W(slot, stmt)      \
+  do {                               \
+    WIDE_WAIT(slot, lane == 0, stmt); \
+    __syncwarp();                    \
+  } while (0)
+#define WIDE_STAMP(slot, on)                                                                             \
+  do {                                                                                                   \
+    if (p.dbg_trace && blockIdx.x < 2 && (on))                                                           \
+      p.dbg_trace[TR_WAITS * kTraceTiles + 32 + 16 * blockIdx.x + (slot)] = (unsigned long long)clock64(); \
+  } while (0)
+// per-stage timeline of CTA 0 for hidden-layer stages [kSeqStage0, +800): the MMA thread's 3 stamps per
+// stage (before the rfull wait, after it, after the stage's last MMA) in trace rows 0..9, the loader's 2
+// (rempty wait returned, stage armed) in rows 10..19
+constexpr uint32_t kSeqStage0 = 4000, kSeqN = 800;
+#define WIDE_SEQ(stage, kind)                                                                            \
+  do {                                                                                                   \
+    if (p.dbg_trace && blockIdx.x == 0 && lane == 0 && (stage) >= kSeqStage0 && (stage) < kSeqStage0 + kSeqN) \
+      p.dbg_trace[3 * ((stage) - kSeqStage0) + (kind)] = (unsigned long long)clock64();                 \
+  } while (0)
+#define WIDE_LSEQ(stage, kind)                                                                           \
+  do {                                                                                                   \
+    if (p.dbg_trace && blockIdx.x == 0 && (stage) >= kSeqStage0 && (stage) < kSeqStage0 + kSeqN)        \
+      p.dbg_trace[10 * kTraceTiles + 2 * ((stage) - kSeqStage0) + (kind)] = (unsigned long long)clock64(); \
+  } while (0)
+#else
+#define WIDE_SEQ(stage, kind)
+#define WIDE_LSEQ(stage, kind)
+#define WIDE_WAIT(slot, on, stmt) stmt
+#define WIDE_WAIT_W(slot, stmt) stmt
+#define WIDE_STAMP(slot, on)
+#endif
+// Diagnostic A/B bits (FLERN_DBG_MODE, diagnostic builds): 1 = the epilogue only hands buffers back (no
+// TMEM loads, math or stores), 2 = no operand loads (the even CTA's loader completes each stage without
+// bytes; the MMAs read stale shared memory).
+#ifdef FLERN_DIAG
+#define WIDE_DBG(bit) ((p.dbg_mode & (bit)) != 0)
+#else
+#define WIDE_DBG(bit) false
+#endif
+// slots: MMA decb 0, dempty 1, rfull(L1) 2, rfull(hidden) 3; loader xfull 4, pair exchange 5, rempty 6,
+// actrdy 7; epilogue WG0 decb 8, dfull 9; WG1 dfull 10, x-exchange 11; stamps: loop start 12, end 13 (MMA /
+// loader), tiles 14
+
 __device__ __forceinline__ void fence_proxy_async_global() {
   asm volatile("fence.proxy.async.global;" ::: "memory");
 }
@@ -161,10 +218,20 @@ __global__ void __launch_bounds__(kThreadsWide, 1) flern_query_wide_kernel(const
       const uint64_t keep = l2_policy_evict_last();
       const uint32_t rfull_cl = mapa_rank(smem_u32(rfull), 0);   // the even CTA's rfull[0]
       uint32_t slot = 0;
+      const bool noload = WIDE_DBG(2);
       auto acquire = [&](uint32_t pair_bytes) -> uint32_t {
         const uint32_t st = slot % RS;
-        mbar_wait_cl(&rempty[st], ((slot / RS) & 1) ^ 1, 40);
-        if (leader) mbar_arrive_expect_tx(&rfull[st], pair_bytes);
+        // polls without a sleep: one stage is re-armed per wake-up, and a __nanosleep back-off wakes
+        // ~1K cycles late, which paced the whole MMA chain at ~940 cycles per 512-cycle stage (r02c)
+        WIDE_WAIT(6, true, mbar_wait_cl_nohint(&rempty[st], ((slot / RS) & 1) ^ 1, 40));
+        WIDE_LSEQ(slot, 0);
+        if (noload) {   // diagnostic: 16 pretend bytes from the odd CTA keep the two loaders in step
+          if (leader) mbar_arrive_expect_tx(&rfull[st], 16);
+          else asm volatile("mbarrier.complete_tx.relaxed.cluster.shared::cluster.b64 [%0], 16;" ::"r"(rfull_cl + st * 8) : "memory");
+        } else if (leader) {
+          mbar_arrive_expect_tx(&rfull[st], pair_bytes);
+        }
+        WIDE_LSEQ(slot, 1);
         ++slot;
         return st;
       };
@@ -173,13 +240,13 @@ __global__ void __launch_bounds__(kThreadsWide, 1) flern_query_wide_kernel(const
         const int s = t % S;
         int32_t cnt = -1;
         if (!out) {
-          mbar_wait(&xfull[s], (t / S) & 1, 41);
+          WIDE_WAIT(4, true, mbar_wait(&xfull[s], (t / S) & 1, 41));
           cnt = *meta_at(smem + P::off_meta, s).count;
           out = cnt < 0;
         }
         int32_t mine;
         if (leader) {
-          mbar_wait_cl(&pstat[s], (t / S) & 1, 49);
+          WIDE_WAIT(5, true, mbar_wait_cl(&pstat[s], (t / S) & 1, 49));
           const int32_t peer = *(volatile int32_t*)&pst[s];
           const bool stop = cnt < 0 && peer < 0;
           mine = stop ? -1 : max(cnt, 0);
@@ -193,7 +260,7 @@ __global__ void __launch_bounds__(kThreadsWide, 1) flern_query_wide_kernel(const
           st_cluster_u32(mapa_rank(smem_u32(&pst[s]), 0), (uint32_t)cnt);
           mbar_arrive_cluster(mapa_rank(smem_u32(&pstat[s]), 0));
           const int d = t % kDec;
-          mbar_wait_cl(&decb[d], (t / kDec) & 1, 50);
+          WIDE_WAIT(5, true, mbar_wait_cl(&decb[d], (t / kDec) & 1, 50));
           mine = *(volatile int32_t*)&dec[d];
         }
         if (mine < 0) break;
@@ -206,16 +273,17 @@ __global__ void __launch_bounds__(kThreadsWide, 1) flern_query_wide_kernel(const
               const int row = (int)(((size_t)n * P::W1C + rank * P::W1H) >> 7);
 #pragma unroll
               for (uint32_t b = 0; b < P::W1H / 4096; ++b)
-                tma_load_2d_pair(dst + b * 4096, &p.tm_w1, 0, row + 32 * b, rfull_cl + st * 8, keep);
+                if (!noload) tma_load_2d_pair(dst + b * 4096, &p.tm_w1, 0, row + 32 * b, rfull_cl + st * 8, keep);
             } else {
               const size_t wl = P::img_w1 + (size_t)(l - 2) * NCH * KB * kBBlock + (size_t)n * KB * kBBlock;
               for (int kb = 0; kb < KB; ++kb) {
                 // K-block kb of layer l's input is N-chunk kb / 4 of layer l-1: wait for that chunk only
                 // (per-chunk hand-off: layer l starts while layer l-1's last chunks are still drained)
                 if (n == 0 && kb % (kNChunk / 64) == 0)
-                  mbar_wait(&actrdy[((l - 2) & 1) * NCH + kb / (kNChunk / 64)], t & 1, 42);
+                  WIDE_WAIT(7, true, mbar_wait(&actrdy[((l - 2) & 1) * NCH + kb / (kNChunk / 64)], t & 1, 42));
                 const uint32_t st = acquire(2 * (kABlock + kBHalf));
                 uint8_t* dst = smem + P::off_ring + st * P::RING;
+                if (noload) continue;
                 tma_load_2d_pair(dst, &p.tm_act, 0, act_row + kb * (int)(kABlock >> 7), rfull_cl + st * 8, keep);
                 tma_load_2d_pair(dst + kABlock, &p.tm_wh, 0, (int)((wl + (size_t)kb * kBBlock + rank * kBHalf) >> 7),
                                  rfull_cl + st * 8, keep);
@@ -234,19 +302,28 @@ __global__ void __launch_bounds__(kThreadsWide, 1) flern_query_wide_kernel(const
       const uint32_t x0 = smem_u32(smem + P::off_x);
       const uint32_t ring = smem_u32(smem + P::off_ring);
       uint32_t slot = 0, c = 0;
+      WIDE_STAMP(12, lane == 0);
+      __syncwarp();
       for (uint32_t t = 0;; ++t) {
         const int s = t % S;
-        mbar_wait_nohint(&decb[t % kDec], (t / kDec) & 1, 43);
-        if (*(volatile int32_t*)&dec[t % kDec] < 0) break;
+        WIDE_WAIT_W(0, mbar_wait_nohint(&decb[t % kDec], (t / kDec) & 1, 43));
+        if (*(volatile int32_t*)&dec[t % kDec] < 0) {
+          WIDE_STAMP(13, lane == 0);
+#ifdef FLERN_DIAG
+          if (p.dbg_trace && blockIdx.x < 2 && lane == 0) p.dbg_trace[TR_WAITS * kTraceTiles + 32 + 16 * blockIdx.x + 14] = t;
+          __syncwarp();
+#endif
+          break;
+        }
         for (int l = 1; l <= NL; ++l) {
           for (int n = 0; n < NCH; ++n, ++c) {
             const uint32_t b = c & 1;
-            mbar_wait_cl_nohint(&dempty[b], ((c >> 1) & 1) ^ 1, 44);
+            WIDE_WAIT_W(1, mbar_wait_cl_nohint(&dempty[b], ((c >> 1) & 1) ^ 1, 44));
             tc_fence_after();
             const uint32_t dcol = tmem_base + b * kNChunk;
             if (l == 1) {
               const uint32_t st = slot % RS;
-              mbar_wait_nohint(&rfull[st], (slot / RS) & 1, 45);
+              WIDE_WAIT_W(2, mbar_wait_nohint(&rfull[st], (slot / RS) & 1, 45));
               tc_fence_after();
               const uint32_t bb = ring + st * P::RING + kABlock;
 #pragma unroll
@@ -260,7 +337,9 @@ __global__ void __launch_bounds__(kThreadsWide, 1) flern_query_wide_kernel(const
             } else {
               for (int kb = 0; kb < KB; ++kb) {
                 const uint32_t st = slot % RS;
-                mbar_wait_nohint(&rfull[st], (slot / RS) & 1, 46);
+                WIDE_SEQ(slot, 0);
+                WIDE_WAIT_W(3, mbar_wait_nohint(&rfull[st], (slot / RS) & 1, 46));
+                WIDE_SEQ(slot, 1);
                 tc_fence_after();
                 const uint32_t ab = ring + st * P::RING, bb = ab + kABlock;
 #pragma unroll
@@ -269,6 +348,7 @@ __global__ void __launch_bounds__(kThreadsWide, 1) flern_query_wide_kernel(const
                   const uint64_t bd = make_sdesc(bb + j * 32, 16, 1024, kLayoutSW128);
                   if (elect_one_sync()) mma_bf16_ss_pair(dcol, ad, bd, idesc, (kb | j) != 0);
                 }
+                WIDE_SEQ(slot, 2);
                 if (elect_one_sync()) mma_commit_pair(&rempty[st], 3);
                 ++slot;
               }
@@ -294,7 +374,7 @@ __global__ void __launch_bounds__(kThreadsWide, 1) flern_query_wide_kernel(const
     uint8_t* scratch = p.scratch + (size_t)blockIdx.x * P::scratch_per_cta;   // act[0] | act[1]
     for (uint32_t t = 0;; ++t) {
       const int s = t % S;
-      mbar_wait_cl(&decb[t % kDec], (t / kDec) & 1, 47);
+      WIDE_WAIT(8, tid == 128, mbar_wait_cl(&decb[t % kDec], (t / kDec) & 1, 47));
       const int count = *(volatile int32_t*)&dec[t % kDec];
       if (count < 0) break;
       const Meta m = meta_at(smem + P::off_meta, s);
@@ -303,10 +383,17 @@ __global__ void __launch_bounds__(kThreadsWide, 1) flern_query_wide_kernel(const
         uint8_t* act = scratch + (size_t)((l - 1) & 1) * KB * kABlock;   // layer l's output buffer
         for (int n = wg; n < NCH; n += 2) {
           const uint32_t c = (t * NL + (l - 1)) * NCH + n;
-          mbar_wait_cl(&dfull[wg], (c >> 1) & 1, 48);
+          WIDE_WAIT(9 + wg, tid == 128 || tid == 256, mbar_wait_cl_nohint(&dfull[wg], (c >> 1) & 1, 48));
           tc_fence_after();
           const float* bias = s_bias + (l - 1) * H + n * kNChunk;
           uint32_t v[2][32];
+          if (WIDE_DBG(1)) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(dempty_cl);
+            if (l < NL && lane == 0) mbar_arrive(&actrdy[((l - 1) & 1) * NCH + n]);
+            continue;
+          }
           tmem_ld32_async(tmem_base + lane_off + wg * kNChunk, v[0]);
           tmem_ld_wait(v[0]);
 #pragma unroll
@@ -369,7 +456,7 @@ __global__ void __launch_bounds__(kThreadsWide, 1) flern_query_wide_kernel(const
         xb[r] = part;
         named_bar_arrive(2, 256);
       } else {
-        named_bar_sync(2, 256);
+        WIDE_WAIT(11, tid == 256, named_bar_sync(2, 256));
         const float logit = part + xb[r] + p.bout;
         agg.tile(p, m, count, r, lane, logit, s_cnt, &xempty[s]);
       }
