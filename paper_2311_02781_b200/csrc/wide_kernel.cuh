@@ -33,9 +33,14 @@ template <int K0P, int H, int NL>
 struct WidePlan {
   static constexpr int NCH = H / kNChunk;      // N-chunks per layer
   static constexpr int KB = H / 64;            // K-blocks of a hidden->hidden layer
-  static constexpr int RS = K0P <= 32 ? 5 : 4;   // operand ring stages (5 x 32 KB: ~2.5K tensor cycles of lookahead)
-  static constexpr int S = 4;                  // X stages
-  static constexpr uint32_t RING = kABlock + kBHalf;
+  // Operand ring: stages of KPS K-blocks ([A_0 | B_0 | A_1 | B_1], 64 KB per CTA), one full / empty hand-off
+  // per stage. Each hand-off of a cta_group::2 MMA chain costs ~150 cycles that the ~2-deep tensor queue
+  // does not hide (scripts/mma_pair_bench.cu: 662 cycles per 4 MMAs with a hand-off every 4, 562 every 8,
+  // 512 without), so a stage carries 8 MMAs.
+  static constexpr int KPS = 2;
+  static constexpr int RS = 2;                   // operand ring stages
+  static constexpr int S = 2;                    // X stages (a tile's MLP takes ~10x its gather)
+  static constexpr uint32_t RING = KPS * (kABlock + kBHalf);
   static constexpr uint32_t XS = (uint32_t)kTile * K0P * 2;
   static constexpr uint32_t W1H = (uint32_t)128 * K0P * 2;           // one CTA's half of a W1 N-chunk
   static constexpr uint32_t W1C = 2 * W1H;                           // one W1 N-chunk (both halves)
@@ -47,7 +52,8 @@ struct WidePlan {
   static constexpr uint32_t off_acc = off_wout + H * 4;
   static constexpr uint32_t off_xchg = off_acc + kMaxGroups * 4 * 8;
   static constexpr uint32_t off_queue = off_xchg + 2 * kTile * 4;
-  static constexpr uint32_t off_norm = off_queue + queue_bytes(32 * kProdWarpsWide);
+  static constexpr uint32_t off_stage = off_queue + queue_bytes(32 * kProdWarpsWide);   // [8 warps][32 rows][64 B]
+  static constexpr uint32_t off_norm = off_stage + 8 * 2048;
   static constexpr uint32_t off_bar = off_norm + kMaxFeat * 8;
   static constexpr uint32_t off_dec = off_bar + 64 * 8;                // [kDec] decisions + [S] peer status
   static constexpr uint32_t off_misc = off_dec + 64;
@@ -60,6 +66,7 @@ struct WidePlan {
   static_assert(H % 512 == 0 && H <= 1024, "wide hidden width (even number of 256-neuron chunks)");
   static_assert(NL >= 2 && NL <= 3, "wide hidden layers");
   static_assert(K0P * 2 <= 128 && K0P % 16 == 0, "layer-1 K");
+  static_assert(KB % KPS == 0 && (kNChunk / 64) % KPS == 0, "a stage's K-blocks come from one N-chunk");
   static_assert(W1H % 4096 == 0, "W1 half = whole 32-row (4 KB) TMA boxes");
   static_assert(img_w1 % 128 == 0, "hidden blocks start on a 128-byte row of the tensor map");
 };
@@ -156,8 +163,8 @@ __global__ void __launch_bounds__(kThreadsWide, 1) flern_query_wide_kernel(const
   uint64_t* rfull = xempty + S;       // [RS] even CTA: its loader's expect_tx + both CTAs' TMA bytes
   uint64_t* rempty = rfull + RS;      // [RS] MMA commit (multicast to both CTAs)
   uint64_t* dfull = rempty + RS;      // [2] MMA commit (multicast) -> epilogue
-  uint64_t* dempty = dfull + 2;       // [2] even CTA: both CTAs' epilogue warps (8) -> MMA
-  uint64_t* actrdy = dempty + 2;      // [2][NCH] N-chunk n of a hidden layer's activations is in scratch buffer b (4)
+  uint64_t* dempty = dfull + 2;       // [2] even CTA: both CTAs' epilogue warps (16) -> MMA
+  uint64_t* actrdy = dempty + 2;      // [2][NCH] N-chunk n of a hidden layer's activations is in scratch buffer b (8)
   uint64_t* decb = actrdy + 2 * NCH;  // [kDec] the pair decision for tile t is in dec[t % kDec] (1)
   uint64_t* pstat = decb + kDec;      // [S] even CTA: the odd CTA's status of tile t is in pst[t % S] (1)
   static_assert(2 * S + 2 * RS + 4 + 2 * NCH + kDec + S <= 64, "barrier block");
@@ -190,8 +197,8 @@ __global__ void __launch_bounds__(kThreadsWide, 1) flern_query_wide_kernel(const
   if (tid == 0) {
     for (int s = 0; s < S; ++s) { mbar_init(&xfull[s], 32 * kProdWarpsWide); mbar_init(&xempty[s], 4); }
     for (int s = 0; s < RS; ++s) { mbar_init(&rfull[s], 1); mbar_init(&rempty[s], 1); }
-    for (int i = 0; i < 2; ++i) { mbar_init(&dfull[i], 1); mbar_init(&dempty[i], 8); }
-    for (int i = 0; i < 2 * NCH; ++i) mbar_init(&actrdy[i], 4);
+    for (int i = 0; i < 2; ++i) { mbar_init(&dfull[i], 1); mbar_init(&dempty[i], 16); }
+    for (int i = 0; i < 2 * NCH; ++i) mbar_init(&actrdy[i], 8);
     for (int i = 0; i < kDec; ++i) mbar_init(&decb[i], 1);
     for (int s = 0; s < S; ++s) mbar_init(&pstat[s], 1);
     fence_mbar_init();
@@ -276,17 +283,22 @@ __global__ void __launch_bounds__(kThreadsWide, 1) flern_query_wide_kernel(const
                 if (!noload) tma_load_2d_pair(dst + b * 4096, &p.tm_w1, 0, row + 32 * b, rfull_cl + st * 8, keep);
             } else {
               const size_t wl = P::img_w1 + (size_t)(l - 2) * NCH * KB * kBBlock + (size_t)n * KB * kBBlock;
-              for (int kb = 0; kb < KB; ++kb) {
+              for (int kb0 = 0; kb0 < KB; kb0 += P::KPS) {
                 // K-block kb of layer l's input is N-chunk kb / 4 of layer l-1: wait for that chunk only
                 // (per-chunk hand-off: layer l starts while layer l-1's last chunks are still drained)
-                if (n == 0 && kb % (kNChunk / 64) == 0)
-                  WIDE_WAIT(7, true, mbar_wait(&actrdy[((l - 2) & 1) * NCH + kb / (kNChunk / 64)], t & 1, 42));
-                const uint32_t st = acquire(2 * (kABlock + kBHalf));
+                if (n == 0 && kb0 % (kNChunk / 64) == 0)
+                  WIDE_WAIT(7, true, mbar_wait(&actrdy[((l - 2) & 1) * NCH + kb0 / (kNChunk / 64)], t & 1, 42));
+                const uint32_t st = acquire(2 * P::RING);
                 uint8_t* dst = smem + P::off_ring + st * P::RING;
                 if (noload) continue;
-                tma_load_2d_pair(dst, &p.tm_act, 0, act_row + kb * (int)(kABlock >> 7), rfull_cl + st * 8, keep);
-                tma_load_2d_pair(dst + kABlock, &p.tm_wh, 0, (int)((wl + (size_t)kb * kBBlock + rank * kBHalf) >> 7),
-                                 rfull_cl + st * 8, keep);
+#pragma unroll
+                for (int q = 0; q < P::KPS; ++q) {
+                  const int kb = kb0 + q;
+                  uint8_t* d = dst + q * (kABlock + kBHalf);
+                  tma_load_2d_pair(d, &p.tm_act, 0, act_row + kb * (int)(kABlock >> 7), rfull_cl + st * 8, keep);
+                  tma_load_2d_pair(d + kABlock, &p.tm_wh, 0, (int)((wl + (size_t)kb * kBBlock + rank * kBHalf) >> 7),
+                                   rfull_cl + st * 8, keep);
+                }
               }
             }
           }
@@ -335,18 +347,21 @@ __global__ void __launch_bounds__(kThreadsWide, 1) flern_query_wide_kernel(const
               if (elect_one_sync()) mma_commit_pair(&rempty[st], 3);
               ++slot;
             } else {
-              for (int kb = 0; kb < KB; ++kb) {
+              for (int kb0 = 0; kb0 < KB; kb0 += P::KPS) {
                 const uint32_t st = slot % RS;
                 WIDE_SEQ(slot, 0);
                 WIDE_WAIT_W(3, mbar_wait_nohint(&rfull[st], (slot / RS) & 1, 46));
                 WIDE_SEQ(slot, 1);
                 tc_fence_after();
-                const uint32_t ab = ring + st * P::RING, bb = ab + kABlock;
 #pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                  const uint64_t ad = make_sdesc(ab + j * 32, 16, 1024, kLayoutSW128);
-                  const uint64_t bd = make_sdesc(bb + j * 32, 16, 1024, kLayoutSW128);
-                  if (elect_one_sync()) mma_bf16_ss_pair(dcol, ad, bd, idesc, (kb | j) != 0);
+                for (int q = 0; q < P::KPS; ++q) {
+                  const uint32_t ab = ring + st * P::RING + q * (kABlock + kBHalf), bb = ab + kABlock;
+#pragma unroll
+                  for (int j = 0; j < 4; ++j) {
+                    const uint64_t ad = make_sdesc(ab + j * 32, 16, 1024, kLayoutSW128);
+                    const uint64_t bd = make_sdesc(bb + j * 32, 16, 1024, kLayoutSW128);
+                    if (elect_one_sync()) mma_bf16_ss_pair(dcol, ad, bd, idesc, (kb0 | q | j) != 0);
+                  }
                 }
                 WIDE_SEQ(slot, 2);
                 if (elect_one_sync()) mma_commit_pair(&rempty[st], 3);
@@ -361,13 +376,15 @@ __global__ void __launch_bounds__(kThreadsWide, 1) flern_query_wide_kernel(const
     __syncwarp();
   } else {
     // =============================== EPILOGUE (warps 4-11) ===================================
-    // warpgroup w drains the N-chunks with n % 2 == w (TMEM buffer w); per tile there are NL*NCH
-    // chunks, an even number, so the chunk parity never changes across tiles.
+    // both warpgroups drain every N-chunk (TMEM buffer c % 2), warpgroup w its columns [128 w, 128 w + 128):
+    // a chunk's drain takes half as long as with one warpgroup per chunk, which is what the ping-pong and
+    // layer 1 (four chunks of 256 tensor cycles each, drained back to back) wait on. Per tile there are
+    // NL*NCH chunks, an even number, so the buffer parity never changes across tiles.
     const int wg = (warp - 4) >> 2;
     const int q = warp & 3;
     const int r = q * 32 + lane;
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
-    const uint32_t dempty_cl = mapa_rank(smem_u32(dempty), 0) + wg * 8;   // the even CTA's dempty[wg]
+    const uint32_t dempty_cl = mapa_rank(smem_u32(dempty), 0);   // the even CTA's dempty[0]
     GroupAgg<(SH::NF < 0)> agg;
     agg.init();
     const uint64_t keep = l2_policy_evict_last();   // activation scratch: keep in L2 for the next layer
@@ -381,25 +398,27 @@ __global__ void __launch_bounds__(kThreadsWide, 1) flern_query_wide_kernel(const
       float2 pa = make_float2(0.f, 0.f), pb = make_float2(0.f, 0.f);
       for (int l = 1; l <= NL; ++l) {
         uint8_t* act = scratch + (size_t)((l - 1) & 1) * KB * kABlock;   // layer l's output buffer
-        for (int n = wg; n < NCH; n += 2) {
-          const uint32_t c = (t * NL + (l - 1)) * NCH + n;
-          WIDE_WAIT(9 + wg, tid == 128 || tid == 256, mbar_wait_cl_nohint(&dfull[wg], (c >> 1) & 1, 48));
+        for (int n = 0; n < NCH; ++n) {
+          const uint32_t c = (t * NL + (l - 1)) * NCH + n, b = c & 1;
+          WIDE_WAIT(9 + wg, tid == 128 || tid == 256, mbar_wait_cl_nohint(&dfull[b], (c >> 1) & 1, 48));
           tc_fence_after();
-          const float* bias = s_bias + (l - 1) * H + n * kNChunk;
+          const int col0 = n * kNChunk + wg * 128;   // this warpgroup's first column of the chunk
+          const float* bias = s_bias + (l - 1) * H + col0;
+          const uint32_t tcol = tmem_base + lane_off + b * kNChunk + wg * 128;
           uint32_t v[2][32];
           if (WIDE_DBG(1)) {
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive_cluster(dempty_cl);
+            if (lane == 0) mbar_arrive_cluster(dempty_cl + b * 8);
             if (l < NL && lane == 0) mbar_arrive(&actrdy[((l - 1) & 1) * NCH + n]);
             continue;
           }
-          tmem_ld32_async(tmem_base + lane_off + wg * kNChunk, v[0]);
+          tmem_ld32_async(tcol, v[0]);
           tmem_ld_wait(v[0]);
 #pragma unroll
-          for (int cc = 0; cc < 8; ++cc) {   // 8 x 32 columns
+          for (int cc = 0; cc < 4; ++cc) {   // 4 x 32 columns
             const int cur = cc & 1;
-            if (cc + 1 < 8) tmem_ld32_async(tmem_base + lane_off + wg * kNChunk + (cc + 1) * 32, v[cur ^ 1]);
+            if (cc + 1 < 4) tmem_ld32_async(tcol + (cc + 1) * 32, v[cur ^ 1]);
             const float4* b4 = reinterpret_cast<const float4*>(bias + cc * 32);
             if (l < NL) {
               uint32_t pk[16];
@@ -413,17 +432,34 @@ __global__ void __launch_bounds__(kThreadsWide, 1) flern_query_wide_kernel(const
                 pk[2 * i] = relu_bf16x2(z0.x, z0.y);
                 pk[2 * i + 1] = relu_bf16x2(z1.x, z1.y);
               }
-              // columns n*256 + cc*32 .. +31 -> K-block kb, 16-byte chunks jj0..jj0+3 of the row,
-              // stored at chunk ^ (row % 8) (128B swizzle, the layout the next layer's MMA reads)
-              const int col = n * kNChunk + cc * 32;
+              // columns col .. col+31 -> K-block kb, 16-byte chunks jj0..jj0+3 of row r, stored at chunk
+              // (jj0 + jj) ^ (r % 8) (128B swizzle, the layout the next layer's MMA reads): one aligned 64-byte
+              // half of the row's 128-byte line, half h_r = (jj0 / 4) ^ ((r / 4) % 2), position jj ^ (r % 4).
+              // The warp transposes through shared memory so that each store instruction writes 8 rows'
+              // halves (16 full sectors) instead of 32 lines at 16 bytes each.
+              const int col = col0 + cc * 32;
               const int kb = col >> 6, jj0 = (col & 63) >> 3;
-              uint8_t* rowp = act + (size_t)kb * kABlock + (r >> 3) * 1024 + (r & 7) * 128;
+              const uint32_t stg = smem_u32(smem + P::off_stage) + (uint32_t)(warp - 4) * 2048u;
 #pragma unroll
-              for (int jj = 0; jj < 4; ++jj)
-                st_global_v4_hint(rowp + (((jj0 + jj) ^ (r & 7)) << 4), pk[4 * jj], pk[4 * jj + 1], pk[4 * jj + 2],
-                                  pk[4 * jj + 3], keep);
+              for (int jj = 0; jj < 4; ++jj) {
+                const int pos = jj ^ (r & 3);
+                st_shared_v4(stg + lane * 64 + ((pos ^ ((lane >> 1) & 3)) << 4), pk[4 * jj], pk[4 * jj + 1],
+                             pk[4 * jj + 2], pk[4 * jj + 3]);
+              }
+              __syncwarp();
+              uint8_t* kbp = act + (size_t)kb * kABlock;
+#pragma unroll
+              for (int k8 = 0; k8 < 4; ++k8) {
+                const int R = 8 * k8 + (lane >> 2), P4 = lane & 3;   // row of this warp's 32, position
+                const int4 v4 = lds128(stg + R * 64 + ((P4 ^ ((R >> 1) & 3)) << 4));
+                const int rr = q * 32 + R;                          // tile row
+                const int h = (jj0 >> 2) ^ ((rr >> 2) & 1);
+                st_global_v4_hint(kbp + (size_t)rr * 128 + h * 64 + P4 * 16, (uint32_t)v4.x, (uint32_t)v4.y,
+                                  (uint32_t)v4.z, (uint32_t)v4.w, keep);
+              }
+              __syncwarp();
             } else {
-              const float4* w4 = reinterpret_cast<const float4*>(s_wout + n * kNChunk + cc * 32);
+              const float4* w4 = reinterpret_cast<const float4*>(s_wout + col0 + cc * 32);
 #pragma unroll
               for (int i = 0; i < 8; ++i) {
                 const float4 bb = b4[i], w = w4[i];
@@ -437,11 +473,11 @@ __global__ void __launch_bounds__(kThreadsWide, 1) flern_query_wide_kernel(const
                 pb = fma2(z1, make_float2(w.z, w.w), pb);
               }
             }
-            if (cc + 1 < 8) tmem_ld_wait(v[cur ^ 1]);
+            if (cc + 1 < 4) tmem_ld_wait(v[cur ^ 1]);
           }
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive_cluster(dempty_cl);
+          if (lane == 0) mbar_arrive_cluster(dempty_cl + b * 8);
           if (l < NL) {   // this chunk of layer l's activations is in the scratch
             fence_proxy_async_global();
             __syncwarp();
