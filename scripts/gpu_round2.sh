@@ -30,13 +30,13 @@ for w in c2 c1x c2s c4p c3 c4 c5 c1 train c2nm c1xnm; do
   timeout 900 ncu --metrics $M --clock-control none -k $k -s 2 -c 1 --csv --log-file gpurun_out/counters_${w}_$TAG.csv \
     python bench.py --workload $ww $extra --steps 2 --warmup 3 --no-cpu-baseline --e2e-steps 1 > /dev/null 2>&1
 done
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:flern_query -s 6 -c 1 -o gpurun_out/prof_c2_$TAG -f \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:flern_query -s 6 -c 1 -o /tmp/prof_c2_$TAG -f \
   python bench.py --steps 5 --warmup 3 --no-cpu-baseline --e2e-steps 1 > gpurun_out/ncu_c2_$TAG.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:flern_query -s 4 -c 1 -o gpurun_out/prof_c1x_$TAG -f \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:flern_query -s 4 -c 1 -o /tmp/prof_c1x_$TAG -f \
   python bench.py --workload c1x --steps 3 --warmup 3 --no-cpu-baseline --e2e-steps 1 > gpurun_out/ncu_c1x_$TAG.log 2>&1
 for w in c2 c1x; do
-  [ -f gpurun_out/prof_${w}_$TAG.ncu-rep ] && python scripts/ncu_summary.py gpurun_out/prof_${w}_$TAG.ncu-rep > gpurun_out/ncusum_${w}_$TAG.md
-  ncu -i gpurun_out/prof_${w}_$TAG.ncu-rep --page source --csv --print-source cuda,sass > /tmp/_src_$w.csv 2>/dev/null
+  [ -f /tmp/prof_${w}_$TAG.ncu-rep ] && python scripts/ncu_summary.py /tmp/prof_${w}_$TAG.ncu-rep > gpurun_out/ncusum_${w}_$TAG.md
+  ncu -i /tmp/prof_${w}_$TAG.ncu-rep --page source --csv --print-source cuda,sass > /tmp/_src_$w.csv 2>/dev/null
   python scripts/ncu_roles.py /tmp/_src_$w.csv 3 > gpurun_out/roles_${w}_$TAG.txt
 done
 rm -f gpurun_out/prof_c1x_$TAG.ncu-rep
