@@ -223,9 +223,16 @@ def cpu_baseline(cfg, db, model, seconds=25.0):
     t0 = time.perf_counter()
     r = O.run(cfg, db, model, nthreads=threads, row_lo=0, row_hi=rows)
     dt = time.perf_counter() - t0
+    # plain single-core speed (BASELINE.md's CPU plan): one thread on a prefix sized for ~3 s
+    one = int(min(db.fact_n, max(64, rows / max(dt, 1e-3) / threads * 3.0)))
+    t1 = time.perf_counter()
+    r1 = O.run(cfg, db, model, nthreads=1, row_lo=0, row_hi=one)
+    dt1 = max(1e-6, time.perf_counter() - t1)
     return {"value": r.rows_joined / dt, "unit": "rows/s", "cores": threads, "kind": "oracle",
             "sample": f"first {rows} of {db.fact_n} lineitem rows of this rank's shard, full query "
-                      f"(unordered_map join + scalar fp64 MLP + predicate + group-by), {dt:.1f} s"}
+                      f"(unordered_map join + scalar fp64 MLP + predicate + group-by), {dt:.1f} s",
+            "single_core": {"value": r1.rows_joined / dt1, "unit": "rows/s", "cores": 1,
+                            "sample": f"first {one} lineitem rows, one thread, {dt1:.1f} s"}}
 
 
 def dist_env():
