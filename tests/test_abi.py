@@ -43,8 +43,9 @@ def test_version_and_launch_count():
 
 
 def test_kernels_are_sm100a_tcgen05():
-    """The library's SASS holds tcgen05 MMAs (UTCHMMA) and TMEM loads (LDTM): the MLP runs on
-    the 5th-generation tensor cores, not mma.sync (HMMA)."""
+    """The library's SASS holds tcgen05 MMAs (UTCHMMA, incl. the CTA-pair form) and TMEM loads (LDTM):
+    the MLP runs on the 5th-generation tensor cores, not mma.sync (HMMA); operands arrive by TMA
+    (UTMALDG) and bulk copies (UBLKCP)."""
     import shutil
     import subprocess
     if not shutil.which("cuobjdump"):
@@ -53,6 +54,10 @@ def test_kernels_are_sm100a_tcgen05():
     assert "sm_100a" in subprocess.run(["cuobjdump", "-lelf", LIB], capture_output=True, text=True).stdout
     assert "UTCHMMA" in sass and "LDTM" in sass
     assert " HMMA" not in sass
+    # the wide kernel: CTA-pair MMAs (cta_group::2) fed by tensor-map TMA
+    assert "UTCHMMA.2CTA" in sass and "UTMALDG" in sass
+    # the fact-column loader and the narrow kernels' operand copies: bulk async copies
+    assert "UBLKCP" in sass
 
 
 def test_no_gpu_means_error_not_fallback():
