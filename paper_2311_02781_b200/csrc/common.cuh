@@ -27,8 +27,10 @@ __host__ __device__ constexpr bool is_prod_warp(int warp) { return (warp >= 1 &&
 // probes in flight per warp for the HBM-bound shapes)
 __host__ __device__ constexpr int rows_per_thread(int K0P, int NL) { return K0P <= 16 ? (NL == 1 ? 4 : 2) : 1; }
 __host__ __device__ constexpr int batch_rows(int K0P, int NL, int npt) { return npt * rows_per_thread(K0P, NL); }
-// pre-filter scan chunk: 8 rows per producer thread (two 16-byte loads)
-__host__ __device__ constexpr int scan_rows(int npt) { return 8 * npt; }
+// pre-filter scan chunk: kScanPerThread rows per producer thread (16-byte loads of 4 rows), compacted with
+// one pair of producer barriers per chunk (16: r02c, half the barriers per scanned row of 8)
+constexpr int kScanPerThread = 16;
+__host__ __device__ constexpr int scan_rows(int npt) { return kScanPerThread * npt; }
 // survivor queue: pending (< one batch) + one scan chunk
 // survivor queue: one scan chunk's survivors on top of a partial gather batch (up to 2 rows per thread)
 __host__ __device__ constexpr uint32_t queue_bytes(int npt) { return (uint32_t)(scan_rows(npt) + 2 * npt) * 4u; }

@@ -511,13 +511,14 @@ __device__ __forceinline__ void producer_loop(const QueryParams& p, const XRing&
     }
   } else {
     int nq = 0;        // survivors queued (uniform across the producer group)
-    // one scan chunk: my 8 filter values x (rows cb + 4t + 4*NPT*j + u, j = 0, 1) -> ballot
+    // one scan chunk: my kScanPerThread filter values x (rows cb + 4t + 4*NPT*j + u, j < kScanPerThread / 4) -> ballot
     // compaction of the survivors into the SMEM queue; full batches of NPT survivors (all of them
     // after the last chunk) go through the probe / gather body, one row per thread
-    auto scan_chunk = [&](int64_t cb, int64_t row_end, const int32_t (&x)[8], bool last) {
+    constexpr int kSV = kScanPerThread, kSJ = kSV / 4;
+    auto scan_chunk = [&](int64_t cb, int64_t row_end, const int32_t (&x)[kSV], bool last) {
       uint32_t bits = 0;
 #pragma unroll
-      for (int j = 0; j < 2; ++j)
+      for (int j = 0; j < kSJ; ++j)
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           const int64_t rr = cb + 4 * t + 4 * NPT * j + u;
@@ -541,7 +542,7 @@ __device__ __forceinline__ void producer_loop(const QueryParams& p, const XRing&
       }
       int pos = nq + woff + incl - my;
 #pragma unroll
-      for (int j = 0; j < 2; ++j)
+      for (int j = 0; j < kSJ; ++j)
 #pragma unroll
         for (int u = 0; u < 4; ++u)
           if (bits & (1u << (4 * j + u))) queue[pos++] = (int32_t)(cb + 4 * t + 4 * NPT * j + u);
@@ -584,12 +585,14 @@ __device__ __forceinline__ void producer_loop(const QueryParams& p, const XRing&
         if (t == 0) FLERN_TRACE(TR_MMA_D2A_FREE, b);
         const int64_t cb = fr.hdr[2 * f];
         const int nrows = (int)fr.hdr[2 * f + 1];
-        int32_t x[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        int32_t x[kSV];
+#pragma unroll
+        for (int u = 0; u < kSV; ++u) x[u] = 0;
         if (nrows > 0) {
           const uint32_t sa = smem_u32(fr.base + f * fr.stage_bytes);
           const int nfull = nrows & ~3;
 #pragma unroll
-          for (int j = 0; j < 2; ++j) {
+          for (int j = 0; j < kSJ; ++j) {
             const int rel = 4 * t + 4 * NPT * j;
             if (rel + 4 <= nfull) {
               const int4 v = lds128(sa + 4u * rel);
@@ -605,7 +608,9 @@ __device__ __forceinline__ void producer_loop(const QueryParams& p, const XRing&
         __syncwarp();
         if (lane == 0) mbar_arrive(&fr.empty[f]);   // the stage is read: the loader may refill it
         if (nrows < 0) {
-          const int32_t none[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+          int32_t none[kSV];
+#pragma unroll
+          for (int u = 0; u < kSV; ++u) none[u] = 0;
           scan_chunk(0, 0, none, true);   // drain the queue
           break;
         }
@@ -613,11 +618,11 @@ __device__ __forceinline__ void producer_loop(const QueryParams& p, const XRing&
         if (t == 0) FLERN_TRACE(TR_MMA_L1_ISSUED, b);
       }
     } else {
-      // scan rows cb + 4t + 4*NPT*j (j = 0, 1; each warp instruction covers 128 contiguous rows); the
+      // scan rows cb + 4t + 4*NPT*j (j < kScanPerThread / 4; each warp instruction covers 128 contiguous rows); the
       // next chunk's loads are issued before this chunk is compacted (software pipeline)
-      auto scan_load = [&](int64_t cb, int64_t row_end, int32_t (&x)[8]) {
+      auto scan_load = [&](int64_t cb, int64_t row_end, int32_t (&x)[kSV]) {
 #pragma unroll
-        for (int j = 0; j < 2; ++j) {
+        for (int j = 0; j < kSJ; ++j) {
           const int64_t r0 = cb + 4 * t + 4 * NPT * j;
           if (r0 + 4 <= row_end) {
             const int4 v = ldg_nc(reinterpret_cast<const int4*>(p.pf_col + r0));
@@ -628,7 +633,7 @@ __device__ __forceinline__ void producer_loop(const QueryParams& p, const XRing&
           }
         }
       };
-      int32_t xnext[8];
+      int32_t xnext[kSV];
       if (cur.lo < n) scan_load(cur.lo, cur.hi, xnext);
       while (cur.lo < n) {
         int64_t a = 0;
@@ -636,9 +641,9 @@ __device__ __forceinline__ void producer_loop(const QueryParams& p, const XRing&
         if (t == 0) s_cnt[0] += cur.hi - cur.lo;   // rows scanned by this CTA
         for (int64_t cb = cur.lo; cb < cur.hi; cb += kScanChunk) {
           const bool last_block = cb + kScanChunk >= cur.hi;
-          int32_t x[8];
+          int32_t x[kSV];
 #pragma unroll
-          for (int u = 0; u < 8; ++u) x[u] = xnext[u];
+          for (int u = 0; u < kSV; ++u) x[u] = xnext[u];
           if (!last_block) scan_load(cb + kScanChunk, cur.hi, xnext);
           else if (nxt.lo < n) scan_load(nxt.lo, nxt.hi, xnext);
           scan_chunk(cb, cur.hi, x, last_block && nxt.lo >= n);
