@@ -161,13 +161,13 @@ __global__ void __launch_bounds__(kThreadsWide, 1) flern_query_wide_kernel(const
   uint64_t* xfull = bars;             // [S] producers -> this CTA's loader (128)
   uint64_t* xempty = xfull + S;       // [S] warpgroup 1 (4 warps) -> producers
   uint64_t* rfull = xempty + S;       // [RS] even CTA: its loader's expect_tx + both CTAs' TMA bytes
-  uint64_t* rempty = rfull + RS;      // [RS] MMA commit (multicast to both CTAs)
-  uint64_t* dfull = rempty + RS;      // [2] MMA commit (multicast) -> epilogue
+  uint64_t* rempty = rfull + RS;      // [RS][KPS] MMA commit per K-block half of a stage (multicast to both CTAs)
+  uint64_t* dfull = rempty + RS * P::KPS;   // [2] MMA commit (multicast) -> epilogue
   uint64_t* dempty = dfull + 2;       // [2] even CTA: both CTAs' epilogue warps (16) -> MMA
   uint64_t* actrdy = dempty + 2;      // [2][NCH] N-chunk n of a hidden layer's activations is in scratch buffer b (8)
   uint64_t* decb = actrdy + 2 * NCH;  // [kDec] the pair decision for tile t is in dec[t % kDec] (1)
   uint64_t* pstat = decb + kDec;      // [S] even CTA: the odd CTA's status of tile t is in pst[t % S] (1)
-  static_assert(2 * S + 2 * RS + 4 + 2 * NCH + kDec + S <= 64, "barrier block");
+  static_assert(2 * S + RS + RS * P::KPS + 4 + 2 * NCH + kDec + S <= 64, "barrier block");
   int32_t* dec = reinterpret_cast<int32_t*>(smem + P::off_dec);        // -1 stop, else this CTA's row count
   int32_t* pst = dec + kDec;                                           // odd CTA's count (-1: out of rows)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + P::off_misc);
@@ -196,7 +196,8 @@ __global__ void __launch_bounds__(kThreadsWide, 1) flern_query_wide_kernel(const
   if (tid == 0) { s_claim[0] = claim0; s_claim[1] = claim0 + 1; }
   if (tid == 0) {
     for (int s = 0; s < S; ++s) { mbar_init(&xfull[s], 32 * kProdWarpsWide); mbar_init(&xempty[s], 4); }
-    for (int s = 0; s < RS; ++s) { mbar_init(&rfull[s], 1); mbar_init(&rempty[s], 1); }
+    for (int s = 0; s < RS; ++s) mbar_init(&rfull[s], 1);
+    for (int s = 0; s < RS * P::KPS; ++s) mbar_init(&rempty[s], 1);
     for (int i = 0; i < 2; ++i) { mbar_init(&dfull[i], 1); mbar_init(&dempty[i], 16); }
     for (int i = 0; i < 2 * NCH; ++i) mbar_init(&actrdy[i], 8);
     for (int i = 0; i < kDec; ++i) mbar_init(&decb[i], 1);
@@ -226,11 +227,14 @@ __global__ void __launch_bounds__(kThreadsWide, 1) flern_query_wide_kernel(const
       const uint32_t rfull_cl = mapa_rank(smem_u32(rfull), 0);   // the even CTA's rfull[0]
       uint32_t slot = 0;
       const bool noload = WIDE_DBG(2);
+      // A stage is re-armed as soon as its first K-block half is free; the second half's loads follow
+      // when the MMAs of that half complete (half_free), so half of every stage gets its operands ~one
+      // half-stage earlier (the ring holds only 2 stages of 8 MMAs).
       auto acquire = [&](uint32_t pair_bytes) -> uint32_t {
         const uint32_t st = slot % RS;
         // polls without a sleep: one stage is re-armed per wake-up, and a __nanosleep back-off wakes
         // ~1K cycles late, which paced the whole MMA chain at ~940 cycles per 512-cycle stage (r02c)
-        WIDE_WAIT(6, true, mbar_wait_cl_nohint(&rempty[st], ((slot / RS) & 1) ^ 1, 40));
+        WIDE_WAIT(6, true, mbar_wait_cl_nohint(&rempty[st * P::KPS], ((slot / RS) & 1) ^ 1, 40));
         WIDE_LSEQ(slot, 0);
         if (noload) {   // diagnostic: 16 pretend bytes from the odd CTA keep the two loaders in step
           if (leader) mbar_arrive_expect_tx(&rfull[st], 16);
@@ -241,6 +245,10 @@ __global__ void __launch_bounds__(kThreadsWide, 1) flern_query_wide_kernel(const
         WIDE_LSEQ(slot, 1);
         ++slot;
         return st;
+      };
+      // K-block half q >= 1 of the stage acquired last (slot - 1) is free
+      auto half_free = [&](uint32_t st, int q) {
+        WIDE_WAIT(6, true, mbar_wait_cl_nohint(&rempty[st * P::KPS + q], (((slot - 1) / RS) & 1) ^ 1, 40));
       };
       bool out = false;   // this CTA's producers have published their last tile
       for (uint32_t t = 0;; ++t) {
@@ -281,6 +289,7 @@ __global__ void __launch_bounds__(kThreadsWide, 1) flern_query_wide_kernel(const
 #pragma unroll
               for (uint32_t b = 0; b < P::W1H / 4096; ++b)
                 if (!noload) tma_load_2d_pair(dst + b * 4096, &p.tm_w1, 0, row + 32 * b, rfull_cl + st * 8, keep);
+              for (int q = 1; q < P::KPS; ++q) half_free(st, q);   // (unused here: keeps the halves' phases in step)
             } else {
               const size_t wl = P::img_w1 + (size_t)(l - 2) * NCH * KB * kBBlock + (size_t)n * KB * kBBlock;
               for (int kb0 = 0; kb0 < KB; kb0 += P::KPS) {
@@ -290,9 +299,10 @@ __global__ void __launch_bounds__(kThreadsWide, 1) flern_query_wide_kernel(const
                   WIDE_WAIT(7, true, mbar_wait(&actrdy[((l - 2) & 1) * NCH + kb0 / (kNChunk / 64)], t & 1, 42));
                 const uint32_t st = acquire(2 * P::RING);
                 uint8_t* dst = smem + P::off_ring + st * P::RING;
-                if (noload) continue;
 #pragma unroll
                 for (int q = 0; q < P::KPS; ++q) {
+                  if (q > 0) half_free(st, q);
+                  if (noload) continue;
                   const int kb = kb0 + q;
                   uint8_t* d = dst + q * (kABlock + kBHalf);
                   tma_load_2d_pair(d, &p.tm_act, 0, act_row + kb * (int)(kABlock >> 7), rfull_cl + st * 8, keep);
@@ -344,7 +354,9 @@ __global__ void __launch_bounds__(kThreadsWide, 1) flern_query_wide_kernel(const
                 const uint64_t bd = make_sdesc(bb + ks * 2 * (128 * 16), 128 * 16, 128, kLayoutNone);
                 if (elect_one_sync()) mma_bf16_ss_pair(dcol, ad, bd, idesc, ks > 0);
               }
-              if (elect_one_sync()) mma_commit_pair(&rempty[st], 3);
+#pragma unroll
+              for (int q = 0; q < P::KPS; ++q)
+                if (elect_one_sync()) mma_commit_pair(&rempty[st * P::KPS + q], 3);
               ++slot;
             } else {
               for (int kb0 = 0; kb0 < KB; kb0 += P::KPS) {
@@ -362,9 +374,9 @@ __global__ void __launch_bounds__(kThreadsWide, 1) flern_query_wide_kernel(const
                     const uint64_t bd = make_sdesc(bb + j * 32, 16, 1024, kLayoutSW128);
                     if (elect_one_sync()) mma_bf16_ss_pair(dcol, ad, bd, idesc, (kb0 | q | j) != 0);
                   }
+                  if (elect_one_sync()) mma_commit_pair(&rempty[st * P::KPS + q], 3);   // half q read
                 }
                 WIDE_SEQ(slot, 2);
-                if (elect_one_sync()) mma_commit_pair(&rempty[st], 3);
                 ++slot;
               }
             }
