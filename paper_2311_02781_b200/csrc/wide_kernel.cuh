@@ -40,6 +40,10 @@ struct WidePlan {
   static constexpr int KPS = 2;
   static constexpr int RS = 2;                   // operand ring stages
   static constexpr int S = 2;                    // X stages (a tile's MLP takes ~10x its gather)
+  // layer 1 of tile t+1 runs interleaved with tile t's last layer (its tiny MMAs in the TMEM buffer the
+  // last layer's ping-pong leaves idle, its drains under the last layer's long chunks); with two hidden
+  // layers the last layer reads layer 1's scratch buffer, so there it follows the last layer instead
+  static constexpr bool kInter = NL >= 3;
   static constexpr uint32_t RING = KPS * (kABlock + kBHalf);
   static constexpr uint32_t XS = (uint32_t)kTile * K0P * 2;
   static constexpr uint32_t W1H = (uint32_t)128 * K0P * 2;           // one CTA's half of a W1 N-chunk
@@ -251,7 +255,8 @@ __global__ void __launch_bounds__(kThreadsWide, 1) flern_query_wide_kernel(const
         WIDE_WAIT(6, true, mbar_wait_cl_nohint(&rempty[st * P::KPS + q], (((slot - 1) / RS) & 1) ^ 1, 40));
       };
       bool out = false;   // this CTA's producers have published their last tile
-      for (uint32_t t = 0;; ++t) {
+      // the pair decision for tile t (the even CTA decides for both; see the kernel comment)
+      auto decide = [&](uint32_t t) -> int32_t {
         const int s = t % S;
         int32_t cnt = -1;
         if (!out) {
@@ -278,40 +283,55 @@ __global__ void __launch_bounds__(kThreadsWide, 1) flern_query_wide_kernel(const
           WIDE_WAIT(5, true, mbar_wait_cl(&decb[d], (t / kDec) & 1, 50));
           mine = *(volatile int32_t*)&dec[d];
         }
-        if (mine < 0) break;
-        for (int l = 1; l <= NL; ++l) {
-          const int act_row = scratch_row0 + (int)((((l - 2) & 1) * KB * kABlock) >> 7);
-          for (int n = 0; n < NCH; ++n) {
-            if (l == 1) {
-              const uint32_t st = acquire(P::W1C);
-              uint8_t* dst = smem + P::off_ring + st * P::RING + kABlock;
-              const int row = (int)(((size_t)n * P::W1C + rank * P::W1H) >> 7);
+        return mine;
+      };
+      auto load_l1 = [&](int n) {   // W1 halves of N-chunk n (the X tile is already in shared memory)
+        const uint32_t st = acquire(P::W1C);
+        uint8_t* dst = smem + P::off_ring + st * P::RING + kABlock;
+        const int row = (int)(((size_t)n * P::W1C + rank * P::W1H) >> 7);
 #pragma unroll
-              for (uint32_t b = 0; b < P::W1H / 4096; ++b)
-                if (!noload) tma_load_2d_pair(dst + b * 4096, &p.tm_w1, 0, row + 32 * b, rfull_cl + st * 8, keep);
-              for (int q = 1; q < P::KPS; ++q) half_free(st, q);   // (unused here: keeps the halves' phases in step)
-            } else {
-              const size_t wl = P::img_w1 + (size_t)(l - 2) * NCH * KB * kBBlock + (size_t)n * KB * kBBlock;
-              for (int kb0 = 0; kb0 < KB; kb0 += P::KPS) {
-                // K-block kb of layer l's input is N-chunk kb / 4 of layer l-1: wait for that chunk only
-                // (per-chunk hand-off: layer l starts while layer l-1's last chunks are still drained)
-                if (n == 0 && kb0 % (kNChunk / 64) == 0)
-                  WIDE_WAIT(7, true, mbar_wait(&actrdy[((l - 2) & 1) * NCH + kb0 / (kNChunk / 64)], t & 1, 42));
-                const uint32_t st = acquire(2 * P::RING);
-                uint8_t* dst = smem + P::off_ring + st * P::RING;
+        for (uint32_t b = 0; b < P::W1H / 4096; ++b)
+          if (!noload) tma_load_2d_pair(dst + b * 4096, &p.tm_w1, 0, row + 32 * b, rfull_cl + st * 8, keep);
+        for (int q = 1; q < P::KPS; ++q) half_free(st, q);   // (unused here: keeps the halves' phases in step)
+      };
+      auto load_hidden = [&](int l, int n, uint32_t t) {   // layer l >= 2, N-chunk n of tile t
+        const int act_row = scratch_row0 + (int)((((l - 2) & 1) * KB * kABlock) >> 7);
+        const size_t wl = P::img_w1 + (size_t)(l - 2) * NCH * KB * kBBlock + (size_t)n * KB * kBBlock;
+        for (int kb0 = 0; kb0 < KB; kb0 += P::KPS) {
+          // K-block kb of layer l's input is N-chunk kb / 4 of layer l-1: wait for that chunk only
+          // (per-chunk hand-off: layer l starts while layer l-1's last chunks are still drained)
+          if (n == 0 && kb0 % (kNChunk / 64) == 0)
+            WIDE_WAIT(7, true, mbar_wait(&actrdy[((l - 2) & 1) * NCH + kb0 / (kNChunk / 64)], t & 1, 42));
+          const uint32_t st = acquire(2 * P::RING);
+          uint8_t* dst = smem + P::off_ring + st * P::RING;
 #pragma unroll
-                for (int q = 0; q < P::KPS; ++q) {
-                  if (q > 0) half_free(st, q);
-                  if (noload) continue;
-                  const int kb = kb0 + q;
-                  uint8_t* d = dst + q * (kABlock + kBHalf);
-                  tma_load_2d_pair(d, &p.tm_act, 0, act_row + kb * (int)(kABlock >> 7), rfull_cl + st * 8, keep);
-                  tma_load_2d_pair(d + kABlock, &p.tm_wh, 0, (int)((wl + (size_t)kb * kBBlock + rank * kBHalf) >> 7),
-                                   rfull_cl + st * 8, keep);
-                }
-              }
-            }
+          for (int q = 0; q < P::KPS; ++q) {
+            if (q > 0) half_free(st, q);
+            if (noload) continue;
+            const int kb = kb0 + q;
+            uint8_t* d = dst + q * (kABlock + kBHalf);
+            tma_load_2d_pair(d, &p.tm_act, 0, act_row + kb * (int)(kABlock >> 7), rfull_cl + st * 8, keep);
+            tma_load_2d_pair(d + kABlock, &p.tm_wh, 0, (int)((wl + (size_t)kb * kBBlock + rank * kBHalf) >> 7),
+                             rfull_cl + st * 8, keep);
           }
+        }
+      };
+      // operand order (the MMA thread consumes the same sequence): layer 1 of tile 0; per tile t, layers
+      // 2 .. NL-1, then the last layer's N-chunks, each followed (kInter) by that N-chunk of tile t+1's
+      // layer 1 -- or (two hidden layers) tile t+1's layer 1 after the last layer
+      if (decide(0) >= 0) {
+        for (int n = 0; n < NCH; ++n) load_l1(n);
+        for (uint32_t t = 0;; ++t) {
+          for (int l = 2; l < NL; ++l)
+            for (int n = 0; n < NCH; ++n) load_hidden(l, n, t);
+          const bool next = decide(t + 1) >= 0;
+          for (int n = 0; n < NCH; ++n) {
+            load_hidden(NL, n, t);
+            if (P::kInter && next) load_l1(n);
+          }
+          if (!P::kInter && next)
+            for (int n = 0; n < NCH; ++n) load_l1(n);
+          if (!next) break;
         }
       }
     }
@@ -324,66 +344,79 @@ __global__ void __launch_bounds__(kThreadsWide, 1) flern_query_wide_kernel(const
       const uint32_t x0 = smem_u32(smem + P::off_x);
       const uint32_t ring = smem_u32(smem + P::off_ring);
       uint32_t slot = 0, c = 0;
-      WIDE_STAMP(12, lane == 0);
-      __syncwarp();
-      for (uint32_t t = 0;; ++t) {
-        const int s = t % S;
-        WIDE_WAIT_W(0, mbar_wait_nohint(&decb[t % kDec], (t / kDec) & 1, 43));
-        if (*(volatile int32_t*)&dec[t % kDec] < 0) {
-          WIDE_STAMP(13, lane == 0);
-#ifdef FLERN_DIAG
-          if (p.dbg_trace && blockIdx.x < 2 && lane == 0) p.dbg_trace[TR_WAITS * kTraceTiles + 32 + 16 * blockIdx.x + 14] = t;
-          __syncwarp();
-#endif
-          break;
-        }
-        for (int l = 1; l <= NL; ++l) {
-          for (int n = 0; n < NCH; ++n, ++c) {
-            const uint32_t b = c & 1;
-            WIDE_WAIT_W(1, mbar_wait_cl_nohint(&dempty[b], ((c >> 1) & 1) ^ 1, 44));
+      // one N-chunk of layer l into TMEM buffer c % 2 (layer 1: A = X stage sx)
+      auto chunk = [&](int l, int sx) {
+        const uint32_t b = c & 1;
+        WIDE_WAIT_W(1, mbar_wait_cl_nohint(&dempty[b], ((c >> 1) & 1) ^ 1, 44));
+        tc_fence_after();
+        const uint32_t dcol = tmem_base + b * kNChunk;
+        if (l == 1) {
+          const uint32_t st = slot % RS;
+          WIDE_WAIT_W(2, mbar_wait_nohint(&rfull[st], (slot / RS) & 1, 45));
+          tc_fence_after();
+          const uint32_t bb = ring + st * P::RING + kABlock;
+#pragma unroll
+          for (int ks = 0; ks < K0P / 16; ++ks) {
+            const uint64_t ad = make_sdesc(x0 + sx * P::XS + ks * 2 * (kTile * 16), kTile * 16, 128, kLayoutNone);
+            const uint64_t bd = make_sdesc(bb + ks * 2 * (128 * 16), 128 * 16, 128, kLayoutNone);
+            if (elect_one_sync()) mma_bf16_ss_pair(dcol, ad, bd, idesc, ks > 0);
+          }
+#pragma unroll
+          for (int q = 0; q < P::KPS; ++q)
+            if (elect_one_sync()) mma_commit_pair(&rempty[st * P::KPS + q], 3);
+          ++slot;
+        } else {
+          for (int kb0 = 0; kb0 < KB; kb0 += P::KPS) {
+            const uint32_t st = slot % RS;
+            WIDE_SEQ(slot, 0);
+            WIDE_WAIT_W(3, mbar_wait_nohint(&rfull[st], (slot / RS) & 1, 46));
+            WIDE_SEQ(slot, 1);
             tc_fence_after();
-            const uint32_t dcol = tmem_base + b * kNChunk;
-            if (l == 1) {
-              const uint32_t st = slot % RS;
-              WIDE_WAIT_W(2, mbar_wait_nohint(&rfull[st], (slot / RS) & 1, 45));
-              tc_fence_after();
-              const uint32_t bb = ring + st * P::RING + kABlock;
 #pragma unroll
-              for (int ks = 0; ks < K0P / 16; ++ks) {
-                const uint64_t ad = make_sdesc(x0 + s * P::XS + ks * 2 * (kTile * 16), kTile * 16, 128, kLayoutNone);
-                const uint64_t bd = make_sdesc(bb + ks * 2 * (128 * 16), 128 * 16, 128, kLayoutNone);
-                if (elect_one_sync()) mma_bf16_ss_pair(dcol, ad, bd, idesc, ks > 0);
+            for (int q = 0; q < P::KPS; ++q) {
+              const uint32_t ab = ring + st * P::RING + q * (kABlock + kBHalf), bb = ab + kABlock;
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                const uint64_t ad = make_sdesc(ab + j * 32, 16, 1024, kLayoutSW128);
+                const uint64_t bd = make_sdesc(bb + j * 32, 16, 1024, kLayoutSW128);
+                if (elect_one_sync()) mma_bf16_ss_pair(dcol, ad, bd, idesc, (kb0 | q | j) != 0);
               }
-#pragma unroll
-              for (int q = 0; q < P::KPS; ++q)
-                if (elect_one_sync()) mma_commit_pair(&rempty[st * P::KPS + q], 3);
-              ++slot;
-            } else {
-              for (int kb0 = 0; kb0 < KB; kb0 += P::KPS) {
-                const uint32_t st = slot % RS;
-                WIDE_SEQ(slot, 0);
-                WIDE_WAIT_W(3, mbar_wait_nohint(&rfull[st], (slot / RS) & 1, 46));
-                WIDE_SEQ(slot, 1);
-                tc_fence_after();
-#pragma unroll
-                for (int q = 0; q < P::KPS; ++q) {
-                  const uint32_t ab = ring + st * P::RING + q * (kABlock + kBHalf), bb = ab + kABlock;
-#pragma unroll
-                  for (int j = 0; j < 4; ++j) {
-                    const uint64_t ad = make_sdesc(ab + j * 32, 16, 1024, kLayoutSW128);
-                    const uint64_t bd = make_sdesc(bb + j * 32, 16, 1024, kLayoutSW128);
-                    if (elect_one_sync()) mma_bf16_ss_pair(dcol, ad, bd, idesc, (kb0 | q | j) != 0);
-                  }
-                  if (elect_one_sync()) mma_commit_pair(&rempty[st * P::KPS + q], 3);   // half q read
-                }
-                WIDE_SEQ(slot, 2);
-                ++slot;
-              }
+              if (elect_one_sync()) mma_commit_pair(&rempty[st * P::KPS + q], 3);   // half q read
             }
-            if (elect_one_sync()) mma_commit_pair(&dfull[b], 3);
+            WIDE_SEQ(slot, 2);
+            ++slot;
           }
         }
+        if (elect_one_sync()) mma_commit_pair(&dfull[b], 3);
+        ++c;
+      };
+      auto decided = [&](uint32_t t) -> bool {   // the pair decision for tile t: run it?
+        WIDE_WAIT_W(0, mbar_wait_nohint(&decb[t % kDec], (t / kDec) & 1, 43));
+        return *(volatile int32_t*)&dec[t % kDec] >= 0;
+      };
+      WIDE_STAMP(12, lane == 0);
+      __syncwarp();
+      uint32_t t = 0;
+      if (decided(0)) {   // the same operand order as the loader's
+        for (int n = 0; n < NCH; ++n) chunk(1, 0);
+        for (;; ++t) {
+          for (int l = 2; l < NL; ++l)
+            for (int n = 0; n < NCH; ++n) chunk(l, 0);
+          const bool next = decided(t + 1);
+          for (int n = 0; n < NCH; ++n) {
+            chunk(NL, 0);
+            if (P::kInter && next) chunk(1, (int)((t + 1) % S));
+          }
+          if (!P::kInter && next)
+            for (int n = 0; n < NCH; ++n) chunk(1, (int)((t + 1) % S));
+          if (!next) { ++t; break; }
+        }
       }
+      WIDE_STAMP(13, lane == 0);
+#ifdef FLERN_DIAG
+      if (p.dbg_trace && blockIdx.x < 2 && lane == 0) p.dbg_trace[TR_WAITS * kTraceTiles + 32 + 16 * blockIdx.x + 14] = t;
+      __syncwarp();
+#endif
     }
     __syncwarp();
   } else {
@@ -401,112 +434,130 @@ __global__ void __launch_bounds__(kThreadsWide, 1) flern_query_wide_kernel(const
     agg.init();
     const uint64_t keep = l2_policy_evict_last();   // activation scratch: keep in L2 for the next layer
     uint8_t* scratch = p.scratch + (size_t)blockIdx.x * P::scratch_per_cta;   // act[0] | act[1]
-    for (uint32_t t = 0;; ++t) {
-      const int s = t % S;
-      WIDE_WAIT(8, tid == 128, mbar_wait_cl(&decb[t % kDec], (t / kDec) & 1, 47));
-      const int count = *(volatile int32_t*)&dec[t % kDec];
-      if (count < 0) break;
-      const Meta m = meta_at(smem + P::off_meta, s);
-      float2 pa = make_float2(0.f, 0.f), pb = make_float2(0.f, 0.f);
-      for (int l = 1; l <= NL; ++l) {
+    uint32_t cseq = 0;   // N-chunks drained so far (the MMA thread's order; buffer cseq % 2)
+    // drain one N-chunk of layer l: bias + ReLU -> bf16 activations into the scratch (l < NL), or the
+    // output dot into (pa, pb) (l == NL)
+    auto drain = [&](int l, int n, float2& pa, float2& pb) {
+        const uint32_t c = cseq++, b = c & 1;
         uint8_t* act = scratch + (size_t)((l - 1) & 1) * KB * kABlock;   // layer l's output buffer
-        for (int n = 0; n < NCH; ++n) {
-          const uint32_t c = (t * NL + (l - 1)) * NCH + n, b = c & 1;
-          WIDE_WAIT(9 + wg, tid == 128 || tid == 256, mbar_wait_cl_nohint(&dfull[b], (c >> 1) & 1, 48));
-          tc_fence_after();
-          const int col0 = n * kNChunk + wg * 128;   // this warpgroup's first column of the chunk
-          const float* bias = s_bias + (l - 1) * H + col0;
-          const uint32_t tcol = tmem_base + lane_off + b * kNChunk + wg * 128;
-          uint32_t v[2][32];
-          if (WIDE_DBG(1)) {
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive_cluster(dempty_cl + b * 8);
-            if (l < NL && lane == 0) mbar_arrive(&actrdy[((l - 1) & 1) * NCH + n]);
-            continue;
-          }
-          tmem_ld32_async(tcol, v[0]);
-          tmem_ld_wait(v[0]);
-#pragma unroll
-          for (int cc = 0; cc < 4; ++cc) {   // 4 x 32 columns
-            const int cur = cc & 1;
-            if (cc + 1 < 4) tmem_ld32_async(tcol + (cc + 1) * 32, v[cur ^ 1]);
-            const float4* b4 = reinterpret_cast<const float4*>(bias + cc * 32);
-            if (l < NL) {
-              uint32_t pk[16];
-#pragma unroll
-              for (int i = 0; i < 8; ++i) {
-                const float4 bb = b4[i];
-                const float2 z0 = add2(make_float2(__uint_as_float(v[cur][4 * i]), __uint_as_float(v[cur][4 * i + 1])),
-                                       make_float2(bb.x, bb.y));
-                const float2 z1 = add2(make_float2(__uint_as_float(v[cur][4 * i + 2]), __uint_as_float(v[cur][4 * i + 3])),
-                                       make_float2(bb.z, bb.w));
-                pk[2 * i] = relu_bf16x2(z0.x, z0.y);
-                pk[2 * i + 1] = relu_bf16x2(z1.x, z1.y);
-              }
-              // columns col .. col+31 -> K-block kb, 16-byte chunks jj0..jj0+3 of row r, stored at chunk
-              // (jj0 + jj) ^ (r % 8) (128B swizzle, the layout the next layer's MMA reads): one aligned 64-byte
-              // half of the row's 128-byte line, half h_r = (jj0 / 4) ^ ((r / 4) % 2), position jj ^ (r % 4).
-              // The warp transposes through shared memory so that each store instruction writes 8 rows'
-              // halves (16 full sectors) instead of 32 lines at 16 bytes each.
-              const int col = col0 + cc * 32;
-              const int kb = col >> 6, jj0 = (col & 63) >> 3;
-              const uint32_t stg = smem_u32(smem + P::off_stage) + (uint32_t)(warp - 4) * 2048u;
-#pragma unroll
-              for (int jj = 0; jj < 4; ++jj) {
-                const int pos = jj ^ (r & 3);
-                st_shared_v4(stg + lane * 64 + ((pos ^ ((lane >> 1) & 3)) << 4), pk[4 * jj], pk[4 * jj + 1],
-                             pk[4 * jj + 2], pk[4 * jj + 3]);
-              }
-              __syncwarp();
-              uint8_t* kbp = act + (size_t)kb * kABlock;
-#pragma unroll
-              for (int k8 = 0; k8 < 4; ++k8) {
-                const int R = 8 * k8 + (lane >> 2), P4 = lane & 3;   // row of this warp's 32, position
-                const int4 v4 = lds128(stg + R * 64 + ((P4 ^ ((R >> 1) & 3)) << 4));
-                const int rr = q * 32 + R;                          // tile row
-                const int h = (jj0 >> 2) ^ ((rr >> 2) & 1);
-                st_global_v4_hint(kbp + (size_t)rr * 128 + h * 64 + P4 * 16, (uint32_t)v4.x, (uint32_t)v4.y,
-                                  (uint32_t)v4.z, (uint32_t)v4.w, keep);
-              }
-              __syncwarp();
-            } else {
-              const float4* w4 = reinterpret_cast<const float4*>(s_wout + col0 + cc * 32);
-#pragma unroll
-              for (int i = 0; i < 8; ++i) {
-                const float4 bb = b4[i], w = w4[i];
-                float2 z0 = add2(make_float2(__uint_as_float(v[cur][4 * i]), __uint_as_float(v[cur][4 * i + 1])),
-                                 make_float2(bb.x, bb.y));
-                float2 z1 = add2(make_float2(__uint_as_float(v[cur][4 * i + 2]), __uint_as_float(v[cur][4 * i + 3])),
-                                 make_float2(bb.z, bb.w));
-                z0.x = fmaxf(z0.x, 0.f); z0.y = fmaxf(z0.y, 0.f);
-                z1.x = fmaxf(z1.x, 0.f); z1.y = fmaxf(z1.y, 0.f);
-                pa = fma2(z0, make_float2(w.x, w.y), pa);
-                pb = fma2(z1, make_float2(w.z, w.w), pb);
-              }
-            }
-            if (cc + 1 < 4) tmem_ld_wait(v[cur ^ 1]);
-          }
+        WIDE_WAIT(9 + wg, tid == 128 || tid == 256, mbar_wait_cl_nohint(&dfull[b], (c >> 1) & 1, 48));
+        tc_fence_after();
+        const int col0 = n * kNChunk + wg * 128;   // this warpgroup's first column of the chunk
+        const float* bias = s_bias + (l - 1) * H + col0;
+        const uint32_t tcol = tmem_base + lane_off + b * kNChunk + wg * 128;
+        uint32_t v[2][32];
+        if (WIDE_DBG(1)) {
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive_cluster(dempty_cl + b * 8);
-          if (l < NL) {   // this chunk of layer l's activations is in the scratch
-            fence_proxy_async_global();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&actrdy[((l - 1) & 1) * NCH + n]);
-          }
+          if (l < NL && lane == 0) mbar_arrive(&actrdy[((l - 1) & 1) * NCH + n]);
+          return;
         }
-      }
-      // combine the two warpgroups' halves of the output dot, then predicate + group-by
-      float* xb = xchg + (t & 1) * kTile;
-      const float part = (pa.x + pa.y) + (pb.x + pb.y);
-      if (wg == 0) {
-        xb[r] = part;
-        named_bar_arrive(2, 256);
-      } else {
-        WIDE_WAIT(11, tid == 256, named_bar_sync(2, 256));
-        const float logit = part + xb[r] + p.bout;
-        agg.tile(p, m, count, r, lane, logit, s_cnt, &xempty[s]);
+        tmem_ld32_async(tcol, v[0]);
+        tmem_ld_wait(v[0]);
+#pragma unroll
+        for (int cc = 0; cc < 4; ++cc) {   // 4 x 32 columns
+          const int cur = cc & 1;
+          if (cc + 1 < 4) tmem_ld32_async(tcol + (cc + 1) * 32, v[cur ^ 1]);
+          const float4* b4 = reinterpret_cast<const float4*>(bias + cc * 32);
+          if (l < NL) {
+            uint32_t pk[16];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const float4 bb = b4[i];
+              const float2 z0 = add2(make_float2(__uint_as_float(v[cur][4 * i]), __uint_as_float(v[cur][4 * i + 1])),
+                                     make_float2(bb.x, bb.y));
+              const float2 z1 = add2(make_float2(__uint_as_float(v[cur][4 * i + 2]), __uint_as_float(v[cur][4 * i + 3])),
+                                     make_float2(bb.z, bb.w));
+              pk[2 * i] = relu_bf16x2(z0.x, z0.y);
+              pk[2 * i + 1] = relu_bf16x2(z1.x, z1.y);
+            }
+            // columns col .. col+31 -> K-block kb, 16-byte chunks jj0..jj0+3 of row r, stored at chunk
+            // (jj0 + jj) ^ (r % 8) (128B swizzle, the layout the next layer's MMA reads): one aligned 64-byte
+            // half of the row's 128-byte line, half h_r = (jj0 / 4) ^ ((r / 4) % 2), position jj ^ (r % 4).
+            // The warp transposes through shared memory so that each store instruction writes 8 rows'
+            // halves (16 full sectors) instead of 32 lines at 16 bytes each.
+            const int col = col0 + cc * 32;
+            const int kb = col >> 6, jj0 = (col & 63) >> 3;
+            const uint32_t stg = smem_u32(smem + P::off_stage) + (uint32_t)(warp - 4) * 2048u;
+#pragma unroll
+            for (int jj = 0; jj < 4; ++jj) {
+              const int pos = jj ^ (r & 3);
+              st_shared_v4(stg + lane * 64 + ((pos ^ ((lane >> 1) & 3)) << 4), pk[4 * jj], pk[4 * jj + 1],
+                           pk[4 * jj + 2], pk[4 * jj + 3]);
+            }
+            __syncwarp();
+            uint8_t* kbp = act + (size_t)kb * kABlock;
+#pragma unroll
+            for (int k8 = 0; k8 < 4; ++k8) {
+              const int R = 8 * k8 + (lane >> 2), P4 = lane & 3;   // row of this warp's 32, position
+              const int4 v4 = lds128(stg + R * 64 + ((P4 ^ ((R >> 1) & 3)) << 4));
+              const int rr = q * 32 + R;                          // tile row
+              const int h = (jj0 >> 2) ^ ((rr >> 2) & 1);
+              st_global_v4_hint(kbp + (size_t)rr * 128 + h * 64 + P4 * 16, (uint32_t)v4.x, (uint32_t)v4.y,
+                                (uint32_t)v4.z, (uint32_t)v4.w, keep);
+            }
+            __syncwarp();
+          } else {
+            const float4* w4 = reinterpret_cast<const float4*>(s_wout + col0 + cc * 32);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const float4 bb = b4[i], w = w4[i];
+              float2 z0 = add2(make_float2(__uint_as_float(v[cur][4 * i]), __uint_as_float(v[cur][4 * i + 1])),
+                               make_float2(bb.x, bb.y));
+              float2 z1 = add2(make_float2(__uint_as_float(v[cur][4 * i + 2]), __uint_as_float(v[cur][4 * i + 3])),
+                               make_float2(bb.z, bb.w));
+              z0.x = fmaxf(z0.x, 0.f); z0.y = fmaxf(z0.y, 0.f);
+              z1.x = fmaxf(z1.x, 0.f); z1.y = fmaxf(z1.y, 0.f);
+              pa = fma2(z0, make_float2(w.x, w.y), pa);
+              pb = fma2(z1, make_float2(w.z, w.w), pb);
+            }
+          }
+          if (cc + 1 < 4) tmem_ld_wait(v[cur ^ 1]);
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(dempty_cl + b * 8);
+        if (l < NL) {   // this chunk of layer l's activations is in the scratch
+          fence_proxy_async_global();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&actrdy[((l - 1) & 1) * NCH + n]);
+        }
+    };
+    auto decided = [&](uint32_t t) -> int {   // the pair decision for tile t: this CTA's row count, or -1
+      WIDE_WAIT(8, tid == 128, mbar_wait_cl(&decb[t % kDec], (t / kDec) & 1, 47));
+      return *(volatile int32_t*)&dec[t % kDec];
+    };
+    int count = decided(0);
+    if (count >= 0) {   // the MMA thread's chunk order (see the loader)
+      float2 ua = make_float2(0.f, 0.f), ub = ua;   // (layer-1 drains add nothing to the dot)
+      for (int n = 0; n < NCH; ++n) drain(1, n, ua, ub);
+      for (uint32_t t = 0;; ++t) {
+        const int s = t % S;
+        const Meta m = meta_at(smem + P::off_meta, s);
+        float2 pa = make_float2(0.f, 0.f), pb = make_float2(0.f, 0.f);
+        for (int l = 2; l < NL; ++l)
+          for (int n = 0; n < NCH; ++n) drain(l, n, pa, pb);
+        const int cnext = decided(t + 1);
+        for (int n = 0; n < NCH; ++n) {
+          drain(NL, n, pa, pb);
+          if (P::kInter && cnext >= 0) drain(1, n, ua, ub);
+        }
+        if (!P::kInter && cnext >= 0)
+          for (int n = 0; n < NCH; ++n) drain(1, n, ua, ub);
+        // combine the two warpgroups' halves of the output dot, then predicate + group-by
+        float* xb = xchg + (t & 1) * kTile;
+        const float part = (pa.x + pa.y) + (pb.x + pb.y);
+        if (wg == 0) {
+          xb[r] = part;
+          named_bar_arrive(2, 256);
+        } else {
+          WIDE_WAIT(11, tid == 256, named_bar_sync(2, 256));
+          const float logit = part + xb[r] + p.bout;
+          agg.tile(p, m, count, r, lane, logit, s_cnt, &xempty[s]);
+        }
+        if (cnext < 0) break;
+        count = cnext;
       }
     }
     if (wg == 1) agg.flush(acc, lane, p.ngroups, s_cnt);
