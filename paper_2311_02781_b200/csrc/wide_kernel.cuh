@@ -7,15 +7,17 @@
 //     2D TMA copies (cp.async.bulk.tensor, cta_group::2) — the image is stored in the exact
 //     128B-swizzled operand layout per (N-chunk, 64-wide K-block, N half), so the tensor maps are plain
 //     [rows][128 B] byte views;
-//   - each N-chunk accumulates in one of two TMEM buffers (256 columns each, ping-pong), so one
-//     epilogue warpgroup drains chunk c while the tensor core computes chunk c+1;
+//   - each N-chunk accumulates in one of two TMEM buffers (256 columns each, ping-pong), so the
+//     epilogue drains chunk c while the tensor core computes chunk c+1; layer 1 of the next tile runs
+//     interleaved with the last layer of the current one (see WidePlan::kInter);
 //   - a hidden layer's bf16 activations ([128 rows x H] per tile, 256 KB at H = 1024: more than an SM
 //     holds) go to a per-CTA scratch in global memory in the same swizzled K-block layout and are
 //     read back as the next layer's A operand by TMA; the scratch (2 x 256 KB per CTA) is
 //     small enough to stay in L2.
 //
 // Warp roles (448 threads = 14 warps per CTA): TMA loader 0, producers 1-3 and 13 (producer.cuh),
-// epilogue warpgroups 4-7 (even N-chunks) and 8-11 (odd N-chunks; also predicate + group-by), warp 12 =
+// epilogue warpgroups 4-7 and 8-11 (each drains 128 of every chunk's 256 columns; 8-11 also predicate +
+// group-by), warp 12 =
 // TMEM allocator + (even CTA) MMA issuer (SMSP 0 holds only the loader, two epilogue warps and the issuer).
 #pragma once
 #include "producer.cuh"
