@@ -349,7 +349,16 @@ __global__ void __launch_bounds__(kThreadsWide, 1) flern_query_wide_kernel(const
       // one N-chunk of layer l into TMEM buffer c % 2 (layer 1: A = X stage sx)
       auto chunk = [&](int l, int sx) {
         const uint32_t b = c & 1;
+#ifdef FLERN_DIAG
+        const long long tq0 = clock64();
+#endif
         WIDE_WAIT_W(1, mbar_wait_cl_nohint(&dempty[b], ((c >> 1) & 1) ^ 1, 44));
+#ifdef FLERN_DIAG
+        // per (layer, position in the tile's chunk sequence) dempty wait, CTA 0: dbg_trace[TR_WAITS][100 + ...]
+        if (p.dbg_trace && blockIdx.x == 0 && lane == 0)
+          atomicAdd(&p.dbg_trace[TR_WAITS * kTraceTiles + 100 + (c % (NL * NCH))], (unsigned long long)(clock64() - tq0));
+        __syncwarp();
+#endif
         tc_fence_after();
         const uint32_t dcol = tmem_base + b * kNChunk;
         if (l == 1) {

@@ -48,3 +48,7 @@ if ok.sum() > 10:
     print("stage: wait issue period | loader: armed-vs-wait-start, rempty-return -> armed")
     for i in range(min(30, len(seq) - 1)):
         print(f"  {idx[i]:4d} {wait[i]:6d} {issue[i]:6d} {period[i]:6d} | {armed_ahead[i]:7d} {lseq[i, 1] - lseq[i, 0]:6d}")
+# dempty waits of CTA 0's MMA thread per position in the tile's chunk sequence (diagnostic builds)
+pos = w[100:100 + 12]
+if pos.sum() > 0:
+    print("dempty wait per chunk position (cycles, summed over tiles):", " ".join(str(int(x)) for x in pos))
