@@ -40,18 +40,23 @@ struct WidePlan {
   // does not hide (scripts/mma_pair_bench.cu: 662 cycles per 4 MMAs with a hand-off every 4, 562 every 8,
   // 512 without), so a stage carries 8 MMAs.
   static constexpr int KPS = 2;
-  static constexpr int RS = 2;                   // operand ring stages
+  // The ring holds NSL slots of one K-block each ([A | B half], 32 KB); stage k takes the KPS slots
+  // n = KPS k + q (mod NSL), so with an odd NSL the stages wrap around the slots (2.5 stages in 160 KB).
+  static constexpr int NSL = K0P <= 32 ? 5 : 4;  // operand slots
+  static constexpr uint32_t SLOT = kABlock + kBHalf;
+  static constexpr int gcd_(int a, int b) { return b == 0 ? a : gcd_(b, a % b); }
+  static constexpr int FP = NSL / gcd_(KPS, NSL);   // stages between two uses of one first slot
   static constexpr int S = 2;                    // X stages (a tile's MLP takes ~10x its gather)
   // layer 1 of tile t+1 runs interleaved with tile t's last layer (its tiny MMAs in the TMEM buffer the
   // last layer's ping-pong leaves idle, its drains under the last layer's long chunks); with two hidden
   // layers the last layer reads layer 1's scratch buffer, so there it follows the last layer instead
   static constexpr bool kInter = NL >= 3;
-  static constexpr uint32_t RING = KPS * (kABlock + kBHalf);
+  static constexpr uint32_t RING = KPS * SLOT;   // bytes of one stage
   static constexpr uint32_t XS = (uint32_t)kTile * K0P * 2;
   static constexpr uint32_t W1H = (uint32_t)128 * K0P * 2;           // one CTA's half of a W1 N-chunk
   static constexpr uint32_t W1C = 2 * W1H;                           // one W1 N-chunk (both halves)
   static constexpr uint32_t off_ring = 0;
-  static constexpr uint32_t off_x = off_ring + RS * RING;
+  static constexpr uint32_t off_x = off_ring + NSL * SLOT;
   static constexpr uint32_t off_meta = off_x + S * XS;
   static constexpr uint32_t off_bias = off_meta + S * kMetaBytes;
   static constexpr uint32_t off_wout = off_bias + NL * H * 4;
@@ -152,7 +157,7 @@ __device__ __forceinline__ void fence_proxy_async_global() {
 template <int K0P, int H, int NL, class SH>
 __global__ void __launch_bounds__(kThreadsWide, 1) flern_query_wide_kernel(const __grid_constant__ QueryParams p) {
   using P = WidePlan<K0P, H, NL>;
-  constexpr int S = P::S, RS = P::RS, NCH = P::NCH, KB = P::KB;
+  constexpr int S = P::S, NSL = P::NSL, NCH = P::NCH, KB = P::KB;
   extern __shared__ __align__(1024) uint8_t smem[];
   const int tid = threadIdx.x;
   const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0), lane = tid & 31;   // warp-uniform (see query_kernel)
@@ -166,14 +171,14 @@ __global__ void __launch_bounds__(kThreadsWide, 1) flern_query_wide_kernel(const
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + P::off_bar);
   uint64_t* xfull = bars;             // [S] producers -> this CTA's loader (128)
   uint64_t* xempty = xfull + S;       // [S] warpgroup 1 (4 warps) -> producers
-  uint64_t* rfull = xempty + S;       // [RS] even CTA: its loader's expect_tx + both CTAs' TMA bytes
-  uint64_t* rempty = rfull + RS;      // [RS][KPS] MMA commit per K-block half of a stage (multicast to both CTAs)
-  uint64_t* dfull = rempty + RS * P::KPS;   // [2] MMA commit (multicast) -> epilogue
+  uint64_t* rfull = xempty + S;       // [NSL] by a stage's first slot, even CTA: its loader's expect_tx + both CTAs' TMA bytes
+  uint64_t* rempty = rfull + NSL;     // [NSL] MMA commit per slot (multicast to both CTAs)
+  uint64_t* dfull = rempty + NSL;     // [2] MMA commit (multicast) -> epilogue
   uint64_t* dempty = dfull + 2;       // [2] even CTA: both CTAs' epilogue warps (16) -> MMA
   uint64_t* actrdy = dempty + 2;      // [2][NCH] N-chunk n of a hidden layer's activations is in scratch buffer b (8)
   uint64_t* decb = actrdy + 2 * NCH;  // [kDec] the pair decision for tile t is in dec[t % kDec] (1)
   uint64_t* pstat = decb + kDec;      // [S] even CTA: the odd CTA's status of tile t is in pst[t % S] (1)
-  static_assert(2 * S + RS + RS * P::KPS + 4 + 2 * NCH + kDec + S <= 64, "barrier block");
+  static_assert(2 * S + 2 * NSL + 4 + 2 * NCH + kDec + S <= 64, "barrier block");
   int32_t* dec = reinterpret_cast<int32_t*>(smem + P::off_dec);        // -1 stop, else this CTA's row count
   int32_t* pst = dec + kDec;                                           // odd CTA's count (-1: out of rows)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + P::off_misc);
@@ -202,8 +207,7 @@ __global__ void __launch_bounds__(kThreadsWide, 1) flern_query_wide_kernel(const
   if (tid == 0) { s_claim[0] = claim0; s_claim[1] = claim0 + 1; }
   if (tid == 0) {
     for (int s = 0; s < S; ++s) { mbar_init(&xfull[s], 32 * kProdWarpsWide); mbar_init(&xempty[s], 4); }
-    for (int s = 0; s < RS; ++s) mbar_init(&rfull[s], 1);
-    for (int s = 0; s < RS * P::KPS; ++s) mbar_init(&rempty[s], 1);
+    for (int s = 0; s < NSL; ++s) { mbar_init(&rfull[s], 1); mbar_init(&rempty[s], 1); }
     for (int i = 0; i < 2; ++i) { mbar_init(&dfull[i], 1); mbar_init(&dempty[i], 16); }
     for (int i = 0; i < 2 * NCH; ++i) mbar_init(&actrdy[i], 8);
     for (int i = 0; i < kDec; ++i) mbar_init(&decb[i], 1);
@@ -233,14 +237,14 @@ __global__ void __launch_bounds__(kThreadsWide, 1) flern_query_wide_kernel(const
       const uint32_t rfull_cl = mapa_rank(smem_u32(rfull), 0);   // the even CTA's rfull[0]
       uint32_t slot = 0;
       const bool noload = WIDE_DBG(2);
-      // A stage is re-armed as soon as its first K-block half is free; the second half's loads follow
-      // when the MMAs of that half complete (half_free), so half of every stage gets its operands ~one
-      // half-stage earlier (the ring holds only 2 stages of 8 MMAs).
+      // A stage is re-armed as soon as its first slot is free; the next slot's loads follow when the MMAs
+      // that read it complete (half_free), so each slot gets its operands as early as the ring allows.
+      // Returns the stage's first slot (its full barrier).
       auto acquire = [&](uint32_t pair_bytes) -> uint32_t {
-        const uint32_t st = slot % RS;
+        const uint32_t n0 = P::KPS * slot, st = n0 % NSL;
         // polls without a sleep: one stage is re-armed per wake-up, and a __nanosleep back-off wakes
         // ~1K cycles late, which paced the whole MMA chain at ~940 cycles per 512-cycle stage (r02c)
-        WIDE_WAIT(6, true, mbar_wait_cl_nohint(&rempty[st * P::KPS], ((slot / RS) & 1) ^ 1, 40));
+        WIDE_WAIT(6, true, mbar_wait_cl_nohint(&rempty[st], ((n0 / NSL) & 1) ^ 1, 40));
         WIDE_LSEQ(slot, 0);
         if (noload) {   // diagnostic: 16 pretend bytes from the odd CTA keep the two loaders in step
           if (leader) mbar_arrive_expect_tx(&rfull[st], 16);
@@ -252,9 +256,11 @@ __global__ void __launch_bounds__(kThreadsWide, 1) flern_query_wide_kernel(const
         ++slot;
         return st;
       };
-      // K-block half q >= 1 of the stage acquired last (slot - 1) is free
-      auto half_free = [&](uint32_t st, int q) {
-        WIDE_WAIT(6, true, mbar_wait_cl_nohint(&rempty[st * P::KPS + q], (((slot - 1) / RS) & 1) ^ 1, 40));
+      // slot q >= 1 of the stage acquired last (slot - 1) is free; returns its index
+      auto half_free = [&](int q) -> uint32_t {
+        const uint32_t n = P::KPS * (slot - 1) + q;
+        WIDE_WAIT(6, true, mbar_wait_cl_nohint(&rempty[n % NSL], ((n / NSL) & 1) ^ 1, 40));
+        return n % NSL;
       };
       bool out = false;   // this CTA's producers have published their last tile
       // the pair decision for tile t (the even CTA decides for both; see the kernel comment)
@@ -289,12 +295,12 @@ __global__ void __launch_bounds__(kThreadsWide, 1) flern_query_wide_kernel(const
       };
       auto load_l1 = [&](int n) {   // W1 halves of N-chunk n (the X tile is already in shared memory)
         const uint32_t st = acquire(P::W1C);
-        uint8_t* dst = smem + P::off_ring + st * P::RING + kABlock;
+        uint8_t* dst = smem + P::off_ring + st * P::SLOT + kABlock;
         const int row = (int)(((size_t)n * P::W1C + rank * P::W1H) >> 7);
 #pragma unroll
         for (uint32_t b = 0; b < P::W1H / 4096; ++b)
           if (!noload) tma_load_2d_pair(dst + b * 4096, &p.tm_w1, 0, row + 32 * b, rfull_cl + st * 8, keep);
-        for (int q = 1; q < P::KPS; ++q) half_free(st, q);   // (unused here: keeps the halves' phases in step)
+        for (int q = 1; q < P::KPS; ++q) half_free(q);   // (unused here: keeps the slots' phases in step)
       };
       auto load_hidden = [&](int l, int n, uint32_t t) {   // layer l >= 2, N-chunk n of tile t
         const int act_row = scratch_row0 + (int)((((l - 2) & 1) * KB * kABlock) >> 7);
@@ -305,13 +311,12 @@ __global__ void __launch_bounds__(kThreadsWide, 1) flern_query_wide_kernel(const
           if (n == 0 && kb0 % (kNChunk / 64) == 0)
             WIDE_WAIT(7, true, mbar_wait(&actrdy[((l - 2) & 1) * NCH + kb0 / (kNChunk / 64)], t & 1, 42));
           const uint32_t st = acquire(2 * P::RING);
-          uint8_t* dst = smem + P::off_ring + st * P::RING;
 #pragma unroll
           for (int q = 0; q < P::KPS; ++q) {
-            if (q > 0) half_free(st, q);
+            const uint32_t sq = q > 0 ? half_free(q) : st;
             if (noload) continue;
             const int kb = kb0 + q;
-            uint8_t* d = dst + q * (kABlock + kBHalf);
+            uint8_t* d = smem + P::off_ring + sq * P::SLOT;
             tma_load_2d_pair(d, &p.tm_act, 0, act_row + kb * (int)(kABlock >> 7), rfull_cl + st * 8, keep);
             tma_load_2d_pair(d + kABlock, &p.tm_wh, 0, (int)((wl + (size_t)kb * kBBlock + rank * kBHalf) >> 7),
                              rfull_cl + st * 8, keep);
@@ -362,10 +367,10 @@ __global__ void __launch_bounds__(kThreadsWide, 1) flern_query_wide_kernel(const
         tc_fence_after();
         const uint32_t dcol = tmem_base + b * kNChunk;
         if (l == 1) {
-          const uint32_t st = slot % RS;
-          WIDE_WAIT_W(2, mbar_wait_nohint(&rfull[st], (slot / RS) & 1, 45));
+          const uint32_t st = (P::KPS * slot) % NSL;
+          WIDE_WAIT_W(2, mbar_wait_nohint(&rfull[st], (slot / P::FP) & 1, 45));
           tc_fence_after();
-          const uint32_t bb = ring + st * P::RING + kABlock;
+          const uint32_t bb = ring + st * P::SLOT + kABlock;
 #pragma unroll
           for (int ks = 0; ks < K0P / 16; ++ks) {
             const uint64_t ad = make_sdesc(x0 + sx * P::XS + ks * 2 * (kTile * 16), kTile * 16, 128, kLayoutNone);
@@ -374,25 +379,26 @@ __global__ void __launch_bounds__(kThreadsWide, 1) flern_query_wide_kernel(const
           }
 #pragma unroll
           for (int q = 0; q < P::KPS; ++q)
-            if (elect_one_sync()) mma_commit_pair(&rempty[st * P::KPS + q], 3);
+            if (elect_one_sync()) mma_commit_pair(&rempty[(P::KPS * slot + q) % NSL], 3);
           ++slot;
         } else {
           for (int kb0 = 0; kb0 < KB; kb0 += P::KPS) {
-            const uint32_t st = slot % RS;
+            const uint32_t st = (P::KPS * slot) % NSL;
             WIDE_SEQ(slot, 0);
-            WIDE_WAIT_W(3, mbar_wait_nohint(&rfull[st], (slot / RS) & 1, 46));
+            WIDE_WAIT_W(3, mbar_wait_nohint(&rfull[st], (slot / P::FP) & 1, 46));
             WIDE_SEQ(slot, 1);
             tc_fence_after();
 #pragma unroll
             for (int q = 0; q < P::KPS; ++q) {
-              const uint32_t ab = ring + st * P::RING + q * (kABlock + kBHalf), bb = ab + kABlock;
+              const uint32_t sq = (P::KPS * slot + q) % NSL;
+              const uint32_t ab = ring + sq * P::SLOT, bb = ab + kABlock;
 #pragma unroll
               for (int j = 0; j < 4; ++j) {
                 const uint64_t ad = make_sdesc(ab + j * 32, 16, 1024, kLayoutSW128);
                 const uint64_t bd = make_sdesc(bb + j * 32, 16, 1024, kLayoutSW128);
                 if (elect_one_sync()) mma_bf16_ss_pair(dcol, ad, bd, idesc, (kb0 | q | j) != 0);
               }
-              if (elect_one_sync()) mma_commit_pair(&rempty[st * P::KPS + q], 3);   // half q read
+              if (elect_one_sync()) mma_commit_pair(&rempty[sq], 3);   // slot q of the stage read
             }
             WIDE_SEQ(slot, 2);
             ++slot;
