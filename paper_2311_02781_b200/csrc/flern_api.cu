@@ -1710,7 +1710,7 @@ extern "C" FLERN_API flern_status flern_train_step(flern_ctx* ctx, const flern_q
   tp.K0 = K0;
   tp.grad = m.tgrad;
   tp.rows = m.trows;
-  const int grid = plan_claims(ctx, p, K0P, 2, 32 * kProdWarpsWide);
+  const int grid = plan_claims(ctx, p, K0P, 2, 32 * kTrainProdWarps);
   if (!te->attr_set) {
     CUDA_TRY(ctx, cudaFuncSetAttribute(te->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)te->smem));
     te->attr_set = true;

@@ -33,8 +33,12 @@ namespace flern {
 constexpr int kTrainH = 128;                // hidden width (M = 128 for the weight-gradient MMAs)
 constexpr int kTrainHA = kTrainH + 16;      // H1 tile width: H + a ones column (db2) + zero padding
 constexpr int kTrainCW = 4;                 // compute warpgroups: each takes H / kTrainCW hidden units of every phase (2: 1.90 ms, 4: 1.68 ms per C2 step)
-constexpr int kTrainMmaWarp = 4 + 4 * kTrainCW;
-constexpr int kTrainThreads = 32 * (kTrainMmaWarp + 1);   // producers 0-3, compute warpgroups 4.., MMA issuer last
+// Warps: producers 0 .. kTrainProdWarps-1, the MMA issuer 3, compute warpgroups 4 .. 4 + 4 kTrainCW - 1 (a
+// warpgroup's warps must cover the four TMEM lane quadrants, warp % 4). 20 warps put at most 5 on an SMSP,
+// which leaves 96 registers per thread (21 warps, with four producers: 80, with spills).
+constexpr int kTrainProdWarps = 3;
+constexpr int kTrainMmaWarp = 3;
+constexpr int kTrainThreads = 32 * (4 + 4 * kTrainCW);
 constexpr uint32_t kIdescAMajorMN = 1u << 15;
 
 // gradient / statistics buffer (fp32, zeroed before each step): G1 [H][K0P] (column K0 = db1),
@@ -77,7 +81,7 @@ struct TrainPlan {
   static constexpr uint32_t off_meta = off_dy + DYB;
   static constexpr uint32_t off_par = off_meta + S * kMetaBytes;   // b1 | b2 | w3 (fp32)
   static constexpr uint32_t off_queue = off_par + 3 * kTrainH * 4;
-  static constexpr uint32_t off_xchg = off_queue + queue_bytes(32 * kProdWarpsWide);   // [2][kTrainCW][128] partial y
+  static constexpr uint32_t off_xchg = off_queue + queue_bytes(32 * kTrainProdWarps);   // [2][kTrainCW][128] partial y
   static constexpr uint32_t off_norm = off_xchg + 2 * kTrainCW * kTile * 4;
   static constexpr uint32_t off_bar = off_norm + kMaxFeat * 8;
   static constexpr uint32_t off_misc = off_bar + 32 * 8;
@@ -158,7 +162,7 @@ __global__ void __launch_bounds__(kTrainThreads, 1) flern_train_kernel(const __g
   }
   fence_proxy_async_smem();
   if (tid == 0) {
-    for (int s = 0; s < S; ++s) { mbar_init(&xfull[s], 32 * kProdWarpsWide); mbar_init(&xempty[s], 1); }
+    for (int s = 0; s < S; ++s) { mbar_init(&xfull[s], 32 * kTrainProdWarps); mbar_init(&xempty[s], 1); }
     mbar_init(z1full, 1);
     mbar_init(h1full, 4 * kTrainCW);
     mbar_init(z2full, 1);
@@ -176,9 +180,9 @@ __global__ void __launch_bounds__(kTrainThreads, 1) flern_train_kernel(const __g
   if (*tmem_slot != 0u) __trap();
   const uint32_t sbase = smem_u32(smem);
 
-  if (warp < 4) {
+  if (warp < kTrainProdWarps) {
     // ---------------------------------------------------------------- producers (producer.cuh)
-    producer_loop<K0P, 2, S, GenericShape, kProdWarpsWide, false>(
+    producer_loop<K0P, 2, S, GenericShape, kTrainProdWarps, false>(
         p, XRing{smem + P::off_x, P::XS, smem + P::off_meta, xfull, xempty}, wcnt, s_norm, s_cnt,
         reinterpret_cast<int32_t*>(smem + P::off_queue), s_claim, FactRing{}, warp * 32 + lane, warp, lane);
   } else if (warp == kTrainMmaWarp) {
