@@ -149,6 +149,21 @@ def test_all_probes_miss(name, miss):
     assert r["gpu"]["rows_joined"] == 0 and r["gpu"]["count"].sum() == 0
 
 
+def test_wide_pairs_unbalanced_tiles():
+    """The wide kernel runs on CTA pairs whose two CTAs produce different numbers of tiles: here the
+    fact rows after the first tenth all miss their first probe, so most CTAs run out of joined rows at
+    once while the CTAs that claimed the first chunks still have many tiles (their pair partners run
+    dummy tiles until the pair stops). Join ids, scores, selection and aggregates against the oracle."""
+    cfg = D.with_sf(D.CONFIGS["c3"], 0.02, match_rate=0.9)
+    db = D.make_database(cfg)
+    fk = db.fact["l_orderkey"].copy()
+    cut = db.fact_n // 10
+    fk[cut:] = np.iinfo(np.int32).max - 7   # no such order key
+    db.fact["l_orderkey"] = fk
+    r = parity.check(cfg, db, _calibrated(cfg, db))
+    assert 0 < r["gpu"]["rows_joined"] <= cut
+
+
 def test_shuffled_fact_rows_same_aggregates():
     """Permutation invariance on the GPU: shuffled lineitem gives bit-identical aggregates
     (integer atomics; the tile decomposition changes, the result must not)."""
